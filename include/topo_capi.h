@@ -1,0 +1,190 @@
+/*
+ * topo_capi.h — C-ABI of the B200-native design-update hot path
+ * (density filter -> volume-preserving Heaviside projection -> SIMP +
+ * lower-triangle stiffness values -> element compliance sensitivity from a
+ * supplied U -> chain-rule back-filter -> OC bisection update).
+ *
+ * The reference (arxiv/paper_2005_05436, /root/reference/proj/include/topopt)
+ * exposes this path as free inline C++ functions; each entry point below names
+ * the reference function it replaces (file:line). Plain pointers and sizes
+ * only. Every array argument may be a HOST pointer (copied through the
+ * context's device buffers) or a DEVICE pointer (used in place); the kind is
+ * detected per call with cudaPointerGetAttributes. Calls are stream-ordered on
+ * the context's stream and synchronous at return.
+ *
+ * Error model: a non-zero topo_status; topo_last_error(ctx) has the message.
+ * The C++ adapter (include/topopt_gpu.hpp) maps TOPO_EINVAL ->
+ * std::invalid_argument, TOPO_EOVERFLOW -> std::overflow_error, TOPO_ENONMONO
+ * / TOPO_ECUDA / TOPO_ENCCL -> std::runtime_error, as the reference throws
+ * (grid.hpp:92, fea.hpp:159-160, filter.hpp:96,120,127,184, oc.hpp:74,140,161).
+ *
+ * Multi-GPU: one context per GPU/rank, x-slab decomposition.
+ * With nranks > 1 every per-element array is the rank's slab
+ * (columns [j0, j1) of the global grid, element order of grid.hpp:42-45) and
+ * U is the rank's node planes [j0, j1] inclusive.
+ */
+#ifndef TOPO_CAPI_H
+#define TOPO_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TOPO_CAPI_VERSION 1
+
+typedef struct topo_ctx topo_ctx;
+
+typedef enum {
+  TOPO_OK = 0,
+  TOPO_EINVAL = 1,    /* std::invalid_argument in the reference */
+  TOPO_EOVERFLOW = 2, /* std::overflow_error (grid.hpp:91-93) */
+  TOPO_ENONMONO = 3,  /* std::runtime_error  (oc.hpp:139-140, :160-161) */
+  TOPO_ECUDA = 4,
+  TOPO_ENCCL = 5,
+  TOPO_ENOMEM = 6
+} topo_status;
+
+/* filter.hpp:14 FilterBC */
+enum { TOPO_BC_NEUMANN = 0, TOPO_BC_DIRICHLET = 1 };
+/* grid.hpp:73-78 DomainPartition as a per-element state byte */
+enum { TOPO_ACTIVE = 0, TOPO_PASSIVE_SOLID = 1, TOPO_PASSIVE_VOID = 2 };
+/* the physical-volume callback of bisect_update (oc.hpp:96), built by
+ * driver.hpp:214-229 per filter mode ft; a std::function cannot cross the
+ * C-ABI, so the callback becomes an enum (plus an optional C callback) */
+enum {
+  TOPO_VOL_CALLBACK = 0,  /* user C callback on the host copy of xNew */
+  TOPO_VOL_MEAN = 1,      /* ft = 1: mean(xc)                    driver.hpp:216     */
+  TOPO_VOL_PROJECTED = 2, /* ft = 2: mean(H(pin(filter(xc))))    driver.hpp:218-222 */
+  TOPO_VOL_FILTERED = 3   /* ft = 3: mean(pin(filter(xc)))       driver.hpp:224-228 */
+};
+
+typedef struct {
+  int32_t nelx, nely, nelz; /* grid.hpp:17-46; nelz = 0 selects 2D Q4 */
+  double rmin;              /* filter.hpp:95 build_filter */
+  int32_t bc;               /* TOPO_BC_* */
+  double nu;                /* Poisson ratio for the element stiffness (fea.hpp:51,73) */
+  int32_t device;           /* CUDA ordinal; -1 = current device */
+  int32_t rank, nranks;     /* x-slab decomposition; single GPU: 0, 1 */
+  int32_t j0, j1;           /* slab columns [j0, j1); j1 <= j0 -> even split by rank */
+} topo_grid_desc;
+
+typedef struct { /* fea.hpp:124-128 SimpParams */
+  double e0, emin, penal;
+} topo_simp;
+
+typedef struct { /* oc.hpp:14-20 OcParams + oc.hpp:81-85 BisectOptions */
+  double move, volfrac, bisect_rel_tol, volume_tol;
+  int32_t lambda_space;
+  double abs_tol, lambda_max;
+} topo_oc_params;
+
+typedef double (*topo_volume_fn)(void* user, const double* xNew, int64_t m);
+
+typedef struct { /* driver.hpp:56-75 RunConfig fields the pass reads (ft = 3) */
+  topo_simp simp;
+  double beta, eta0;
+  double move, volfrac;
+  double eta_override; /* NaN: solve eta (filter.hpp:182); else use it as given */
+  int32_t volume_mode; /* TOPO_VOL_FILTERED for ft = 3 */
+  int32_t write_sk;    /* 1: produce the m*P lower-triangle values (fea.hpp:162-169) */
+} topo_pass_params;
+
+typedef struct {
+  /* caller buffers (host or device, length m unless noted) or NULL to skip */
+  double *xTilde, *xPhys, *dcPhys, *dc, *dV, *xNew;
+  double* sK; /* m*P; NULL keeps the values in the context (topo_device_buffer) */
+  double eta, c, lambda;
+  int32_t eta_iters, bisections, evaluations;
+} topo_pass_out;
+
+/* device buffers owned by the context, for zero-copy consumers (the state
+ * solve) */
+enum { TOPO_BUF_SK = 0, TOPO_BUF_IK = 1, TOPO_BUF_JK = 2, TOPO_BUF_XNEW = 3, TOPO_BUF_XPHYS = 4 };
+
+/* ---- lifecycle ---------------------------------------------------------- */
+/* ke_full (d*d, column-major) / ke_lower (d(d+1)/2, fea.hpp:33-40 order) are
+ * the host-built element matrices (fea.hpp:51-121); NULL builds them from
+ * desc->nu with topo_element_stiffness. elem_state: m_local bytes of
+ * TOPO_ACTIVE/..., or NULL (all active). */
+topo_status topo_ctx_create(const topo_grid_desc* desc, const double* ke_full,
+                            const double* ke_lower, const uint8_t* elem_state, topo_ctx** out);
+void topo_ctx_destroy(topo_ctx* ctx);
+const char* topo_last_error(const topo_ctx* ctx);
+/* run on an external stream (e.g. torch.cuda.current_stream().cuda_stream) */
+topo_status topo_set_stream(topo_ctx* ctx, void* cuda_stream);
+topo_status topo_sync(topo_ctx* ctx);
+topo_status topo_device_buffer(topo_ctx* ctx, int which, void** ptr, int64_t* count);
+/* sizes: m (local elements), n (local DOFs), P (pairs/element), ntaps, reach,
+ * j0, j1 */
+topo_status topo_ctx_info(const topo_ctx* ctx, int64_t* m, int64_t* n, int32_t* P,
+                          int32_t* ntaps, int32_t* reach, int32_t* j0, int32_t* j1);
+/* multi-GPU: join an NCCL clique (nccl_unique_id = 128 bytes from rank 0) */
+topo_status topo_comm_init_nccl(topo_ctx* ctx, const void* nccl_unique_id);
+
+/* ---- host setup helpers (no device work) -------------------------------- */
+/* fea.hpp:51-68 (dim 2) / fea.hpp:73-121 (dim 3) */
+topo_status topo_element_stiffness(int dim, double nu, double* ke_full, double* ke_lower);
+/* SURVEY.md Appendix B counter-based generator (splitmix64):
+ * kind 0 uniform [a, b), kind 1 normal(a, b) via Box-Muller on pairs */
+void topo_generate(uint64_t seed, uint64_t stream, int kind, double a, double b, int64_t offset,
+                   int64_t count, double* out);
+
+/* ---- K0: grid.hpp:89-153 ------------------------------------------------ */
+topo_status topo_build_connectivity(topo_ctx* ctx, int32_t* dofs);          /* m*d */
+topo_status topo_build_index_pairs(topo_ctx* ctx, int32_t* iK, int32_t* jK); /* m*P; NULL=keep */
+
+/* ---- fea.hpp ------------------------------------------------------------ */
+/* fea.hpp:135-146 simp_interpolate */
+topo_status topo_simp_interpolate(topo_ctx* ctx, const double* xhat, const topo_simp* prm,
+                                  double* sK, double* dsK);
+/* fea.hpp:154-176 assemble_lower, value generation (:162-169): vals[e*P+q] =
+ * sK[e] * Ke_lower[q] (duplicates are summed by the consumer) */
+topo_status topo_assemble_values(topo_ctx* ctx, const double* sK, double* vals);
+/* fea.hpp:248-272 compliance_and_sensitivity (c is the rank-local partial) */
+topo_status topo_sensitivity(topo_ctx* ctx, const double* U, const double* xhat,
+                             const topo_simp* prm, double* c, double* dc);
+
+/* ---- filter.hpp --------------------------------------------------------- */
+topo_status topo_filter(topo_ctx* ctx, const double* x, double* xTilde, int pin); /* :119-122 */
+topo_status topo_filter_adjoint(topo_ctx* ctx, const double* g, double* out);      /* :126-129 */
+topo_status topo_project(topo_ctx* ctx, const double* xt, double eta, double beta,
+                         double* out); /* :137-144 */
+topo_status topo_project_derivative(topo_ctx* ctx, const double* xt, double eta, double beta,
+                                    double* out); /* :146-154 */
+topo_status topo_backfilter(topo_ctx* ctx, const double* g, const double* xt, double eta,
+                            double beta, int proj_on, double* out); /* :166-171 */
+topo_status topo_solve_eta(topo_ctx* ctx, const double* xTilde, double beta, double eta0,
+                           double* eta, int32_t* iters); /* :182-228 (active set from ctx) */
+/* filter taps in reference order (filter.hpp:107-113) and hs */
+topo_status topo_filter_taps(topo_ctx* ctx, int32_t* di, int32_t* dj, int32_t* dk, double* w);
+topo_status topo_filter_hs(topo_ctx* ctx, double* hs);
+
+/* ---- oc.hpp ------------------------------------------------------------- */
+/* oc.hpp:31-39, compact active arrays of length nact */
+topo_status topo_lambda_upper(topo_ctx* ctx, int64_t nact, const double* xAct,
+                              const double* dcAct, const double* dVAct, double volfrac,
+                              int64_t mTotal, double* lambda);
+/* oc.hpp:72-79 */
+topo_status topo_oc_candidate(topo_ctx* ctx, int64_t nact, const double* xAct,
+                              const double* dcAct, const double* dVAct, double lambda,
+                              double move, double* out);
+/* oc.hpp:93-174 bisect_update over full-length x, dc, dV (passives from ctx).
+ * eta/beta are used by TOPO_VOL_PROJECTED; cb/user by TOPO_VOL_CALLBACK. */
+topo_status topo_oc_bisect(topo_ctx* ctx, const double* x, const double* dc, const double* dV,
+                           const topo_oc_params* prm, int volume_mode, double eta, double beta,
+                           topo_volume_fn cb, void* user, double* xNew, double* lambda,
+                           int32_t* bisections, int32_t* evaluations);
+
+/* ---- fused pass: driver.hpp:183-231 (ft = 3) minus the state solve ------ */
+topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
+                             const topo_pass_params* prm, topo_pass_out* out);
+/* number of this library's kernel launches issued by the last call */
+int64_t topo_last_launch_count(const topo_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOPO_CAPI_H */

@@ -364,6 +364,12 @@ class Oracle:
                                                C.byref(eta), C.byref(it)))
         return eta.value, it.value
 
+    def eta_mismatch(self, xt, beta, eta, state=None):
+        """port only: g(eta) of filter.hpp:187-196 (already divided by m)."""
+        xt = _f64(xt)
+        st = None if state is None else np.ascontiguousarray(state, np.uint8)
+        return self.lib.orc_eta_mismatch(len(xt), _p(xt), beta, eta, _p(st))
+
     # --------------------------------------------------------------- oc.hpp
     def lambda_upper(self, x, dc, dV, volfrac, mtotal):
         x, dc, dV = _f64(x), _f64(dc), _f64(dV)

@@ -1,0 +1,1228 @@
+// C-ABI implementation (include/topo_capi.h): context, buffers, host/device
+// staging, and the stream-ordered orchestration of the kernels in
+// kernels.cuh. One context per GPU (x-slab rank).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/topo_capi.h"
+#include "comm.h"
+#include "kernels.cuh"
+
+using namespace topo;
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t b) {
+    if (b <= bytes && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, b ? b : 16);
+    if (e == cudaSuccess) bytes = b;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+struct topo_ctx {
+  std::string err;
+  int device = 0;
+  cudaStream_t stream = nullptr, aux = nullptr;
+  bool own_stream = true;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int sm_count = 148;
+  Geo G{};
+  int rank = 0, nranks = 1;
+  int reach = 0, rk = 0;
+  double rmin = 1.0;
+  long long m_st = 0;  // stored (halo-extended) elements
+  long long n = 0;     // local DOFs
+  // taps
+  std::vector<int> di, dj, dk;
+  std::vector<double> w;
+  std::vector<TapRow> rows;
+  DevBuf d_rows, d_w;
+  // element matrices
+  std::vector<double> ke_full, ke_lower;
+  DevBuf d_ke_lower;
+  // partition
+  DevBuf d_state;
+  bool has_state = false;
+  long long nS_local = 0, nV_local = 0;
+  double nS_total = 0;  // |P1| over all ranks
+  double m_total = 0;   // global element count
+  // fields
+  DevBuf hs, hs_st, cw, x_st, xt, xphys, dcphys, dc, dV, xnew, a1_st, a2_st, rec, u, tmp0, tmp1,
+      tmp_st;
+  DevBuf sK, iK, jK;
+  DevBuf partials, partials0, result;
+  double* h_result = nullptr;  // pinned
+  int conv_jt = 1;             // outputs per thread along x
+  int coop_blocks = 148;
+  long long launches = 0;
+  Comm* comm = nullptr;
+};
+
+namespace {
+
+topo_status fail(topo_ctx* c, topo_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return s;
+}
+
+#define CK(x)                                                                      \
+  do {                                                                             \
+    cudaError_t e_ = (x);                                                          \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(ctx, TOPO_ECUDA, "%s failed: %s", #x, cudaGetErrorString(e_));   \
+  } while (0)
+
+#define LAUNCHED()                                                                 \
+  do {                                                                             \
+    cudaError_t e_ = cudaGetLastError();                                           \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(ctx, TOPO_ECUDA, "kernel launch failed (%s:%d): %s", __FILE__,   \
+                  __LINE__, cudaGetErrorString(e_));                               \
+    ++ctx->launches;                                                               \
+  } while (0)
+
+#define TRY(...)                      \
+  do {                                \
+    topo_status s_ = (__VA_ARGS__);   \
+    if (s_ != TOPO_OK) return s_;     \
+  } while (0)
+
+int grid_for(const topo_ctx* c, long long work, int per_block = kThreads) {
+  long long b = (work + per_block - 1) / per_block;
+  const long long cap = (long long)c->sm_count * 8;
+  if (b > cap) b = cap;
+  return int(b < 1 ? 1 : b);
+}
+
+// Input array -> device pointer (host arrays are copied into `scratch`).
+topo_status stage_in(topo_ctx* ctx, const double* p, long long count, DevBuf& scratch,
+                     const double** out) {
+  if (!p) return fail(ctx, TOPO_EINVAL, "null input array");
+  if (is_device_ptr(p)) {
+    *out = p;
+    return TOPO_OK;
+  }
+  CK(scratch.ensure(sizeof(double) * size_t(count)));
+  CK(cudaMemcpyAsync(scratch.p, p, sizeof(double) * size_t(count), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  *out = scratch.as<double>();
+  return TOPO_OK;
+}
+
+// Input field -> storage (halo-extended) device array, halo filled.
+topo_status stage_field_storage(topo_ctx* ctx, const double* p, DevBuf& st_buf,
+                                const double** out) {
+  const Geo& G = ctx->G;
+  if (!p) return fail(ctx, TOPO_EINVAL, "null input field");
+  const bool dev = is_device_ptr(p);
+  if (dev && ctx->m_st == G.m) {  // no halo: use in place
+    *out = p;
+    return TOPO_OK;
+  }
+  CK(st_buf.ensure(sizeof(double) * size_t(ctx->m_st)));
+  double* dst = st_buf.as<double>() + (long long)(G.j0 - G.sj0) * G.S;
+  CK(cudaMemcpyAsync(dst, p, sizeof(double) * size_t(G.m),
+                     dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+  if (ctx->comm) TRY(comm_halo(ctx->comm, ctx, st_buf.as<double>()));
+  *out = st_buf.as<double>();
+  return TOPO_OK;
+}
+
+// Output array: device pointers are written in place; host pointers go
+// through `scratch` and are copied back by finish_out().
+double* out_ptr(topo_ctx* ctx, double* user, DevBuf& scratch, long long count, bool* host) {
+  *host = false;
+  if (user && is_device_ptr(user)) return user;
+  if (scratch.ensure(sizeof(double) * size_t(count)) != cudaSuccess) return nullptr;
+  *host = user != nullptr;
+  (void)ctx;
+  return scratch.as<double>();
+}
+
+topo_status finish_out(topo_ctx* ctx, double* user, const double* dev, long long count,
+                       bool host) {
+  if (host)
+    CK(cudaMemcpyAsync(user, dev, sizeof(double) * size_t(count), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+  return TOPO_OK;
+}
+
+// ------------------------------------------------------------ convolution
+size_t conv_smem_bytes(const topo_ctx* c, int nf, int jt) {
+  const Geo& G = c->G;
+  const int TI = 32, TK = G.is3d ? 4 : 1, TJ = (G.is3d ? 2 : 8) * jt;
+  const long long tile =
+      (long long)(TI + 2 * c->reach) * (TK + 2 * c->rk) * (TJ + 2 * c->reach);
+  return sizeof(double) * size_t(c->w.size() + 2 * c->rows.size() + nf * tile);
+}
+
+template <int NF, int MODE, int JT>
+topo_status launch_conv_t(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* nblocks) {
+  const int TK = G.is3d ? 4 : 1, TZ = G.is3d ? 2 : 8;
+  dim3 block(32, TK, TZ);
+  dim3 grid((G.nely + 31) / 32, (G.nz + TK - 1) / TK, (G.jn + TZ * JT - 1) / (TZ * JT));
+  const size_t smem = conv_smem_bytes(ctx, NF, JT);
+  static bool attr_done = false;  // per instantiation
+  if (!attr_done) {
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, k_conv<NF, MODE, JT>));
+    CK(cudaFuncSetAttribute(k_conv<NF, MODE, JT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            optin - int(fa.sharedSizeBytes)));
+    attr_done = true;
+  }
+  k_conv<NF, MODE, JT><<<grid, block, smem, ctx->stream>>>(
+      G, ctx->d_rows.as<TapRow>(), int(ctx->rows.size()), ctx->d_w.as<double>(),
+      int(ctx->w.size()), ctx->reach, ctx->rk, A);
+  LAUNCHED();
+  if (nblocks) *nblocks = int(grid.x * grid.y * grid.z);
+  return TOPO_OK;
+}
+
+template <int NF, int MODE>
+topo_status launch_conv(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* nblocks = nullptr) {
+  if (ctx->conv_jt == 2) return launch_conv_t<NF, MODE, 2>(ctx, G, A, nblocks);
+  return launch_conv_t<NF, MODE, 1>(ctx, G, A, nblocks);
+}
+
+int conv_blocks(const topo_ctx* ctx) {
+  const Geo& G = ctx->G;
+  const int TK = G.is3d ? 4 : 1, TZ = G.is3d ? 2 : 8;
+  return ((G.nely + 31) / 32) * ((G.nz + TK - 1) / TK) *
+         ((G.jn + TZ * ctx->conv_jt - 1) / (TZ * ctx->conv_jt));
+}
+
+// ------------------------------------------------------- reductions / comm
+// sums `count` partial records (stride N) into ctx->h_result[0..N) (global)
+template <int N>
+topo_status reduce_to_host(topo_ctx* ctx, const double* partials, int count) {
+  k_reduce_partials<N><<<1, 32, 0, ctx->stream>>>(partials, count, N, ctx->result.as<double>());
+  LAUNCHED();
+  if (ctx->comm) TRY(comm_allreduce(ctx->comm, ctx, ctx->result.as<double>(), N));
+  CK(cudaMemcpyAsync(ctx->h_result, ctx->result.p, sizeof(double) * N, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+topo_status coop_launch(topo_ctx* ctx, const void* fn, void* args) {
+  void* kargs[] = {args};
+  CK(cudaLaunchCooperativeKernel(fn, dim3(ctx->coop_blocks), dim3(kThreads), kargs, 0,
+                                 ctx->stream));
+  ++ctx->launches;
+  return TOPO_OK;
+}
+
+// ------------------------------------------------------------------ eta
+topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
+                    const double* partials0, int n0, double* eta_dev_out) {
+  EtaArgs A;
+  A.G = ctx->G;
+  A.xt = xt;
+  A.state = ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr;
+  A.beta = beta;
+  A.eta0 = eta0;
+  A.mtotal = ctx->m_total;
+  A.partials0 = partials0;
+  A.n0 = n0;
+  A.partials = ctx->partials.as<double>();
+  A.result = eta_dev_out;
+  if (!ctx->comm) return coop_launch(ctx, (const void*)k_eta_solve, &A);
+  // multi-GPU: host-driven replay, one allreduce of (g, g') per evaluation
+  EtaCtl ctl;
+  ctl.init(eta0);
+  double g, gp;
+  if (partials0) {
+    TRY(reduce_to_host<3>(ctx, partials0, n0));
+  } else {
+    k_eta_partials<<<ctx->coop_blocks, kThreads, 0, ctx->stream>>>(A, ctl.eta);
+    LAUNCHED();
+    TRY(reduce_to_host<2>(ctx, A.partials, ctx->coop_blocks));
+  }
+  g = ctx->h_result[0];
+  gp = ctx->h_result[1];
+  while (ctl.feed(g / ctx->m_total, gp / ctx->m_total)) {
+    k_eta_partials<<<ctx->coop_blocks, kThreads, 0, ctx->stream>>>(A, ctl.eta);
+    LAUNCHED();
+    TRY(reduce_to_host<2>(ctx, A.partials, ctx->coop_blocks));
+    g = ctx->h_result[0];
+    gp = ctx->h_result[1];
+  }
+  const double res[3] = {ctl.eta, double(ctl.it), ctl.g};
+  CK(cudaMemcpyAsync(eta_dev_out, res, sizeof res, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+// ------------------------------------------------------------------- OC
+// records (ctx->rec) and prep partials must be ready; writes xNew (device)
+topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const double* prep,
+                   int n_prep, double* xnew_dev, double* lam, int32_t* bis, int32_t* evals,
+                   double eta, double beta, topo_volume_fn cb, void* user) {
+  const Geo& G = ctx->G;
+  const double add_const = mode == TOPO_VOL_FILTERED ? ctx->nS_total : 0.0;
+  if ((mode == TOPO_VOL_MEAN || mode == TOPO_VOL_FILTERED) && !ctx->comm) {
+    OcArgs A;
+    A.m = G.m;
+    A.rec = ctx->rec.as<double4>();
+    A.prep_partials = prep;
+    A.n_prep = n_prep;
+    A.volfrac = prm->volfrac;
+    A.rel_tol = prm->bisect_rel_tol;
+    A.vol_tol = prm->volume_tol;
+    A.abs_tol = prm->abs_tol;
+    A.lambda_max = prm->lambda_max;
+    A.mtotal = ctx->m_total;
+    A.add_const = add_const;
+    A.lambda_space = prm->lambda_space;
+    A.margin = 1e-12;
+    A.partials = ctx->partials.as<double>();
+    A.xNew = xnew_dev;
+    A.result = ctx->result.as<double>() + 8;
+    TRY(coop_launch(ctx, (const void*)k_oc_bisect, &A));
+    CK(cudaMemcpyAsync(ctx->h_result + 8, A.result, sizeof(double) * 7, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const double* r = ctx->h_result + 8;
+    if (int(r[3]) == OcCtl::ST_NONMONO)
+      return fail(ctx, TOPO_ENONMONO, "oc: candidate volume is not monotone in the multiplier");
+    *lam = r[0];
+    *bis = int32_t(r[1]);
+    *evals = int32_t(r[2]);
+    return TOPO_OK;
+  }
+  // host-driven replay: multi-GPU identity volumes, projected volume, callback
+  TRY(reduce_to_host<3>(ctx, prep, n_prep));
+  double lamMax = prm->lambda_max;
+  if (!(prm->lambda_max > 0)) {
+    const double root = ctx->h_result[0] / (ctx->m_total * prm->volfrac);
+    lamMax = root * root;
+  }
+  OcCtl ctl;
+  ctl.init(lamMax, prm->volfrac, prm->bisect_rel_tol, prm->volume_tol, prm->lambda_space,
+           prm->abs_tol);
+  std::vector<double> hx;
+  const int nb = grid_for(ctx, G.m);
+  while (ctl.pending()) {
+    const double s = ctl.s_req;
+    double v = 0;
+    k_oc_candidates<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->rec.as<double4>(), s, xnew_dev);
+    LAUNCHED();
+    if (mode == TOPO_VOL_CALLBACK) {
+      if (!cb) return fail(ctx, TOPO_EINVAL, "oc: volume callback is null");
+      hx.resize(size_t(G.m));
+      CK(cudaMemcpyAsync(hx.data(), xnew_dev, sizeof(double) * size_t(G.m),
+                         cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      v = cb(user, hx.data(), G.m);
+    } else if (mode == TOPO_VOL_PROJECTED) {
+      const double* xs = nullptr;
+      TRY(stage_field_storage(ctx, xnew_dev, ctx->tmp_st, &xs));
+      ConvArgs C{};
+      C.in0 = xs;
+      C.hs = ctx->hs.as<double>();
+      C.out0 = ctx->tmp1.as<double>();
+      C.state = ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr;
+      C.pin = 1;
+      TRY(launch_conv<1, CONV_FWD>(ctx, G, C));
+      k_sum<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->tmp1.as<double>(), 1, eta, beta,
+                                               ctx->partials.as<double>());
+      LAUNCHED();
+      TRY(reduce_to_host<1>(ctx, ctx->partials.as<double>(), nb));
+      v = ctx->h_result[0] / ctx->m_total;
+    } else {  // multi-GPU identity volume (ft = 1 / ft = 3)
+      TRY(comm_oc_volume(ctx->comm, ctx, s, add_const, &v));
+    }
+    ctl.feed(v);
+  }
+  if (ctl.status == OcCtl::ST_NONMONO)
+    return fail(ctx, TOPO_ENONMONO, "oc: candidate volume is not monotone in the multiplier");
+  k_oc_candidates<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->rec.as<double4>(), ctl.s_final,
+                                                    xnew_dev);
+  LAUNCHED();
+  *lam = ctl.lam_result;
+  *bis = ctl.bis;
+  *evals = ctl.evals;
+  return TOPO_OK;
+}
+
+topo_status validate_slab(topo_ctx* ctx) {
+  // every tap of every owned element must land in a stored column
+  const Geo& G = ctx->G;
+  for (int j = G.j0 - ctx->reach; j < G.j0 + G.jn + ctx->reach; ++j) {
+    int jf = j;
+    if (G.bc == 0)
+      jf = reflect_index(j, G.nelx);
+    else if (j < 0 || j >= G.nelx)
+      continue;
+    if (jf < G.sj0 || jf >= G.sj0 + G.sjn)
+      return fail(ctx, TOPO_EINVAL,
+                  "slab [%d, %d) with filter reach %d needs column %d outside its halo; use "
+                  "fewer ranks or a smaller rmin",
+                  G.j0, G.j0 + G.jn, ctx->reach, jf);
+  }
+  return TOPO_OK;
+}
+
+topo_status setup_filter_fields(topo_ctx* ctx) {
+  const Geo& G = ctx->G;
+  // hs over the stored columns: conv(1) (filter.hpp:115)
+  Geo Gs = G;
+  Gs.j0 = G.sj0;
+  Gs.jn = G.sjn;
+  Gs.m = (long long)G.sjn * G.S;
+  ConvArgs A{};
+  A.in0 = nullptr;
+  A.out0 = ctx->hs_st.as<double>();
+  TRY(launch_conv<1, CONV_PLAIN>(ctx, Gs, A));
+  CK(cudaMemcpyAsync(ctx->hs.p, ctx->hs_st.as<double>() + (long long)(G.j0 - G.sj0) * G.S,
+                     sizeof(double) * size_t(G.m), cudaMemcpyDeviceToDevice, ctx->stream));
+  // volume weights c = H' 1_notP = conv(1_notP / hs)
+  std::vector<uint8_t> st;
+  std::vector<double> notP(size_t(G.m), 1.0);
+  if (ctx->has_state) {
+    st.resize(size_t(G.m));
+    CK(cudaMemcpy(st.data(), ctx->d_state.p, size_t(G.m), cudaMemcpyDeviceToHost));
+    for (long long e = 0; e < G.m; ++e) notP[size_t(e)] = st[size_t(e)] == 0 ? 1.0 : 0.0;
+  }
+  CK(ctx->tmp0.ensure(sizeof(double) * size_t(G.m)));
+  CK(cudaMemcpyAsync(ctx->tmp0.p, notP.data(), sizeof(double) * size_t(G.m),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  const double* src = nullptr;
+  TRY(stage_field_storage(ctx, ctx->tmp0.as<double>(), ctx->tmp_st, &src));
+  ConvArgs B{};
+  B.in0 = src;
+  B.hs_st = ctx->hs_st.as<double>();
+  B.out0 = ctx->cw.as<double>();
+  TRY(launch_conv<1, CONV_ADJ_DIV>(ctx, G, B));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+const char* topo_last_error(const topo_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+int64_t topo_last_launch_count(const topo_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
+                            const double* ke_lower, const uint8_t* elem_state, topo_ctx** out) {
+  if (!d || !out) return TOPO_EINVAL;
+  *out = nullptr;
+  topo_ctx* ctx = new topo_ctx;
+  auto bail = [&](topo_status s) {
+    *out = ctx;  // keep the context so the caller can read the message
+    return s;
+  };
+  if (d->nelx < 1 || d->nely < 1 || d->nelz < 0)  // grid.hpp:82-85
+    return bail(fail(ctx, TOPO_EINVAL, "grid: element counts must be >= 1 per active axis"));
+  if (d->rmin < 1.0)  // filter.hpp:96
+    return bail(fail(ctx, TOPO_EINVAL, "filter: rmin must be >= 1 element"));
+  if (d->bc != TOPO_BC_NEUMANN && d->bc != TOPO_BC_DIRICHLET)
+    return bail(fail(ctx, TOPO_EINVAL, "filter: unknown boundary condition %d", d->bc));
+  const bool is3d = d->nelz > 0;
+  const long long nn = (long long)(d->nelx + 1) * (d->nely + 1) * (is3d ? d->nelz + 1 : 1);
+  const long long ndof = (is3d ? 3 : 2) * nn;
+  if (ndof > 2147483647LL)  // grid.hpp:91-93
+    return bail(fail(ctx, TOPO_EOVERFLOW, "grid: DOF count %lld exceeds 32-bit index range", ndof));
+  if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks)
+    return bail(fail(ctx, TOPO_EINVAL, "bad rank %d of %d", d->rank, d->nranks));
+
+  ctx->device = d->device;
+  if (ctx->device < 0) cudaGetDevice(&ctx->device);
+  cudaError_t ce = cudaSetDevice(ctx->device);
+  if (ce != cudaSuccess)
+    return bail(fail(ctx, TOPO_ECUDA, "cudaSetDevice(%d): %s", ctx->device, cudaGetErrorString(ce)));
+  cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, ctx->device);
+  int cc_major = 0, cc_minor = 0;
+  cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, ctx->device);
+  cudaDeviceGetAttribute(&cc_minor, cudaDevAttrComputeCapabilityMinor, ctx->device);
+  if (cc_major != 10 || cc_minor != 0)
+    return bail(fail(ctx, TOPO_ECUDA, "this library is built for sm_100a (B200); device %d is sm_%d%d",
+                     ctx->device, cc_major, cc_minor));
+
+  Geo& G = ctx->G;
+  G.nelx = d->nelx;
+  G.nely = d->nely;
+  G.nelz = d->nelz;
+  G.nz = is3d ? d->nelz : 1;
+  G.is3d = is3d;
+  G.dim = is3d ? 3 : 2;
+  G.d = is3d ? 24 : 8;
+  G.P = G.d * (G.d + 1) / 2;
+  G.S = (long long)d->nely * G.nz;
+  G.bc = d->bc;
+  ctx->rank = d->rank;
+  ctx->nranks = d->nranks;
+  if (d->j1 > d->j0) {
+    G.j0 = d->j0;
+    G.jn = d->j1 - d->j0;
+  } else {
+    const int base = d->nelx / d->nranks, rem = d->nelx % d->nranks;
+    G.j0 = d->rank * base + std::min(d->rank, rem);
+    G.jn = base + (d->rank < rem ? 1 : 0);
+  }
+  if (G.j0 < 0 || G.jn < 1 || G.j0 + G.jn > d->nelx)
+    return bail(fail(ctx, TOPO_EINVAL, "empty or out-of-range slab [%d, %d)", G.j0, G.j0 + G.jn));
+  G.m = (long long)G.jn * G.S;
+  ctx->m_total = double((long long)d->nelx * G.S);
+  ctx->rmin = d->rmin;
+  ctx->reach = int(ceil(d->rmin)) - 1;  // filter.hpp:105
+  ctx->rk = is3d ? ctx->reach : 0;
+  const int halo = d->nranks > 1 ? ctx->reach : 0;
+  G.sj0 = std::max(0, G.j0 - halo);
+  G.sjn = std::min(d->nelx, G.j0 + G.jn + halo) - G.sj0;
+  ctx->m_st = (long long)G.sjn * G.S;
+  ctx->n = (long long)G.dim * (G.jn + 1) * (d->nely + 1) * (is3d ? d->nelz + 1 : 1);
+  if (d->nranks > 1) {
+    topo_status s = validate_slab(ctx);
+    if (s) return bail(s);
+  }
+
+  // filter taps in reference order (filter.hpp:105-113), grouped in di rows
+  {
+    const int reach = ctx->reach, dkMax = is3d ? reach : 0;
+    for (int dj_ = -reach; dj_ <= reach; ++dj_)
+      for (int dk_ = -dkMax; dk_ <= dkMax; ++dk_) {
+        TapRow row{dj_, dk_, -1, int(ctx->w.size())};
+        int first = 1 << 30;
+        for (int di_ = -reach; di_ <= reach; ++di_) {
+          const double dist = sqrt(double(di_) * di_ + double(dj_) * dj_ + double(dk_) * dk_);
+          const double wv = d->rmin - dist;
+          if (wv > 0) {
+            if (first == (1 << 30)) first = di_;
+            ctx->di.push_back(di_);
+            ctx->dj.push_back(dj_);
+            ctx->dk.push_back(dk_);
+            ctx->w.push_back(wv);
+          }
+        }
+        if (first != (1 << 30)) {
+          row.a = -first;  // positive weights form the symmetric run [-a, a]
+          ctx->rows.push_back(row);
+        }
+      }
+  }
+  // element matrices
+  ctx->ke_full.resize(size_t(G.d * G.d));
+  ctx->ke_lower.resize(size_t(G.P));
+  if (ke_full && ke_lower) {
+    memcpy(ctx->ke_full.data(), ke_full, sizeof(double) * ctx->ke_full.size());
+    memcpy(ctx->ke_lower.data(), ke_lower, sizeof(double) * ctx->ke_lower.size());
+  } else if (topo_element_stiffness(G.dim, d->nu, ctx->ke_full.data(), ctx->ke_lower.data())) {
+    return bail(fail(ctx, TOPO_EINVAL, "element stiffness: Poisson ratio must lie in (-1, 0.5)"));
+  }
+
+  // conv tile size (outputs per thread along x) that fits shared memory
+  ctx->conv_jt = conv_smem_bytes(ctx, 2, 2) <= 226 * 1024 ? 2 : 1;
+  if (conv_smem_bytes(ctx, 2, 1) > 226 * 1024)
+    return bail(fail(ctx, TOPO_EINVAL, "filter: rmin %.3g too large for the shared-memory tile",
+                     d->rmin));
+
+#define CKC(x)                                                                          \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess)                                                              \
+      return bail(fail(ctx, TOPO_ECUDA, "%s failed: %s", #x, cudaGetErrorString(e_)));  \
+  } while (0)
+  CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CKC(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+  CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  CKC(cudaMallocHost(&ctx->h_result, 64 * sizeof(double)));
+
+  const size_t md = sizeof(double) * size_t(G.m), sd = sizeof(double) * size_t(ctx->m_st);
+  CKC(ctx->d_rows.ensure(sizeof(TapRow) * ctx->rows.size()));
+  CKC(ctx->d_w.ensure(sizeof(double) * ctx->w.size()));
+  CKC(cudaMemcpy(ctx->d_rows.p, ctx->rows.data(), sizeof(TapRow) * ctx->rows.size(),
+                 cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(ctx->d_w.p, ctx->w.data(), sizeof(double) * ctx->w.size(), cudaMemcpyHostToDevice));
+  CKC(ctx->d_ke_lower.ensure(sizeof(double) * size_t(G.P)));
+  CKC(cudaMemcpy(ctx->d_ke_lower.p, ctx->ke_lower.data(), sizeof(double) * size_t(G.P),
+                 cudaMemcpyHostToDevice));
+  for (DevBuf* b : {&ctx->hs, &ctx->cw, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
+                    &ctx->xnew, &ctx->tmp0, &ctx->tmp1})
+    CKC(b->ensure(md));
+  for (DevBuf* b : {&ctx->hs_st, &ctx->a1_st, &ctx->a2_st, &ctx->tmp_st}) CKC(b->ensure(sd));
+  CKC(ctx->rec.ensure(sizeof(double4) * size_t(G.m)));
+  CKC(ctx->u.ensure(sizeof(double) * size_t(ctx->n)));
+  if (d->nranks > 1) CKC(ctx->x_st.ensure(sd));
+
+  int occ = 0;
+  CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_oc_bisect, kThreads, 0));
+  int occ2 = 0;
+  CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_eta_solve, kThreads, 0));
+  if (occ < 1 || occ2 < 1)
+    return bail(fail(ctx, TOPO_ECUDA, "cooperative kernels cannot be resident"));
+  ctx->coop_blocks = ctx->sm_count;  // one block per SM (leaves room for the sK stream)
+  const size_t npart = std::max<size_t>(
+      {size_t(conv_blocks(ctx)) * 3, size_t(ctx->coop_blocks) * 2 * kOcK * 2,
+       size_t(ctx->sm_count) * 8 * 4});
+  CKC(ctx->partials.ensure(sizeof(double) * npart));
+  CKC(ctx->partials0.ensure(sizeof(double) * npart));
+  CKC(ctx->result.ensure(sizeof(double) * 64));
+
+  if (elem_state) {
+    ctx->has_state = true;
+    CKC(ctx->d_state.ensure(size_t(G.m)));
+    CKC(cudaMemcpy(ctx->d_state.p, elem_state, size_t(G.m), cudaMemcpyHostToDevice));
+    for (long long e = 0; e < G.m; ++e) {
+      if (elem_state[e] == TOPO_PASSIVE_SOLID) ++ctx->nS_local;
+      else if (elem_state[e] == TOPO_PASSIVE_VOID) ++ctx->nV_local;
+      else if (elem_state[e] != TOPO_ACTIVE)
+        return bail(fail(ctx, TOPO_EINVAL, "element %lld has invalid state %d", e, elem_state[e]));
+    }
+  }
+  ctx->nS_total = double(ctx->nS_local);
+  if (d->nranks == 1) {
+    topo_status s = setup_filter_fields(ctx);
+    if (s) return bail(s);
+  }
+#undef CKC
+  *out = ctx;
+  return TOPO_OK;
+}
+
+void topo_ctx_destroy(topo_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->device >= 0) cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm) comm_destroy(ctx->comm);
+  for (DevBuf* b : {&ctx->d_rows, &ctx->d_w, &ctx->d_ke_lower, &ctx->d_state, &ctx->hs, &ctx->hs_st,
+                    &ctx->cw, &ctx->x_st, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
+                    &ctx->xnew, &ctx->a1_st, &ctx->a2_st, &ctx->rec, &ctx->u, &ctx->tmp0,
+                    &ctx->tmp1, &ctx->tmp_st, &ctx->sK, &ctx->iK, &ctx->jK, &ctx->partials,
+                    &ctx->partials0, &ctx->result})
+    b->release();
+  if (ctx->h_result) cudaFreeHost(ctx->h_result);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->stream && ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+topo_status topo_set_stream(topo_ctx* ctx, void* s) {
+  if (!ctx) return TOPO_EINVAL;
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  ctx->stream = static_cast<cudaStream_t>(s);
+  ctx->own_stream = false;
+  return TOPO_OK;
+}
+
+topo_status topo_sync(topo_ctx* ctx) {
+  if (!ctx) return TOPO_EINVAL;
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaStreamSynchronize(ctx->aux));
+  return TOPO_OK;
+}
+
+topo_status topo_ctx_info(const topo_ctx* ctx, int64_t* m, int64_t* n, int32_t* P,
+                          int32_t* ntaps, int32_t* reach, int32_t* j0, int32_t* j1) {
+  if (!ctx) return TOPO_EINVAL;
+  if (m) *m = ctx->G.m;
+  if (n) *n = ctx->n;
+  if (P) *P = ctx->G.P;
+  if (ntaps) *ntaps = int32_t(ctx->w.size());
+  if (reach) *reach = ctx->reach;
+  if (j0) *j0 = ctx->G.j0;
+  if (j1) *j1 = ctx->G.j0 + ctx->G.jn;
+  return TOPO_OK;
+}
+
+topo_status topo_device_buffer(topo_ctx* ctx, int which, void** ptr, int64_t* count) {
+  if (!ctx || !ptr) return TOPO_EINVAL;
+  const Geo& G = ctx->G;
+  switch (which) {
+    case TOPO_BUF_SK: *ptr = ctx->sK.p; if (count) *count = ctx->sK.p ? G.m * G.P : 0; break;
+    case TOPO_BUF_IK: *ptr = ctx->iK.p; if (count) *count = ctx->iK.p ? G.m * G.P : 0; break;
+    case TOPO_BUF_JK: *ptr = ctx->jK.p; if (count) *count = ctx->jK.p ? G.m * G.P : 0; break;
+    case TOPO_BUF_XNEW: *ptr = ctx->xnew.p; if (count) *count = G.m; break;
+    case TOPO_BUF_XPHYS: *ptr = ctx->xphys.p; if (count) *count = G.m; break;
+    default: return fail(ctx, TOPO_EINVAL, "unknown buffer %d", which);
+  }
+  return TOPO_OK;
+}
+
+topo_status topo_filter_taps(topo_ctx* ctx, int32_t* di, int32_t* dj, int32_t* dk, double* w) {
+  if (!ctx) return TOPO_EINVAL;
+  for (size_t t = 0; t < ctx->w.size(); ++t) {
+    if (di) di[t] = ctx->di[t];
+    if (dj) dj[t] = ctx->dj[t];
+    if (dk) dk[t] = ctx->dk[t];
+    if (w) w[t] = ctx->w[t];
+  }
+  return TOPO_OK;
+}
+
+topo_status topo_filter_hs(topo_ctx* ctx, double* hs) {
+  if (!ctx) return TOPO_EINVAL;
+  ctx->launches = 0;
+  bool host;
+  double* o = out_ptr(ctx, hs, ctx->tmp1, ctx->G.m, &host);
+  CK(cudaMemcpyAsync(o, ctx->hs.p, sizeof(double) * size_t(ctx->G.m), cudaMemcpyDeviceToDevice,
+                     ctx->stream));
+  TRY(finish_out(ctx, hs, o, ctx->G.m, host));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+// ---------------------------------------------------------------- K0
+topo_status topo_build_connectivity(topo_ctx* ctx, int32_t* dofs) {
+  if (!ctx || !dofs) return TOPO_EINVAL;
+  ctx->launches = 0;
+  const Geo& G = ctx->G;
+  const size_t bytes = sizeof(int32_t) * size_t(G.m) * G.d;
+  const bool dev = is_device_ptr(dofs);
+  DevBuf tmp;
+  int* o = dofs;
+  if (!dev) {
+    CK(tmp.ensure(bytes));
+    o = tmp.as<int>();
+  }
+  if (G.is3d)
+    k_connectivity<24><<<grid_for(ctx, G.m), kThreads, 0, ctx->stream>>>(G, o);
+  else
+    k_connectivity<8><<<grid_for(ctx, G.m), kThreads, 0, ctx->stream>>>(G, o);
+  LAUNCHED();
+  if (!dev) CK(cudaMemcpyAsync(dofs, o, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  tmp.release();
+  return TOPO_OK;
+}
+
+topo_status topo_build_index_pairs(topo_ctx* ctx, int32_t* iK, int32_t* jK) {
+  if (!ctx) return TOPO_EINVAL;
+  ctx->launches = 0;
+  const Geo& G = ctx->G;
+  const size_t bytes = sizeof(int32_t) * size_t(G.m) * size_t(G.P);
+  int *oi, *oj;
+  const bool di = is_device_ptr(iK), dj = is_device_ptr(jK);
+  if (di && dj) {
+    oi = iK;
+    oj = jK;
+  } else {
+    CK(ctx->iK.ensure(bytes));
+    CK(ctx->jK.ensure(bytes));
+    oi = ctx->iK.as<int>();
+    oj = ctx->jK.as<int>();
+  }
+  const int nb = ctx->sm_count * 4;
+  if (G.is3d)
+    k_index_pairs<24, 16><<<nb, kThreads, 0, ctx->stream>>>(G, oi, oj);
+  else
+    k_index_pairs<8, 64><<<nb, kThreads, 0, ctx->stream>>>(G, oi, oj);
+  LAUNCHED();
+  if (!(di && dj)) {
+    if (iK) CK(cudaMemcpyAsync(iK, oi, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (jK) CK(cudaMemcpyAsync(jK, oj, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+// ---------------------------------------------------------------- fea.hpp
+topo_status topo_simp_interpolate(topo_ctx* ctx, const double* xhat, const topo_simp* prm,
+                                  double* sK, double* dsK) {
+  if (!ctx || !prm) return TOPO_EINVAL;
+  ctx->launches = 0;
+  const long long m = ctx->G.m;
+  const double* x;
+  TRY(stage_in(ctx, xhat, m, ctx->tmp0, &x));
+  bool h1, h2;
+  double* o1 = out_ptr(ctx, sK, ctx->tmp1, m, &h1);
+  double* o2 = out_ptr(ctx, dsK, ctx->dcphys, m, &h2);
+  k_simp<<<grid_for(ctx, m), kThreads, 0, ctx->stream>>>(m, x, prm->e0, prm->emin, prm->penal,
+                                                         o1, o2);
+  LAUNCHED();
+  TRY(finish_out(ctx, sK, o1, m, h1));
+  TRY(finish_out(ctx, dsK, o2, m, h2));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+topo_status topo_assemble_values(topo_ctx* ctx, const double* sKe, double* vals) {
+  if (!ctx) return TOPO_EINVAL;
+  ctx->launches = 0;
+  const Geo& G = ctx->G;
+  const double* s;
+  TRY(stage_in(ctx, sKe, G.m, ctx->tmp0, &s));
+  const long long cnt = G.m * G.P;
+  double* o = vals;
+  const bool dev = is_device_ptr(vals);
+  if (!dev) {
+    CK(ctx->sK.ensure(sizeof(double) * size_t(cnt)));
+    o = ctx->sK.as<double>();
+  }
+  SkArgs A{};
+  A.xt = nullptr;
+  A.sKe = s;
+  A.ke_lower = ctx->d_ke_lower.as<double>();
+  A.sK = o;
+  if (G.is3d)
+    k_sk_store<300, 16><<<ctx->sm_count * 2, kThreads, 0, ctx->stream>>>(G, A);
+  else
+    k_sk_store<36, 128><<<ctx->sm_count * 2, kThreads, 0, ctx->stream>>>(G, A);
+  LAUNCHED();
+  if (!dev && vals)
+    CK(cudaMemcpyAsync(vals, o, sizeof(double) * size_t(cnt), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+static topo_status launch_elem(topo_ctx* ctx, const ElemArgs& A, int nb) {
+  const Geo& G = ctx->G;
+  if (G.is3d) {
+    KeFull<24> K;
+    memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
+    k_elem_sens<24><<<nb, kThreads, 0, ctx->stream>>>(G, K, A);
+  } else {
+    KeFull<8> K;
+    memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
+    k_elem_sens<8><<<nb, kThreads, 0, ctx->stream>>>(G, K, A);
+  }
+  LAUNCHED();
+  return TOPO_OK;
+}
+
+topo_status topo_sensitivity(topo_ctx* ctx, const double* U, const double* xhat,
+                             const topo_simp* prm, double* c, double* dc) {
+  if (!ctx || !prm) return TOPO_EINVAL;
+  ctx->launches = 0;
+  const Geo& G = ctx->G;
+  const double *u, *x;
+  TRY(stage_in(ctx, U, ctx->n, ctx->u, &u));
+  TRY(stage_in(ctx, xhat, G.m, ctx->tmp0, &x));
+  bool h;
+  double* o = out_ptr(ctx, dc, ctx->dcphys, G.m, &h);
+  ElemArgs A{};
+  A.xt = x;
+  A.input_is_phys = 1;
+  A.U = u;
+  A.state = ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr;
+  A.hs = ctx->hs.as<double>();
+  A.beta = 1.0;
+  A.e0 = prm->e0;
+  A.emin = prm->emin;
+  A.penal = prm->penal;
+  A.inv_m = 1.0 / ctx->m_total;
+  A.dcPhys = o;
+  A.partials = ctx->partials.as<double>();
+  const int nb = grid_for(ctx, G.m);
+  TRY(launch_elem(ctx, A, nb));
+  TRY(finish_out(ctx, dc, o, G.m, h));
+  k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(A.partials, nb, 1, ctx->result.as<double>());
+  LAUNCHED();
+  CK(cudaMemcpyAsync(ctx->h_result, ctx->result.p, sizeof(double), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (c) *c = ctx->h_result[0];
+  return TOPO_OK;
+}
+
+// ------------------------------------------------------------- filter.hpp
+topo_status topo_filter(topo_ctx* ctx, const double* x, double* xTilde, int pin) {
+  if (!ctx) return TOPO_EINVAL;
+  ctx->launches = 0;
+  const Geo& G = ctx->G;
+  const double* xs;
+  TRY(stage_field_storage(ctx, x, ctx->x_st.p ? ctx->x_st : ctx->tmp_st, &xs));
+  bool h;
+  double* o = out_ptr(ctx, xTilde, ctx->tmp1, G.m, &h);
+  ConvArgs A{};
+  A.in0 = xs;
+  A.hs = ctx->hs.as<double>();
+  A.out0 = o;
+  A.state = ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr;
+  A.pin = pin;
+  TRY(launch_conv<1, CONV_FWD>(ctx, G, A));
+  TRY(finish_out(ctx, xTilde, o, G.m, h));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+topo_status topo_filter_adjoint(topo_ctx* ctx, const double* g, double* out) {
+  if (!ctx) return TOPO_EINVAL;
+  ctx->launches = 0;
+  const Geo& G = ctx->G;
+  const double* gs;
+  TRY(stage_field_storage(ctx, g, ctx->tmp_st, &gs));
+  bool h;
+  double* o = out_ptr(ctx, out, ctx->tmp1, G.m, &h);
+  ConvArgs A{};
+  A.in0 = gs;
+  A.hs_st = ctx->hs_st.as<double>();
+  A.out0 = o;
+  TRY(launch_conv<1, CONV_ADJ_DIV>(ctx, G, A));
+  TRY(finish_out(ctx, out, o, G.m, h));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+static topo_status project_impl(topo_ctx* ctx, const double* xt, double eta, double beta,
+                                double* out, int deriv) {
+  if (!ctx) return TOPO_EINVAL;
+  ctx->launches = 0;
+  const long long m = ctx->G.m;
+  const double* x;
+  TRY(stage_in(ctx, xt, m, ctx->tmp0, &x));
+  bool h;
+  double* o = out_ptr(ctx, out, ctx->tmp1, m, &h);
+  k_project<<<grid_for(ctx, m), kThreads, 0, ctx->stream>>>(m, x, eta, beta, o, deriv);
+  LAUNCHED();
+  TRY(finish_out(ctx, out, o, m, h));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+topo_status topo_project(topo_ctx* ctx, const double* xt, double eta, double beta, double* out) {
+  return project_impl(ctx, xt, eta, beta, out, 0);
+}
+topo_status topo_project_derivative(topo_ctx* ctx, const double* xt, double eta, double beta,
+                                    double* out) {
+  return project_impl(ctx, xt, eta, beta, out, 1);
+}
+
+topo_status topo_backfilter(topo_ctx* ctx, const double* g, const double* xt, double eta,
+                            double beta, int proj_on, double* out) {
+  if (!ctx) return TOPO_EINVAL;
+  ctx->launches = 0;
+  const Geo& G = ctx->G;
+  const double *gd, *xd = nullptr;
+  TRY(stage_in(ctx, g, G.m, ctx->tmp0, &gd));
+  if (proj_on) TRY(stage_in(ctx, xt, G.m, ctx->tmp1, &xd));
+  CK(ctx->a1_st.ensure(sizeof(double) * size_t(ctx->m_st)));
+  k_prescale<<<grid_for(ctx, G.m), kThreads, 0, ctx->stream>>>(
+      G, gd, xd, eta, beta, proj_on, ctx->hs.as<double>(), ctx->a1_st.as<double>());
+  LAUNCHED();
+  if (ctx->comm) TRY(comm_halo(ctx->comm, ctx, ctx->a1_st.as<double>()));
+  bool h;
+  double* o = out_ptr(ctx, out, ctx->dc, G.m, &h);
+  ConvArgs A{};
+  A.in0 = ctx->a1_st.as<double>();
+  A.out0 = o;
+  TRY(launch_conv<1, CONV_PLAIN>(ctx, G, A));
+  TRY(finish_out(ctx, out, o, G.m, h));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+topo_status topo_solve_eta(topo_ctx* ctx, const double* xTilde, double beta, double eta0,
+                           double* eta, int32_t* iters) {
+  if (!ctx) return TOPO_EINVAL;
+  ctx->launches = 0;
+  if (!(beta > 0)) return fail(ctx, TOPO_EINVAL, "eta solve: beta must be positive");
+  const double* x;
+  TRY(stage_in(ctx, xTilde, ctx->G.m, ctx->tmp0, &x));
+  TRY(run_eta(ctx, x, beta, eta0, nullptr, 0, ctx->result.as<double>()));
+  CK(cudaMemcpyAsync(ctx->h_result, ctx->result.p, sizeof(double) * 3, cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (eta) *eta = ctx->h_result[0];
+  if (iters) *iters = int32_t(ctx->h_result[1]);
+  return TOPO_OK;
+}
+
+// ----------------------------------------------------------------- oc.hpp
+topo_status topo_lambda_upper(topo_ctx* ctx, int64_t nact, const double* xAct,
+                              const double* dcAct, const double* dVAct, double volfrac,
+                              int64_t mTotal, double* lambda) {
+  if (!ctx || !lambda) return TOPO_EINVAL;
+  ctx->launches = 0;
+  if (nact == 0) {
+    const double root = 0.0 / (double(mTotal) * volfrac);
+    *lambda = root * root;
+    return TOPO_OK;
+  }
+  const double *x, *dc, *dV;
+  DevBuf b0, b1, b2;
+  TRY(stage_in(ctx, xAct, nact, b0, &x));
+  TRY(stage_in(ctx, dcAct, nact, b1, &dc));
+  TRY(stage_in(ctx, dVAct, nact, b2, &dV));
+  const int nb = grid_for(ctx, nact);
+  k_oc_compact<<<nb, kThreads, 0, ctx->stream>>>(nact, x, dc, dV, 1.0, 0.0, nullptr,
+                                                 ctx->partials.as<double>());
+  LAUNCHED();
+  k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(ctx->partials.as<double>(), nb, 1,
+                                                  ctx->result.as<double>());
+  LAUNCHED();
+  CK(cudaMemcpyAsync(ctx->h_result, ctx->result.p, sizeof(double), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const double root = ctx->h_result[0] / (double(mTotal) * volfrac);  // oc.hpp:37-38
+  *lambda = root * root;
+  b0.release();
+  b1.release();
+  b2.release();
+  return TOPO_OK;
+}
+
+topo_status topo_oc_candidate(topo_ctx* ctx, int64_t nact, const double* xAct,
+                              const double* dcAct, const double* dVAct, double lambda,
+                              double move, double* out) {
+  if (!ctx) return TOPO_EINVAL;
+  ctx->launches = 0;
+  if (!(lambda > 0)) return fail(ctx, TOPO_EINVAL, "oc: multiplier must be positive");  // oc.hpp:74
+  if (nact == 0) return TOPO_OK;
+  const double *x, *dc, *dV;
+  DevBuf b0, b1, b2, bo;
+  TRY(stage_in(ctx, xAct, nact, b0, &x));
+  TRY(stage_in(ctx, dcAct, nact, b1, &dc));
+  TRY(stage_in(ctx, dVAct, nact, b2, &dV));
+  bool h;
+  double* o = out_ptr(ctx, out, bo, nact, &h);
+  k_oc_compact<<<grid_for(ctx, nact), kThreads, 0, ctx->stream>>>(nact, x, dc, dV, sqrt(lambda),
+                                                                  move, o, nullptr);
+  LAUNCHED();
+  TRY(finish_out(ctx, out, o, nact, h));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+topo_status topo_oc_bisect(topo_ctx* ctx, const double* x, const double* dc, const double* dV,
+                           const topo_oc_params* prm, int volume_mode, double eta, double beta,
+                           topo_volume_fn cb, void* user, double* xNew, double* lambda,
+                           int32_t* bisections, int32_t* evaluations) {
+  if (!ctx || !prm) return TOPO_EINVAL;
+  ctx->launches = 0;
+  if (volume_mode < TOPO_VOL_CALLBACK || volume_mode > TOPO_VOL_FILTERED)
+    return fail(ctx, TOPO_EINVAL, "oc: unknown volume mode %d", volume_mode);
+  const Geo& G = ctx->G;
+  const double *xd, *dcd, *dVd;
+  DevBuf b0;
+  TRY(stage_in(ctx, x, G.m, ctx->tmp0, &xd));
+  TRY(stage_in(ctx, dc, G.m, ctx->tmp1, &dcd));
+  TRY(stage_in(ctx, dV, G.m, b0, &dVd));
+  const int nb = grid_for(ctx, G.m);
+  k_oc_prep<<<nb, kThreads, 0, ctx->stream>>>(
+      G.m, xd, dcd, dVd, ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr,
+      volume_mode == TOPO_VOL_FILTERED ? ctx->cw.as<double>() : nullptr, prm->move,
+      ctx->rec.as<double4>(), ctx->partials0.as<double>());
+  LAUNCHED();
+  bool h;
+  double* o = out_ptr(ctx, xNew, ctx->xnew, G.m, &h);
+  double lam = 0;
+  int32_t bis = 0, ev = 0;
+  TRY(run_oc(ctx, prm, volume_mode, ctx->partials0.as<double>(), nb, o, &lam, &bis, &ev, eta,
+             beta, cb, user));
+  TRY(finish_out(ctx, xNew, o, G.m, h));
+  CK(cudaStreamSynchronize(ctx->stream));
+  b0.release();
+  if (lambda) *lambda = lam;
+  if (bisections) *bisections = bis;
+  if (evaluations) *evaluations = ev;
+  return TOPO_OK;
+}
+
+// ------------------------------------------------------------ fused pass
+// driver.hpp:183-231 (ft = 3) with U supplied:
+//   main stream: K1 filter+pin+eta0 terms -> K2 eta -> K3a elem -> K4 adjoint+OC prep -> K5/6 OC
+//   aux  stream:                          \-> K3b sK store (overlaps K3a..K6)
+topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
+                             const topo_pass_params* prm, topo_pass_out* out) {
+  if (!ctx || !prm || !out) return TOPO_EINVAL;
+  ctx->launches = 0;
+  const Geo& G = ctx->G;
+  if (!(prm->beta > 0)) return fail(ctx, TOPO_EINVAL, "eta solve: beta must be positive");
+  const int vmode = prm->volume_mode;
+  if (vmode != TOPO_VOL_FILTERED && vmode != TOPO_VOL_MEAN)
+    return fail(ctx, TOPO_EINVAL, "design pass: volume mode %d not supported in the fused pass",
+                vmode);
+  const uint8_t* state = ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr;
+  const double *xs, *ud;
+  TRY(stage_field_storage(ctx, x, ctx->x_st.p ? ctx->x_st : ctx->tmp_st, &xs));
+  TRY(stage_in(ctx, U, ctx->n, ctx->u, &ud));
+  const double* xown = xs + (long long)(G.j0 - G.sj0) * G.S;
+  double* res = ctx->result.as<double>();
+
+  // K1 (+ first eta evaluation)
+  const bool solve = isnan(prm->eta_override);
+  ConvArgs A1{};
+  A1.in0 = xs;
+  A1.hs = ctx->hs.as<double>();
+  A1.out0 = ctx->xt.as<double>();
+  A1.state = state;
+  A1.pin = 1;
+  A1.beta = prm->beta;
+  A1.eta0 = prm->eta0 < 0.0 ? 0.0 : (prm->eta0 > 1.0 ? 1.0 : prm->eta0);
+  A1.partials = ctx->partials0.as<double>();
+  int nb1 = 0;
+  if (solve)
+    TRY((launch_conv<1, CONV_FWD_ETA>(ctx, G, A1, &nb1)));
+  else
+    TRY((launch_conv<1, CONV_FWD>(ctx, G, A1, &nb1)));
+  // K2
+  if (solve) {
+    TRY(run_eta(ctx, ctx->xt.as<double>(), prm->beta, prm->eta0, ctx->partials0.as<double>(),
+                nb1, res));
+  } else {
+    const double r[3] = {prm->eta_override, 0.0, 0.0};
+    CK(cudaMemcpyAsync(res, r, sizeof r, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  // K3b on the aux stream
+  const bool want_sk = prm->write_sk != 0;
+  double* skp = nullptr;
+  if (want_sk) {
+    const long long cnt = G.m * G.P;
+    if (out->sK && is_device_ptr(out->sK)) {
+      skp = out->sK;
+    } else {
+      CK(ctx->sK.ensure(sizeof(double) * size_t(cnt)));
+      skp = ctx->sK.as<double>();
+    }
+    CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
+    SkArgs S{};
+    S.xt = ctx->xt.as<double>();
+    S.eta_ptr = res;
+    S.beta = prm->beta;
+    S.e0 = prm->simp.e0;
+    S.emin = prm->simp.emin;
+    S.penal = prm->simp.penal;
+    S.ke_lower = ctx->d_ke_lower.as<double>();
+    S.sK = skp;
+    if (G.is3d)
+      k_sk_store<300, 16><<<ctx->sm_count, kThreads, 0, ctx->aux>>>(G, S);
+    else
+      k_sk_store<36, 128><<<ctx->sm_count, kThreads, 0, ctx->aux>>>(G, S);
+    LAUNCHED();
+    CK(cudaEventRecord(ctx->ev_join, ctx->aux));
+  }
+  // K3a
+  ElemArgs E{};
+  E.xt = ctx->xt.as<double>();
+  E.eta_ptr = res;
+  E.U = ud;
+  E.state = state;
+  E.hs = ctx->hs.as<double>();
+  E.beta = prm->beta;
+  E.e0 = prm->simp.e0;
+  E.emin = prm->simp.emin;
+  E.penal = prm->simp.penal;
+  E.inv_m = 1.0 / ctx->m_total;
+  E.xPhys = ctx->xphys.as<double>();
+  E.dcPhys = ctx->dcphys.as<double>();
+  E.a1 = ctx->a1_st.as<double>();
+  E.a2 = ctx->a2_st.as<double>();
+  E.partials = ctx->partials.as<double>() + 0;
+  const int nbe = grid_for(ctx, G.m);
+  TRY(launch_elem(ctx, E, nbe));
+  k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(E.partials, nbe, 1, res + 4);
+  LAUNCHED();
+  if (ctx->comm) {
+    TRY(comm_halo(ctx->comm, ctx, ctx->a1_st.as<double>()));
+    TRY(comm_halo(ctx->comm, ctx, ctx->a2_st.as<double>()));
+  }
+  // K4
+  ConvArgs A4{};
+  A4.in0 = ctx->a1_st.as<double>();
+  A4.in1 = ctx->a2_st.as<double>();
+  A4.out0 = ctx->dc.as<double>();
+  A4.out1 = ctx->dV.as<double>();
+  A4.state = state;
+  A4.x = xown;
+  A4.cw = vmode == TOPO_VOL_FILTERED ? ctx->cw.as<double>() : nullptr;
+  A4.move = prm->move;
+  A4.ocrec = ctx->rec.as<double4>();
+  A4.partials = ctx->partials0.as<double>();
+  int nb4 = 0;
+  TRY((launch_conv<2, CONV_ADJ2_OC>(ctx, G, A4, &nb4)));
+  // K5 + K6
+  topo_oc_params oc{prm->move, prm->volfrac, 1e-4, 1e-3, 0, 1e-8, 0.0};  // oc.hpp:14-20 defaults
+  double lam = 0;
+  int32_t bis = 0, ev = 0;
+  TRY(run_oc(ctx, &oc, vmode, ctx->partials0.as<double>(), nb4, ctx->xnew.as<double>(), &lam,
+             &bis, &ev, 0.0, prm->beta, nullptr, nullptr));
+  if (want_sk) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+  CK(cudaMemcpyAsync(ctx->h_result, res, sizeof(double) * 5, cudaMemcpyDeviceToHost, ctx->stream));
+  // outputs
+  struct {
+    double* user;
+    const DevBuf* src;
+  } outs[] = {{out->xTilde, &ctx->xt}, {out->xPhys, &ctx->xphys}, {out->dcPhys, &ctx->dcphys},
+              {out->dc, &ctx->dc},     {out->dV, &ctx->dV},       {out->xNew, &ctx->xnew}};
+  for (auto& o : outs)
+    if (o.user)
+      CK(cudaMemcpyAsync(o.user, o.src->p, sizeof(double) * size_t(G.m), cudaMemcpyDefault,
+                         ctx->stream));
+  if (want_sk && out->sK && skp != out->sK)
+    CK(cudaMemcpyAsync(out->sK, skp, sizeof(double) * size_t(G.m * G.P), cudaMemcpyDefault,
+                       ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  double c = ctx->h_result[4];
+  if (ctx->comm) TRY(comm_allreduce_host(ctx->comm, ctx, &c, 1));
+  out->eta = ctx->h_result[0];
+  out->eta_iters = int32_t(ctx->h_result[1]);
+  out->c = c;
+  out->lambda = lam;
+  out->bisections = bis;
+  out->evaluations = ev;
+  return TOPO_OK;
+}
+
+}  // extern "C"
+
+// ======================================================= multi-GPU (stub)
+struct Comm {
+  int dummy;
+};
+topo_status comm_halo(Comm*, topo_ctx* ctx, double*) {
+  return fail(ctx, TOPO_ENCCL, "multi-GPU communication is not available");
+}
+topo_status comm_allreduce(Comm*, topo_ctx* ctx, double*, int) {
+  return fail(ctx, TOPO_ENCCL, "multi-GPU communication is not available");
+}
+topo_status comm_allreduce_host(Comm*, topo_ctx* ctx, double*, int) {
+  return fail(ctx, TOPO_ENCCL, "multi-GPU communication is not available");
+}
+topo_status comm_oc_volume(Comm*, topo_ctx* ctx, double, double, double*) {
+  return fail(ctx, TOPO_ENCCL, "multi-GPU communication is not available");
+}
+void comm_destroy(Comm* c) { delete c; }
+extern "C" topo_status topo_comm_init_nccl(topo_ctx* ctx, const void*) {
+  return fail(ctx, TOPO_ENCCL, "multi-GPU communication is not available");
+}

@@ -1,0 +1,799 @@
+// sm_100a kernels of the design-update pass (SURVEY.md §2 "Kernels": K0-K7).
+// All FP64. Memory-bound streams use 16-byte vector stores with the
+// streaming (.cs) hint; stencils stage halo tiles in shared memory; scalar
+// reductions are deterministic (fixed warp/block/grid trees).
+#pragma once
+
+#include "common.cuh"
+#include "control.h"
+
+namespace topo {
+
+constexpr int kThreads = 256;
+
+// ============================================================================
+// K0: element DOFs and lower-triangle index pairs (grid.hpp:89-153)
+// ============================================================================
+
+// DOFs of element (i, k, j) in the node order of grid.hpp:105-107 / :118-122.
+// `jbase` shifts global node columns for slab-local U indexing (0 = global).
+__device__ __forceinline__ void element_dofs(const Geo& G, int i, int k, int j, int jbase,
+                                             int* dofs) {
+  const long long ny1 = G.nely + 1;
+  if (!G.is3d) {
+    const int jj = j - jbase;
+    const int n0 = int((long long)jj * ny1 + i + 1), n1 = int((long long)(jj + 1) * ny1 + i + 1);
+    const int n2 = int((long long)(jj + 1) * ny1 + i), n3 = int((long long)jj * ny1 + i);
+    const int nodes[4] = {n0, n1, n2, n3};
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      dofs[2 * a] = 2 * nodes[a];
+      dofs[2 * a + 1] = 2 * nodes[a] + 1;
+    }
+  } else {
+    const long long nz1 = G.nelz + 1;
+    const int jj = j - jbase;
+    auto node = [&](int ii, int kk, int jc) { return int(((long long)jc * nz1 + kk) * ny1 + ii); };
+    const int nodes[8] = {node(i + 1, k, jj),     node(i + 1, k, jj + 1),
+                          node(i, k, jj + 1),     node(i, k, jj),
+                          node(i + 1, k + 1, jj), node(i + 1, k + 1, jj + 1),
+                          node(i, k + 1, jj + 1), node(i, k + 1, jj)};
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      dofs[3 * a] = 3 * nodes[a];
+      dofs[3 * a + 1] = 3 * nodes[a] + 1;
+      dofs[3 * a + 2] = 3 * nodes[a] + 2;
+    }
+  }
+}
+
+__device__ __forceinline__ void elem_ijk(const Geo& G, long long e, int& i, int& k, int& j) {
+  i = int(e % G.nely);
+  const long long r = e / G.nely;
+  k = int(r % G.nz);
+  j = G.j0 + int(r / G.nz);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_connectivity(Geo G, int* __restrict__ dofs) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < G.m;
+       e += (long long)gridDim.x * blockDim.x) {
+    int i, k, j;
+    elem_ijk(G, e, i, k, j);
+    int d[24];
+    element_dofs(G, i, k, j, 0, d);
+#pragma unroll
+    for (int a = 0; a < D; ++a) dofs[e * D + a] = d[a];
+  }
+}
+
+// One block stages EB elements' DOFs in smem, then streams iK/jK as int4
+// vectors (P is a multiple of 4 for Q4 and H8).
+template <int D, int EB>
+__global__ void __launch_bounds__(kThreads) k_index_pairs(Geo G, int* __restrict__ iK,
+                                                          int* __restrict__ jK) {
+  constexpr int P = D * (D + 1) / 2;
+  constexpr int PV = P / 4;
+  __shared__ int sd[EB][D];
+  __shared__ unsigned char sil[P], sjl[P];
+  for (int q = threadIdx.x; q < P; q += blockDim.x) {  // grid.hpp:143-144 pair order
+    int t = q, jl = 0;
+    while (t >= D - jl) {
+      t -= D - jl;
+      ++jl;
+    }
+    sil[q] = (unsigned char)(jl + t);
+    sjl[q] = (unsigned char)jl;
+  }
+  const long long nchunks = (G.m + EB - 1) / EB;
+  for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const long long e0 = c * EB;
+    const int ne = int(min((long long)EB, G.m - e0));
+    __syncthreads();
+    for (int t = threadIdx.x; t < ne; t += blockDim.x) {
+      int i, k, j;
+      elem_ijk(G, e0 + t, i, k, j);
+      int d[24];
+      element_dofs(G, i, k, j, 0, d);
+#pragma unroll
+      for (int a = 0; a < D; ++a) sd[t][a] = d[a];
+    }
+    __syncthreads();
+    const int nv = ne * PV;
+    int4* oi = reinterpret_cast<int4*>(iK + e0 * P);
+    int4* oj = reinterpret_cast<int4*>(jK + e0 * P);
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+      const int el = v / PV, q0 = (v - el * PV) * 4;
+      int a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int x = sd[el][sil[q0 + u]], y = sd[el][sjl[q0 + u]];
+        a[u] = max(x, y);
+        b[u] = min(x, y);
+      }
+      __stcs(oi + v, make_int4(a[0], a[1], a[2], a[3]));
+      __stcs(oj + v, make_int4(b[0], b[1], b[2], b[3]));
+    }
+  }
+}
+
+// ============================================================================
+// K1 / K4 / K7: cone convolution (filter.hpp:50-91) with smem halo tiles
+// ============================================================================
+
+enum ConvMode {
+  CONV_PLAIN = 0,   // out = conv(in)                         (hs, adjoint of pre-divided input)
+  CONV_FWD = 1,     // out = conv(in) / hs, optional pin      (apply_filter + pin_passives)
+  CONV_FWD_ETA = 2, // CONV_FWD + (g, g') partials at eta0    (K1 fused with the first eta pass)
+  CONV_ADJ_DIV = 3, // out = conv(in / hs)                    (apply_filter_adjoint)
+  CONV_ADJ2_OC = 4  // dc, dV = conv(a1), conv(a2) + OC record + (sum ocP, V(0), V(inf)) partials
+};
+
+struct ConvArgs {
+  const double* in0;  // storage-indexed (halo-extended) inputs
+  const double* in1;
+  const double* hs;   // owned-indexed
+  const double* hs_st;  // storage-indexed hs (CONV_ADJ_DIV)
+  double* out0;       // owned-indexed outputs
+  double* out1;
+  const uint8_t* state;
+  int pin;
+  // CONV_FWD_ETA
+  double beta, eta0;
+  double* partials;  // per block
+  // CONV_ADJ2_OC
+  const double* x;   // design (owned)
+  const double* cw;  // volume weights (owned)
+  double move;
+  double4* ocrec;    // (lb, ub, ocP, cw) per element
+};
+
+// eta pass terms for one filtered value t (filter.hpp:187-201)
+struct EtaConsts {
+  double a, denom, c0;  // tanh(b eta), a + tanh(b (1 - eta)), -b / sinh(b)
+};
+__device__ __forceinline__ EtaConsts eta_consts(double beta, double eta) {
+  EtaConsts c;
+  c.a = tanh(beta * eta);
+  c.denom = c.a + tanh(beta * (1.0 - eta));
+  c.c0 = -beta / sinh(beta);
+  return c;
+}
+__device__ __forceinline__ void eta_terms(const EtaConsts& c, double beta, double eta, double t,
+                                          double& g, double& gp) {
+  g = (c.a + tanh(beta * (t - eta))) / c.denom - t;
+  const double sech = 1.0 / cosh(beta * (t - eta));
+  gp = c.c0 * sech * sech * sinh(beta * t) * sinh(beta * (1.0 - t));
+}
+
+// Candidate record of oc.hpp:44-61 for one element; passives get lb = ub = x,
+// which makes every candidate equal x (their xNew entries stay untouched).
+__device__ __forceinline__ double4 oc_record(double x, double dc, double dV, double cw, double move,
+                                             bool active) {
+  if (!active) return make_double4(x, x, 0.0, cw);
+  const double ocP = x * sqrt(std_max(0.0, -dc / dV));
+  return make_double4(std_max(0.0, x - move), std_min(1.0, x + move), ocP, cw);
+}
+// oc.hpp:47-51
+__device__ __forceinline__ double oc_cand(const double4& r, double s) {
+  const double f = s > 0 ? r.z / s : (r.z > 0 ? INFINITY : 0.0);
+  return std_min(std_max(f, r.x), r.y);
+}
+
+template <int NF, int MODE, int JT>
+__global__ void __launch_bounds__(kThreads) k_conv(Geo G, const TapRow* __restrict__ rows,
+                                                   int nrows, const double* __restrict__ wts,
+                                                   int nw, int r, int rk, ConvArgs A) {
+  extern __shared__ double smem[];
+  const int TI = blockDim.x, TK = blockDim.y, TJ = blockDim.z * JT;
+  const int PI = TI + 2 * r, PK = TK + 2 * rk, PJ = TJ + 2 * r;
+  const int tileN = PI * PK * PJ;
+  double* sw = smem;                                     // nw weights
+  TapRow* sr = reinterpret_cast<TapRow*>(smem + nw);     // nrows rows (16 B each)
+  double* st = smem + nw + 2 * nrows;                    // NF tiles
+  const int tid = threadIdx.x + TI * (threadIdx.y + TK * threadIdx.z);
+  const int nthr = TI * TK * blockDim.z;
+
+  for (int q = tid; q < nw; q += nthr) sw[q] = wts[q];
+  for (int q = tid; q < nrows; q += nthr) sr[q] = rows[q];
+
+  // tile origin (global coordinates of output (0,0,0) of this block)
+  const int bi = blockIdx.x * TI, bk = blockIdx.y * TK, bj = G.j0 + blockIdx.z * TJ;
+  for (int q = tid; q < tileN; q += nthr) {
+    const int ti = q % PI, rest = q / PI, tk = rest % PK, tj = rest / PK;
+    int gi = bi + ti - r, gk = bk + tk - rk, gj = bj + tj - r;
+    bool inside = true;
+    if (G.bc == 0) {
+      gi = reflect_index(gi, G.nely);
+      gk = reflect_index(gk, G.nz);
+      gj = reflect_index(gj, G.nelx);
+    } else {
+      inside = gi >= 0 && gi < G.nely && gk >= 0 && gk < G.nz && gj >= 0 && gj < G.nelx;
+    }
+    // a stored column is guaranteed by the slab/halo setup (host checks it)
+    const long long src = ((long long)(gj - G.sj0) * G.nz + gk) * G.nely + gi;
+    double v0 = 0.0, v1 = 0.0;
+    if (inside) {
+      v0 = A.in0 ? A.in0[src] : 1.0;  // null input: the all-ones field (hs)
+      if (MODE == CONV_ADJ_DIV) v0 = v0 / A.hs_st[src];
+      if (NF == 2) v1 = A.in1[src];
+    }
+    st[q] = v0;
+    if (NF == 2) st[tileN + q] = v1;
+  }
+  __syncthreads();
+
+  const int ti = threadIdx.x, tk = threadIdx.y;
+  const int gi = bi + ti, gk = bk + tk;
+  double acc0[JT], acc1[JT];
+#pragma unroll
+  for (int u = 0; u < JT; ++u) acc0[u] = acc1[u] = 0.0;
+  // taps in the reference order: rows (dj asc, dk asc), di asc inside a row
+  for (int rr = 0; rr < nrows; ++rr) {
+    const TapRow R = sr[rr];
+    const double* w = sw + R.woff;
+    const int n = 2 * R.a + 1;
+#pragma unroll
+    for (int u = 0; u < JT; ++u) {
+      const int tj = threadIdx.z * JT + u;
+      const double* p0 = st + ((long long)(tj + r + R.dj) * PK + (tk + rk + R.dk)) * PI + (ti + r - R.a);
+      double s0 = acc0[u], s1 = acc1[u];
+      for (int q = 0; q < n; ++q) {
+        s0 = fma(w[q], p0[q], s0);
+        if (NF == 2) s1 = fma(w[q], p0[tileN + q], s1);
+      }
+      acc0[u] = s0;
+      acc1[u] = s1;
+    }
+  }
+
+  // epilogue
+  double red[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int u = 0; u < JT; ++u) {
+    const int gj = bj + threadIdx.z * JT + u;
+    if (gi >= G.nely || gk >= G.nz || gj >= G.j0 + G.jn) continue;
+    const long long e = ((long long)(gj - G.j0) * G.nz + gk) * G.nely + gi;
+    if (MODE == CONV_PLAIN || MODE == CONV_ADJ_DIV) {
+      A.out0[e] = acc0[u];
+    } else if (MODE == CONV_FWD || MODE == CONV_FWD_ETA) {
+      double v = acc0[u] / A.hs[e];  // filter.hpp:121 cwiseQuotient(hs)
+      const int s = elem_state(A.state, e);
+      if (A.pin && s == 1) v = 1.0;  // driver.hpp:130-133
+      if (A.pin && s == 2) v = 0.0;
+      A.out0[e] = v;
+      if (MODE == CONV_FWD_ETA && s == 0) {
+        const EtaConsts c = eta_consts(A.beta, A.eta0);
+        double g, gp;
+        eta_terms(c, A.beta, A.eta0, v, g, gp);
+        red[0] += g;
+        red[1] += gp;
+      }
+    } else if (MODE == CONV_ADJ2_OC) {
+      const double dc = acc0[u], dV = acc1[u];
+      if (A.out0) A.out0[e] = dc;
+      if (A.out1) A.out1[e] = dV;
+      const bool act = elem_state(A.state, e) == 0;
+      const double4 rec = oc_record(A.x[e], dc, dV, A.cw[e], A.move, act);
+      A.ocrec[e] = rec;
+      if (act) red[0] += rec.z;
+      red[1] += rec.w * oc_cand(rec, 0.0);
+      red[2] += rec.w * std_min(std_max(0.0, rec.x), rec.y);  // V(s -> inf)
+    }
+  }
+  if (MODE == CONV_FWD_ETA || MODE == CONV_ADJ2_OC) {
+    __shared__ double scratch[3 * 32];
+    block_sum<3>(red, scratch);
+    const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (tid == 0) {
+      A.partials[3 * b] = red[0];
+      A.partials[3 * b + 1] = red[1];
+      A.partials[3 * b + 2] = red[2];
+    }
+  }
+}
+
+// ============================================================================
+// K2: volume-preserving eta (filter.hpp:182-228), cooperative Newton replay
+// ============================================================================
+
+struct EtaArgs {
+  Geo G;
+  const double* xt;
+  const uint8_t* state;
+  double beta, eta0, mtotal;
+  const double* partials0;  // K1 partials at eta0 (stride 3) or null
+  int n0;
+  double* partials;         // [2][gridDim][2]
+  double* result;           // eta, iterations (as double), g
+};
+
+__device__ __forceinline__ void eta_block_eval(const EtaArgs& A, double eta, double (&red)[2]) {
+  const EtaConsts c = eta_consts(A.beta, eta);
+  red[0] = red[1] = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < A.G.m;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (elem_state(A.state, e) != 0) continue;
+    double g, gp;
+    eta_terms(c, A.beta, eta, A.xt[e], g, gp);
+    red[0] += g;
+    red[1] += gp;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_eta_solve(EtaArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ EtaCtl ctl;
+  __shared__ double scratch[2 * 32];
+  __shared__ double gv[2];
+  __shared__ int cont;
+  if (threadIdx.x == 0) ctl.init(A.eta0);
+  __syncthreads();
+  int buf = 0;
+  if (A.partials0) {
+    if (threadIdx.x < 32) {
+      double s[2];
+      warp_sum_partials<2>(A.partials0, A.n0, 3, s);
+      if (threadIdx.x == 0) {
+        gv[0] = s[0];
+        gv[1] = s[1];
+      }
+    }
+  } else {
+    double red[2];
+    eta_block_eval(A, ctl.eta, red);
+    block_sum<2>(red, scratch);
+    if (threadIdx.x == 0) {
+      A.partials[2 * blockIdx.x] = red[0];
+      A.partials[2 * blockIdx.x + 1] = red[1];
+    }
+    grid.sync();
+    if (threadIdx.x < 32) {
+      double s[2];
+      warp_sum_partials<2>(A.partials, gridDim.x, 2, s);
+      if (threadIdx.x == 0) {
+        gv[0] = s[0];
+        gv[1] = s[1];
+      }
+    }
+    buf = 1;
+  }
+  __syncthreads();
+  for (;;) {
+    if (threadIdx.x == 0) cont = ctl.feed(gv[0] / A.mtotal, gv[1] / A.mtotal);
+    __syncthreads();
+    if (!cont) break;
+    double red[2];
+    eta_block_eval(A, ctl.eta, red);
+    block_sum<2>(red, scratch);
+    double* P = A.partials + (long long)buf * 2 * gridDim.x;
+    if (threadIdx.x == 0) {
+      P[2 * blockIdx.x] = red[0];
+      P[2 * blockIdx.x + 1] = red[1];
+    }
+    grid.sync();
+    if (threadIdx.x < 32) {
+      double s[2];
+      warp_sum_partials<2>(P, gridDim.x, 2, s);
+      if (threadIdx.x == 0) {
+        gv[0] = s[0];
+        gv[1] = s[1];
+      }
+    }
+    buf ^= 1;
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.result[0] = ctl.eta;
+    A.result[1] = double(ctl.it);
+    A.result[2] = ctl.g;
+  }
+}
+
+// plain (g, g') partial sums at one eta: the multi-GPU / host-driven variant
+__global__ void __launch_bounds__(kThreads) k_eta_partials(EtaArgs A, double eta) {
+  __shared__ double scratch[2 * 32];
+  double red[2];
+  eta_block_eval(A, eta, red);
+  block_sum<2>(red, scratch);
+  if (threadIdx.x == 0) {
+    A.partials[2 * blockIdx.x] = red[0];
+    A.partials[2 * blockIdx.x + 1] = red[1];
+  }
+}
+
+// ============================================================================
+// K3a: projection + SIMP + sensitivity + pre-adjoint fields (one element/thread)
+//   filter.hpp:137-154, fea.hpp:135-146, fea.hpp:248-272, filter.hpp:170
+// ============================================================================
+
+template <int D>
+struct KeFull {
+  double k[D * D];  // column-major (fea.hpp ElementStiffness::full)
+};
+
+struct ElemArgs {
+  const double* xt;      // owned filtered field (or xPhys when input_is_phys)
+  int input_is_phys;     // 1: xt already holds xPhys (compliance_and_sensitivity API)
+  const double* eta_ptr; // device scalar eta (written by K2)
+  const double* U;       // slab node planes [j0, j0 + jn]
+  const uint8_t* state;
+  const double* hs;      // owned
+  double beta, e0, emin, penal, inv_m;
+  double* xPhys;         // owned, may be null
+  double* dcPhys;        // owned, may be null
+  double* a1;            // storage-indexed pre-adjoint fields (dH dcPhys / hs, dH dV0 / hs)
+  double* a2;
+  double* partials;      // per block: compliance partial
+};
+
+__device__ __forceinline__ double simp_xp(double x, double p) {
+  const double pm1 = p - 1.0;
+  return pm1 == 2.0 ? x * x : pow(x, pm1);  // std::pow(x, p - 1), fea.hpp:141
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads) k_elem_sens(Geo G, KeFull<D> K, ElemArgs A) {
+  __shared__ double scratch[32];
+  const double eta = A.input_is_phys ? 0.5 : *A.eta_ptr;
+  const double a = tanh(A.beta * eta);
+  const double denom = a + tanh(A.beta * (1.0 - eta));
+  const double de = A.e0 - A.emin;
+  double csum = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < G.m;
+       e += (long long)gridDim.x * blockDim.x) {
+    int i, k, j;
+    elem_ijk(G, e, i, k, j);
+    const double t = A.xt[e];
+    double xphys, dH = 0.0;
+    if (A.input_is_phys) {
+      xphys = t;
+    } else {
+      const double th = tanh(A.beta * (t - eta));
+      xphys = (a + th) / denom;                               // filter.hpp:142
+      dH = A.beta * (1.0 - th * th) / denom;                  // filter.hpp:151
+    }
+    const double xp = simp_xp(xphys, A.penal);
+    const double sK = A.emin + xp * xphys * de;               // fea.hpp:142
+    const double dsK = A.penal * xp * de;                     // fea.hpp:143
+    int dofs[24];
+    element_dofs(G, i, k, j, G.j0, dofs);
+    double ue[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) ue[q] = __ldg(A.U + dofs[q]);
+    double quad = 0.0;  // ue . (Ke ue), fea.hpp:267
+#pragma unroll
+    for (int r = 0; r < D; ++r) {
+      double s = 0.0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) s = fma(K.k[c * D + r], ue[c], s);
+      quad = fma(ue[r], s, quad);
+    }
+    csum = fma(sK, quad, csum);
+    const int st = elem_state(A.state, e);
+    const double dcp = st == 0 ? -dsK * quad : 0.0;
+    const double dv0 = st == 0 ? A.inv_m : 0.0;               // driver.hpp:155
+    if (A.xPhys) A.xPhys[e] = xphys;
+    if (A.dcPhys) A.dcPhys[e] = dcp;
+    if (A.a1) {
+      const double h = A.hs[e];
+      const long long es = e + (long long)(G.j0 - G.sj0) * G.S;
+      A.a1[es] = (dH * dcp) / h;                              // backfilter, filter.hpp:170, :128
+      A.a2[es] = (dH * dv0) / h;
+    }
+  }
+  double red[1] = {csum};
+  block_sum<1>(red, scratch);
+  if (threadIdx.x == 0) A.partials[blockIdx.x] = red[0];
+}
+
+// ============================================================================
+// K3b: lower-triangle stiffness values sK[e*P + q] = E(xPhys_e) Ke_lower[q]
+//   (fea.hpp:135-146 + :162-169); the dominant HBM store stream
+// ============================================================================
+
+struct SkArgs {
+  const double* xt;  // owned filtered field (null: use sKe directly)
+  const double* sKe; // per-element modulus (topo_assemble_values)
+  const double* ke_lower;
+  const double* eta_ptr;  // device scalar eta
+  double beta, e0, emin, penal;
+  double* sK;
+};
+
+template <int P, int EB>
+__global__ void __launch_bounds__(kThreads) k_sk_store(Geo G, SkArgs A) {
+  constexpr int PV = P / 2;  // double2 per element
+  __shared__ double2 kl[PV];
+  __shared__ double se[EB];
+  for (int q = threadIdx.x; q < PV; q += blockDim.x)
+    kl[q] = make_double2(A.ke_lower[2 * q], A.ke_lower[2 * q + 1]);
+  double a = 0, denom = 1, de = 0, eta = 0;
+  if (A.xt) {
+    eta = *A.eta_ptr;
+    a = tanh(A.beta * eta);
+    denom = a + tanh(A.beta * (1.0 - eta));
+    de = A.e0 - A.emin;
+  }
+  const long long nchunks = (G.m + EB - 1) / EB;
+  for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const long long e0 = c * EB;
+    const int ne = int(min((long long)EB, G.m - e0));
+    __syncthreads();
+    for (int t = threadIdx.x; t < ne; t += blockDim.x) {
+      double s;
+      if (A.xt) {
+        const double xphys = (a + tanh(A.beta * (A.xt[e0 + t] - eta))) / denom;
+        const double xp = simp_xp(xphys, A.penal);
+        s = A.emin + xp * xphys * de;
+      } else {
+        s = A.sKe[e0 + t];
+      }
+      se[t] = s;
+    }
+    __syncthreads();
+    double2* out = reinterpret_cast<double2*>(A.sK + e0 * P);
+    const int nv = ne * PV;
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+      const int el = v / PV, q = v - el * PV;
+      const double s = se[el];
+      const double2 k = kl[q];
+      __stcs(out + v, make_double2(s * k.x, s * k.y));
+    }
+  }
+}
+
+// ============================================================================
+// elementwise helpers for the stage-level API
+// ============================================================================
+
+__global__ void k_project(long long m, const double* __restrict__ xt, double eta, double beta,
+                          double* __restrict__ out, int derivative) {
+  const double a = tanh(beta * eta);
+  const double denom = a + tanh(beta * (1.0 - eta));
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double th = tanh(beta * (xt[e] - eta));
+    out[e] = derivative ? beta * (1.0 - th * th) / denom : (a + th) / denom;
+  }
+}
+
+__global__ void k_simp(long long m, const double* __restrict__ x, double e0, double emin,
+                       double p, double* __restrict__ sK, double* __restrict__ dsK) {
+  const double de = e0 - emin;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double xp = simp_xp(x[e], p);
+    if (sK) sK[e] = emin + xp * x[e] * de;
+    if (dsK) dsK[e] = p * xp * de;
+  }
+}
+
+// out_storage[e] = (dH[e] * g[e]) (projection on) or g[e]; already divided by
+// hs when `div_hs` (backfilter pre-adjoint field)
+__global__ void k_prescale(Geo G, const double* __restrict__ g, const double* __restrict__ xt,
+                           double eta, double beta, int proj_on, const double* __restrict__ hs,
+                           double* __restrict__ out_st) {
+  const double denom = tanh(beta * eta) + tanh(beta * (1.0 - eta));
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < G.m;
+       e += (long long)gridDim.x * blockDim.x) {
+    double v = g[e];
+    if (proj_on) {
+      const double th = tanh(beta * (xt[e] - eta));
+      v = (beta * (1.0 - th * th) / denom) * v;
+    }
+    out_st[e + (long long)(G.j0 - G.sj0) * G.S] = v / hs[e];
+  }
+}
+
+__global__ void k_copy_to_storage(Geo G, const double* __restrict__ in, double* __restrict__ out_st) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < G.m;
+       e += (long long)gridDim.x * blockDim.x)
+    out_st[e + (long long)(G.j0 - G.sj0) * G.S] = in[e];
+}
+
+// compact active gathers (oc.hpp:63-67 take) are done on the host side of the
+// API; the OC kernels below work on full-length element arrays.
+
+// OC record + (sum ocP, V(0), V(inf)) partials from full-length x, dc, dV
+__global__ void __launch_bounds__(kThreads) k_oc_prep(long long m, const double* __restrict__ x,
+                                                      const double* __restrict__ dc,
+                                                      const double* __restrict__ dV,
+                                                      const uint8_t* __restrict__ state,
+                                                      const double* __restrict__ cw, double move,
+                                                      double4* __restrict__ rec,
+                                                      double* __restrict__ partials) {
+  __shared__ double scratch[3 * 32];
+  double red[3] = {0.0, 0.0, 0.0};
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x) {
+    const bool act = elem_state(state, e) == 0;
+    const double4 r = oc_record(x[e], dc[e], dV[e], cw ? cw[e] : 1.0, move, act);
+    rec[e] = r;
+    if (act) red[0] += r.z;
+    red[1] += r.w * oc_cand(r, 0.0);
+    red[2] += r.w * std_min(std_max(0.0, r.x), r.y);
+  }
+  block_sum<3>(red, scratch);
+  if (threadIdx.x == 0) {
+    partials[3 * blockIdx.x] = red[0];
+    partials[3 * blockIdx.x + 1] = red[1];
+    partials[3 * blockIdx.x + 2] = red[2];
+  }
+}
+
+// ============================================================================
+// K5 + K6: OC bisection (oc.hpp:93-174), cooperative; volume of a candidate
+// from the exact identity mean(pin(H xc)) = (|P1| + c . xc) / m with
+// c = H' 1_notP (ft = 3) or c = 1, |P1| -> 0 (ft = 1). Speculative batches
+// evaluate every multiplier the replay can request in the next kDepth steps.
+// ============================================================================
+
+constexpr int kOcK = 16;
+constexpr int kOcDepth = 4;
+
+struct OcArgs {
+  long long m;
+  const double4* rec;
+  const double* prep_partials;  // stride 3, count n_prep
+  int n_prep;
+  double volfrac, rel_tol, vol_tol, abs_tol, lambda_max, mtotal, add_const;
+  int lambda_space;
+  double margin;      // bound-shortcut margin
+  double* partials;   // [2][kOcK][gridDim]
+  double* xNew;       // full length (passives = x via their records)
+  double* result;     // lambda, bisections, evaluations, status, batches, shortcut
+};
+
+__global__ void __launch_bounds__(kThreads) k_oc_bisect(OcArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ OcCtl ctl;
+  __shared__ double sreq[kOcK];
+  __shared__ double sval[kOcK];
+  __shared__ int nreq, mode, nbatch;
+  __shared__ double scratch[kOcK * 32];
+  if (threadIdx.x < 32) {
+    double s[3];
+    warp_sum_partials<3>(A.prep_partials, A.n_prep, 3, s);
+    if (threadIdx.x == 0) {
+      // oc.hpp:112-116 lambda# = [sum x sqrt(-dc/dV) / (m volfrac)]^2
+      double lamMax = A.lambda_max;
+      if (!(A.lambda_max > 0)) {
+        const double root = s[0] / (A.mtotal * A.volfrac);
+        lamMax = root * root;
+      }
+      ctl.init(lamMax, A.volfrac, A.rel_tol, A.vol_tol, A.lambda_space, A.abs_tol);
+      const double V0 = (A.add_const + s[1]) / A.mtotal;
+      const double Vinf = (A.add_const + s[2]) / A.mtotal;
+      // every candidate volume lies in [V(inf), V(0)] (monotone, c >= 0):
+      // when the whole interval is decisively on one side, every decision of
+      // the reference is known without evaluating (SURVEY.md §7 hard part 2)
+      mode = 0;
+      if (Vinf > A.volfrac + 0.5 * A.vol_tol + A.margin) mode = 1;
+      if (V0 < A.volfrac - 0.5 * A.vol_tol - A.margin) mode = -1;
+      nbatch = 0;
+    }
+  }
+  __syncthreads();
+  int buf = 0;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      nreq = 0;
+      if (mode != 0) {
+        ctl.check_mono = 0;
+        while (ctl.pending()) ctl.feed(mode > 0 ? INFINITY : -INFINITY);
+      } else if (ctl.pending()) {
+        nreq = oc_speculate<kOcK>(ctl, kOcDepth, sreq);
+      }
+    }
+    __syncthreads();
+    if (nreq == 0) break;
+    const int K = nreq;
+    double acc[kOcK];
+#pragma unroll
+    for (int q = 0; q < kOcK; ++q) acc[q] = 0.0;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < A.m;
+         e += (long long)gridDim.x * blockDim.x) {
+      const double4 r = A.rec[e];
+#pragma unroll
+      for (int q = 0; q < kOcK; ++q)
+        if (q < K) acc[q] = fma(r.w, oc_cand(r, sreq[q]), acc[q]);
+    }
+    block_sum<kOcK>(acc, scratch);
+    double* P = A.partials + (long long)buf * kOcK * gridDim.x;
+    if (threadIdx.x == 0)
+      for (int q = 0; q < K; ++q) P[(long long)q * gridDim.x + blockIdx.x] = acc[q];
+    grid.sync();
+    // every block reduces the same partials in the same order
+    for (int q = 0; q < K; ++q) {
+      if (threadIdx.x < 32) {
+        double s[1];
+        warp_sum_partials<1>(P + (long long)q * gridDim.x, gridDim.x, 1, s);
+        if (threadIdx.x == 0) sval[q] = (A.add_const + s[0]) / A.mtotal;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      ++nbatch;
+      while (ctl.pending()) {
+        int hit = -1;
+        for (int q = 0; q < K; ++q)
+          if (sreq[q] == ctl.s_req) hit = q;
+        if (hit < 0) break;
+        ctl.feed(sval[hit]);
+      }
+    }
+    buf ^= 1;
+    __syncthreads();
+  }
+  // K6: xNew at the final multiplier (oc.hpp:108, :171)
+  const double sf = ctl.s_final;
+  if (ctl.status == OcCtl::ST_OK)
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < A.m;
+         e += (long long)gridDim.x * blockDim.x)
+      A.xNew[e] = oc_cand(A.rec[e], sf);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.result[0] = ctl.lam_result;
+    A.result[1] = ctl.bis;
+    A.result[2] = ctl.evals;
+    A.result[3] = ctl.status;
+    A.result[4] = nbatch;
+    A.result[5] = mode;
+    A.result[6] = ctl.s_final;
+  }
+}
+
+// candidate at one multiplier (host-driven OC modes and final write)
+__global__ void k_oc_candidates(long long m, const double4* __restrict__ rec, double s,
+                                double* __restrict__ out) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = oc_cand(rec[e], s);
+}
+
+// block partial sums of v (optionally projected: mean(H(v)))
+__global__ void __launch_bounds__(kThreads) k_sum(long long m, const double* __restrict__ v,
+                                                  int project, double eta, double beta,
+                                                  double* __restrict__ partials) {
+  __shared__ double scratch[32];
+  double a = 0, denom = 1;
+  if (project) {
+    a = tanh(beta * eta);
+    denom = a + tanh(beta * (1.0 - eta));
+  }
+  double red[1] = {0.0};
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x)
+    red[0] += project ? (a + tanh(beta * (v[e] - eta))) / denom : v[e];
+  block_sum<1>(red, scratch);
+  if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
+}
+
+// fixed-order final reduction of `count` partials (stride) into out[0..N)
+template <int N>
+__global__ void k_reduce_partials(const double* __restrict__ p, int count, int stride,
+                                  double* __restrict__ out) {
+  double s[N];
+  warp_sum_partials<N>(p, count, stride, s);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < N; ++q) out[q] = s[q];
+}
+
+// oc.hpp:31-39 / :72-79 on compact arrays
+__global__ void k_oc_compact(long long n, const double* __restrict__ x,
+                             const double* __restrict__ dc, const double* __restrict__ dV,
+                             double sqrt_lambda, double move, double* __restrict__ out,
+                             double* __restrict__ partials) {
+  __shared__ double scratch[32];
+  double red[1] = {0.0};
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double4 r = oc_record(x[e], dc[e], dV[e], 1.0, move, true);
+    red[0] += r.z;
+    if (out) out[e] = oc_cand(r, sqrt_lambda);
+  }
+  block_sum<1>(red, scratch);
+  if (threadIdx.x == 0 && partials) partials[blockIdx.x] = red[0];
+}
+
+}  // namespace topo

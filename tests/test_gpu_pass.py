@@ -1,0 +1,110 @@
+"""Fused design-update pass (topo_design_pass) against the CPU oracle with the
+conditioned, stage-wise protocol of SURVEY.md §8(c):
+
+1. eta: |eta_gpu - eta_oracle| <= 5e-8 and the oracle's |g(eta_gpu)| <= 1e-6;
+2. with eta := eta_gpu: xTilde, xPhys, sK, dcPhys, dc, dV <= 1e-12
+   (max|a-b| / max|b|); lambda <= 1e-10 relative; equal bisection count;
+   xNew <= 1e-12.
+
+The oracle runs the literal ft = 3 volume callback (one filter per OC
+evaluation) where that finishes in seconds, else the exact identity
+V = (|P1| + (H' 1_notP) . xc) / m (bitwise-equivalent decisions, verified in
+tests/test_oracle.py against the literal callback)."""
+import math
+
+import numpy as np
+import pytest
+
+from tests.common import rand_case, rel
+
+pytestmark = pytest.mark.gpu
+
+LITERAL, IDENTITY = 3, 4
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2005_05436_b200 as P
+    return P
+
+
+def check_pass(P, oracle_port, cfg, x, u, state, oracle_mode, check_sk=True, tol=1e-12):
+    grid = cfg.grid
+    f = oracle_port.filter(grid, cfg.rmin)
+    kf, kl = oracle_port.element_stiffness(3 if cfg.nelz else 2, cfg.nu)
+    with P.Context(*grid, rmin=cfg.rmin, nu=cfg.nu, state=state) as ctx:
+        g = ctx.design_pass(x, u, beta=cfg.beta, eta0=cfg.eta0, move=cfg.move,
+                            volfrac=cfg.volfrac, return_sk=check_sk)
+    # stage 1: eta
+    ro = oracle_port.design_pass(grid, cfg.rmin, x, u, state, beta=cfg.beta, eta0=cfg.eta0,
+                                 move=cfg.move, volfrac=cfg.volfrac, volume_mode=oracle_mode,
+                                 filt=f)
+    assert abs(g.eta - ro.eta) <= 5e-8, (g.eta, ro.eta)
+    assert abs(oracle_port.eta_mismatch(ro.xTilde, cfg.beta, g.eta, state)) <= 1e-6
+    # stage 2: everything downstream at eta_gpu
+    rc = oracle_port.design_pass(grid, cfg.rmin, x, u, state, beta=cfg.beta, eta0=cfg.eta0,
+                                 move=cfg.move, volfrac=cfg.volfrac, volume_mode=oracle_mode,
+                                 filt=f, eta_override=g.eta)
+    errs = {k: rel(getattr(g, k), getattr(rc, k)) for k in
+            ("xTilde", "xPhys", "dcPhys", "dc", "dV", "xNew")}
+    for k, e in errs.items():
+        assert e <= tol, (k, e, errs)
+    assert abs(g.c - rc.c) <= tol * abs(rc.c)
+    assert g.bisections == rc.bisections, (g.bisections, rc.bisections)
+    assert g.evaluations == rc.evaluations
+    assert abs(g.lam - rc.lam) <= 1e-10 * abs(rc.lam), (g.lam, rc.lam)
+    if check_sk:
+        sk_ref = oracle_port.assemble_values(rc.sKe, kl)
+        assert rel(g.sK, sk_ref) <= tol
+    return g, ro, rc
+
+
+@pytest.mark.parametrize("grid,rmin,beta,passives,seed", [
+    ((30, 10, 0), 2.4, 2.0, False, 1), ((30, 10, 0), 1.5, 4.0, True, 2),
+    ((60, 20, 0), 2.4, 2.0, False, 3), ((40, 17, 0), 4.6, 8.0, True, 4),
+    ((3, 2, 0), 4.5, 2.0, False, 5), ((1, 1, 0), 1.0, 2.0, False, 6),
+    ((12, 7, 6), 2.3, 2.0, True, 7), ((8, 8, 8), math.sqrt(3.0), 2.0, False, 8),
+    ((6, 5, 4), 4.0, 4.0, False, 9), ((1, 1, 1), 1.0, 2.0, False, 10)])
+def test_pass_small(P, oracle_port, grid, rmin, beta, passives, seed):
+    from paper_2005_05436_b200.configs import Config
+    cfg = Config(0, "small", *grid, rmin=rmin, beta=beta, move=0.2, volfrac=0.5)
+    x, u, state = rand_case(grid, seed, passives)
+    check_pass(P, oracle_port, cfg, x, u, state, LITERAL)
+
+
+@pytest.mark.parametrize("cid", [1, 2, 4])
+def test_pass_config_literal(P, oracle_port, cid):
+    from paper_2005_05436_b200.configs import CONFIGS, make_inputs
+    cfg = CONFIGS[cid]
+    x, u, state = make_inputs(cfg)
+    oracle_port.set_threads(0)
+    g, ro, rc = check_pass(P, oracle_port, cfg, x, u, state, LITERAL if cid == 1 else IDENTITY)
+    if cid == 4:  # degenerate OC regime, 243 volume evaluations
+        assert g.bisections == 200 and g.evaluations == 243
+
+
+def test_pass_config3_identity(P, oracle_port):
+    from paper_2005_05436_b200.configs import CONFIGS, make_inputs
+    cfg = CONFIGS[3]
+    x, u, state = make_inputs(cfg)
+    check_pass(P, oracle_port, cfg, x, u, state, IDENTITY, check_sk=False)
+
+
+def test_pass_config5_subgrid(P, oracle_port):
+    # C5 physics (rmin 4, beta 4, move 0.1, volfrac 0.12) on a 24 x 48 x 48 grid
+    from paper_2005_05436_b200.configs import CONFIGS
+    cfg = CONFIGS[5].scaled(24, 48, 48)
+    x, u, state = rand_case(cfg.grid, 55)
+    g, _, _ = check_pass(P, oracle_port, cfg, x, u, state, IDENTITY)
+    assert g.bisections == 200 and g.evaluations == 243
+
+
+def test_pass_deterministic(P):
+    from paper_2005_05436_b200.configs import CONFIGS, make_inputs
+    cfg = CONFIGS[1]
+    x, u, _ = make_inputs(cfg)
+    with P.Context(*cfg.grid, rmin=cfg.rmin) as ctx:
+        a = ctx.design_pass(x, u, beta=cfg.beta, move=cfg.move, volfrac=cfg.volfrac)
+        b = ctx.design_pass(x, u, beta=cfg.beta, move=cfg.move, volfrac=cfg.volfrac)
+    assert a.eta == b.eta and a.lam == b.lam and a.c == b.c
+    assert np.array_equal(a.xNew, b.xNew) and np.array_equal(a.dc, b.dc)
