@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark of one design-update pass (filter -> eta -> projection -> SIMP +
+lower-triangle stiffness values -> sensitivity from a supplied U ->
+back-filter -> OC bisection) on B200, BASELINE.json's metric:
+Melem/s per pass, FP64, with the HBM-roofline fraction.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
+
+N > 1 is launched by torchrun (one rank per GPU, x-slab decomposition of the
+same grid: strong scaling). Rank 0 prints ONE JSON line.
+
+Timing: W untimed passes, then K passes bracketed by barrier + synchronize,
+timed with CUDA events on the context's stream (device time, max over ranks).
+Inputs are resident in HBM and larger than L2 for C4/C5 (C5 writes 34 GB of
+stiffness values per pass); for C1-C3 the L2 is flushed between passes.
+e2e repeats the measurement through the C-ABI with pinned HOST buffers (H2D of
+x and U, D2H of xNew and the scalars inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Melem/s per design-update pass (assemble+filter+sens+OC), FP64; % HBM roofline"
+UNIT = "Melem/s"
+
+
+def algorithmic_bytes_per_elem(cfg) -> float:
+    """x + U (read once) + xPhys + sK + dc + dV + xnew [+ state byte]."""
+    b = 8 + 8.0 * cfg.n / cfg.m + 8 + 8 * cfg.P + 8 + 8 + 8
+    if cfg.passives:
+        b += 1
+    return b
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(cid: int):
+    """ncu dram bytes per sK-store launch, committed under profiles/ (or None)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(f"C{cid}", {}).get("sk_store_dram_bytes")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        except Exception:
+            self.ok = False
+        return self
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+            getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake",
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in names.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join(timeout=1)
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------- CPU samples
+def cpu_sample_config(cfg, scale: float = 1.0):
+    """A bounded sample of the workload with the same physics, filter and OC
+    parameters (per-element cost of the reference is linear in m)."""
+    from paper_2005_05436_b200.configs import Config
+    shapes = {1: (300, 100, 0), 2: (150, 50, 0), 3: (16, 400, 0), 4: (12, 48, 48),
+              5: (2, 48, 48)}
+    nx, ny, nz = shapes.get(cfg.cid, (cfg.nelx, cfg.nely, cfg.nelz))
+    nx = max(1, int(round(nx * scale)))
+    return cfg.scaled(nx, ny, nz, name=f"{cfg.name} sample {nx}x{ny}x{nz}")
+
+
+def sample_inputs(cfg, base):
+    """Seeded inputs of the sample grid (passive layout / smoothing re-derived
+    for the sample's own dimensions)."""
+    from paper_2005_05436_b200.configs import make_inputs
+    return make_inputs(cfg)
+
+
+def run_cpu(cfg, steps: int, warmup: int, threads: int):
+    """Times the reference CPU path (oracle/_ref = the reference's own headers,
+    else the C restatement) on `threads` concurrent sample instances."""
+    from oracle import oracle as O
+    kind = "reference" if os.path.exists(O.REF_LIB) else "port"
+    if not os.path.exists(O.PORT_LIB):
+        O.build()
+    orc = O.Oracle(kind)
+    if kind == "port":
+        orc.set_threads(1)
+    scfg = cpu_sample_config(cfg)
+    x, u, state = sample_inputs(scfg, cfg)
+    grid = scfg.grid
+    handles = []
+    for _ in range(threads):
+        if kind == "reference":
+            handles.append(orc.problem(grid, scfg.rmin, 0, scfg.nu, state))
+        else:
+            handles.append(orc.filter(grid, scfg.rmin))
+
+    def one(h):
+        if kind == "reference":
+            orc.design_pass(grid, scfg.rmin, x, u, state, beta=scfg.beta, move=scfg.move,
+                            volfrac=scfg.volfrac, problem=h)
+        else:
+            orc.design_pass(grid, scfg.rmin, x, u, state, beta=scfg.beta, move=scfg.move,
+                            volfrac=scfg.volfrac, filt=h)
+
+    def step():
+        ts = [threading.Thread(target=one, args=(h,)) for h in handles]
+        t0 = time.perf_counter()
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return time.perf_counter() - t0
+
+    for _ in range(warmup):
+        step()
+    times = [step() for _ in range(steps)]
+    wall = sum(times) / len(times)
+    value = threads * scfg.m / wall / 1e6
+    sample = (f"{threads} concurrent instance(s) of {scfg.nelx}x{scfg.nely}x{scfg.nelz} "
+              f"({scfg.m} elements each; {cfg.name} filter/projection/OC parameters; "
+              f"literal ft=3 OC volume callback), {steps} timed step(s)")
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
+            "sec_per_step": wall}
+
+
+# ------------------------------------------------------------------- ours
+def run_ours(args, cfg, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import paper_2005_05436_b200 as P
+    from paper_2005_05436_b200 import _lib as L
+    from paper_2005_05436_b200.configs import make_inputs, slab_of
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    x, u, state = make_inputs(cfg)
+
+    if world == 1:
+        ctx = P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu, device=local_rank, state=state)
+    else:
+        S = cfg.nely * (cfg.nelz or 1)
+        base, rem = divmod(cfg.nelx, world)
+        j0 = rank * base + min(rank, rem)
+        j1 = j0 + base + (1 if rank < rem else 0)
+        xs, us = slab_of(cfg, x, u, j0, j1)
+        st = None if state is None else state[j0 * S:j1 * S]
+        ctx = P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu, device=local_rank, rank=rank,
+                        nranks=world, j0=j0, j1=j1, state=st)
+        import torch.distributed as dist
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            uid = torch.from_numpy(np.frombuffer(P.nccl_unique_id(), dtype=np.uint8).copy())
+        dist.broadcast(uid, 0)
+        ctx.comm_init(bytes(uid.numpy()))
+        x, u = xs, us
+    m_local = ctx.m
+    xd = torch.from_numpy(x).to(dev)
+    ud = torch.from_numpy(u).to(dev)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.set_timing(True)
+    kw = dict(beta=cfg.beta, eta0=cfg.eta0, move=cfg.move, volfrac=cfg.volfrac, outputs=False)
+    flush = None
+    if cfg.m * algorithmic_bytes_per_elem(cfg) < 3 * 126e6:
+        flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    stage_acc = {k: 0.0 for k in L.STAGES}
+    launches = 0
+    for _ in range(args.warmup):
+        ctx.design_pass(xd, ud, **kw)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        t_total = 0.0
+        for _ in range(args.steps):
+            if flush is not None:
+                with torch.cuda.stream(stream):
+                    flush.fill_(1.0)
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            r = ctx.design_pass(xd, ud, **kw)
+            ev1.record(stream)
+            ev1.synchronize()
+            t_total += ev0.elapsed_time(ev1)
+            launches += r.launches
+            for k, v in ctx.stage_times().items():
+                stage_acc[k] += v
+        torch.cuda.synchronize()
+        barrier()
+    ms = t_total / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    stages = {k: v / args.steps for k, v in stage_acc.items()}
+
+    # e2e through the C-ABI with pinned host buffers
+    xh = torch.from_numpy(x).pin_memory()
+    uh = torch.from_numpy(u).pin_memory()
+    xnh = torch.empty(m_local, dtype=torch.float64).pin_memory()
+    pp = L.PassParams(L.Simp(cfg.e0, cfg.emin, cfg.penal), cfg.beta, cfg.eta0, cfg.move,
+                      cfg.volfrac, math.nan, L.VOL_FILTERED, 1)
+    po = L.PassOut(None, None, None, None, None, xnh.data_ptr(), None)
+    lib = ctx.lib
+    for _ in range(max(1, args.warmup)):
+        ctx._check(lib.topo_design_pass(ctx.h, xh.data_ptr(), uh.data_ptr(), C.byref(pp),
+                                        C.byref(po)))
+    barrier()
+    torch.cuda.synchronize()
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        ctx._check(lib.topo_design_pass(ctx.h, xh.data_ptr(), uh.data_ptr(), C.byref(pp),
+                                        C.byref(po)))
+        ev1.record(stream)
+        ev1.synchronize()
+        e2e_ms += ev0.elapsed_time(ev1)
+    e2e_ms /= args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = 8 * (x.size + u.size) * world
+    d2h = (8 * m_local + 8 * 5) * world
+    return dict(ms=ms, e2e_ms=e2e_ms, stages=stages, launches=launches, clocks=clk.summary(),
+                h2d=h2d, d2h=d2h, r=r, m_local=m_local, flushed=flush is not None)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2005_05436_b200.configs import CONFIGS
+    cfg = CONFIGS[args.config]
+    threads = args.cpu_threads or (os.cpu_count() or 1)
+    workload = {"workload": cfg.name, "grid": list(cfg.grid), "m": cfg.m, "n_dofs": cfg.n,
+                "rmin": cfg.rmin, "taps": None, "beta": cfg.beta, "move": cfg.move,
+                "volfrac": cfg.volfrac, "filter_bc": "neumann (mirror)", "ft": 3,
+                "parallelism": f"x-slab x{world}"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cb = run_cpu(cfg, args.steps, args.warmup, threads)
+        line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": cb["sec_per_step"] * 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": workload,
+                "cpu_baseline": {"value": cb["value"], "unit": UNIT, "cores": cb["cores"],
+                                 "kind": cb["kind"], "sample": cb["sample"]},
+                "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group(backend="gloo")
+    res = run_ours(args, cfg, rank, world, local_rank)
+    if rank != 0:
+        return
+    peak, peak_kind = load_peaks()
+    m = cfg.m
+    value = m / (res["ms"] * 1e-3) / 1e6
+    e2e_value = m / (res["e2e_ms"] * 1e-3) / 1e6
+    # dominant kernel: K3b sK store (reads xTilde, writes m*P values)
+    sk_ms = res["stages"]["sk_store"]
+    sk_bytes = res["m_local"] * (8 * cfg.P + 8)
+    sk_gbs = sk_bytes / (sk_ms * 1e-3) / 1e9 if sk_ms > 0 else None
+    traffic = load_traffic(cfg.cid)
+    b_elem = algorithmic_bytes_per_elem(cfg)
+    pass_gbs = m * b_elem / (res["ms"] * 1e-3) / 1e9 / max(1, args.gpus)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded x~U(0.01,1), U~N(0,1); SURVEY.md Appendix B)",
+        "config": dict(workload, l2=("flushed between passes (256 MiB write)" if res["flushed"]
+                                     else "inputs/outputs larger than L2 (no flush)")),
+        "roofline": {"bound": "hbm", "kernel": "k_sk_store (K3b, fea.hpp:135-146 + :162-169)",
+                     "achieved": sk_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": (sk_gbs / peak) if sk_gbs else None, "traffic": traffic,
+                     "bytes_per_launch": sk_bytes, "ms_per_launch": sk_ms,
+                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
+                     if peak_kind == "measured" else "fallback 6650 GB/s (B200_PROFILING.md)"},
+        "pass_roofline": {"bound": "hbm", "algorithmic_bytes_per_elem": b_elem,
+                          "achieved": pass_gbs, "peak": peak, "unit": "GB/s",
+                          "frac": pass_gbs / peak,
+                          "ceiling_melem_s": peak * 1e9 / b_elem / 1e6 * max(1, args.gpus)},
+        "stages_ms": res["stages"],
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": res["h2d"],
+                "d2h_bytes_per_step": res["d2h"], "ms_per_step": res["e2e_ms"]},
+        "gpu_launches": res["launches"],
+        "clocks": res["clocks"],
+        "result": {"eta": res["r"].eta, "eta_iters": res["r"].eta_iters, "lambda": res["r"].lam,
+                   "bisections": res["r"].bisections, "evaluations": res["r"].evaluations,
+                   "c": res["r"].c},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        cb = run_cpu(cfg, 1, 0, threads)
+        line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"],
+                                "kind": cb["kind"], "sample": cb["sample"]}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -183,6 +183,14 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
                              const topo_pass_params* prm, topo_pass_out* out);
 /* number of this library's kernel launches issued by the last call */
 int64_t topo_last_launch_count(const topo_ctx* ctx);
+/* per-stage CUDA-event timing of topo_design_pass (off by default). times_ms
+ * receives TOPO_NSTAGES values for the last pass, each measured with events
+ * on the stream its kernel runs on: K1 filter, K2 eta, K3a element, K4
+ * adjoint+OC prep, K5/K6 OC, K3b sK store (aux stream), whole pass. */
+enum { TOPO_STAGE_FILTER = 0, TOPO_STAGE_ETA, TOPO_STAGE_ELEM, TOPO_STAGE_ADJOINT, TOPO_STAGE_OC,
+       TOPO_STAGE_SK, TOPO_STAGE_PASS, TOPO_NSTAGES };
+topo_status topo_set_timing(topo_ctx* ctx, int on);
+topo_status topo_stage_times(topo_ctx* ctx, double* times_ms);
 
 #ifdef __cplusplus
 }

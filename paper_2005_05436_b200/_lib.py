@@ -27,7 +27,9 @@ EXPORTS = [
     "topo_filter_adjoint", "topo_project", "topo_project_derivative", "topo_backfilter",
     "topo_solve_eta", "topo_filter_taps", "topo_filter_hs", "topo_lambda_upper",
     "topo_oc_candidate", "topo_oc_bisect", "topo_design_pass", "topo_last_launch_count",
+    "topo_set_timing", "topo_stage_times",
 ]
+STAGES = ["filter", "eta", "elem", "adjoint", "oc", "sk_store", "pass"]
 
 
 class GridDesc(C.Structure):
@@ -112,6 +114,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
                                      p(C.c_int32)]),
         "topo_design_pass": (C.c_int, [vp, vp, vp, p(PassParams), p(PassOut)]),
         "topo_last_launch_count": (C.c_int64, [vp]),
+        "topo_set_timing": (C.c_int, [vp, C.c_int]),
+        "topo_stage_times": (C.c_int, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -273,6 +273,15 @@ class Context:
     def launches(self) -> int:
         return int(self.lib.topo_last_launch_count(self.h))
 
+    def set_timing(self, on: bool = True):
+        """Per-stage CUDA-event timing of design_pass (events on each kernel's stream)."""
+        self._check(self.lib.topo_set_timing(self.h, int(on)))
+
+    def stage_times(self) -> dict:
+        t = np.zeros(len(L.STAGES))
+        self._check(self.lib.topo_stage_times(self.h, t.ctypes.data))
+        return dict(zip(L.STAGES, t.tolist()))
+
     def set_stream(self, cuda_stream_handle: int):
         self._check(self.lib.topo_set_stream(self.h, cuda_stream_handle))
 

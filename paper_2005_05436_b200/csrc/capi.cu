@@ -91,6 +91,10 @@ struct topo_ctx {
   int coop_blocks = 148;
   long long launches = 0;
   Comm* comm = nullptr;
+  // per-stage timing (topo_set_timing)
+  bool timing = false;
+  cudaEvent_t tev[2 * TOPO_NSTAGES] = {};
+  double stage_ms[TOPO_NSTAGES] = {};
 };
 
 namespace {
@@ -185,6 +189,11 @@ topo_status finish_out(topo_ctx* ctx, double* user, const double* dev, long long
     CK(cudaMemcpyAsync(user, dev, sizeof(double) * size_t(count), cudaMemcpyDeviceToHost,
                        ctx->stream));
   return TOPO_OK;
+}
+
+// stage timing: events bracket each stage on the stream it runs on
+inline void tmark(topo_ctx* c, int stage, int end, cudaStream_t s) {
+  if (c->timing) cudaEventRecord(c->tev[2 * stage + end], s);
 }
 
 // ------------------------------------------------------------ convolution
@@ -638,11 +647,27 @@ void topo_ctx_destroy(topo_ctx* ctx) {
                     &ctx->partials0, &ctx->result})
     b->release();
   if (ctx->h_result) cudaFreeHost(ctx->h_result);
+  for (int q = 0; q < 2 * TOPO_NSTAGES; ++q)
+    if (ctx->tev[q]) cudaEventDestroy(ctx->tev[q]);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->stream && ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
+}
+
+topo_status topo_set_timing(topo_ctx* ctx, int on) {
+  if (!ctx) return TOPO_EINVAL;
+  if (on && !ctx->tev[0])
+    for (int q = 0; q < 2 * TOPO_NSTAGES; ++q) CK(cudaEventCreate(&ctx->tev[q]));
+  ctx->timing = on != 0;
+  return TOPO_OK;
+}
+
+topo_status topo_stage_times(topo_ctx* ctx, double* times_ms) {
+  if (!ctx || !times_ms) return TOPO_EINVAL;
+  for (int q = 0; q < TOPO_NSTAGES; ++q) times_ms[q] = ctx->stage_ms[q];
+  return TOPO_OK;
 }
 
 topo_status topo_set_stream(topo_ctx* ctx, void* s) {
@@ -1080,6 +1105,8 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   double* res = ctx->result.as<double>();
 
   // K1 (+ first eta evaluation)
+  tmark(ctx, TOPO_STAGE_PASS, 0, ctx->stream);
+  tmark(ctx, TOPO_STAGE_FILTER, 0, ctx->stream);
   const bool solve = isnan(prm->eta_override);
   ConvArgs A1{};
   A1.in0 = xs;
@@ -1095,7 +1122,9 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     TRY((launch_conv<1, CONV_FWD_ETA>(ctx, G, A1, &nb1)));
   else
     TRY((launch_conv<1, CONV_FWD>(ctx, G, A1, &nb1)));
+  tmark(ctx, TOPO_STAGE_FILTER, 1, ctx->stream);
   // K2
+  tmark(ctx, TOPO_STAGE_ETA, 0, ctx->stream);
   if (solve) {
     TRY(run_eta(ctx, ctx->xt.as<double>(), prm->beta, prm->eta0, ctx->partials0.as<double>(),
                 nb1, res));
@@ -1103,6 +1132,7 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     const double r[3] = {prm->eta_override, 0.0, 0.0};
     CK(cudaMemcpyAsync(res, r, sizeof r, cudaMemcpyHostToDevice, ctx->stream));
   }
+  tmark(ctx, TOPO_STAGE_ETA, 1, ctx->stream);
   // K3b on the aux stream
   const bool want_sk = prm->write_sk != 0;
   double* skp = nullptr;
@@ -1125,14 +1155,17 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     S.penal = prm->simp.penal;
     S.ke_lower = ctx->d_ke_lower.as<double>();
     S.sK = skp;
+    tmark(ctx, TOPO_STAGE_SK, 0, ctx->aux);
     if (G.is3d)
       k_sk_store<300, 16><<<ctx->sm_count, kThreads, 0, ctx->aux>>>(G, S);
     else
       k_sk_store<36, 128><<<ctx->sm_count, kThreads, 0, ctx->aux>>>(G, S);
     LAUNCHED();
+    tmark(ctx, TOPO_STAGE_SK, 1, ctx->aux);
     CK(cudaEventRecord(ctx->ev_join, ctx->aux));
   }
   // K3a
+  tmark(ctx, TOPO_STAGE_ELEM, 0, ctx->stream);
   ElemArgs E{};
   E.xt = ctx->xt.as<double>();
   E.eta_ptr = res;
@@ -1157,7 +1190,9 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     TRY(comm_halo(ctx->comm, ctx, ctx->a1_st.as<double>()));
     TRY(comm_halo(ctx->comm, ctx, ctx->a2_st.as<double>()));
   }
+  tmark(ctx, TOPO_STAGE_ELEM, 1, ctx->stream);
   // K4
+  tmark(ctx, TOPO_STAGE_ADJOINT, 0, ctx->stream);
   ConvArgs A4{};
   A4.in0 = ctx->a1_st.as<double>();
   A4.in1 = ctx->a2_st.as<double>();
@@ -1171,13 +1206,17 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   A4.partials = ctx->partials0.as<double>();
   int nb4 = 0;
   TRY((launch_conv<2, CONV_ADJ2_OC>(ctx, G, A4, &nb4)));
+  tmark(ctx, TOPO_STAGE_ADJOINT, 1, ctx->stream);
   // K5 + K6
+  tmark(ctx, TOPO_STAGE_OC, 0, ctx->stream);
   topo_oc_params oc{prm->move, prm->volfrac, 1e-4, 1e-3, 0, 1e-8, 0.0};  // oc.hpp:14-20 defaults
   double lam = 0;
   int32_t bis = 0, ev = 0;
   TRY(run_oc(ctx, &oc, vmode, ctx->partials0.as<double>(), nb4, ctx->xnew.as<double>(), &lam,
              &bis, &ev, 0.0, prm->beta, nullptr, nullptr));
+  tmark(ctx, TOPO_STAGE_OC, 1, ctx->stream);
   if (want_sk) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+  tmark(ctx, TOPO_STAGE_PASS, 1, ctx->stream);
   CK(cudaMemcpyAsync(ctx->h_result, res, sizeof(double) * 5, cudaMemcpyDeviceToHost, ctx->stream));
   // outputs
   struct {
@@ -1195,6 +1234,17 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   CK(cudaStreamSynchronize(ctx->stream));
   double c = ctx->h_result[4];
   if (ctx->comm) TRY(comm_allreduce_host(ctx->comm, ctx, &c, 1));
+  if (ctx->timing) {
+    for (int q = 0; q < TOPO_NSTAGES; ++q) {
+      float ms = 0.f;
+      ctx->stage_ms[q] = 0.0;
+      if (q == TOPO_STAGE_SK && !want_sk) continue;
+      if (cudaEventElapsedTime(&ms, ctx->tev[2 * q], ctx->tev[2 * q + 1]) == cudaSuccess)
+        ctx->stage_ms[q] = ms;
+      else
+        cudaGetLastError();
+    }
+  }
   out->eta = ctx->h_result[0];
   out->eta_iters = int32_t(ctx->h_result[1]);
   out->c = c;
