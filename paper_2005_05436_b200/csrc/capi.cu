@@ -70,8 +70,10 @@ struct topo_ctx {
   // taps
   std::vector<int> di, dj, dk;
   std::vector<double> w;
-  std::vector<TapRow> rows;
-  DevBuf d_rows, d_w;
+  std::vector<ConvCol> cols;  // canonical stencil columns (4, 2, 1 mirrors), weights padded to R
+  int ncol[3] = {0, 0, 0};
+  std::vector<double> wpad;
+  DevBuf d_cols, d_wpad;
   // element matrices
   std::vector<double> ke_full, ke_lower;
   DevBuf d_ke_lower;
@@ -87,8 +89,10 @@ struct topo_ctx {
   DevBuf sK, iK, jK;
   DevBuf partials, partials0, result;
   double* h_result = nullptr;  // pinned
-  int conv_jt = 1;             // outputs per thread along x
-  int coop_blocks = 148;
+  int conv_R = 4;              // outputs per thread along the run axis (4 in 3D, 8 in 2D)
+  bool overlap_sk = false;     // run the sK store concurrently with K3a..K6
+  int coop_blocks = 148;  // OC bisection grid (cooperative)
+  int coop_eta = 148;     // eta Newton grid (cooperative)
   long long launches = 0;
   Comm* comm = nullptr;
   // per-stage timing (topo_set_timing)
@@ -197,33 +201,74 @@ inline void tmark(topo_ctx* c, int stage, int end, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------ convolution
-size_t conv_smem_bytes(const topo_ctx* c, int nf, int jt) {
-  const Geo& G = c->G;
-  const int TI = 32, TK = G.is3d ? 4 : 1, TJ = (G.is3d ? 2 : 8) * jt;
-  const long long tile =
-      (long long)(TI + 2 * c->reach) * (TK + 2 * c->rk) * (TJ + 2 * c->reach);
-  return sizeof(double) * size_t(c->w.size() + 2 * c->rows.size() + nf * tile);
+// Tile geometry for a launch over the owned (or stored) columns of G.
+ConvGeom conv_geom(const topo_ctx* c, const Geo& G, int WI, int WR, int WO) {
+  ConvGeom T;
+  const int R = c->conv_R;
+  T.WI = WI;
+  T.WR = WR;
+  T.WO = WO;
+  T.TI = 32 * WI;
+  T.TR = R * WR;
+  T.TO = WO;
+  T.reach = c->reach;
+  T.reach_o = G.is3d ? c->reach : 0;
+  T.EI = T.TI + 2 * T.reach;
+  T.ER = T.TR + 2 * T.reach + R;
+  T.EO = T.TO + 2 * T.reach_o;
+  T.run_n = G.is3d ? G.nz : G.jn;
+  T.other_n = G.is3d ? G.jn : 1;
+  for (int q = 0; q < 3; ++q) T.ncol[q] = c->ncol[q];
+  return T;
 }
 
-template <int NF, int MODE, int JT>
+size_t conv_smem(const ConvGeom& T) {
+  return sizeof(double) * size_t(T.EI) * T.ER * T.EO + sizeof(int) * size_t(T.EI + T.ER + T.EO);
+}
+
+// 8 warps per block; pick the warp split that loads the fewest tile values per
+// output (halo overhead and partial tiles) within the shared-memory budget
+ConvGeom pick_geom(const topo_ctx* c, const Geo& G) {
+  static const int opts3[][3] = {{1, 2, 4}, {1, 4, 2}, {1, 1, 8}, {1, 8, 1}};
+  static const int opts2[][3] = {{2, 4, 1}, {4, 2, 1}, {1, 8, 1}, {8, 1, 1}};
+  ConvGeom best{};
+  double best_cost = 1e300;
+  for (int q = 0; q < 4; ++q) {
+    const int* o = G.is3d ? opts3[q] : opts2[q];
+    ConvGeom T = conv_geom(c, G, o[0], o[1], o[2]);
+    if (conv_smem(T) > 200 * 1024) continue;
+    const double outs = double(T.TI) * T.TR * T.TO;
+    const double fi = std::ceil(double(G.nely) / T.TI) * T.TI / G.nely;
+    const double fr = std::ceil(double(T.run_n) / T.TR) * T.TR / T.run_n;
+    const double fo = std::ceil(double(T.other_n) / T.TO) * T.TO / T.other_n;
+    const double cost = (double(T.EI) * T.ER * T.EO / outs + 64.0) * fi * fr * fo;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = T;
+    }
+  }
+  return best;
+}
+
+template <int NF, int MODE, int R>
 topo_status launch_conv_t(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* nblocks) {
-  const int TK = G.is3d ? 4 : 1, TZ = G.is3d ? 2 : 8;
-  dim3 block(32, TK, TZ);
-  dim3 grid((G.nely + 31) / 32, (G.nz + TK - 1) / TK, (G.jn + TZ * JT - 1) / (TZ * JT));
-  const size_t smem = conv_smem_bytes(ctx, NF, JT);
+  const ConvGeom T = pick_geom(ctx, G);
+  if (T.TI == 0) return fail(ctx, TOPO_EINVAL, "filter: rmin too large for the shared-memory tile");
+  dim3 grid((G.nely + T.TI - 1) / T.TI, (T.run_n + T.TR - 1) / T.TR,
+            (T.other_n + T.TO - 1) / T.TO);
+  const size_t smem = conv_smem(T);
   static bool attr_done = false;  // per instantiation
   if (!attr_done) {
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     cudaFuncAttributes fa;
-    CK(cudaFuncGetAttributes(&fa, k_conv<NF, MODE, JT>));
-    CK(cudaFuncSetAttribute(k_conv<NF, MODE, JT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncGetAttributes(&fa, k_conv<NF, MODE, R>));
+    CK(cudaFuncSetAttribute(k_conv<NF, MODE, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             optin - int(fa.sharedSizeBytes)));
     attr_done = true;
   }
-  k_conv<NF, MODE, JT><<<grid, block, smem, ctx->stream>>>(
-      G, ctx->d_rows.as<TapRow>(), int(ctx->rows.size()), ctx->d_w.as<double>(),
-      int(ctx->w.size()), ctx->reach, ctx->rk, A);
+  k_conv<NF, MODE, R><<<grid, kThreads, smem, ctx->stream>>>(
+      G, T, ctx->d_cols.as<ConvCol>(), int(ctx->cols.size()), ctx->d_wpad.as<double>(), A);
   LAUNCHED();
   if (nblocks) *nblocks = int(grid.x * grid.y * grid.z);
   return TOPO_OK;
@@ -231,15 +276,28 @@ topo_status launch_conv_t(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* n
 
 template <int NF, int MODE>
 topo_status launch_conv(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* nblocks = nullptr) {
-  if (ctx->conv_jt == 2) return launch_conv_t<NF, MODE, 2>(ctx, G, A, nblocks);
-  return launch_conv_t<NF, MODE, 1>(ctx, G, A, nblocks);
+  if (ctx->conv_R == 8) return launch_conv_t<NF, MODE, 8>(ctx, G, A, nblocks);
+  return launch_conv_t<NF, MODE, 4>(ctx, G, A, nblocks);
 }
 
 int conv_blocks(const topo_ctx* ctx) {
   const Geo& G = ctx->G;
-  const int TK = G.is3d ? 4 : 1, TZ = G.is3d ? 2 : 8;
-  return ((G.nely + 31) / 32) * ((G.nz + TK - 1) / TK) *
-         ((G.jn + TZ * ctx->conv_jt - 1) / (TZ * ctx->conv_jt));
+  const ConvGeom T = pick_geom(ctx, G);
+  if (T.TI == 0) return 1;
+  return ((G.nely + T.TI - 1) / T.TI) * ((T.run_n + T.TR - 1) / T.TR) *
+         ((T.other_n + T.TO - 1) / T.TO);
+}
+
+// K3b: grid sized for full occupancy (no shared-memory or barrier limits)
+topo_status launch_sk(topo_ctx* ctx, const SkArgs& S, cudaStream_t st) {
+  const Geo& G = ctx->G;
+  const int nb = grid_for(ctx, (G.m + 31) / 32 * 32);
+  if (G.is3d)
+    k_sk_store<300><<<nb, kThreads, 0, st>>>(G, S);
+  else
+    k_sk_store<36><<<nb, kThreads, 0, st>>>(G, S);
+  LAUNCHED();
+  return TOPO_OK;
 }
 
 // ------------------------------------------------------- reductions / comm
@@ -255,10 +313,9 @@ topo_status reduce_to_host(topo_ctx* ctx, const double* partials, int count) {
   return TOPO_OK;
 }
 
-topo_status coop_launch(topo_ctx* ctx, const void* fn, void* args) {
+topo_status coop_launch(topo_ctx* ctx, const void* fn, void* args, int blocks) {
   void* kargs[] = {args};
-  CK(cudaLaunchCooperativeKernel(fn, dim3(ctx->coop_blocks), dim3(kThreads), kargs, 0,
-                                 ctx->stream));
+  CK(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kThreads), kargs, 0, ctx->stream));
   ++ctx->launches;
   return TOPO_OK;
 }
@@ -277,7 +334,7 @@ topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
   A.n0 = n0;
   A.partials = ctx->partials.as<double>();
   A.result = eta_dev_out;
-  if (!ctx->comm) return coop_launch(ctx, (const void*)k_eta_solve, &A);
+  if (!ctx->comm) return coop_launch(ctx, (const void*)k_eta_solve, &A, ctx->coop_eta);
   // multi-GPU: host-driven replay, one allreduce of (g, g') per evaluation
   EtaCtl ctl;
   ctl.init(eta0);
@@ -285,16 +342,16 @@ topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
   if (partials0) {
     TRY(reduce_to_host<3>(ctx, partials0, n0));
   } else {
-    k_eta_partials<<<ctx->coop_blocks, kThreads, 0, ctx->stream>>>(A, ctl.eta);
+    k_eta_partials<<<ctx->coop_eta, kThreads, 0, ctx->stream>>>(A, ctl.eta);
     LAUNCHED();
-    TRY(reduce_to_host<2>(ctx, A.partials, ctx->coop_blocks));
+    TRY(reduce_to_host<2>(ctx, A.partials, ctx->coop_eta));
   }
   g = ctx->h_result[0];
   gp = ctx->h_result[1];
   while (ctl.feed(g / ctx->m_total, gp / ctx->m_total)) {
-    k_eta_partials<<<ctx->coop_blocks, kThreads, 0, ctx->stream>>>(A, ctl.eta);
+    k_eta_partials<<<ctx->coop_eta, kThreads, 0, ctx->stream>>>(A, ctl.eta);
     LAUNCHED();
-    TRY(reduce_to_host<2>(ctx, A.partials, ctx->coop_blocks));
+    TRY(reduce_to_host<2>(ctx, A.partials, ctx->coop_eta));
     g = ctx->h_result[0];
     gp = ctx->h_result[1];
   }
@@ -329,7 +386,7 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
     A.partials = ctx->partials.as<double>();
     A.xNew = xnew_dev;
     A.result = ctx->result.as<double>() + 8;
-    TRY(coop_launch(ctx, (const void*)k_oc_bisect, &A));
+    TRY(coop_launch(ctx, (const void*)k_oc_bisect, &A, ctx->coop_blocks));
     CK(cudaMemcpyAsync(ctx->h_result + 8, A.result, sizeof(double) * 7, cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -531,29 +588,44 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
     if (s) return bail(s);
   }
 
-  // filter taps in reference order (filter.hpp:105-113), grouped in di rows
+  // filter taps in reference order (filter.hpp:105-113)
   {
     const int reach = ctx->reach, dkMax = is3d ? reach : 0;
+    auto weight = [&](int di_, int dj_, int dk_) {
+      return d->rmin - sqrt(double(di_) * di_ + double(dj_) * dj_ + double(dk_) * dk_);
+    };
     for (int dj_ = -reach; dj_ <= reach; ++dj_)
-      for (int dk_ = -dkMax; dk_ <= dkMax; ++dk_) {
-        TapRow row{dj_, dk_, -1, int(ctx->w.size())};
-        int first = 1 << 30;
+      for (int dk_ = -dkMax; dk_ <= dkMax; ++dk_)
         for (int di_ = -reach; di_ <= reach; ++di_) {
-          const double dist = sqrt(double(di_) * di_ + double(dj_) * dj_ + double(dk_) * dk_);
-          const double wv = d->rmin - dist;
+          const double wv = weight(di_, dj_, dk_);
           if (wv > 0) {
-            if (first == (1 << 30)) first = di_;
             ctx->di.push_back(di_);
             ctx->dj.push_back(dj_);
             ctx->dk.push_back(dk_);
             ctx->w.push_back(wv);
           }
         }
-        if (first != (1 << 30)) {
-          row.a = -first;  // positive weights form the symmetric run [-a, a]
-          ctx->rows.push_back(row);
+    // the same taps as canonical columns along the run axis (k in 3D, j in
+    // 2D) with di >= 0 and other >= 0, grouped by mirror count 4 / 2 / 1; the
+    // weights are the reference's values, only the summation order differs
+    ctx->conv_R = is3d ? 4 : 8;
+    const int R = ctx->conv_R;
+    for (int group = 0; group < 3; ++group) {
+      for (int o = 0; o <= dkMax; ++o)  // other axis: dj in 3D, none in 2D
+        for (int di_ = 0; di_ <= reach; ++di_) {
+          const int nm = (di_ > 0 ? 2 : 1) * (o > 0 ? 2 : 1);
+          if (nm != (group == 0 ? 4 : group == 1 ? 2 : 1)) continue;
+          auto wcol = [&](int t) { return is3d ? weight(di_, o, t) : weight(di_, t, 0); };
+          if (!(wcol(0) > 0)) continue;
+          int a = 0;
+          while (a + 1 <= reach && wcol(a + 1) > 0) ++a;
+          ConvCol col{di_, is3d ? o : 0, a, int(ctx->wpad.size())};
+          const int n = 2 * a + 1, npad = (n + R - 1) / R * R;
+          for (int t = 0; t < npad; ++t) ctx->wpad.push_back(t < n ? wcol(t - a) : 0.0);
+          ctx->cols.push_back(col);
+          ++ctx->ncol[group];
         }
-      }
+    }
   }
   // element matrices
   ctx->ke_full.resize(size_t(G.d * G.d));
@@ -565,11 +637,13 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
     return bail(fail(ctx, TOPO_EINVAL, "element stiffness: Poisson ratio must lie in (-1, 0.5)"));
   }
 
-  // conv tile size (outputs per thread along x) that fits shared memory
-  ctx->conv_jt = conv_smem_bytes(ctx, 2, 2) <= 226 * 1024 ? 2 : 1;
-  if (conv_smem_bytes(ctx, 2, 1) > 226 * 1024)
+  if (pick_geom(ctx, G).TI == 0)
     return bail(fail(ctx, TOPO_EINVAL, "filter: rmin %.3g too large for the shared-memory tile",
                      d->rmin));
+  {
+    const char* ov = getenv("TOPO_SK_OVERLAP");
+    ctx->overlap_sk = ov && ov[0] == '1';
+  }
 
 #define CKC(x)                                                                          \
   do {                                                                                  \
@@ -584,11 +658,12 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   CKC(cudaMallocHost(&ctx->h_result, 64 * sizeof(double)));
 
   const size_t md = sizeof(double) * size_t(G.m), sd = sizeof(double) * size_t(ctx->m_st);
-  CKC(ctx->d_rows.ensure(sizeof(TapRow) * ctx->rows.size()));
-  CKC(ctx->d_w.ensure(sizeof(double) * ctx->w.size()));
-  CKC(cudaMemcpy(ctx->d_rows.p, ctx->rows.data(), sizeof(TapRow) * ctx->rows.size(),
+  CKC(ctx->d_cols.ensure(sizeof(ConvCol) * ctx->cols.size()));
+  CKC(ctx->d_wpad.ensure(sizeof(double) * ctx->wpad.size()));
+  CKC(cudaMemcpy(ctx->d_cols.p, ctx->cols.data(), sizeof(ConvCol) * ctx->cols.size(),
                  cudaMemcpyHostToDevice));
-  CKC(cudaMemcpy(ctx->d_w.p, ctx->w.data(), sizeof(double) * ctx->w.size(), cudaMemcpyHostToDevice));
+  CKC(cudaMemcpy(ctx->d_wpad.p, ctx->wpad.data(), sizeof(double) * ctx->wpad.size(),
+                 cudaMemcpyHostToDevice));
   CKC(ctx->d_ke_lower.ensure(sizeof(double) * size_t(G.P)));
   CKC(cudaMemcpy(ctx->d_ke_lower.p, ctx->ke_lower.data(), sizeof(double) * size_t(G.P),
                  cudaMemcpyHostToDevice));
@@ -606,9 +681,13 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_eta_solve, kThreads, 0));
   if (occ < 1 || occ2 < 1)
     return bail(fail(ctx, TOPO_ECUDA, "cooperative kernels cannot be resident"));
-  ctx->coop_blocks = ctx->sm_count;  // one block per SM (leaves room for the sK stream)
+  // all blocks resident (cooperative); one per SM in overlap mode, where the
+  // sK stream shares the SMs
+  ctx->coop_eta = ctx->sm_count * occ2;
+  ctx->coop_blocks = ctx->overlap_sk ? ctx->sm_count : ctx->sm_count * occ;
   const size_t npart = std::max<size_t>(
       {size_t(conv_blocks(ctx)) * 3, size_t(ctx->coop_blocks) * 2 * kOcK * 2,
+       size_t(ctx->coop_eta) * 2 * 2,
        size_t(ctx->sm_count) * 8 * 4});
   CKC(ctx->partials.ensure(sizeof(double) * npart));
   CKC(ctx->partials0.ensure(sizeof(double) * npart));
@@ -640,7 +719,7 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   if (ctx->device >= 0) cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) comm_destroy(ctx->comm);
-  for (DevBuf* b : {&ctx->d_rows, &ctx->d_w, &ctx->d_ke_lower, &ctx->d_state, &ctx->hs, &ctx->hs_st,
+  for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_ke_lower, &ctx->d_state, &ctx->hs, &ctx->hs_st,
                     &ctx->cw, &ctx->x_st, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
                     &ctx->xnew, &ctx->a1_st, &ctx->a2_st, &ctx->rec, &ctx->u, &ctx->tmp0,
                     &ctx->tmp1, &ctx->tmp_st, &ctx->sK, &ctx->iK, &ctx->jK, &ctx->partials,
@@ -828,10 +907,7 @@ topo_status topo_assemble_values(topo_ctx* ctx, const double* sKe, double* vals)
   A.sKe = s;
   A.ke_lower = ctx->d_ke_lower.as<double>();
   A.sK = o;
-  if (G.is3d)
-    k_sk_store<300, 16><<<ctx->sm_count * 2, kThreads, 0, ctx->stream>>>(G, A);
-  else
-    k_sk_store<36, 128><<<ctx->sm_count * 2, kThreads, 0, ctx->stream>>>(G, A);
+  TRY(launch_sk(ctx, A, ctx->stream));
   LAUNCHED();
   if (!dev && vals)
     CK(cudaMemcpyAsync(vals, o, sizeof(double) * size_t(cnt), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1133,9 +1209,11 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     CK(cudaMemcpyAsync(res, r, sizeof r, cudaMemcpyHostToDevice, ctx->stream));
   }
   tmark(ctx, TOPO_STAGE_ETA, 1, ctx->stream);
-  // K3b on the aux stream
+  // K3b: after eta it depends on nothing else; either overlapped on the aux
+  // stream with K3a..K6, or last on the main stream
   const bool want_sk = prm->write_sk != 0;
   double* skp = nullptr;
+  SkArgs S{};
   if (want_sk) {
     const long long cnt = G.m * G.P;
     if (out->sK && is_device_ptr(out->sK)) {
@@ -1144,9 +1222,6 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
       CK(ctx->sK.ensure(sizeof(double) * size_t(cnt)));
       skp = ctx->sK.as<double>();
     }
-    CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
-    CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
-    SkArgs S{};
     S.xt = ctx->xt.as<double>();
     S.eta_ptr = res;
     S.beta = prm->beta;
@@ -1155,12 +1230,13 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     S.penal = prm->simp.penal;
     S.ke_lower = ctx->d_ke_lower.as<double>();
     S.sK = skp;
+  }
+  const bool overlap = want_sk && ctx->overlap_sk && !ctx->comm;
+  if (overlap) {
+    CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
     tmark(ctx, TOPO_STAGE_SK, 0, ctx->aux);
-    if (G.is3d)
-      k_sk_store<300, 16><<<ctx->sm_count, kThreads, 0, ctx->aux>>>(G, S);
-    else
-      k_sk_store<36, 128><<<ctx->sm_count, kThreads, 0, ctx->aux>>>(G, S);
-    LAUNCHED();
+    TRY(launch_sk(ctx, S, ctx->aux));
     tmark(ctx, TOPO_STAGE_SK, 1, ctx->aux);
     CK(cudaEventRecord(ctx->ev_join, ctx->aux));
   }
@@ -1215,7 +1291,13 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   TRY(run_oc(ctx, &oc, vmode, ctx->partials0.as<double>(), nb4, ctx->xnew.as<double>(), &lam,
              &bis, &ev, 0.0, prm->beta, nullptr, nullptr));
   tmark(ctx, TOPO_STAGE_OC, 1, ctx->stream);
-  if (want_sk) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+  if (overlap) {
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+  } else if (want_sk) {
+    tmark(ctx, TOPO_STAGE_SK, 0, ctx->stream);
+    TRY(launch_sk(ctx, S, ctx->stream));
+    tmark(ctx, TOPO_STAGE_SK, 1, ctx->stream);
+  }
   tmark(ctx, TOPO_STAGE_PASS, 1, ctx->stream);
   CK(cudaMemcpyAsync(ctx->h_result, res, sizeof(double) * 5, cudaMemcpyDeviceToHost, ctx->stream));
   // outputs

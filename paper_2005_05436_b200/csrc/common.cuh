@@ -39,10 +39,6 @@ struct Geo {
   int bc;                // 0 Neumann (mirror), 1 Dirichlet (zero)
 };
 
-struct TapRow {  // one (dj, dk) row of the cone stencil; di runs over [-a, a]
-  int dj, dk, a, woff;
-};
-
 // Per-element state byte: 0 active, 1 passive solid, 2 passive void.
 __device__ __forceinline__ int elem_state(const uint8_t* st, long long e) {
   return st ? int(st[e]) : 0;

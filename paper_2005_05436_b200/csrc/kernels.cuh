@@ -148,22 +148,28 @@ struct ConvArgs {
   double4* ocrec;    // (lb, ub, ocP, cw) per element
 };
 
-// eta pass terms for one filtered value t (filter.hpp:187-201)
+// eta pass terms for one filtered value t (filter.hpp:187-201). The slope
+// uses the exact identities sech^2(u) = 1 - tanh^2(u) and
+// sinh(b t) sinh(b (1 - t)) = (cosh(b) - cosh(b (2 t - 1))) / 2, so one tanh
+// and one cosh serve both sums (rounding differs from the reference's
+// expression at the 1e-16 level; eta parity is judged by SURVEY.md §8(c)).
 struct EtaConsts {
-  double a, denom, c0;  // tanh(b eta), a + tanh(b (1 - eta)), -b / sinh(b)
+  double a, denom, c0, coshb;  // tanh(b eta), a + tanh(b (1 - eta)), -b / sinh(b), cosh(b)
 };
 __device__ __forceinline__ EtaConsts eta_consts(double beta, double eta) {
   EtaConsts c;
   c.a = tanh(beta * eta);
   c.denom = c.a + tanh(beta * (1.0 - eta));
   c.c0 = -beta / sinh(beta);
+  c.coshb = cosh(beta);
   return c;
 }
 __device__ __forceinline__ void eta_terms(const EtaConsts& c, double beta, double eta, double t,
                                           double& g, double& gp) {
-  g = (c.a + tanh(beta * (t - eta))) / c.denom - t;
-  const double sech = 1.0 / cosh(beta * (t - eta));
-  gp = c.c0 * sech * sech * sinh(beta * t) * sinh(beta * (1.0 - t));
+  const double th = tanh(beta * (t - eta));
+  g = (c.a + th) / c.denom - t;
+  const double s = 0.5 * (c.coshb - cosh(beta * (2.0 * t - 1.0)));
+  gp = c.c0 * (1.0 - th * th) * s;
 }
 
 // Candidate record of oc.hpp:44-61 for one element; passives get lb = ub = x,
@@ -180,101 +186,169 @@ __device__ __forceinline__ double oc_cand(const double4& r, double s) {
   return std_min(std_max(f, r.x), r.y);
 }
 
-template <int NF, int MODE, int JT>
-__global__ void __launch_bounds__(kThreads) k_conv(Geo G, const TapRow* __restrict__ rows,
-                                                   int nrows, const double* __restrict__ wts,
-                                                   int nw, int r, int rk, ConvArgs A) {
-  extern __shared__ double smem[];
-  const int TI = blockDim.x, TK = blockDim.y, TJ = blockDim.z * JT;
-  const int PI = TI + 2 * r, PK = TK + 2 * rk, PJ = TJ + 2 * r;
-  const int tileN = PI * PK * PJ;
-  double* sw = smem;                                     // nw weights
-  TapRow* sr = reinterpret_cast<TapRow*>(smem + nw);     // nrows rows (16 B each)
-  double* st = smem + nw + 2 * nrows;                    // NF tiles
-  const int tid = threadIdx.x + TI * (threadIdx.y + TK * threadIdx.z);
-  const int nthr = TI * TK * blockDim.z;
+// Tile geometry of one conv launch. Lanes run along i (the fastest memory
+// axis); each thread owns R consecutive outputs along the "run" axis (k in 3D,
+// j in 2D) so that every tile value it loads feeds up to R accumulators.
+// Taps are grouped in columns (fixed di and other-axis offset) whose run
+// offsets form the symmetric interval [-a, a]; column weights are zero-padded
+// to a multiple of R (zero-weight FMAs leave the sums unchanged). The cone is
+// even in di and in the other offset, so mirrored columns share weights: only
+// canonical columns (di >= 0, other >= 0) are stored, and the values of their
+// 1, 2 or 4 mirrors are summed before the weights are applied.
+struct ConvGeom {
+  int WI, WR, WO;      // warps along i / run / other
+  int TI, TR, TO;      // outputs per tile along i / run / other
+  int EI, ER, EO;      // shared-memory tile extents
+  int reach, reach_o;  // halo along i and run / along other (0 in 2D)
+  int run_n, other_n;  // owned extents of the run / other axes
+  int ncol[3];         // canonical columns with 4, 2, 1 mirrors (stored in that order)
+};
 
-  for (int q = tid; q < nw; q += nthr) sw[q] = wts[q];
-  for (int q = tid; q < nrows; q += nthr) sr[q] = rows[q];
+struct ConvCol {  // one canonical column of the cone stencil
+  int di, dother, a, woff;
+};
 
-  // tile origin (global coordinates of output (0,0,0) of this block)
-  const int bi = blockIdx.x * TI, bk = blockIdx.y * TK, bj = G.j0 + blockIdx.z * TJ;
-  for (int q = tid; q < tileN; q += nthr) {
-    const int ti = q % PI, rest = q / PI, tk = rest % PK, tj = rest / PK;
-    int gi = bi + ti - r, gk = bk + tk - rk, gj = bj + tj - r;
-    bool inside = true;
-    if (G.bc == 0) {
-      gi = reflect_index(gi, G.nely);
-      gk = reflect_index(gk, G.nz);
-      gj = reflect_index(gj, G.nelx);
-    } else {
-      inside = gi >= 0 && gi < G.nely && gk >= 0 && gk < G.nz && gj >= 0 && gj < G.nelx;
+// accumulate the columns [c0, c1), each with NM mirrors, into acc
+template <int NM, int R>
+__device__ __forceinline__ void conv_columns(const double* __restrict__ tile, int sb, int sEI,
+                                             int sPlane, const ConvCol* __restrict__ cols, int c0,
+                                             int c1, const double* __restrict__ wts,
+                                             double (&acc)[R]) {
+  for (int c = c0; c < c1; ++c) {
+    const ConvCol col = cols[c];
+    const int base = sb - col.a * sEI;
+    const int oi = col.di, oo = col.dother * sPlane;
+    const double* p0 = tile + base + oi + oo;
+    const double* p1 = tile + base - oi - oo;  // NM == 2: the one nonzero offset flipped
+    const double* p2 = tile + base - oi + oo;  // NM == 4
+    const double* p3 = tile + base + oi - oo;
+    auto colval = [&](int s) {
+      const int o = s * sEI;
+      double v = p0[o];
+      if (NM == 2) v += p1[o];
+      if (NM == 4) v = (v + p1[o]) + (p2[o] + p3[o]);
+      return v;
+    };
+    const double2* w2 = reinterpret_cast<const double2*>(wts + col.woff);
+    const int nch = (2 * col.a + R) / R;  // ceil((2a + 1) / R)
+    double v[2 * R - 1];
+#pragma unroll
+    for (int s = 0; s < R - 1; ++s) v[s] = colval(s);
+    for (int ch = 0; ch < nch; ++ch) {
+#pragma unroll
+      for (int s = 0; s < R; ++s) v[R - 1 + s] = colval(ch * R + R - 1 + s);
+      double wv[R];
+#pragma unroll
+      for (int t = 0; t < R / 2; ++t) {
+        const double2 ww = __ldg(w2 + ch * (R / 2) + t);
+        wv[2 * t] = ww.x;
+        wv[2 * t + 1] = ww.y;
+      }
+#pragma unroll
+      for (int t = 0; t < R; ++t)
+#pragma unroll
+        for (int r = 0; r < R; ++r) acc[r] = fma(wv[t], v[r + t], acc[r]);
+#pragma unroll
+      for (int s = 0; s < R - 1; ++s) v[s] = v[R + s];
     }
-    // a stored column is guaranteed by the slab/halo setup (host checks it)
-    const long long src = ((long long)(gj - G.sj0) * G.nz + gk) * G.nely + gi;
-    double v0 = 0.0, v1 = 0.0;
-    if (inside) {
-      v0 = A.in0 ? A.in0[src] : 1.0;  // null input: the all-ones field (hs)
-      if (MODE == CONV_ADJ_DIV) v0 = v0 / A.hs_st[src];
-      if (NF == 2) v1 = A.in1[src];
-    }
-    st[q] = v0;
-    if (NF == 2) st[tileN + q] = v1;
   }
+}
+
+template <int NF, int MODE, int R>
+__global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const ConvCol* __restrict__ cols,
+                                                   int ncols, const double* __restrict__ wts,
+                                                   ConvArgs A) {
+  extern __shared__ double tile[];
+  // folded source coordinates of the tile's i / run / other lines (-1: zero pad)
+  int* mapI = reinterpret_cast<int*>(tile + T.EI * T.ER * T.EO);
+  int* mapR = mapI + T.EI;
+  int* mapO = mapR + T.ER;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wi = warp % T.WI, wr = (warp / T.WI) % T.WR, wo = warp / (T.WI * T.WR);
+  const int bi = blockIdx.x * T.TI, br = blockIdx.y * T.TR, bo = blockIdx.z * T.TO;
+  const int sEI = T.EI, sPlane = T.EI * T.ER;
+  // thread base: its first output (r = 0) in tile coordinates
+  const int sb = (wo + T.reach_o) * sPlane + (wr * R + T.reach) * sEI + (wi * 32 + lane + T.reach);
+
+  auto fold = [&](int t, int n) {  // mirror (Neumann) or -1 outside (Dirichlet)
+    if (t >= 0 && t < n) return t;
+    return G.bc == 0 ? reflect_index(t, n) : -1;
+  };
+  for (int q = tid; q < T.EI; q += blockDim.x) mapI[q] = fold(bi + q - T.reach, G.nely);
+  for (int q = tid; q < T.ER; q += blockDim.x)
+    mapR[q] = G.is3d ? fold(br + q - T.reach, G.nz) : fold(G.j0 + br + q - T.reach, G.nelx);
+  for (int q = tid; q < T.EO; q += blockDim.x)
+    mapO[q] = G.is3d ? fold(G.j0 + bo + q - T.reach_o, G.nelx) : 0;
   __syncthreads();
 
-  const int ti = threadIdx.x, tk = threadIdx.y;
-  const int gi = bi + ti, gk = bk + tk;
-  double acc0[JT], acc1[JT];
+  double acc[NF][R];
 #pragma unroll
-  for (int u = 0; u < JT; ++u) acc0[u] = acc1[u] = 0.0;
-  // taps in the reference order: rows (dj asc, dk asc), di asc inside a row
-  for (int rr = 0; rr < nrows; ++rr) {
-    const TapRow R = sr[rr];
-    const double* w = sw + R.woff;
-    const int n = 2 * R.a + 1;
+  for (int f = 0; f < NF; ++f)
 #pragma unroll
-    for (int u = 0; u < JT; ++u) {
-      const int tj = threadIdx.z * JT + u;
-      const double* p0 = st + ((long long)(tj + r + R.dj) * PK + (tk + rk + R.dk)) * PI + (ti + r - R.a);
-      double s0 = acc0[u], s1 = acc1[u];
-      for (int q = 0; q < n; ++q) {
-        s0 = fma(w[q], p0[q], s0);
-        if (NF == 2) s1 = fma(w[q], p0[tileN + q], s1);
+    for (int r = 0; r < R; ++r) acc[f][r] = 0.0;
+
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const double* in = f == 0 ? A.in0 : A.in1;
+    if (f > 0) __syncthreads();
+    // tile load: one warp per (other, run) line, lanes along i (coalesced)
+    const int nlines = T.EO * T.ER;
+    for (int line = warp; line < nlines; line += kThreads / 32) {
+      const int to = line / T.ER, tr = line - to * T.ER;
+      const int jo = mapO[to], jr = mapR[tr];
+      long long rowbase = -1;
+      if (jo >= 0 && jr >= 0)  // a stored column is guaranteed by the slab setup
+        rowbase = G.is3d ? ((long long)(jo - G.sj0) * G.nz + jr) * G.nely
+                         : (long long)(jr - G.sj0) * G.nely;
+      double* dst = tile + line * sEI;
+      for (int ti = lane; ti < T.EI; ti += 32) {
+        const int ii = mapI[ti];
+        double v = 0.0;
+        if (rowbase >= 0 && ii >= 0) {
+          const long long src = rowbase + ii;
+          v = in ? in[src] : 1.0;  // null input: the all-ones field (hs)
+          if (MODE == CONV_ADJ_DIV) v = v / A.hs_st[src];
+        }
+        dst[ti] = v;
       }
-      acc0[u] = s0;
-      acc1[u] = s1;
     }
+    __syncthreads();
+    conv_columns<4, R>(tile, sb, sEI, sPlane, cols, 0, T.ncol[0], wts, acc[f]);
+    conv_columns<2, R>(tile, sb, sEI, sPlane, cols, T.ncol[0], T.ncol[0] + T.ncol[1], wts, acc[f]);
+    conv_columns<1, R>(tile, sb, sEI, sPlane, cols, T.ncol[0] + T.ncol[1], ncols, wts, acc[f]);
   }
 
   // epilogue
   double red[3] = {0.0, 0.0, 0.0};
+  EtaConsts ec;
+  if (MODE == CONV_FWD_ETA) ec = eta_consts(A.beta, A.eta0);
+  const int gi = bi + wi * 32 + lane, go = bo + wo;
 #pragma unroll
-  for (int u = 0; u < JT; ++u) {
-    const int gj = bj + threadIdx.z * JT + u;
-    if (gi >= G.nely || gk >= G.nz || gj >= G.j0 + G.jn) continue;
-    const long long e = ((long long)(gj - G.j0) * G.nz + gk) * G.nely + gi;
+  for (int r = 0; r < R; ++r) {
+    const int grun = br + wr * R + r;
+    if (gi >= G.nely || grun >= T.run_n || go >= T.other_n) continue;
+    const long long e = ((long long)go * T.run_n + grun) * G.nely + gi;
     if (MODE == CONV_PLAIN || MODE == CONV_ADJ_DIV) {
-      A.out0[e] = acc0[u];
+      A.out0[e] = acc[0][r];
     } else if (MODE == CONV_FWD || MODE == CONV_FWD_ETA) {
-      double v = acc0[u] / A.hs[e];  // filter.hpp:121 cwiseQuotient(hs)
+      double v = acc[0][r] / A.hs[e];  // filter.hpp:121 cwiseQuotient(hs)
       const int s = elem_state(A.state, e);
       if (A.pin && s == 1) v = 1.0;  // driver.hpp:130-133
       if (A.pin && s == 2) v = 0.0;
       A.out0[e] = v;
       if (MODE == CONV_FWD_ETA && s == 0) {
-        const EtaConsts c = eta_consts(A.beta, A.eta0);
         double g, gp;
-        eta_terms(c, A.beta, A.eta0, v, g, gp);
+        eta_terms(ec, A.beta, A.eta0, v, g, gp);
         red[0] += g;
         red[1] += gp;
       }
     } else if (MODE == CONV_ADJ2_OC) {
-      const double dc = acc0[u], dV = acc1[u];
+      const double dc = acc[0][r], dV = acc[NF - 1][r];
       if (A.out0) A.out0[e] = dc;
       if (A.out1) A.out1[e] = dV;
       const bool act = elem_state(A.state, e) == 0;
-      const double4 rec = oc_record(A.x[e], dc, dV, A.cw[e], A.move, act);
+      const double4 rec = oc_record(A.x[e], dc, dV, A.cw ? A.cw[e] : 1.0, A.move, act);
       A.ocrec[e] = rec;
       if (act) red[0] += rec.z;
       red[1] += rec.w * oc_cand(rec, 0.0);
@@ -433,7 +507,7 @@ __device__ __forceinline__ double simp_xp(double x, double p) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads) k_elem_sens(Geo G, KeFull<D> K, ElemArgs A) {
+__global__ void __launch_bounds__(kThreads, 3) k_elem_sens(Geo G, KeFull<D> K, ElemArgs A) {
   __shared__ double scratch[32];
   const double eta = A.input_is_phys ? 0.5 : *A.eta_ptr;
   const double a = tanh(A.beta * eta);
@@ -461,14 +535,16 @@ __global__ void __launch_bounds__(kThreads) k_elem_sens(Geo G, KeFull<D> K, Elem
     double ue[D];
 #pragma unroll
     for (int q = 0; q < D; ++q) ue[q] = __ldg(A.U + dofs[q]);
-    double quad = 0.0;  // ue . (Ke ue), fea.hpp:267
+    // quad = ue . (Ke ue) (fea.hpp:267), evaluated on the symmetric upper half
+    double quad = 0.0;
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-      double s = 0.0;
+      double s = 0.5 * K.k[r * D + r] * ue[r];
 #pragma unroll
-      for (int c = 0; c < D; ++c) s = fma(K.k[c * D + r], ue[c], s);
+      for (int c = r + 1; c < D; ++c) s = fma(K.k[c * D + r], ue[c], s);
       quad = fma(ue[r], s, quad);
     }
+    quad = 2.0 * quad;
     csum = fma(sK, quad, csum);
     const int st = elem_state(A.state, e);
     const double dcp = st == 0 ? -dsK * quad : 0.0;
@@ -501,13 +577,25 @@ struct SkArgs {
   double* sK;
 };
 
-template <int P, int EB>
+// 256-bit streaming store (STG.E.EF.ENL2.256 on sm_100a): evict-first, the
+// values are consumed by the solver, not by this pass.
+__device__ __forceinline__ void st256_cs(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d)
+               : "memory");
+}
+
+// One warp owns 32 consecutive elements: lane l computes the modulus of
+// element l (one tanh + SIMP), then the warp streams the group's 32*P values
+// as 32-byte vectors (fully coalesced, no block barriers), taking each value's
+// modulus from its owner lane by shuffle and Ke_lower from shared memory.
+template <int P>
 __global__ void __launch_bounds__(kThreads) k_sk_store(Geo G, SkArgs A) {
-  constexpr int PV = P / 2;  // double2 per element
-  __shared__ double2 kl[PV];
-  __shared__ double se[EB];
+  constexpr int PV = P / 4;  // double4 per element
+  __shared__ double4 kl[PV];
   for (int q = threadIdx.x; q < PV; q += blockDim.x)
-    kl[q] = make_double2(A.ke_lower[2 * q], A.ke_lower[2 * q + 1]);
+    kl[q] = make_double4(A.ke_lower[4 * q], A.ke_lower[4 * q + 1], A.ke_lower[4 * q + 2],
+                         A.ke_lower[4 * q + 3]);
   double a = 0, denom = 1, de = 0, eta = 0;
   if (A.xt) {
     eta = *A.eta_ptr;
@@ -515,30 +603,35 @@ __global__ void __launch_bounds__(kThreads) k_sk_store(Geo G, SkArgs A) {
     denom = a + tanh(A.beta * (1.0 - eta));
     de = A.e0 - A.emin;
   }
-  const long long nchunks = (G.m + EB - 1) / EB;
-  for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
-    const long long e0 = c * EB;
-    const int ne = int(min((long long)EB, G.m - e0));
-    __syncthreads();
-    for (int t = threadIdx.x; t < ne; t += blockDim.x) {
-      double s;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const long long ngroups = (G.m + 31) >> 5;
+  for (long long g = warp0; g < ngroups; g += nwarps) {
+    const long long e0 = g << 5;
+    const int ne = int(min(32LL, G.m - e0));
+    double s = 0.0;
+    if (lane < ne) {
       if (A.xt) {
-        const double xphys = (a + tanh(A.beta * (A.xt[e0 + t] - eta))) / denom;
+        const double xphys = (a + tanh(A.beta * (A.xt[e0 + lane] - eta))) / denom;  // :142
         const double xp = simp_xp(xphys, A.penal);
-        s = A.emin + xp * xphys * de;
+        s = A.emin + xp * xphys * de;  // fea.hpp:142
       } else {
-        s = A.sKe[e0 + t];
+        s = A.sKe[e0 + lane];
       }
-      se[t] = s;
     }
-    __syncthreads();
-    double2* out = reinterpret_cast<double2*>(A.sK + e0 * P);
+    double* out = A.sK + e0 * P;
     const int nv = ne * PV;
-    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-      const int el = v / PV, q = v - el * PV;
-      const double s = se[el];
-      const double2 k = kl[q];
-      __stcs(out + v, make_double2(s * k.x, s * k.y));
+#pragma unroll 4
+    for (int base = 0; base < nv; base += 32) {
+      const int v = base + lane;
+      const int el = min(v / PV, 31);
+      const double se = __shfl_sync(0xffffffffu, s, el);
+      if (v < nv) {
+        const double4 k = kl[v - el * PV];
+        st256_cs(out + 4 * (long long)v, se * k.x, se * k.y, se * k.z, se * k.w);  // fea.hpp:168
+      }
     }
   }
 }
