@@ -214,16 +214,21 @@ ConvGeom conv_geom(const topo_ctx* c, const Geo& G, int WI, int WR, int WO) {
   T.reach = c->reach;
   T.reach_o = G.is3d ? c->reach : 0;
   T.EI = T.TI + 2 * T.reach;
-  T.ER = T.TR + 2 * T.reach + R;
+  // last run offset read: TR + 2 reach + R - 2 (zero-padded chunks); odd for
+  // a conflict-free lane stride
+  T.ER = (T.TR + 2 * T.reach + R - 1) | 1;
   T.EO = T.TO + 2 * T.reach_o;
   T.run_n = G.is3d ? G.nz : G.jn;
   T.other_n = G.is3d ? G.jn : 1;
   for (int q = 0; q < 3; ++q) T.ncol[q] = c->ncol[q];
+  T.magicEI = unsigned((1ull << 32) / unsigned(T.EI) + 1);
   return T;
 }
 
 size_t conv_smem(const ConvGeom& T) {
-  return sizeof(double) * size_t(T.EI) * T.ER * T.EO + sizeof(int) * size_t(T.EI + T.ER + T.EO);
+  const size_t lines = size_t(T.ER) * T.EO;
+  return sizeof(double) * size_t(T.EI) * T.ER * T.EO + (sizeof(long long) + sizeof(int)) * lines +
+         sizeof(int) * size_t(T.EI) + 16;
 }
 
 // 8 warps per block; pick the warp split that loads the fewest tile values per
@@ -236,7 +241,7 @@ ConvGeom pick_geom(const topo_ctx* c, const Geo& G) {
   for (int q = 0; q < 4; ++q) {
     const int* o = G.is3d ? opts3[q] : opts2[q];
     ConvGeom T = conv_geom(c, G, o[0], o[1], o[2]);
-    if (conv_smem(T) > 200 * 1024) continue;
+    if (conv_smem(T) > 200 * 1024 || double(T.EI) * T.ER * T.EO >= (1 << 20)) continue;
     const double outs = double(T.TI) * T.TR * T.TO;
     const double fi = std::ceil(double(G.nely) / T.TI) * T.TI / G.nely;
     const double fr = std::ceil(double(T.run_n) / T.TR) * T.TR / T.run_n;
@@ -302,6 +307,14 @@ topo_status launch_sk(topo_ctx* ctx, const SkArgs& S, cudaStream_t st) {
 
 // ------------------------------------------------------- reductions / comm
 // sums `count` partial records (stride N) into ctx->h_result[0..N) (global)
+// fixed-order block reduction of `count` partial records into dst[0..N)
+template <int N>
+topo_status reduce_on_device(topo_ctx* ctx, const double* partials, int count, double* dst) {
+  k_reduce_block<N><<<1, 1024, 0, ctx->stream>>>(partials, count, N, dst);
+  LAUNCHED();
+  return TOPO_OK;
+}
+
 template <int N>
 topo_status reduce_to_host(topo_ctx* ctx, const double* partials, int count) {
   k_reduce_partials<N><<<1, 32, 0, ctx->stream>>>(partials, count, N, ctx->result.as<double>());
@@ -332,6 +345,12 @@ topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
   A.mtotal = ctx->m_total;
   A.partials0 = partials0;
   A.n0 = n0;
+  if (partials0 && !ctx->comm) {  // one fixed-order pre-reduction instead of one per block
+    double* pre = ctx->result.as<double>() + 24;
+    TRY(reduce_on_device<3>(ctx, partials0, n0, pre));
+    A.partials0 = pre;
+    A.n0 = 1;
+  }
   A.partials = ctx->partials.as<double>();
   A.result = eta_dev_out;
   if (!ctx->comm) return coop_launch(ctx, (const void*)k_eta_solve, &A, ctx->coop_eta);
@@ -372,8 +391,10 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
     OcArgs A;
     A.m = G.m;
     A.rec = ctx->rec.as<double4>();
-    A.prep_partials = prep;
-    A.n_prep = n_prep;
+    double* pre = ctx->result.as<double>() + 32;
+    TRY(reduce_on_device<3>(ctx, prep, n_prep, pre));
+    A.prep_partials = pre;
+    A.n_prep = 1;
     A.volfrac = prm->volfrac;
     A.rel_tol = prm->bisect_rel_tol;
     A.vol_tol = prm->volume_tol;
@@ -387,6 +408,8 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
     A.xNew = xnew_dev;
     A.result = ctx->result.as<double>() + 8;
     TRY(coop_launch(ctx, (const void*)k_oc_bisect, &A, ctx->coop_blocks));
+    k_oc_final<<<grid_for(ctx, G.m), kThreads, 0, ctx->stream>>>(G.m, A.rec, A.result, xnew_dev);
+    LAUNCHED();
     CK(cudaMemcpyAsync(ctx->h_result + 8, A.result, sizeof(double) * 7, cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));

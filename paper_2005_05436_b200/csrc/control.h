@@ -195,44 +195,75 @@ struct OcCtl {
   }
 };
 
-/// Speculative request set: every s the controller may request within the
-/// next `depth` feeds, on either side of each decision (v > volfrac or not).
-/// Values are produced by the controller's own arithmetic, so they compare
-/// bit-equal with the requests made during the replay.
+/// Speculative request set: every multiplier the controller can request in
+/// the next few feeds, generated with the controller's own arithmetic (so
+/// the values compare bit-equal with the replayed requests):
+///   widening: sqrt(lamMax * 4^k) for the next 4 widenings, then 0 (vLo),
+///             then the first 3 bisection levels under hi = sqrt(lamMax);
+///   vLo:      0, then 4 bisection levels;
+///   bisection (sqrt or lambda space): the full tree of the next 4 levels.
 template <int KMAX>
-__host__ __device__ inline int oc_speculate(const OcCtl& start, int depth, double* out) {
-  OcCtl stack[8];
-  int dstack[8];
-  int sp = 0, n = 0;
-  stack[sp] = start;
-  stack[sp].check_mono = 0;
-  dstack[sp++] = depth;
-  while (sp > 0) {
-    --sp;
-    OcCtl c = stack[sp];
-    const int d = dstack[sp];
-    if (!c.pending() || d == 0) continue;
-    bool seen = false;
-    for (int q = 0; q < n; ++q) seen |= (out[q] == c.s_req);
-    if (!seen) {
-      if (n >= KMAX) return n;
-      out[n++] = c.s_req;
-    }
-    const bool br = c.branching();
-    OcCtl a = c;
-    a.feed(c.volfrac + 1.0);  // decisively above: v > volfrac, |v - volfrac| large
-    if (sp < 8) {
-      stack[sp] = a;
-      dstack[sp++] = d - 1;
-    }
-    if (br) {
-      OcCtl b = c;
-      b.feed(c.volfrac - 1.0);
-      if (sp < 8) {
-        stack[sp] = b;
-        dstack[sp++] = d - 1;
+__host__ __device__ inline int oc_speculate(const OcCtl& c, double* out) {
+  int n = 0;
+  auto push = [&](double v) {
+    for (int q = 0; q < n; ++q)
+      if (out[q] == v) return;
+    if (n < KMAX) out[n++] = v;
+  };
+  // breadth-first midpoints of [lo, hi] (sqrt space, or lambda space -> sqrt)
+  auto tree = [&](double lo, double hi, int depth, bool lambda_space) {
+    double los[16], his[16];
+    int cnt = 1;
+    los[0] = lo;
+    his[0] = hi;
+    for (int d = 0; d < depth; ++d) {
+      double nlo[16], nhi[16];
+      int nn = 0;
+      for (int q = 0; q < cnt; ++q) {
+        const double mid = 0.5 * (los[q] + his[q]);
+        push(lambda_space ? sqrt(mid) : mid);
+        if (nn + 2 <= 16) {
+          nlo[nn] = los[q];
+          nhi[nn++] = mid;
+          nlo[nn] = mid;
+          nhi[nn++] = his[q];
+        }
       }
+      for (int q = 0; q < nn; ++q) {
+        los[q] = nlo[q];
+        his[q] = nhi[q];
+      }
+      cnt = nn;
     }
+  };
+  if (c.pending()) push(c.s_req);  // the pending request first
+  switch (c.phase) {
+    case OcCtl::P_WIDEN0:
+    case OcCtl::P_WIDEN: {
+      double lm = c.lamMax;
+      push(sqrt(lm));
+      for (int k = 0; k < 3; ++k) {
+        lm *= 4.0;
+        push(sqrt(lm));
+      }
+      push(0.0);
+      if (!c.lambdaSpace) tree(0.0, sqrt(c.lamMax), 3, false);
+      else tree(0.0, c.lamMax, 3, true);
+      break;
+    }
+    case OcCtl::P_VLO:
+      push(0.0);
+      if (!c.lambdaSpace) tree(0.0, sqrt(c.lamMax), 4, false);
+      else tree(0.0, c.lamMax, 4, true);
+      break;
+    case OcCtl::P_BIS:
+      tree(c.lo, c.hi, 4, false);
+      break;
+    case OcCtl::P_LSBIS:
+      tree(c.lo, c.hi, 4, true);
+      break;
+    default:
+      break;
   }
   return n;
 }

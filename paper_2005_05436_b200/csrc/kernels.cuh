@@ -198,10 +198,11 @@ __device__ __forceinline__ double oc_cand(const double4& r, double s) {
 struct ConvGeom {
   int WI, WR, WO;      // warps along i / run / other
   int TI, TR, TO;      // outputs per tile along i / run / other
-  int EI, ER, EO;      // shared-memory tile extents
+  int EI, ER, EO;      // shared-memory tile extents; ER is odd (run axis contiguous)
   int reach, reach_o;  // halo along i and run / along other (0 in 2D)
   int run_n, other_n;  // owned extents of the run / other axes
   int ncol[3];         // canonical columns with 4, 2, 1 mirrors (stored in that order)
+  unsigned magicEI;    // floor(2^32 / EI) + 1: q / EI == umulhi(q, magicEI) for q < 2^20
 };
 
 struct ConvCol {  // one canonical column of the cone stencil
@@ -209,21 +210,25 @@ struct ConvCol {  // one canonical column of the cone stencil
 };
 
 // accumulate the columns [c0, c1), each with NM mirrors, into acc
+// Shared-memory layout [other][i][run] with the run axis contiguous: the
+// values of a column are consecutive words (immediate-offset LDS), and lanes
+// (consecutive i) are ER words apart, ER odd, so 64-bit accesses are
+// bank-conflict free.
 template <int NM, int R>
-__device__ __forceinline__ void conv_columns(const double* __restrict__ tile, int sb, int sEI,
+__device__ __forceinline__ void conv_columns(const double* __restrict__ tile, int sb, int sI,
                                              int sPlane, const ConvCol* __restrict__ cols, int c0,
                                              int c1, const double* __restrict__ wts,
                                              double (&acc)[R]) {
   for (int c = c0; c < c1; ++c) {
     const ConvCol col = cols[c];
-    const int base = sb - col.a * sEI;
-    const int oi = col.di, oo = col.dother * sPlane;
+    const int base = sb - col.a;
+    const int oi = col.di * sI, oo = col.dother * sPlane;
     const double* p0 = tile + base + oi + oo;
     const double* p1 = tile + base - oi - oo;  // NM == 2: the one nonzero offset flipped
     const double* p2 = tile + base - oi + oo;  // NM == 4
     const double* p3 = tile + base + oi - oo;
     auto colval = [&](int s) {
-      const int o = s * sEI;
+      const int o = s;
       double v = p0[o];
       if (NM == 2) v += p1[o];
       if (NM == 4) v = (v + p1[o]) + (p2[o] + p3[o]);
@@ -259,27 +264,42 @@ __global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const Conv
                                                    int ncols, const double* __restrict__ wts,
                                                    ConvArgs A) {
   extern __shared__ double tile[];
-  // folded source coordinates of the tile's i / run / other lines (-1: zero pad)
-  int* mapI = reinterpret_cast<int*>(tile + T.EI * T.ER * T.EO);
-  int* mapR = mapI + T.EI;
-  int* mapO = mapR + T.ER;
+  const int tileN = T.EI * T.ER * T.EO, nlines = T.EO * T.ER;
+  // per tile line (other, run): source offset of its i = 0 element (-1: zero
+  // pad) and its first smem word; per i: folded source i (-1: zero pad)
+  long long* lineSrc = reinterpret_cast<long long*>(tile + tileN);
+  int* lineDst = reinterpret_cast<int*>(lineSrc + nlines);
+  int* mapI = lineDst + nlines;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int wi = warp % T.WI, wr = (warp / T.WI) % T.WR, wo = warp / (T.WI * T.WR);
   const int bi = blockIdx.x * T.TI, br = blockIdx.y * T.TR, bo = blockIdx.z * T.TO;
-  const int sEI = T.EI, sPlane = T.EI * T.ER;
+  const int sI = T.ER, sPlane = T.EI * T.ER;
   // thread base: its first output (r = 0) in tile coordinates
-  const int sb = (wo + T.reach_o) * sPlane + (wr * R + T.reach) * sEI + (wi * 32 + lane + T.reach);
+  const int sb = (wo + T.reach_o) * sPlane + (wi * 32 + lane + T.reach) * sI + (wr * R + T.reach);
 
   auto fold = [&](int t, int n) {  // mirror (Neumann) or -1 outside (Dirichlet)
     if (t >= 0 && t < n) return t;
     return G.bc == 0 ? reflect_index(t, n) : -1;
   };
   for (int q = tid; q < T.EI; q += blockDim.x) mapI[q] = fold(bi + q - T.reach, G.nely);
-  for (int q = tid; q < T.ER; q += blockDim.x)
-    mapR[q] = G.is3d ? fold(br + q - T.reach, G.nz) : fold(G.j0 + br + q - T.reach, G.nelx);
-  for (int q = tid; q < T.EO; q += blockDim.x)
-    mapO[q] = G.is3d ? fold(G.j0 + bo + q - T.reach_o, G.nelx) : 0;
+  for (int line = tid; line < nlines; line += blockDim.x) {
+    const int to = line / T.ER, tr = line - to * T.ER;
+    int jo, jr;
+    if (G.is3d) {
+      jo = fold(G.j0 + bo + to - T.reach_o, G.nelx);
+      jr = fold(br + tr - T.reach, G.nz);
+    } else {
+      jo = 0;
+      jr = fold(G.j0 + br + tr - T.reach, G.nelx);
+    }
+    long long src = -1;
+    if (jo >= 0 && jr >= 0)  // a stored column is guaranteed by the slab setup
+      src = G.is3d ? ((long long)(jo - G.sj0) * G.nz + jr) * G.nely
+                   : (long long)(jr - G.sj0) * G.nely;
+    lineSrc[line] = src;
+    lineDst[line] = to * sPlane + tr;
+  }
   __syncthreads();
 
   double acc[NF][R];
@@ -290,33 +310,27 @@ __global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const Conv
 
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
-    const double* in = f == 0 ? A.in0 : A.in1;
+    const double* __restrict__ in = f == 0 ? A.in0 : A.in1;
     if (f > 0) __syncthreads();
-    // tile load: one warp per (other, run) line, lanes along i (coalesced)
-    const int nlines = T.EO * T.ER;
-    for (int line = warp; line < nlines; line += kThreads / 32) {
-      const int to = line / T.ER, tr = line - to * T.ER;
-      const int jo = mapO[to], jr = mapR[tr];
-      long long rowbase = -1;
-      if (jo >= 0 && jr >= 0)  // a stored column is guaranteed by the slab setup
-        rowbase = G.is3d ? ((long long)(jo - G.sj0) * G.nz + jr) * G.nely
-                         : (long long)(jr - G.sj0) * G.nely;
-      double* dst = tile + line * sEI;
-      for (int ti = lane; ti < T.EI; ti += 32) {
-        const int ii = mapI[ti];
-        double v = 0.0;
-        if (rowbase >= 0 && ii >= 0) {
-          const long long src = rowbase + ii;
-          v = in ? in[src] : 1.0;  // null input: the all-ones field (hs)
-          if (MODE == CONV_ADJ_DIV) v = v / A.hs_st[src];
-        }
-        dst[ti] = v;
+    // tile load, flat over (line, i): coalesced along i; line = q / EI by a
+    // multiply-high with the host-computed magic (exact for q < 2^20)
+    for (int q = tid; q < tileN; q += kThreads) {
+      const int line = int(__umulhi(unsigned(q), T.magicEI));
+      const int ti = q - line * T.EI;
+      const long long rb = lineSrc[line];
+      const int ii = mapI[ti];
+      double v = 0.0;
+      if (rb >= 0 && ii >= 0) {
+        const long long src = rb + ii;
+        v = in ? __ldg(in + src) : 1.0;  // null input: the all-ones field (hs)
+        if (MODE == CONV_ADJ_DIV) v = v / __ldg(A.hs_st + src);
       }
+      tile[lineDst[line] + ti * sI] = v;
     }
     __syncthreads();
-    conv_columns<4, R>(tile, sb, sEI, sPlane, cols, 0, T.ncol[0], wts, acc[f]);
-    conv_columns<2, R>(tile, sb, sEI, sPlane, cols, T.ncol[0], T.ncol[0] + T.ncol[1], wts, acc[f]);
-    conv_columns<1, R>(tile, sb, sEI, sPlane, cols, T.ncol[0] + T.ncol[1], ncols, wts, acc[f]);
+    conv_columns<4, R>(tile, sb, sI, sPlane, cols, 0, T.ncol[0], wts, acc[f]);
+    conv_columns<2, R>(tile, sb, sI, sPlane, cols, T.ncol[0], T.ncol[0] + T.ncol[1], wts, acc[f]);
+    conv_columns<1, R>(tile, sb, sI, sPlane, cols, T.ncol[0] + T.ncol[1], ncols, wts, acc[f]);
   }
 
   // epilogue
@@ -723,7 +737,6 @@ __global__ void __launch_bounds__(kThreads) k_oc_prep(long long m, const double*
 // ============================================================================
 
 constexpr int kOcK = 16;
-constexpr int kOcDepth = 4;
 
 struct OcArgs {
   long long m;
@@ -776,7 +789,7 @@ __global__ void __launch_bounds__(kThreads) k_oc_bisect(OcArgs A) {
         ctl.check_mono = 0;
         while (ctl.pending()) ctl.feed(mode > 0 ? INFINITY : -INFINITY);
       } else if (ctl.pending()) {
-        nreq = oc_speculate<kOcK>(ctl, kOcDepth, sreq);
+        nreq = oc_speculate<kOcK>(ctl, sreq);
       }
     }
     __syncthreads();
@@ -797,13 +810,16 @@ __global__ void __launch_bounds__(kThreads) k_oc_bisect(OcArgs A) {
     if (threadIdx.x == 0)
       for (int q = 0; q < K; ++q) P[(long long)q * gridDim.x + blockIdx.x] = acc[q];
     grid.sync();
-    // every block reduces the same partials in the same order
-    for (int q = 0; q < K; ++q) {
-      if (threadIdx.x < 32) {
-        double s[1];
-        warp_sum_partials<1>(P + (long long)q * gridDim.x, gridDim.x, 1, s);
-        if (threadIdx.x == 0) sval[q] = (A.add_const + s[0]) / A.mtotal;
-      }
+    // every block reduces the same partials in the same fixed order: 16
+    // threads per request, all requests in parallel
+    {
+      const int q = threadIdx.x >> 4, sub = threadIdx.x & 15;
+      double sum = 0.0;
+      if (q < K)
+        for (int i = sub; i < (int)gridDim.x; i += 16) sum += __ldcg(P + (long long)q * gridDim.x + i);
+#pragma unroll
+      for (int off = 8; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+      if (sub == 0 && q < K) sval[q] = (A.add_const + sum) / A.mtotal;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -819,12 +835,7 @@ __global__ void __launch_bounds__(kThreads) k_oc_bisect(OcArgs A) {
     buf ^= 1;
     __syncthreads();
   }
-  // K6: xNew at the final multiplier (oc.hpp:108, :171)
-  const double sf = ctl.s_final;
-  if (ctl.status == OcCtl::ST_OK)
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < A.m;
-         e += (long long)gridDim.x * blockDim.x)
-      A.xNew[e] = oc_cand(A.rec[e], sf);
+  // K6 (xNew at the final multiplier) runs as k_oc_final with full occupancy
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.result[0] = ctl.lam_result;
     A.result[1] = ctl.bis;
@@ -834,6 +845,18 @@ __global__ void __launch_bounds__(kThreads) k_oc_bisect(OcArgs A) {
     A.result[5] = mode;
     A.result[6] = ctl.s_final;
   }
+}
+
+// K6: xNew at the final multiplier s = result[6] (oc.hpp:108, :171), skipped
+// when the bisection reported an error (result[3])
+__global__ void __launch_bounds__(kThreads) k_oc_final(long long m, const double4* __restrict__ rec,
+                                                       const double* __restrict__ result,
+                                                       double* __restrict__ out) {
+  if (result[3] != 0.0) return;
+  const double s = result[6];
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = oc_cand(rec[e], s);
 }
 
 // candidate at one multiplier (host-driven OC modes and final write)
@@ -870,6 +893,23 @@ __global__ void k_reduce_partials(const double* __restrict__ p, int count, int s
   warp_sum_partials<N>(p, count, stride, s);
   if (threadIdx.x == 0)
     for (int q = 0; q < N; ++q) out[q] = s[q];
+}
+
+// fixed-order reduction of `count` partial records with one block (any size)
+template <int N>
+__global__ void k_reduce_block(const double* __restrict__ p, int count, int stride,
+                               double* __restrict__ out) {
+  __shared__ double scratch[N * 32];
+  double v[N];
+#pragma unroll
+  for (int q = 0; q < N; ++q) v[q] = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < N; ++q) v[q] += p[(long long)i * stride + q];
+  block_sum<N>(v, scratch);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int q = 0; q < N; ++q) out[q] = v[q];
 }
 
 // oc.hpp:31-39 / :72-79 on compact arrays
