@@ -84,12 +84,14 @@ struct topo_ctx {
   double nS_total = 0;  // |P1| over all ranks
   double m_total = 0;   // global element count
   // fields
+  DevBuf e1;  // exp(2 beta xTilde) for the eta passes
   DevBuf hs, hs_st, cw, x_st, xt, xphys, dcphys, dc, dV, xnew, a1_st, a2_st, rec, u, tmp0, tmp1,
       tmp_st;
   DevBuf sK, iK, jK;
   DevBuf partials, partials0, result;
   double* h_result = nullptr;  // pinned
-  int conv_R = 4;              // outputs per thread along the run axis (4 in 3D, 8 in 2D)
+  int conv_R = 8;              // outputs per thread along the run axis
+  int conv_A = 0;              // > 0: small-reach direct variant with half-width bound A
   bool overlap_sk = false;     // run the sK store concurrently with K3a..K6
   int coop_blocks = 148;  // OC bisection grid (cooperative)
   int coop_eta = 148;     // eta Newton grid (cooperative)
@@ -216,7 +218,7 @@ ConvGeom conv_geom(const topo_ctx* c, const Geo& G, int WI, int WR, int WO) {
   T.EI = T.TI + 2 * T.reach;
   // last run offset read: TR + 2 reach + R - 2 (zero-padded chunks); odd for
   // a conflict-free lane stride
-  T.ER = (T.TR + 2 * T.reach + R - 1) | 1;
+  T.ER = (T.TR + 2 * T.reach + (c->conv_A > 0 ? 0 : R - 1)) | 1;
   T.EO = T.TO + 2 * T.reach_o;
   T.run_n = G.is3d ? G.nz : G.jn;
   T.other_n = G.is3d ? G.jn : 1;
@@ -255,7 +257,7 @@ ConvGeom pick_geom(const topo_ctx* c, const Geo& G) {
   return best;
 }
 
-template <int NF, int MODE, int R>
+template <int NF, int MODE, int R, int AW>
 topo_status launch_conv_t(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* nblocks) {
   const ConvGeom T = pick_geom(ctx, G);
   if (T.TI == 0) return fail(ctx, TOPO_EINVAL, "filter: rmin too large for the shared-memory tile");
@@ -267,12 +269,12 @@ topo_status launch_conv_t(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* n
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     cudaFuncAttributes fa;
-    CK(cudaFuncGetAttributes(&fa, k_conv<NF, MODE, R>));
-    CK(cudaFuncSetAttribute(k_conv<NF, MODE, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncGetAttributes(&fa, k_conv<NF, MODE, R, AW>));
+    CK(cudaFuncSetAttribute(k_conv<NF, MODE, R, AW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             optin - int(fa.sharedSizeBytes)));
     attr_done = true;
   }
-  k_conv<NF, MODE, R><<<grid, kThreads, smem, ctx->stream>>>(
+  k_conv<NF, MODE, R, AW><<<grid, kThreads, smem, ctx->stream>>>(
       G, T, ctx->d_cols.as<ConvCol>(), int(ctx->cols.size()), ctx->d_wpad.as<double>(), A);
   LAUNCHED();
   if (nblocks) *nblocks = int(grid.x * grid.y * grid.z);
@@ -281,8 +283,13 @@ topo_status launch_conv_t(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* n
 
 template <int NF, int MODE>
 topo_status launch_conv(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* nblocks = nullptr) {
-  if (ctx->conv_R == 8) return launch_conv_t<NF, MODE, 8>(ctx, G, A, nblocks);
-  return launch_conv_t<NF, MODE, 4>(ctx, G, A, nblocks);
+  switch (ctx->conv_A) {
+    case 1: return launch_conv_t<NF, MODE, 8, 1>(ctx, G, A, nblocks);
+    case 2: return launch_conv_t<NF, MODE, 8, 2>(ctx, G, A, nblocks);
+    case 3: return launch_conv_t<NF, MODE, 8, 3>(ctx, G, A, nblocks);
+    case 4: return launch_conv_t<NF, MODE, 8, 4>(ctx, G, A, nblocks);
+    default: return launch_conv_t<NF, MODE, 8, 0>(ctx, G, A, nblocks);
+  }
 }
 
 int conv_blocks(const topo_ctx* ctx) {
@@ -335,7 +342,7 @@ topo_status coop_launch(topo_ctx* ctx, const void* fn, void* args, int blocks) {
 
 // ------------------------------------------------------------------ eta
 topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
-                    const double* partials0, int n0, double* eta_dev_out) {
+                    double* eta_dev_out) {
   EtaArgs A;
   A.G = ctx->G;
   A.xt = xt;
@@ -343,36 +350,20 @@ topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
   A.beta = beta;
   A.eta0 = eta0;
   A.mtotal = ctx->m_total;
-  A.partials0 = partials0;
-  A.n0 = n0;
-  if (partials0 && !ctx->comm) {  // one fixed-order pre-reduction instead of one per block
-    double* pre = ctx->result.as<double>() + 24;
-    TRY(reduce_on_device<3>(ctx, partials0, n0, pre));
-    A.partials0 = pre;
-    A.n0 = 1;
-  }
+  A.e1 = ctx->e1.as<double>();
   A.partials = ctx->partials.as<double>();
   A.result = eta_dev_out;
   if (!ctx->comm) return coop_launch(ctx, (const void*)k_eta_solve, &A, ctx->coop_eta);
   // multi-GPU: host-driven replay, one allreduce of (g, g') per evaluation
   EtaCtl ctl;
   ctl.init(eta0);
-  double g, gp;
-  if (partials0) {
-    TRY(reduce_to_host<3>(ctx, partials0, n0));
-  } else {
-    k_eta_partials<<<ctx->coop_eta, kThreads, 0, ctx->stream>>>(A, ctl.eta);
+  int first = 1;
+  for (;;) {
+    k_eta_partials<<<ctx->coop_eta, kThreads, 0, ctx->stream>>>(A, ctl.eta, first);
     LAUNCHED();
+    first = 0;
     TRY(reduce_to_host<2>(ctx, A.partials, ctx->coop_eta));
-  }
-  g = ctx->h_result[0];
-  gp = ctx->h_result[1];
-  while (ctl.feed(g / ctx->m_total, gp / ctx->m_total)) {
-    k_eta_partials<<<ctx->coop_eta, kThreads, 0, ctx->stream>>>(A, ctl.eta);
-    LAUNCHED();
-    TRY(reduce_to_host<2>(ctx, A.partials, ctx->coop_eta));
-    g = ctx->h_result[0];
-    gp = ctx->h_result[1];
+    if (!ctl.feed(ctx->h_result[0] / ctx->m_total, ctx->h_result[1] / ctx->m_total)) break;
   }
   const double res[3] = {ctl.eta, double(ctl.it), ctl.g};
   CK(cudaMemcpyAsync(eta_dev_out, res, sizeof res, cudaMemcpyHostToDevice, ctx->stream));
@@ -631,8 +622,9 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
     // the same taps as canonical columns along the run axis (k in 3D, j in
     // 2D) with di >= 0 and other >= 0, grouped by mirror count 4 / 2 / 1; the
     // weights are the reference's values, only the summation order differs
-    ctx->conv_R = is3d ? 4 : 8;
-    const int R = ctx->conv_R;
+    ctx->conv_R = 8;
+    ctx->conv_A = (is3d && reach >= 1 && reach <= 4) ? reach : 0;
+    const int R = ctx->conv_R, AW = ctx->conv_A;
     for (int group = 0; group < 3; ++group) {
       for (int o = 0; o <= dkMax; ++o)  // other axis: dj in 3D, none in 2D
         for (int di_ = 0; di_ <= reach; ++di_) {
@@ -643,8 +635,13 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
           int a = 0;
           while (a + 1 <= reach && wcol(a + 1) > 0) ++a;
           ConvCol col{di_, is3d ? o : 0, a, int(ctx->wpad.size())};
-          const int n = 2 * a + 1, npad = (n + R - 1) / R * R;
-          for (int t = 0; t < npad; ++t) ctx->wpad.push_back(t < n ? wcol(t - a) : 0.0);
+          if (AW > 0) {  // centred on [-AW, AW], zeros outside [-a, a], padded to 2 AW + 2
+            for (int t = -AW; t <= AW + 1; ++t)
+              ctx->wpad.push_back((t >= -a && t <= a) ? wcol(t) : 0.0);
+          } else {
+            const int n = 2 * a + 1, npad = (n + R - 1) / R * R;
+            for (int t = 0; t < npad; ++t) ctx->wpad.push_back(t < n ? wcol(t - a) : 0.0);
+          }
           ctx->cols.push_back(col);
           ++ctx->ncol[group];
         }
@@ -691,7 +688,7 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   CKC(cudaMemcpy(ctx->d_ke_lower.p, ctx->ke_lower.data(), sizeof(double) * size_t(G.P),
                  cudaMemcpyHostToDevice));
   for (DevBuf* b : {&ctx->hs, &ctx->cw, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
-                    &ctx->xnew, &ctx->tmp0, &ctx->tmp1})
+                    &ctx->xnew, &ctx->tmp0, &ctx->tmp1, &ctx->e1})
     CKC(b->ensure(md));
   for (DevBuf* b : {&ctx->hs_st, &ctx->a1_st, &ctx->a2_st, &ctx->tmp_st}) CKC(b->ensure(sd));
   CKC(ctx->rec.ensure(sizeof(double4) * size_t(G.m)));
@@ -746,7 +743,7 @@ void topo_ctx_destroy(topo_ctx* ctx) {
                     &ctx->cw, &ctx->x_st, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
                     &ctx->xnew, &ctx->a1_st, &ctx->a2_st, &ctx->rec, &ctx->u, &ctx->tmp0,
                     &ctx->tmp1, &ctx->tmp_st, &ctx->sK, &ctx->iK, &ctx->jK, &ctx->partials,
-                    &ctx->partials0, &ctx->result})
+                    &ctx->partials0, &ctx->result, &ctx->e1})
     b->release();
   if (ctx->h_result) cudaFreeHost(ctx->h_result);
   for (int q = 0; q < 2 * TOPO_NSTAGES; ++q)
@@ -943,11 +940,15 @@ static topo_status launch_elem(topo_ctx* ctx, const ElemArgs& A, int nb) {
   if (G.is3d) {
     KeFull<24> K;
     memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
-    k_elem_sens<24><<<nb, kThreads, 0, ctx->stream>>>(G, K, A);
+    static const int ne = getenv("TOPO_ELEM_NE") ? atoi(getenv("TOPO_ELEM_NE")) : 1;
+    if (ne == 2)
+      k_elem_sens<24, 2><<<nb, kThreads, 0, ctx->stream>>>(G, K, A);
+    else
+      k_elem_sens<24, 1><<<nb, kThreads, 0, ctx->stream>>>(G, K, A);
   } else {
     KeFull<8> K;
     memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
-    k_elem_sens<8><<<nb, kThreads, 0, ctx->stream>>>(G, K, A);
+    k_elem_sens<8, 1><<<nb, kThreads, 0, ctx->stream>>>(G, K, A);
   }
   LAUNCHED();
   return TOPO_OK;
@@ -1082,7 +1083,7 @@ topo_status topo_solve_eta(topo_ctx* ctx, const double* xTilde, double beta, dou
   if (!(beta > 0)) return fail(ctx, TOPO_EINVAL, "eta solve: beta must be positive");
   const double* x;
   TRY(stage_in(ctx, xTilde, ctx->G.m, ctx->tmp0, &x));
-  TRY(run_eta(ctx, x, beta, eta0, nullptr, 0, ctx->result.as<double>()));
+  TRY(run_eta(ctx, x, beta, eta0, ctx->result.as<double>()));
   CK(cudaMemcpyAsync(ctx->h_result, ctx->result.p, sizeof(double) * 3, cudaMemcpyDeviceToHost,
                      ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1213,20 +1214,12 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   A1.out0 = ctx->xt.as<double>();
   A1.state = state;
   A1.pin = 1;
-  A1.beta = prm->beta;
-  A1.eta0 = prm->eta0 < 0.0 ? 0.0 : (prm->eta0 > 1.0 ? 1.0 : prm->eta0);
-  A1.partials = ctx->partials0.as<double>();
-  int nb1 = 0;
-  if (solve)
-    TRY((launch_conv<1, CONV_FWD_ETA>(ctx, G, A1, &nb1)));
-  else
-    TRY((launch_conv<1, CONV_FWD>(ctx, G, A1, &nb1)));
+  TRY((launch_conv<1, CONV_FWD>(ctx, G, A1)));
   tmark(ctx, TOPO_STAGE_FILTER, 1, ctx->stream);
   // K2
   tmark(ctx, TOPO_STAGE_ETA, 0, ctx->stream);
   if (solve) {
-    TRY(run_eta(ctx, ctx->xt.as<double>(), prm->beta, prm->eta0, ctx->partials0.as<double>(),
-                nb1, res));
+    TRY(run_eta(ctx, ctx->xt.as<double>(), prm->beta, prm->eta0, res));
   } else {
     const double r[3] = {prm->eta_override, 0.0, 0.0};
     CK(cudaMemcpyAsync(res, r, sizeof r, cudaMemcpyHostToDevice, ctx->stream));

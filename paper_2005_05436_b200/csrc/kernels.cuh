@@ -124,7 +124,6 @@ __global__ void __launch_bounds__(kThreads) k_index_pairs(Geo G, int* __restrict
 enum ConvMode {
   CONV_PLAIN = 0,   // out = conv(in)                         (hs, adjoint of pre-divided input)
   CONV_FWD = 1,     // out = conv(in) / hs, optional pin      (apply_filter + pin_passives)
-  CONV_FWD_ETA = 2, // CONV_FWD + (g, g') partials at eta0    (K1 fused with the first eta pass)
   CONV_ADJ_DIV = 3, // out = conv(in / hs)                    (apply_filter_adjoint)
   CONV_ADJ2_OC = 4  // dc, dV = conv(a1), conv(a2) + OC record + (sum ocP, V(0), V(inf)) partials
 };
@@ -138,9 +137,7 @@ struct ConvArgs {
   double* out1;
   const uint8_t* state;
   int pin;
-  // CONV_FWD_ETA
-  double beta, eta0;
-  double* partials;  // per block
+  double* partials;  // per block (CONV_ADJ2_OC)
   // CONV_ADJ2_OC
   const double* x;   // design (owned)
   const double* cw;  // volume weights (owned)
@@ -148,28 +145,35 @@ struct ConvArgs {
   double4* ocrec;    // (lb, ub, ocP, cw) per element
 };
 
-// eta pass terms for one filtered value t (filter.hpp:187-201). The slope
-// uses the exact identities sech^2(u) = 1 - tanh^2(u) and
-// sinh(b t) sinh(b (1 - t)) = (cosh(b) - cosh(b (2 t - 1))) / 2, so one tanh
-// and one cosh serve both sums (rounding differs from the reference's
-// expression at the 1e-16 level; eta parity is judged by SURVEY.md §8(c)).
+// eta pass terms for one filtered value t (filter.hpp:187-201), evaluated
+// through E1 = exp(2 b t), computed once per element in the first pass:
+//   tanh(b (t - eta)) = (E - 1) / (E + 1),  E = E1 exp(-2 b eta)
+//   sech^2 = 1 - tanh^2
+//   sinh(b t) sinh(b (1 - t)) = cosh(b) / 2 - (E1 e^-b + e^b / E1) / 4
+// (exact identities; rounding differs from the reference's tanh / cosh /
+// sinh expression at the 1e-16 level, and eta parity is judged by the
+// conditioned protocol of SURVEY.md §8(c)).
 struct EtaConsts {
-  double a, denom, c0, coshb;  // tanh(b eta), a + tanh(b (1 - eta)), -b / sinh(b), cosh(b)
+  double a, den, c0, k, half_coshb, eb, emb;
 };
 __device__ __forceinline__ EtaConsts eta_consts(double beta, double eta) {
   EtaConsts c;
   c.a = tanh(beta * eta);
-  c.denom = c.a + tanh(beta * (1.0 - eta));
+  c.den = c.a + tanh(beta * (1.0 - eta));
   c.c0 = -beta / sinh(beta);
-  c.coshb = cosh(beta);
+  c.k = exp(-2.0 * beta * eta);
+  c.half_coshb = 0.5 * cosh(beta);
+  c.eb = exp(beta);
+  c.emb = exp(-beta);
   return c;
 }
-__device__ __forceinline__ void eta_terms(const EtaConsts& c, double beta, double eta, double t,
-                                          double& g, double& gp) {
-  const double th = tanh(beta * (t - eta));
-  g = (c.a + th) / c.denom - t;
-  const double s = 0.5 * (c.coshb - cosh(beta * (2.0 * t - 1.0)));
-  gp = c.c0 * (1.0 - th * th) * s;
+__device__ __forceinline__ void eta_terms(const EtaConsts& c, double t, double E1, double& g,
+                                          double& gp) {
+  const double E = E1 * c.k;
+  const double th = (E - 1.0) / (E + 1.0);
+  g = (c.a + th) / c.den - t;  // true division: unbiased like the reference's
+  const double S = c.half_coshb - 0.25 * fma(E1, c.emb, c.eb / E1);
+  gp = c.c0 * (1.0 - th * th) * S;
 }
 
 // Candidate record of oc.hpp:44-61 for one element; passives get lb = ub = x,
@@ -259,7 +263,48 @@ __device__ __forceinline__ void conv_columns(const double* __restrict__ tile, in
   }
 }
 
-template <int NF, int MODE, int R>
+// Small-reach variant (compile-time half-width bound A): all R + 2A mirror-
+// summed values of a column are loaded once into registers and every column
+// applies 2A + 1 weights (zero outside its own [-a, a]; woff points at the
+// centred, zero-padded 2A + 2 weights), fully unrolled.
+template <int NM, int R, int A>
+__device__ __forceinline__ void conv_columns_direct(const double* __restrict__ tile, int sb, int sI,
+                                                    int sPlane, const ConvCol* __restrict__ cols,
+                                                    int c0, int c1,
+                                                    const double* __restrict__ wts,
+                                                    double (&acc)[R]) {
+  for (int c = c0; c < c1; ++c) {
+    const ConvCol col = cols[c];
+    const int base = sb - A;
+    const int oi = col.di * sI, oo = col.dother * sPlane;
+    const double* p0 = tile + base + oi + oo;
+    const double* p1 = tile + base - oi - oo;
+    const double* p2 = tile + base - oi + oo;
+    const double* p3 = tile + base + oi - oo;
+    double v[R + 2 * A];
+#pragma unroll
+    for (int q = 0; q < R + 2 * A; ++q) {
+      double t = p0[q];
+      if (NM == 2) t += p1[q];
+      if (NM == 4) t = (t + p1[q]) + (p2[q] + p3[q]);
+      v[q] = t;
+    }
+    const double2* w2 = reinterpret_cast<const double2*>(wts + col.woff);
+    double w[2 * A + 2];
+#pragma unroll
+    for (int t = 0; t < A + 1; ++t) {
+      const double2 ww = __ldg(w2 + t);
+      w[2 * t] = ww.x;
+      w[2 * t + 1] = ww.y;
+    }
+#pragma unroll
+    for (int d = 0; d < 2 * A + 1; ++d)
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = fma(w[d], v[r + d], acc[r]);
+  }
+}
+
+template <int NF, int MODE, int R, int AW>
 __global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const ConvCol* __restrict__ cols,
                                                    int ncols, const double* __restrict__ wts,
                                                    ConvArgs A) {
@@ -328,15 +373,22 @@ __global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const Conv
       tile[lineDst[line] + ti * sI] = v;
     }
     __syncthreads();
-    conv_columns<4, R>(tile, sb, sI, sPlane, cols, 0, T.ncol[0], wts, acc[f]);
-    conv_columns<2, R>(tile, sb, sI, sPlane, cols, T.ncol[0], T.ncol[0] + T.ncol[1], wts, acc[f]);
-    conv_columns<1, R>(tile, sb, sI, sPlane, cols, T.ncol[0] + T.ncol[1], ncols, wts, acc[f]);
+    if (AW > 0) {
+      conv_columns_direct<4, R, AW>(tile, sb, sI, sPlane, cols, 0, T.ncol[0], wts, acc[f]);
+      conv_columns_direct<2, R, AW>(tile, sb, sI, sPlane, cols, T.ncol[0], T.ncol[0] + T.ncol[1],
+                                    wts, acc[f]);
+      conv_columns_direct<1, R, AW>(tile, sb, sI, sPlane, cols, T.ncol[0] + T.ncol[1], ncols, wts,
+                                   acc[f]);
+    } else {
+      conv_columns<4, R>(tile, sb, sI, sPlane, cols, 0, T.ncol[0], wts, acc[f]);
+      conv_columns<2, R>(tile, sb, sI, sPlane, cols, T.ncol[0], T.ncol[0] + T.ncol[1], wts,
+                         acc[f]);
+      conv_columns<1, R>(tile, sb, sI, sPlane, cols, T.ncol[0] + T.ncol[1], ncols, wts, acc[f]);
+    }
   }
 
   // epilogue
   double red[3] = {0.0, 0.0, 0.0};
-  EtaConsts ec;
-  if (MODE == CONV_FWD_ETA) ec = eta_consts(A.beta, A.eta0);
   const int gi = bi + wi * 32 + lane, go = bo + wo;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -345,18 +397,12 @@ __global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const Conv
     const long long e = ((long long)go * T.run_n + grun) * G.nely + gi;
     if (MODE == CONV_PLAIN || MODE == CONV_ADJ_DIV) {
       A.out0[e] = acc[0][r];
-    } else if (MODE == CONV_FWD || MODE == CONV_FWD_ETA) {
+    } else if (MODE == CONV_FWD) {
       double v = acc[0][r] / A.hs[e];  // filter.hpp:121 cwiseQuotient(hs)
       const int s = elem_state(A.state, e);
       if (A.pin && s == 1) v = 1.0;  // driver.hpp:130-133
       if (A.pin && s == 2) v = 0.0;
       A.out0[e] = v;
-      if (MODE == CONV_FWD_ETA && s == 0) {
-        double g, gp;
-        eta_terms(ec, A.beta, A.eta0, v, g, gp);
-        red[0] += g;
-        red[1] += gp;
-      }
     } else if (MODE == CONV_ADJ2_OC) {
       const double dc = acc[0][r], dV = acc[NF - 1][r];
       if (A.out0) A.out0[e] = dc;
@@ -369,7 +415,7 @@ __global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const Conv
       red[2] += rec.w * std_min(std_max(0.0, rec.x), rec.y);  // V(s -> inf)
     }
   }
-  if (MODE == CONV_FWD_ETA || MODE == CONV_ADJ2_OC) {
+  if (MODE == CONV_ADJ2_OC) {
     __shared__ double scratch[3 * 32];
     block_sum<3>(red, scratch);
     const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
@@ -390,69 +436,48 @@ struct EtaArgs {
   const double* xt;
   const uint8_t* state;
   double beta, eta0, mtotal;
-  const double* partials0;  // K1 partials at eta0 (stride 3) or null
-  int n0;
+  double* e1;               // exp(2 b t) per element, written by the first pass
   double* partials;         // [2][gridDim][2]
   double* result;           // eta, iterations (as double), g
 };
 
-__device__ __forceinline__ void eta_block_eval(const EtaArgs& A, double eta, double (&red)[2]) {
+__device__ __forceinline__ void eta_block_eval(const EtaArgs& A, double eta, bool first,
+                                               double (&red)[2]) {
   const EtaConsts c = eta_consts(A.beta, eta);
   red[0] = red[1] = 0.0;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < A.G.m;
        e += (long long)gridDim.x * blockDim.x) {
-    if (elem_state(A.state, e) != 0) continue;
+    if (elem_state(A.state, e) != 0) continue;  // active set only (filter.hpp:190)
+    const double t = A.xt[e];
+    double E1;
+    if (first) {
+      E1 = exp(2.0 * A.beta * t);
+      A.e1[e] = E1;
+    } else {
+      E1 = A.e1[e];
+    }
     double g, gp;
-    eta_terms(c, A.beta, eta, A.xt[e], g, gp);
+    eta_terms(c, t, E1, g, gp);
     red[0] += g;
     red[1] += gp;
   }
 }
 
+// one (g, g') evaluation per grid-wide step; every block reduces the same
+// partials in the same order and takes the same Newton decision
 __global__ void __launch_bounds__(kThreads) k_eta_solve(EtaArgs A) {
   cg::grid_group grid = cg::this_grid();
   __shared__ EtaCtl ctl;
   __shared__ double scratch[2 * 32];
-  __shared__ double gv[2];
   __shared__ int cont;
   if (threadIdx.x == 0) ctl.init(A.eta0);
   __syncthreads();
   int buf = 0;
-  if (A.partials0) {
-    if (threadIdx.x < 32) {
-      double s[2];
-      warp_sum_partials<2>(A.partials0, A.n0, 3, s);
-      if (threadIdx.x == 0) {
-        gv[0] = s[0];
-        gv[1] = s[1];
-      }
-    }
-  } else {
-    double red[2];
-    eta_block_eval(A, ctl.eta, red);
-    block_sum<2>(red, scratch);
-    if (threadIdx.x == 0) {
-      A.partials[2 * blockIdx.x] = red[0];
-      A.partials[2 * blockIdx.x + 1] = red[1];
-    }
-    grid.sync();
-    if (threadIdx.x < 32) {
-      double s[2];
-      warp_sum_partials<2>(A.partials, gridDim.x, 2, s);
-      if (threadIdx.x == 0) {
-        gv[0] = s[0];
-        gv[1] = s[1];
-      }
-    }
-    buf = 1;
-  }
-  __syncthreads();
+  bool first = true;
   for (;;) {
-    if (threadIdx.x == 0) cont = ctl.feed(gv[0] / A.mtotal, gv[1] / A.mtotal);
-    __syncthreads();
-    if (!cont) break;
     double red[2];
-    eta_block_eval(A, ctl.eta, red);
+    eta_block_eval(A, ctl.eta, first, red);
+    first = false;
     block_sum<2>(red, scratch);
     double* P = A.partials + (long long)buf * 2 * gridDim.x;
     if (threadIdx.x == 0) {
@@ -461,15 +486,13 @@ __global__ void __launch_bounds__(kThreads) k_eta_solve(EtaArgs A) {
     }
     grid.sync();
     if (threadIdx.x < 32) {
-      double s[2];
-      warp_sum_partials<2>(P, gridDim.x, 2, s);
-      if (threadIdx.x == 0) {
-        gv[0] = s[0];
-        gv[1] = s[1];
-      }
+      double s2[2];
+      warp_sum_partials<2>(P, gridDim.x, 2, s2);
+      if (threadIdx.x == 0) cont = ctl.feed(s2[0] / A.mtotal, s2[1] / A.mtotal);
     }
     buf ^= 1;
     __syncthreads();
+    if (!cont) break;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.result[0] = ctl.eta;
@@ -479,10 +502,10 @@ __global__ void __launch_bounds__(kThreads) k_eta_solve(EtaArgs A) {
 }
 
 // plain (g, g') partial sums at one eta: the multi-GPU / host-driven variant
-__global__ void __launch_bounds__(kThreads) k_eta_partials(EtaArgs A, double eta) {
+__global__ void __launch_bounds__(kThreads) k_eta_partials(EtaArgs A, double eta, int first) {
   __shared__ double scratch[2 * 32];
   double red[2];
-  eta_block_eval(A, eta, red);
+  eta_block_eval(A, eta, first != 0, red);
   block_sum<2>(red, scratch);
   if (threadIdx.x == 0) {
     A.partials[2 * blockIdx.x] = red[0];
@@ -520,56 +543,82 @@ __device__ __forceinline__ double simp_xp(double x, double p) {
   return pm1 == 2.0 ? x * x : pow(x, pm1);  // std::pow(x, p - 1), fea.hpp:141
 }
 
-template <int D>
-__global__ void __launch_bounds__(kThreads, 3) k_elem_sens(Geo G, KeFull<D> K, ElemArgs A) {
+// Each thread handles NE elements (e, e + H, ...) so every Ke coefficient
+// fetched from the constant bank feeds NE FMAs.
+template <int D, int NE>
+__global__ void __launch_bounds__(kThreads, 4 - NE) k_elem_sens(Geo G, KeFull<D> K, ElemArgs A) {
   __shared__ double scratch[32];
   const double eta = A.input_is_phys ? 0.5 : *A.eta_ptr;
   const double a = tanh(A.beta * eta);
   const double denom = a + tanh(A.beta * (1.0 - eta));
   const double de = A.e0 - A.emin;
+  const long long H = (G.m + NE - 1) / NE;  // element stride between a thread's elements
   double csum = 0.0;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < G.m;
-       e += (long long)gridDim.x * blockDim.x) {
-    int i, k, j;
-    elem_ijk(G, e, i, k, j);
-    const double t = A.xt[e];
-    double xphys, dH = 0.0;
-    if (A.input_is_phys) {
-      xphys = t;
-    } else {
-      const double th = tanh(A.beta * (t - eta));
-      xphys = (a + th) / denom;                               // filter.hpp:142
-      dH = A.beta * (1.0 - th * th) / denom;                  // filter.hpp:151
-    }
-    const double xp = simp_xp(xphys, A.penal);
-    const double sK = A.emin + xp * xphys * de;               // fea.hpp:142
-    const double dsK = A.penal * xp * de;                     // fea.hpp:143
-    int dofs[24];
-    element_dofs(G, i, k, j, G.j0, dofs);
-    double ue[D];
+  for (long long e0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; e0 < H;
+       e0 += (long long)gridDim.x * blockDim.x) {
+    double ue[NE][D];
+    double xphys[NE], dH[NE];
+    bool ok[NE];
 #pragma unroll
-    for (int q = 0; q < D; ++q) ue[q] = __ldg(A.U + dofs[q]);
-    // quad = ue . (Ke ue) (fea.hpp:267), evaluated on the symmetric upper half
-    double quad = 0.0;
+    for (int n = 0; n < NE; ++n) {
+      const long long e = e0 + n * H;
+      ok[n] = e < G.m;
+      const long long ec = ok[n] ? e : e0;
+      int i, k, j;
+      elem_ijk(G, ec, i, k, j);
+      const double t = A.xt[ec];
+      if (A.input_is_phys) {
+        xphys[n] = t;
+        dH[n] = 0.0;
+      } else {
+        const double th = tanh(A.beta * (t - eta));
+        xphys[n] = (a + th) / denom;                          // filter.hpp:142
+        dH[n] = A.beta * (1.0 - th * th) / denom;             // filter.hpp:151
+      }
+      int dofs[24];
+      element_dofs(G, i, k, j, G.j0, dofs);
+#pragma unroll
+      for (int q = 0; q < D; ++q) ue[n][q] = __ldg(A.U + dofs[q]);
+    }
+    // quad = ue . (Ke ue) (fea.hpp:267), on the symmetric upper half
+    double quad[NE];
+#pragma unroll
+    for (int n = 0; n < NE; ++n) quad[n] = 0.0;
 #pragma unroll
     for (int r = 0; r < D; ++r) {
-      double s = 0.5 * K.k[r * D + r] * ue[r];
+      const double hk = 0.5 * K.k[r * D + r];
+      double s[NE];
 #pragma unroll
-      for (int c = r + 1; c < D; ++c) s = fma(K.k[c * D + r], ue[c], s);
-      quad = fma(ue[r], s, quad);
+      for (int n = 0; n < NE; ++n) s[n] = hk * ue[n][r];
+#pragma unroll
+      for (int c = r + 1; c < D; ++c) {
+        const double kc = K.k[c * D + r];
+#pragma unroll
+        for (int n = 0; n < NE; ++n) s[n] = fma(kc, ue[n][c], s[n]);
+      }
+#pragma unroll
+      for (int n = 0; n < NE; ++n) quad[n] = fma(ue[n][r], s[n], quad[n]);
     }
-    quad = 2.0 * quad;
-    csum = fma(sK, quad, csum);
-    const int st = elem_state(A.state, e);
-    const double dcp = st == 0 ? -dsK * quad : 0.0;
-    const double dv0 = st == 0 ? A.inv_m : 0.0;               // driver.hpp:155
-    if (A.xPhys) A.xPhys[e] = xphys;
-    if (A.dcPhys) A.dcPhys[e] = dcp;
-    if (A.a1) {
-      const double h = A.hs[e];
-      const long long es = e + (long long)(G.j0 - G.sj0) * G.S;
-      A.a1[es] = (dH * dcp) / h;                              // backfilter, filter.hpp:170, :128
-      A.a2[es] = (dH * dv0) / h;
+#pragma unroll
+    for (int n = 0; n < NE; ++n) {
+      if (!ok[n]) continue;
+      const long long e = e0 + n * H;
+      const double q2 = 2.0 * quad[n];
+      const double xp = simp_xp(xphys[n], A.penal);
+      const double sK = A.emin + xp * xphys[n] * de;          // fea.hpp:142
+      const double dsK = A.penal * xp * de;                   // fea.hpp:143
+      csum = fma(sK, q2, csum);
+      const int st = elem_state(A.state, e);
+      const double dcp = st == 0 ? -dsK * q2 : 0.0;
+      const double dv0 = st == 0 ? A.inv_m : 0.0;             // driver.hpp:155
+      if (A.xPhys) A.xPhys[e] = xphys[n];
+      if (A.dcPhys) A.dcPhys[e] = dcp;
+      if (A.a1) {
+        const double ih = 1.0 / A.hs[e];
+        const long long es = e + (long long)(G.j0 - G.sj0) * G.S;
+        A.a1[es] = (dH[n] * dcp) * ih;                        // backfilter, filter.hpp:170, :128
+        A.a2[es] = (dH[n] * dv0) * ih;
+      }
     }
   }
   double red[1] = {csum};
