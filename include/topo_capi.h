@@ -132,6 +132,16 @@ topo_status topo_element_stiffness(int dim, double nu, double* ke_full, double* 
 void topo_generate(uint64_t seed, uint64_t stream, int kind, double a, double b, int64_t offset,
                    int64_t count, double* out);
 
+/* host replays of the scalar control flow (no device work): oc.hpp:93-174
+ * driven by V(s) = vol(user, sqrt-multiplier), optionally in the speculative
+ * batches of the device kernel; filter.hpp:182-228 driven by (g, g')(eta) */
+typedef double (*topo_sfun)(void* user, double s);
+typedef void (*topo_gfun)(void* user, double eta, double* g, double* gp);
+int topo_host_oc_replay(const topo_oc_params* prm, double lamMax, topo_sfun vol, void* user,
+                        int speculative, double* lambda, int32_t* bisections,
+                        int32_t* evaluations, double* s_final, int32_t* batches);
+int topo_host_eta_replay(double eta0, topo_gfun gf, void* user, double* eta, int32_t* iters);
+
 /* ---- K0: grid.hpp:89-153 ------------------------------------------------ */
 topo_status topo_build_connectivity(topo_ctx* ctx, int32_t* dofs);          /* m*d */
 topo_status topo_build_index_pairs(topo_ctx* ctx, int32_t* iK, int32_t* jK); /* m*P; NULL=keep */

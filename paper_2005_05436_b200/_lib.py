@@ -27,7 +27,7 @@ EXPORTS = [
     "topo_filter_adjoint", "topo_project", "topo_project_derivative", "topo_backfilter",
     "topo_solve_eta", "topo_filter_taps", "topo_filter_hs", "topo_lambda_upper",
     "topo_oc_candidate", "topo_oc_bisect", "topo_design_pass", "topo_last_launch_count",
-    "topo_set_timing", "topo_stage_times",
+    "topo_set_timing", "topo_stage_times", "topo_host_oc_replay", "topo_host_eta_replay",
 ]
 STAGES = ["filter", "eta", "elem", "adjoint", "oc", "sk_store", "pass"]
 
@@ -64,6 +64,8 @@ class PassOut(C.Structure):
 
 
 VOLUME_FN = C.CFUNCTYPE(C.c_double, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
+SFUN = C.CFUNCTYPE(C.c_double, C.c_void_p, C.c_double)
+GFUN = C.CFUNCTYPE(None, C.c_void_p, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double))
 
 _lib = None
 
@@ -116,6 +118,10 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         "topo_last_launch_count": (C.c_int64, [vp]),
         "topo_set_timing": (C.c_int, [vp, C.c_int]),
         "topo_stage_times": (C.c_int, [vp, vp]),
+        "topo_host_oc_replay": (C.c_int, [p(OcParams), C.c_double, SFUN, vp, C.c_int,
+                                          p(C.c_double), p(C.c_int32), p(C.c_int32),
+                                          p(C.c_double), p(C.c_int32)]),
+        "topo_host_eta_replay": (C.c_int, [C.c_double, GFUN, vp, p(C.c_double), p(C.c_int32)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

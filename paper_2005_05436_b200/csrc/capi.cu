@@ -303,7 +303,12 @@ int conv_blocks(const topo_ctx* ctx) {
 // K3b: grid sized for full occupancy (no shared-memory or barrier limits)
 topo_status launch_sk(topo_ctx* ctx, const SkArgs& S, cudaStream_t st) {
   const Geo& G = ctx->G;
-  const int nb = grid_for(ctx, (G.m + 31) / 32 * 32);
+  int nb = grid_for(ctx, (G.m + 31) / 32 * 32);
+  if (st == ctx->aux) {  // overlapped: leave SM room for K3a..K6 on the main stream
+    const char* e = getenv("TOPO_SK_BPS");
+    const int bps = e ? atoi(e) : 2;
+    nb = std::min(nb, ctx->sm_count * std::max(1, bps));
+  }
   if (G.is3d)
     k_sk_store<300><<<nb, kThreads, 0, st>>>(G, S);
   else

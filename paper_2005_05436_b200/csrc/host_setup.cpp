@@ -128,3 +128,65 @@ void topo_generate(uint64_t seed, uint64_t stream, int kind, double a, double b,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Host replays of the device control state machines (control.h), driven by
+// caller-supplied scalar functions. The multi-GPU path runs exactly these
+// replays on the host; the CPU test suite checks them against the oracle's
+// bisect_update / solve_volume_preserving_eta on the same volume functions.
+#include "control.h"
+
+extern "C" {
+
+typedef double (*topo_sfun)(void* user, double s);
+typedef void (*topo_gfun)(void* user, double eta, double* g, double* gp);
+
+// oc.hpp:93-174 replay; V(s) from `vol`. speculative = 1 evaluates requests
+// in the batches the device kernel uses (oc_speculate) and replays them.
+int topo_host_oc_replay(const topo_oc_params* prm, double lamMax, topo_sfun vol, void* user,
+                        int speculative, double* lambda, int32_t* bisections,
+                        int32_t* evaluations, double* s_final, int32_t* batches) {
+  topo::OcCtl c;
+  c.init(lamMax, prm->volfrac, prm->bisect_rel_tol, prm->volume_tol, prm->lambda_space,
+         prm->abs_tol);
+  int nb = 0;
+  if (!speculative) {
+    while (c.pending()) c.feed(vol(user, c.s_req));
+  } else {
+    double req[16], val[16];
+    while (c.pending()) {
+      const int n = topo::oc_speculate<16>(c, req);
+      for (int q = 0; q < n; ++q) val[q] = vol(user, req[q]);
+      ++nb;
+      while (c.pending()) {
+        int hit = -1;
+        for (int q = 0; q < n; ++q)
+          if (req[q] == c.s_req) hit = q;
+        if (hit < 0) break;
+        c.feed(val[hit]);
+      }
+    }
+  }
+  if (lambda) *lambda = c.lam_result;
+  if (bisections) *bisections = c.bis;
+  if (evaluations) *evaluations = c.evals;
+  if (s_final) *s_final = c.s_final;
+  if (batches) *batches = nb;
+  return c.status;
+}
+
+// filter.hpp:182-228 replay; (g, g') at eta from `gf` (already divided by m)
+int topo_host_eta_replay(double eta0, topo_gfun gf, void* user, double* eta, int32_t* iters) {
+  topo::EtaCtl c;
+  c.init(eta0);
+  for (;;) {
+    double g, gp;
+    gf(user, c.eta, &g, &gp);
+    if (!c.feed(g, gp)) break;
+  }
+  if (eta) *eta = c.eta;
+  if (iters) *iters = c.it;
+  return 0;
+}
+
+}  // extern "C"
