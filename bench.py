@@ -66,58 +66,57 @@ def load_traffic(cid: int):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
+    """nvidia-smi in a separate process, sampling every 200 ms during the timed
+    region (B200_PROFILING.md clocks line); no in-process NVML calls, which
+    would contend with the CUDA driver on the timed thread."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
-        self.reasons = set()
-        self.max_mhz = None
-        self._stop = threading.Event()
-        self.ok = False
+        self.proc = None
+        self.lines = []
 
     def __enter__(self):
-        try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self.ok = True
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
-        except Exception:
-            self.ok = False
+        import shutil
+        import subprocess
+        import tempfile
+        if shutil.which("nvidia-smi"):
+            self.tmp = tempfile.TemporaryFile(mode="w+")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.tmp,
+                stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
         return self
 
-    def _run(self):
-        nv = self.nv
-        names = {
-            getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
-            getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
-            getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
-            getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
-            getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake",
-        }
-        while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
-                for bit, name in names.items():
-                    if r & bit:
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            self._stop.wait(0.05)
-
     def __exit__(self, *a):
-        self._stop.set()
-        if self.ok:
-            self.t.join(timeout=1)
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.tmp.seek(0)
+            self.lines = [ln.strip() for ln in self.tmp.read().splitlines() if ln.strip()]
 
     def summary(self):
-        if not self.ok or not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        rows = []
+        for ln in self.lines:
+            f = [v.strip() for v in ln.split(",")]
+            if len(f) >= 9:
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(rows)}
 
 
 # ------------------------------------------------------------- CPU samples
@@ -223,7 +222,6 @@ def run_ours(args, cfg, rank, world, local_rank):
     ud = torch.from_numpy(u).to(dev)
     stream = torch.cuda.Stream(device=dev)
     ctx.set_stream(stream.cuda_stream)
-    ctx.set_timing(True)
     kw = dict(beta=cfg.beta, eta0=cfg.eta0, move=cfg.move, volfrac=cfg.volfrac, outputs=False)
     flush = None
     if cfg.m * algorithmic_bytes_per_elem(cfg) < 3 * 126e6:
@@ -254,10 +252,16 @@ def run_ours(args, cfg, rank, world, local_rank):
             ev1.synchronize()
             t_total += ev0.elapsed_time(ev1)
             launches += r.launches
-            for k, v in ctx.stage_times().items():
-                stage_acc[k] += v
         torch.cuda.synchronize()
         barrier()
+    # per-stage breakdown (CUDA events on each kernel's stream), measured in
+    # extra passes after the timed region so the events do not perturb it
+    ctx.set_timing(True)
+    for _ in range(args.steps):
+        ctx.design_pass(xd, ud, **kw)
+        for k, v in ctx.stage_times().items():
+            stage_acc[k] += v
+    ctx.set_timing(False)
     ms = t_total / args.steps
     if world > 1:
         import torch.distributed as dist
