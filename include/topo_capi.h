@@ -121,8 +121,26 @@ topo_status topo_device_buffer(topo_ctx* ctx, int which, void** ptr, int64_t* co
  * j0, j1 */
 topo_status topo_ctx_info(const topo_ctx* ctx, int64_t* m, int64_t* n, int32_t* P,
                           int32_t* ntaps, int32_t* reach, int32_t* j0, int32_t* j1);
-/* multi-GPU: join an NCCL clique (nccl_unique_id = 128 bytes from rank 0) */
+/* multi-GPU: join an NCCL clique (nccl_unique_id = 128 bytes from rank 0's
+ * topo_nccl_unique_id, broadcast by the caller); halos and scalar sums then
+ * travel over NCCL (NVLink) on the context's stream */
+topo_status topo_nccl_unique_id(void* out128);
 topo_status topo_comm_init_nccl(topo_ctx* ctx, const void* nccl_unique_id);
+/* ...or through host callbacks (the caller moves host buffers, e.g. with
+ * torch.distributed); `exchange` sends n_send_left / n_send_right doubles to
+ * rank - 1 / rank + 1 and fills the receive buffers from them */
+typedef struct {
+  void* user;
+  int (*exchange)(void* user, const double* send_left, int64_t n_send_left,
+                  const double* send_right, int64_t n_send_right, double* recv_left,
+                  int64_t n_recv_left, double* recv_right, int64_t n_recv_right);
+  int (*allreduce_sum)(void* user, double* values, int n);
+} topo_host_comm;
+topo_status topo_comm_init_host(topo_ctx* ctx, const topo_host_comm* comm);
+/* host-only slab plan of a rank: out[0..8) = j0, j1, sj0, sj1 (owned and
+ * stored columns) and the columns sent to / received from the left and right
+ * neighbours; TOPO_EINVAL if the slab is narrower than the filter reach */
+topo_status topo_slab_plan(const topo_grid_desc* desc, int64_t* out);
 
 /* ---- host setup helpers (no device work) -------------------------------- */
 /* fea.hpp:51-68 (dim 2) / fea.hpp:73-121 (dim 3) */

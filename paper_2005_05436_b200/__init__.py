@@ -8,7 +8,7 @@ C-ABI in include/topo_capi.h. See DESIGN.md.
 from . import _lib
 from .api import (Context, CudaError, IndexOverflow, InvalidArgument, NonMonotone, OcParams,
                   PassResult, SimpParams, TopoError, UpdateResult, element_stiffness, generate,
-                  partition_domain)
+                  nccl_unique_id, partition_domain, slab_plan)
 from .configs import CONFIGS, Config, make_inputs
 
 BC_NEUMANN, BC_DIRICHLET = _lib.BC_NEUMANN, _lib.BC_DIRICHLET

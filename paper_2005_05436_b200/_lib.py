@@ -28,6 +28,7 @@ EXPORTS = [
     "topo_solve_eta", "topo_filter_taps", "topo_filter_hs", "topo_lambda_upper",
     "topo_oc_candidate", "topo_oc_bisect", "topo_design_pass", "topo_last_launch_count",
     "topo_set_timing", "topo_stage_times", "topo_host_oc_replay", "topo_host_eta_replay",
+    "topo_nccl_unique_id", "topo_comm_init_host", "topo_slab_plan",
 ]
 STAGES = ["filter", "eta", "elem", "adjoint", "oc", "sk_store", "pass"]
 
@@ -66,6 +67,14 @@ class PassOut(C.Structure):
 VOLUME_FN = C.CFUNCTYPE(C.c_double, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
 SFUN = C.CFUNCTYPE(C.c_double, C.c_void_p, C.c_double)
 GFUN = C.CFUNCTYPE(None, C.c_void_p, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double))
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64,
+                          C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double), C.c_int64,
+                          C.POINTER(C.c_double), C.c_int64)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int)
+
+
+class HostComm(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("exchange", EXCHANGE_FN), ("allreduce_sum", ALLREDUCE_FN)]
 
 _lib = None
 
@@ -122,6 +131,9 @@ def load(build_if_missing: bool = True) -> C.CDLL:
                                           p(C.c_double), p(C.c_int32), p(C.c_int32),
                                           p(C.c_double), p(C.c_int32)]),
         "topo_host_eta_replay": (C.c_int, [C.c_double, GFUN, vp, p(C.c_double), p(C.c_int32)]),
+        "topo_nccl_unique_id": (C.c_int, [vp]),
+        "topo_comm_init_host": (C.c_int, [vp, p(HostComm)]),
+        "topo_slab_plan": (C.c_int, [p(GridDesc), vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -184,6 +184,31 @@ def generate(seed: int, stream: int, kind: str, a: float, b: float, count: int,
     return out
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL clique id (rank 0 creates it, the caller broadcasts it)."""
+    lib = L.load()
+    buf = (C.c_char * 128)()
+    st = lib.topo_nccl_unique_id(buf)
+    if st:
+        _raise(st, "ncclGetUniqueId failed (is libnccl.so.2 loadable?)")
+    return bytes(buf)
+
+
+def slab_plan(nelx: int, nely: int, nelz: int, rmin: float, rank: int, nranks: int,
+              j0: int = 0, j1: int = 0) -> dict:
+    """x-slab of a rank (host only): owned / stored columns and the halo columns
+    exchanged with the neighbours (the plan the library's halo exchange uses)."""
+    lib = L.load()
+    desc = L.GridDesc(nelx, nely, nelz, rmin, 0, 0.3, -1, rank, nranks, j0, j1)
+    out = np.zeros(8, np.int64)
+    st = lib.topo_slab_plan(C.byref(desc), out.ctypes.data)
+    keys = ["j0", "j1", "sj0", "sj1", "send_left", "send_right", "recv_left", "recv_right"]
+    plan = dict(zip(keys, (int(v) for v in out)))
+    if st:
+        _raise(st, f"slab {plan['j0']}..{plan['j1']} narrower than the filter reach")
+    return plan
+
+
 def partition_domain(grid, pasS=(), pasV=()) -> np.ndarray:
     """grid.hpp:155-188 as a per-element state byte array (0 act / 1 solid / 2 void)."""
     nelx, nely, nelz = grid
@@ -281,6 +306,39 @@ class Context:
         t = np.zeros(len(L.STAGES))
         self._check(self.lib.topo_stage_times(self.h, t.ctypes.data))
         return dict(zip(L.STAGES, t.tolist()))
+
+    def comm_init(self, unique_id: bytes):
+        """Join the NCCL clique of this x-slab decomposition (all ranks call it)."""
+        buf = (C.c_char * 128).from_buffer_copy(unique_id)
+        self._check(self.lib.topo_comm_init_nccl(self.h, buf))
+
+    def comm_init_host(self, exchange, allreduce_sum):
+        """Host-callback communicator: exchange(send_left, send_right, recv_left,
+        recv_right) with numpy views (recv_* to be filled in place) and
+        allreduce_sum(values) in place."""
+
+        def _ex(_u, sl, nsl, sr, nsr, rl, nrl, rr, nrr):
+            try:
+                view = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)) if n else np.zeros(0)
+                exchange(view(sl, nsl), view(sr, nsr), view(rl, nrl), view(rr, nrr))
+                return 0
+            except Exception:  # noqa: BLE001 - reported as a status code
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        def _ar(_u, p, n):
+            try:
+                allreduce_sum(np.ctypeslib.as_array(p, shape=(n,)))
+                return 0
+            except Exception:  # noqa: BLE001
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._host_comm_cbs = (L.EXCHANGE_FN(_ex), L.ALLREDUCE_FN(_ar))
+        hc = L.HostComm(None, *self._host_comm_cbs)
+        self._check(self.lib.topo_comm_init_host(self.h, C.byref(hc)))
 
     def set_stream(self, cuda_stream_handle: int):
         self._check(self.lib.topo_set_stream(self.h, cuda_stream_handle))

@@ -429,6 +429,31 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
            prm->abs_tol);
   std::vector<double> hx;
   const int nb = grid_for(ctx, G.m);
+  if (mode == TOPO_VOL_MEAN || mode == TOPO_VOL_FILTERED) {
+    // multi-GPU identity volumes: the device kernel's bound shortcut and
+    // speculative batches, one allreduce of K sums per batch
+    const double V0 = (add_const + ctx->h_result[1]) / ctx->m_total;
+    const double Vinf = (add_const + ctx->h_result[2]) / ctx->m_total;
+    int smode = 0;
+    if (Vinf > prm->volfrac + 0.5 * prm->volume_tol + 1e-12) smode = 1;
+    if (V0 < prm->volfrac - 0.5 * prm->volume_tol - 1e-12) smode = -1;
+    if (smode != 0) {
+      ctl.check_mono = 0;
+      while (ctl.pending()) ctl.feed(smode > 0 ? INFINITY : -INFINITY);
+    }
+    double req[kOcK], val[kOcK];
+    while (ctl.pending()) {
+      const int K = oc_speculate<kOcK>(ctl, req);
+      TRY(comm_oc_volumes(ctx->comm, ctx, req, K, add_const, val));
+      while (ctl.pending()) {
+        int hit = -1;
+        for (int q = 0; q < K; ++q)
+          if (req[q] == ctl.s_req) hit = q;
+        if (hit < 0) break;
+        ctl.feed(val[hit]);
+      }
+    }
+  }
   while (ctl.pending()) {
     const double s = ctl.s_req;
     double v = 0;
@@ -472,9 +497,28 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
   return TOPO_OK;
 }
 
+// owned columns [j0, j0 + jn) and stored (halo-extended) columns [sj0, sj0 + sjn)
+void slab_columns(const topo_grid_desc* d, int reach, int* j0, int* jn, int* sj0, int* sjn) {
+  if (d->j1 > d->j0) {
+    *j0 = d->j0;
+    *jn = d->j1 - d->j0;
+  } else {
+    const int base = d->nelx / d->nranks, rem = d->nelx % d->nranks;
+    *j0 = d->rank * base + std::min(d->rank, rem);
+    *jn = base + (d->rank < rem ? 1 : 0);
+  }
+  const int halo = d->nranks > 1 ? reach : 0;
+  *sj0 = std::max(0, *j0 - halo);
+  *sjn = std::min(d->nelx, *j0 + *jn + halo) - *sj0;
+}
+
 topo_status validate_slab(topo_ctx* ctx) {
   // every tap of every owned element must land in a stored column
   const Geo& G = ctx->G;
+  if (G.jn < ctx->reach)
+    return fail(ctx, TOPO_EINVAL,
+                "slab [%d, %d) is narrower than the filter reach %d; use fewer ranks", G.j0,
+                G.j0 + G.jn, ctx->reach);
   for (int j = G.j0 - ctx->reach; j < G.j0 + G.jn + ctx->reach; ++j) {
     int jf = j;
     if (G.bc == 0)
@@ -582,14 +626,7 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   G.bc = d->bc;
   ctx->rank = d->rank;
   ctx->nranks = d->nranks;
-  if (d->j1 > d->j0) {
-    G.j0 = d->j0;
-    G.jn = d->j1 - d->j0;
-  } else {
-    const int base = d->nelx / d->nranks, rem = d->nelx % d->nranks;
-    G.j0 = d->rank * base + std::min(d->rank, rem);
-    G.jn = base + (d->rank < rem ? 1 : 0);
-  }
+  slab_columns(d, int(ceil(d->rmin)) - 1, &G.j0, &G.jn, &G.sj0, &G.sjn);
   if (G.j0 < 0 || G.jn < 1 || G.j0 + G.jn > d->nelx)
     return bail(fail(ctx, TOPO_EINVAL, "empty or out-of-range slab [%d, %d)", G.j0, G.j0 + G.jn));
   G.m = (long long)G.jn * G.S;
@@ -597,9 +634,6 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   ctx->rmin = d->rmin;
   ctx->reach = int(ceil(d->rmin)) - 1;  // filter.hpp:105
   ctx->rk = is3d ? ctx->reach : 0;
-  const int halo = d->nranks > 1 ? ctx->reach : 0;
-  G.sj0 = std::max(0, G.j0 - halo);
-  G.sjn = std::min(d->nelx, G.j0 + G.jn + halo) - G.sj0;
   ctx->m_st = (long long)G.sjn * G.S;
   ctx->n = (long long)G.dim * (G.jn + 1) * (d->nely + 1) * (is3d ? d->nelz + 1 : 1);
   if (d->nranks > 1) {
@@ -1197,6 +1231,8 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   if (!ctx || !prm || !out) return TOPO_EINVAL;
   ctx->launches = 0;
   const Geo& G = ctx->G;
+  if (ctx->nranks > 1 && !ctx->comm)
+    return fail(ctx, TOPO_EINVAL, "multi-rank context: call topo_comm_init_nccl/_host first");
   if (!(prm->beta > 0)) return fail(ctx, TOPO_EINVAL, "eta solve: beta must be positive");
   const int vmode = prm->volume_mode;
   if (vmode != TOPO_VOL_FILTERED && vmode != TOPO_VOL_MEAN)
@@ -1359,23 +1395,246 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
 
 }  // extern "C"
 
-// ======================================================= multi-GPU (stub)
-struct Comm {
-  int dummy;
+// ============================================================ multi-GPU
+// x-slab decomposition: halo exchange of filter inputs
+// between neighbouring ranks and allreduce of the scalar sums. Two backends:
+// NCCL over NVLink (device buffers, loaded with dlopen so single-GPU use has
+// no NCCL dependency) and host callbacks (the caller moves host buffers, e.g.
+// with torch.distributed; used to run several ranks on one GPU in tests).
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string* err) {
+    if (h) return true;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) {
+      *err = "cannot dlopen libnccl.so.2";
+      return false;
+    }
+    auto sym = [&](const char* n) { return dlsym(h, n); };
+    GetUniqueId = (decltype(GetUniqueId))sym("ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))sym("ncclCommInitRank");
+    CommDestroy = (decltype(CommDestroy))sym("ncclCommDestroy");
+    AllReduce = (decltype(AllReduce))sym("ncclAllReduce");
+    Send = (decltype(Send))sym("ncclSend");
+    Recv = (decltype(Recv))sym("ncclRecv");
+    GroupStart = (decltype(GroupStart))sym("ncclGroupStart");
+    GroupEnd = (decltype(GroupEnd))sym("ncclGroupEnd");
+    GetErrorString = (decltype(GetErrorString))sym("ncclGetErrorString");
+    if (!GetUniqueId || !CommInitRank || !AllReduce || !Send || !Recv || !GroupStart ||
+        !GroupEnd) {
+      *err = "libnccl.so.2 lacks required symbols";
+      return false;
+    }
+    return true;
+  }
 };
-topo_status comm_halo(Comm*, topo_ctx* ctx, double*) {
-  return fail(ctx, TOPO_ENCCL, "multi-GPU communication is not available");
+NcclApi g_nccl;
+}  // namespace
+
+struct Comm {
+  int kind = 0;  // 1 NCCL, 2 host callbacks
+  ncclComm_t nccl = nullptr;
+  topo_host_comm hc{};
+  std::vector<double> sl, sr, rl, rr, tmp;  // host staging (callback backend)
+  DevBuf dtmp;
+};
+
+#define NCK(x)                                                                        \
+  do {                                                                                \
+    ncclResult_t r_ = (x);                                                            \
+    if (r_ != ncclSuccess)                                                            \
+      return fail(ctx, TOPO_ENCCL, "%s failed: %s", #x,                               \
+                  g_nccl.GetErrorString ? g_nccl.GetErrorString(r_) : "nccl error");  \
+  } while (0)
+
+// columns exchanged with the neighbours of this slab
+static void halo_plan(const topo_ctx* ctx, long long* sendL, long long* sendR, long long* recvL,
+                      long long* recvR) {
+  const Geo& G = ctx->G;
+  const int j1 = G.j0 + G.jn, h = ctx->reach, nx = G.nelx;
+  const bool left = G.j0 > 0, right = j1 < nx;
+  *recvL = left ? (long long)(G.j0 - G.sj0) : 0;
+  *recvR = right ? (long long)(G.sj0 + G.sjn - j1) : 0;
+  // what the neighbours store of this slab: their halos reach h columns in
+  *sendL = left ? std::min<long long>(h, G.jn) : 0;
+  *sendR = right ? std::min<long long>(h, G.jn) : 0;
 }
-topo_status comm_allreduce(Comm*, topo_ctx* ctx, double*, int) {
-  return fail(ctx, TOPO_ENCCL, "multi-GPU communication is not available");
+
+topo_status comm_halo(Comm* c, topo_ctx* ctx, double* st) {
+  const Geo& G = ctx->G;
+  long long sL, sR, rL, rR;
+  halo_plan(ctx, &sL, &sR, &rL, &rR);
+  const long long S = G.S;
+  double* own = st + (long long)(G.j0 - G.sj0) * S;
+  const double* sendL = own;
+  const double* sendR = own + (long long)(G.jn - sR) * S;
+  double* recvL = st;
+  double* recvR = own + (long long)G.jn * S;
+  if (c->kind == 1) {
+    NCK(g_nccl.GroupStart());
+    if (sL) NCK(g_nccl.Send(sendL, size_t(sL * S), ncclDouble, ctx->rank - 1, c->nccl, ctx->stream));
+    if (rL) NCK(g_nccl.Recv(recvL, size_t(rL * S), ncclDouble, ctx->rank - 1, c->nccl, ctx->stream));
+    if (sR) NCK(g_nccl.Send(sendR, size_t(sR * S), ncclDouble, ctx->rank + 1, c->nccl, ctx->stream));
+    if (rR) NCK(g_nccl.Recv(recvR, size_t(rR * S), ncclDouble, ctx->rank + 1, c->nccl, ctx->stream));
+    NCK(g_nccl.GroupEnd());
+    return TOPO_OK;
+  }
+  c->sl.resize(size_t(sL * S));
+  c->sr.resize(size_t(sR * S));
+  c->rl.resize(size_t(rL * S));
+  c->rr.resize(size_t(rR * S));
+  if (sL) CK(cudaMemcpyAsync(c->sl.data(), sendL, sizeof(double) * c->sl.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  if (sR) CK(cudaMemcpyAsync(c->sr.data(), sendR, sizeof(double) * c->sr.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (c->hc.exchange(c->hc.user, c->sl.data(), sL * S, c->sr.data(), sR * S, c->rl.data(), rL * S,
+                     c->rr.data(), rR * S))
+    return fail(ctx, TOPO_ENCCL, "host halo exchange callback failed");
+  if (rL) CK(cudaMemcpyAsync(recvL, c->rl.data(), sizeof(double) * c->rl.size(), cudaMemcpyHostToDevice, ctx->stream));
+  if (rR) CK(cudaMemcpyAsync(recvR, c->rr.data(), sizeof(double) * c->rr.size(), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
 }
-topo_status comm_allreduce_host(Comm*, topo_ctx* ctx, double*, int) {
-  return fail(ctx, TOPO_ENCCL, "multi-GPU communication is not available");
+
+topo_status comm_allreduce(Comm* c, topo_ctx* ctx, double* dev, int n) {
+  if (c->kind == 1) {
+    NCK(g_nccl.AllReduce(dev, dev, size_t(n), ncclDouble, ncclSum, c->nccl, ctx->stream));
+    return TOPO_OK;
+  }
+  c->tmp.resize(size_t(n));
+  CK(cudaMemcpyAsync(c->tmp.data(), dev, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (c->hc.allreduce_sum(c->hc.user, c->tmp.data(), n))
+    return fail(ctx, TOPO_ENCCL, "host allreduce callback failed");
+  CK(cudaMemcpyAsync(dev, c->tmp.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
 }
-topo_status comm_oc_volume(Comm*, topo_ctx* ctx, double, double, double*) {
-  return fail(ctx, TOPO_ENCCL, "multi-GPU communication is not available");
+
+topo_status comm_allreduce_host(Comm* c, topo_ctx* ctx, double* host, int n) {
+  if (c->kind == 2) {
+    if (c->hc.allreduce_sum(c->hc.user, host, n))
+      return fail(ctx, TOPO_ENCCL, "host allreduce callback failed");
+    return TOPO_OK;
+  }
+  CK(c->dtmp.ensure(sizeof(double) * size_t(n)));
+  CK(cudaMemcpyAsync(c->dtmp.p, host, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  NCK(g_nccl.AllReduce(c->dtmp.p, c->dtmp.p, size_t(n), ncclDouble, ncclSum, c->nccl, ctx->stream));
+  CK(cudaMemcpyAsync(host, c->dtmp.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
 }
-void comm_destroy(Comm* c) { delete c; }
-extern "C" topo_status topo_comm_init_nccl(topo_ctx* ctx, const void*) {
-  return fail(ctx, TOPO_ENCCL, "multi-GPU communication is not available");
+
+// K speculative OC volume sums over this slab, allreduced: V(s_q) for q < K
+topo_status comm_oc_volumes(Comm* c, topo_ctx* ctx, const double* s, int K, double add_const,
+                            double* v) {
+  const Geo& G = ctx->G;
+  const int nb = grid_for(ctx, G.m);
+  double* dreq = ctx->result.as<double>() + 40;  // K <= 16 requests
+  CK(cudaMemcpyAsync(dreq, s, sizeof(double) * K, cudaMemcpyHostToDevice, ctx->stream));
+  k_oc_batch<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->rec.as<double4>(), dreq, K,
+                                                ctx->partials.as<double>());
+  LAUNCHED();
+  double* sums = ctx->partials0.as<double>();
+  k_reduce_rows<<<K, 256, 0, ctx->stream>>>(ctx->partials.as<double>(), nb, sums);
+  LAUNCHED();
+  TRY(comm_allreduce(c, ctx, sums, K));
+  CK(cudaMemcpyAsync(v, sums, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  for (int q = 0; q < K; ++q) v[q] = (add_const + v[q]) / ctx->m_total;
+  return TOPO_OK;
+}
+
+topo_status comm_oc_volume(Comm* c, topo_ctx* ctx, double s, double add_const, double* v) {
+  return comm_oc_volumes(c, ctx, &s, 1, add_const, v);
+}
+
+void comm_destroy(Comm* c) {
+  if (!c) return;
+  if (c->kind == 1 && c->nccl && g_nccl.CommDestroy) g_nccl.CommDestroy(c->nccl);
+  c->dtmp.release();
+  delete c;
+}
+
+// after the communicator exists: |P1| over all ranks, hs and the volume
+// weights over the halo-extended slab
+static topo_status comm_finish_setup(topo_ctx* ctx) {
+  double ns = double(ctx->nS_local);
+  TRY(comm_allreduce_host(ctx->comm, ctx, &ns, 1));
+  ctx->nS_total = ns;
+  return setup_filter_fields(ctx);
+}
+
+extern "C" topo_status topo_nccl_unique_id(void* out128) {
+  std::string err;
+  if (!g_nccl.load(&err)) return TOPO_ENCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return TOPO_ENCCL;
+  memcpy(out128, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return TOPO_OK;
+}
+
+extern "C" topo_status topo_comm_init_nccl(topo_ctx* ctx, const void* uid) {
+  if (!ctx || !uid) return TOPO_EINVAL;
+  if (ctx->comm) return fail(ctx, TOPO_EINVAL, "communicator already initialised");
+  std::string err;
+  if (!g_nccl.load(&err)) return fail(ctx, TOPO_ENCCL, "%s", err.c_str());
+  CK(cudaSetDevice(ctx->device));
+  ncclUniqueId id;
+  memcpy(id.internal, uid, NCCL_UNIQUE_ID_BYTES);
+  Comm* c = new Comm;
+  c->kind = 1;
+  ncclResult_t r = g_nccl.CommInitRank(&c->nccl, ctx->nranks, id, ctx->rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(ctx, TOPO_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r));
+  }
+  ctx->comm = c;
+  return comm_finish_setup(ctx);
+}
+
+extern "C" topo_status topo_comm_init_host(topo_ctx* ctx, const topo_host_comm* hc) {
+  if (!ctx || !hc || !hc->exchange || !hc->allreduce_sum) return TOPO_EINVAL;
+  if (ctx->comm) return fail(ctx, TOPO_EINVAL, "communicator already initialised");
+  Comm* c = new Comm;
+  c->kind = 2;
+  c->hc = *hc;
+  ctx->comm = c;
+  return comm_finish_setup(ctx);
+}
+
+// host-only slab plan (no device work): j0, j1, sj0, sj1 and the halo columns
+// exchanged with the left / right neighbours (send L, send R, recv L, recv R)
+extern "C" topo_status topo_slab_plan(const topo_grid_desc* d, int64_t* out) {
+  if (!d || !out || d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks) return TOPO_EINVAL;
+  const int reach = int(ceil(d->rmin)) - 1;
+  int j0, jn, sj0, sjn;
+  slab_columns(d, reach, &j0, &jn, &sj0, &sjn);
+  const int j1 = j0 + jn;
+  const bool left = j0 > 0, right = j1 < d->nelx;
+  out[0] = j0;
+  out[1] = j1;
+  out[2] = sj0;
+  out[3] = sj0 + sjn;
+  out[4] = left ? std::min(reach, jn) : 0;
+  out[5] = right ? std::min(reach, jn) : 0;
+  out[6] = left ? j0 - sj0 : 0;
+  out[7] = right ? sj0 + sjn - j1 : 0;
+  return (d->nranks > 1 && jn < reach) ? TOPO_EINVAL : TOPO_OK;
 }

@@ -908,6 +908,39 @@ __global__ void __launch_bounds__(kThreads) k_oc_final(long long m, const double
     out[e] = oc_cand(rec[e], s);
 }
 
+// K block partial volume sums at the multipliers s[0..K) (multi-GPU OC round)
+__global__ void __launch_bounds__(kThreads) k_oc_batch(long long m, const double4* __restrict__ rec,
+                                                       const double* __restrict__ s, int K,
+                                                       double* __restrict__ partials) {
+  __shared__ double scratch[kOcK * 32];
+  __shared__ double sreq[kOcK];
+  if (threadIdx.x < kOcK) sreq[threadIdx.x] = threadIdx.x < K ? s[threadIdx.x] : 0.0;
+  __syncthreads();
+  double acc[kOcK];
+#pragma unroll
+  for (int q = 0; q < kOcK; ++q) acc[q] = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double4 r = rec[e];
+#pragma unroll
+    for (int q = 0; q < kOcK; ++q)
+      if (q < K) acc[q] = fma(r.w, oc_cand(r, sreq[q]), acc[q]);
+  }
+  block_sum<kOcK>(acc, scratch);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < K; ++q) partials[(long long)q * gridDim.x + blockIdx.x] = acc[q];
+}
+
+// row q of a [rows][count] partial table summed in a fixed order by block q
+__global__ void k_reduce_rows(const double* __restrict__ p, int count, double* __restrict__ out) {
+  __shared__ double scratch[32];
+  double v[1] = {0.0};
+  const double* row = p + (long long)blockIdx.x * count;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) v[0] += row[i];
+  block_sum<1>(v, scratch);
+  if (threadIdx.x == 0) out[blockIdx.x] = v[0];
+}
+
 // candidate at one multiplier (host-driven OC modes and final write)
 __global__ void k_oc_candidates(long long m, const double4* __restrict__ rec, double s,
                                 double* __restrict__ out) {

@@ -1,0 +1,100 @@
+"""x-slab decomposition on the GPU: N rank contexts (threads, one GPU, host
+exchange through ThreadHostComm) reproduce the single-context pass. The
+kernels of different ranks never wait on one another; every exchange and
+allreduce happens on the host between launches. With >= 2 GPUs the same
+ranks also run over NCCL."""
+import threading
+
+import numpy as np
+import pytest
+
+from tests.common import rand_case, rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2005_05436_b200 as P
+    return P
+
+
+def run_ranks(P, cfg, x, u, state, nranks, nccl=False):
+    from paper_2005_05436_b200.dist import ThreadHostComm, make_rank_context, slab_views
+    comm = ThreadHostComm(nranks)
+    out = [None] * nranks
+    err = [None] * nranks
+
+    def work(r):
+        try:
+            j0, j1, xs, us, st = slab_views(cfg, x, u, state, r, nranks)
+            ctx = make_rank_context(cfg, st, r, nranks, comm=comm.for_rank(r))
+            try:
+                out[r] = ctx.design_pass(xs, us, beta=cfg.beta, move=cfg.move, volfrac=cfg.volfrac,
+                                         return_sk=True)
+            finally:
+                ctx.close()
+        except Exception as e:  # noqa: BLE001
+            import traceback
+            err[r] = traceback.format_exc()
+            comm.barrier.abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in err:
+        assert e is None, e
+    return out
+
+
+def cat(rs, k):
+    return np.concatenate([getattr(r, k) for r in rs])
+
+
+@pytest.mark.parametrize("case,nranks", [("c4", 2), ("c4", 4), ("c2s", 2), ("c2s", 3),
+                                         ("c5s", 2), ("c3s", 2), ("c1", 4)])
+def test_slab_ranks_match_single_context(P, oracle_port, case, nranks):
+    from paper_2005_05436_b200.configs import CONFIGS, make_inputs
+    if case == "c4":
+        cfg = CONFIGS[4]
+    elif case == "c2s":
+        cfg = CONFIGS[2].scaled(150, 50)
+    elif case == "c5s":
+        cfg = CONFIGS[5].scaled(24, 24, 24)
+    elif case == "c3s":
+        cfg = CONFIGS[3].scaled(160, 80)
+    else:
+        cfg = CONFIGS[1]
+    x, u, state = make_inputs(cfg)
+    with P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu, state=state) as ctx:
+        ref = ctx.design_pass(x, u, beta=cfg.beta, move=cfg.move, volfrac=cfg.volfrac,
+                              return_sk=True)
+    rs = run_ranks(P, cfg, x, u, state, nranks)
+    eta = rs[0].eta
+    assert all(r.eta == eta for r in rs)  # every rank takes the same decisions
+    assert abs(eta - ref.eta) <= 5e-8
+    assert rel(cat(rs, "xTilde"), ref.xTilde) <= 1e-12
+    assert abs(sum(r.c for r in rs[:1]) - ref.c) <= 1e-12 * abs(ref.c)  # c is allreduced
+    if eta == ref.eta:
+        for k in ("xPhys", "dcPhys", "dc", "dV", "sK"):
+            assert rel(cat(rs, k), getattr(ref, k)) <= 1e-12, k
+    # conditioned on the ranks' eta: the oracle of the whole domain
+    rc = oracle_port.design_pass(cfg.grid, cfg.rmin, x, u, state, beta=cfg.beta, move=cfg.move,
+                                 volfrac=cfg.volfrac, eta_override=eta, volume_mode=4)
+    for k in ("xPhys", "dc", "dV", "xNew"):
+        assert rel(cat(rs, k), getattr(rc, k)) <= 1e-12, k
+    assert all(r.bisections == rc.bisections and r.lam == rs[0].lam for r in rs)
+    assert abs(rs[0].lam - rc.lam) <= 1e-10 * abs(rc.lam)
+
+
+def test_slab_narrower_than_reach_rejected(P):
+    with pytest.raises(ValueError):
+        P.Context(64, 10, 0, rmin=35.0, rank=1, nranks=4)
+
+
+def test_nccl_two_gpus(P):
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs (NCCL ranks cannot share a GPU)")
