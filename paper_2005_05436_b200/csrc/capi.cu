@@ -327,12 +327,16 @@ topo_status reduce_on_device(topo_ctx* ctx, const double* partials, int count, d
   return TOPO_OK;
 }
 
+// device scratch layout of ctx->result (64 doubles): [0..5) pass scalars
+// (eta, iterations, g, -, c), [8..15) OC results, [24..36) pre-reductions,
+// [40..56) OC requests, [56..64) reduce_to_host
 template <int N>
 topo_status reduce_to_host(topo_ctx* ctx, const double* partials, int count) {
-  k_reduce_partials<N><<<1, 32, 0, ctx->stream>>>(partials, count, N, ctx->result.as<double>());
+  double* dst = ctx->result.as<double>() + 56;
+  k_reduce_partials<N><<<1, 32, 0, ctx->stream>>>(partials, count, N, dst);
   LAUNCHED();
-  if (ctx->comm) TRY(comm_allreduce(ctx->comm, ctx, ctx->result.as<double>(), N));
-  CK(cudaMemcpyAsync(ctx->h_result, ctx->result.p, sizeof(double) * N, cudaMemcpyDeviceToHost,
+  if (ctx->comm) TRY(comm_allreduce(ctx->comm, ctx, dst, N));
+  CK(cudaMemcpyAsync(ctx->h_result, dst, sizeof(double) * N, cudaMemcpyDeviceToHost,
                      ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return TOPO_OK;
@@ -383,7 +387,8 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
                    double eta, double beta, topo_volume_fn cb, void* user) {
   const Geo& G = ctx->G;
   const double add_const = mode == TOPO_VOL_FILTERED ? ctx->nS_total : 0.0;
-  if ((mode == TOPO_VOL_MEAN || mode == TOPO_VOL_FILTERED) && !ctx->comm) {
+  static const bool force_host = getenv("TOPO_OC_HOST") != nullptr;  // debugging aid
+  if ((mode == TOPO_VOL_MEAN || mode == TOPO_VOL_FILTERED) && !ctx->comm && !force_host) {
     OcArgs A;
     A.m = G.m;
     A.rec = ctx->rec.as<double4>();
@@ -442,9 +447,16 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
       while (ctl.pending()) ctl.feed(smode > 0 ? INFINITY : -INFINITY);
     }
     double req[kOcK], val[kOcK];
+    static const bool dbg = getenv("TOPO_DEBUG") != nullptr;
+    if (dbg)
+      fprintf(stderr, "[rank %d] oc host: lamMax %.17g V0 %.17g Vinf %.17g add %.17g smode %d\n",
+              ctx->rank, lamMax, V0, Vinf, add_const, smode);
     while (ctl.pending()) {
       const int K = oc_speculate<kOcK>(ctl, req);
       TRY(comm_oc_volumes(ctx->comm, ctx, req, K, add_const, val));
+      if (dbg)
+        for (int q = 0; q < K; ++q)
+          fprintf(stderr, "[rank %d]   s %.17g V %.17g\n", ctx->rank, req[q], val[q]);
       while (ctl.pending()) {
         int hit = -1;
         for (int q = 0; q < K; ++q)
@@ -846,6 +858,9 @@ topo_status topo_device_buffer(topo_ctx* ctx, int which, void** ptr, int64_t* co
     case TOPO_BUF_JK: *ptr = ctx->jK.p; if (count) *count = ctx->jK.p ? G.m * G.P : 0; break;
     case TOPO_BUF_XNEW: *ptr = ctx->xnew.p; if (count) *count = G.m; break;
     case TOPO_BUF_XPHYS: *ptr = ctx->xphys.p; if (count) *count = G.m; break;
+    case 100: *ptr = ctx->cw.p; if (count) *count = G.m; break;       // debugging aids
+    case 101: *ptr = ctx->hs_st.p; if (count) *count = ctx->m_st; break;
+    case 102: *ptr = ctx->hs.p; if (count) *count = G.m; break;
     default: return fail(ctx, TOPO_EINVAL, "unknown buffer %d", which);
   }
   return TOPO_OK;
@@ -1554,7 +1569,7 @@ topo_status comm_oc_volumes(Comm* c, topo_ctx* ctx, const double* s, int K, doub
   double* sums = ctx->partials0.as<double>();
   k_reduce_rows<<<K, 256, 0, ctx->stream>>>(ctx->partials.as<double>(), nb, sums);
   LAUNCHED();
-  TRY(comm_allreduce(c, ctx, sums, K));
+  if (c) TRY(comm_allreduce(c, ctx, sums, K));
   CK(cudaMemcpyAsync(v, sums, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   for (int q = 0; q < K; ++q) v[q] = (add_const + v[q]) / ctx->m_total;

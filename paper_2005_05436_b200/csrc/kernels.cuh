@@ -338,10 +338,20 @@ __global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const Conv
       jo = 0;
       jr = fold(G.j0 + br + tr - T.reach, G.nelx);
     }
+    // -1: zero line (outside the domain, Dirichlet; or, with an input field,
+    // a column this slab does not store: such values only meet zero-padded
+    // weights or outputs beyond the tile, the slab setup guarantees every
+    // real tap is stored). A null input is the all-ones field: any in-domain
+    // line is valid (index 0 marks it).
     long long src = -1;
-    if (jo >= 0 && jr >= 0)  // a stored column is guaranteed by the slab setup
-      src = G.is3d ? ((long long)(jo - G.sj0) * G.nz + jr) * G.nely
-                   : (long long)(jr - G.sj0) * G.nely;
+    const int jcol = G.is3d ? jo : jr;
+    if (jo >= 0 && jr >= 0) {
+      if (A.in0 == nullptr)
+        src = 0;
+      else if (jcol >= G.sj0 && jcol < G.sj0 + G.sjn)
+        src = G.is3d ? ((long long)(jo - G.sj0) * G.nz + jr) * G.nely
+                     : (long long)(jr - G.sj0) * G.nely;
+    }
     lineSrc[line] = src;
     lineDst[line] = to * sPlane + tr;
   }
