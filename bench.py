@@ -193,7 +193,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     import torch
     import paper_2005_05436_b200 as P
     from paper_2005_05436_b200 import _lib as L
-    from paper_2005_05436_b200.configs import make_inputs, slab_of
+    from paper_2005_05436_b200.configs import make_inputs
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -201,22 +201,10 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     if world == 1:
         ctx = P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu, device=local_rank, state=state)
-    else:
-        S = cfg.nely * (cfg.nelz or 1)
-        base, rem = divmod(cfg.nelx, world)
-        j0 = rank * base + min(rank, rem)
-        j1 = j0 + base + (1 if rank < rem else 0)
-        xs, us = slab_of(cfg, x, u, j0, j1)
-        st = None if state is None else state[j0 * S:j1 * S]
-        ctx = P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu, device=local_rank, rank=rank,
-                        nranks=world, j0=j0, j1=j1, state=st)
-        import torch.distributed as dist
-        uid = torch.zeros(128, dtype=torch.uint8)
-        if rank == 0:
-            uid = torch.from_numpy(np.frombuffer(P.nccl_unique_id(), dtype=np.uint8).copy())
-        dist.broadcast(uid, 0)
-        ctx.comm_init(bytes(uid.numpy()))
-        x, u = xs, us
+    else:  # x-slab of this rank; halos and sums over NCCL (NVLink)
+        from paper_2005_05436_b200.dist import make_rank_context, slab_views
+        _, _, x, u, st = slab_views(cfg, x, u, state, rank, world)
+        ctx = make_rank_context(cfg, st, rank, world, device=local_rank)
     m_local = ctx.m
     xd = torch.from_numpy(x).to(dev)
     ud = torch.from_numpy(u).to(dev)
