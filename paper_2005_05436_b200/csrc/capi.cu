@@ -384,7 +384,8 @@ topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
 // records (ctx->rec) and prep partials must be ready; writes xNew (device)
 topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const double* prep,
                    int n_prep, double* xnew_dev, double* lam, int32_t* bis, int32_t* evals,
-                   double eta, double beta, topo_volume_fn cb, void* user) {
+                   double eta, double beta, topo_volume_fn cb, void* user,
+                   bool* deferred = nullptr) {
   const Geo& G = ctx->G;
   const double add_const = mode == TOPO_VOL_FILTERED ? ctx->nS_total : 0.0;
   static const bool force_host = getenv("TOPO_OC_HOST") != nullptr;  // debugging aid
@@ -408,11 +409,30 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
     A.partials = ctx->partials.as<double>();
     A.xNew = xnew_dev;
     A.result = ctx->result.as<double>() + 8;
-    TRY(coop_launch(ctx, (const void*)k_oc_bisect, &A, ctx->coop_blocks));
+    A.dbg = nullptr;
+    static const bool prof = getenv("TOPO_OC_PROFILE") != nullptr;  // profiling aid
+    if (prof) {
+      CK(ctx->tmp1.ensure(sizeof(long long) * 128));
+      A.dbg = ctx->tmp1.as<long long>();
+    }
+    // 4 bisection levels per grid-wide round (k_oc_bisect<32> does 5 levels;
+    // measured slower on C1-C3: 224 registers, one block per SM)
+    TRY(coop_launch(ctx, (const void*)k_oc_bisect<16>, &A, ctx->coop_blocks));
+    if (prof) {
+      long long h[128];
+      CK(cudaMemcpy(h, A.dbg, sizeof h, cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[oc profile] blocks %d marks %lld:", ctx->coop_blocks, h[127]);
+      for (int q = 1; q < h[127]; ++q) fprintf(stderr, " %lld", h[q] - h[q - 1]);
+      fprintf(stderr, "\n");
+    }
     k_oc_final<<<grid_for(ctx, G.m), kThreads, 0, ctx->stream>>>(G.m, A.rec, A.result, xnew_dev);
     LAUNCHED();
     CK(cudaMemcpyAsync(ctx->h_result + 8, A.result, sizeof(double) * 7, cudaMemcpyDeviceToHost,
                        ctx->stream));
+    if (deferred) {  // the caller reads h_result[8..15) after its own final sync
+      *deferred = true;
+      return TOPO_OK;
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     const double* r = ctx->h_result + 8;
     if (int(r[3]) == OcCtl::ST_NONMONO)
@@ -747,17 +767,20 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   if (d->nranks > 1) CKC(ctx->x_st.ensure(sd));
 
   int occ = 0;
-  CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_oc_bisect, kThreads, 0));
+  CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_oc_bisect<16>, kThreads, 0));
   int occ2 = 0;
   CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_eta_solve, kThreads, 0));
   if (occ < 1 || occ2 < 1)
     return bail(fail(ctx, TOPO_ECUDA, "cooperative kernels cannot be resident"));
   // all blocks resident (cooperative); one per SM in overlap mode, where the
   // sK stream shares the SMs
-  ctx->coop_eta = ctx->sm_count * occ2;
-  ctx->coop_blocks = ctx->overlap_sk ? ctx->sm_count : ctx->sm_count * occ;
+  // (small grids: fewer blocks, cheaper grid-wide barriers)
+  const int want = int(std::min<long long>(1LL << 20, (G.m + 1023) / 1024));
+  ctx->coop_eta = std::max(1, std::min(ctx->sm_count * occ2, want));
+  ctx->coop_blocks =
+      std::max(1, std::min(ctx->overlap_sk ? ctx->sm_count : ctx->sm_count * occ, want));
   const size_t npart = std::max<size_t>(
-      {size_t(conv_blocks(ctx)) * 3, size_t(ctx->coop_blocks) * 2 * kOcK * 2,
+      {size_t(conv_blocks(ctx)) * 3, size_t(ctx->coop_blocks) * 2 * 32 * 2,
        size_t(ctx->coop_eta) * 2 * 2,
        size_t(ctx->sm_count) * 8 * 4});
   CKC(ctx->partials.ensure(sizeof(double) * npart));
@@ -1360,8 +1383,9 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   topo_oc_params oc{prm->move, prm->volfrac, 1e-4, 1e-3, 0, 1e-8, 0.0};  // oc.hpp:14-20 defaults
   double lam = 0;
   int32_t bis = 0, ev = 0;
+  bool oc_deferred = false;
   TRY(run_oc(ctx, &oc, vmode, ctx->partials0.as<double>(), nb4, ctx->xnew.as<double>(), &lam,
-             &bis, &ev, 0.0, prm->beta, nullptr, nullptr));
+             &bis, &ev, 0.0, prm->beta, nullptr, nullptr, &oc_deferred));
   tmark(ctx, TOPO_STAGE_OC, 1, ctx->stream);
   if (overlap) {
     CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
@@ -1387,6 +1411,14 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
                        ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   double c = ctx->h_result[4];
+  if (oc_deferred) {
+    const double* r = ctx->h_result + 8;
+    if (int(r[3]) == OcCtl::ST_NONMONO)
+      return fail(ctx, TOPO_ENONMONO, "oc: candidate volume is not monotone in the multiplier");
+    lam = r[0];
+    bis = int32_t(r[1]);
+    ev = int32_t(r[2]);
+  }
   if (ctx->comm) TRY(comm_allreduce_host(ctx->comm, ctx, &c, 1));
   if (ctx->timing) {
     for (int q = 0; q < TOPO_NSTAGES; ++q) {

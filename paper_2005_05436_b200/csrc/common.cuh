@@ -75,6 +75,19 @@ __device__ __forceinline__ void block_sum(double (&v)[N], double* scratch) {
   __syncthreads();
 }
 
+// Fixed-order sum of p[start], p[start + step], ... (< n), read through L2
+// (__ldcg: written by other blocks) with 8 loads in flight.
+__device__ __forceinline__ double strided_sum_l2(const double* p, int n, int start, int step,
+                                                 int elem_stride = 1, int comp = 0) {
+  double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int i = start;
+  for (; i + 7 * step < n; i += 8 * step)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] += __ldcg(p + (long long)(i + u * step) * elem_stride + comp);
+  for (int u = 0; i < n; i += step, ++u) a[u] += __ldcg(p + (long long)i * elem_stride + comp);
+  return ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+}
+
 // Sum `count` partial records of stride `stride` (component q at p[i*stride+q])
 // with one warp, in a fixed order; every lane of the calling warp gets the
 // totals. Used identically by every block of a cooperative kernel so that all
@@ -84,10 +97,7 @@ __device__ __forceinline__ void warp_sum_partials(const double* p, int count, in
                                                   double (&out)[N]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int q = 0; q < N; ++q) out[q] = 0.0;
-  for (int i = lane; i < count; i += 32)
-#pragma unroll
-    for (int q = 0; q < N; ++q) out[q] += __ldcg(p + (long long)i * stride + q);
+  for (int q = 0; q < N; ++q) out[q] = strided_sum_l2(p, count, lane, 32, stride, q);
   warp_sum<N>(out);
 }
 

@@ -202,65 +202,66 @@ struct OcCtl {
 ///             then the first 3 bisection levels under hi = sqrt(lamMax);
 ///   vLo:      0, then 4 bisection levels;
 ///   bisection (sqrt or lambda space): the full tree of the next 4 levels.
+// Breadth-first midpoints of [lo, hi] for DEPTH levels (2^DEPTH - 1 values),
+// fully unrolled so the arrays stay in registers on the device.
+template <int DEPTH>
+__host__ __device__ inline int oc_tree(double lo, double hi, bool lambda_space, double* out) {
+  constexpr int W = 1 << DEPTH;  // interval endpoints of the deepest level
+  double b[W + 1];               // endpoints in order: b[0] = lo, b[W] = hi
+  b[0] = lo;
+  b[W] = hi;
+  int n = 0;
+#pragma unroll
+  for (int d = 0; d < DEPTH; ++d) {
+    const int stride = W >> d, half = stride >> 1;
+#pragma unroll
+    for (int q = 0; q < (1 << d); ++q) {
+      const double mid = 0.5 * (b[q * stride] + b[q * stride + stride]);  // oc.hpp:158
+      b[q * stride + half] = mid;
+      out[n++] = lambda_space ? sqrt(mid) : mid;
+    }
+  }
+  return n;
+}
+
+/// Speculative request set: every multiplier the controller can request in
+/// the next few feeds, generated with the controller's own arithmetic (so
+/// the values compare bit-equal with the replayed requests):
+///   widening: sqrt(lamMax * 4^k) for the next 4 widenings, then 0 (vLo),
+///             then the first 3 bisection levels under hi = sqrt(lamMax);
+///   vLo:      0, then 4 bisection levels;
+///   bisection (sqrt or lambda space): the full tree of the next 4 levels.
+/// KMAX 16: 4 levels per batch; KMAX >= 32: 5 levels (fewer grid-wide
+/// rounds when evaluating is cheap).
 template <int KMAX>
 __host__ __device__ inline int oc_speculate(const OcCtl& c, double* out) {
+  static_assert(KMAX >= 16, "request buffer too small");
+  constexpr int L = KMAX >= 32 ? 5 : 4;
   int n = 0;
-  auto push = [&](double v) {
-    for (int q = 0; q < n; ++q)
-      if (out[q] == v) return;
-    if (n < KMAX) out[n++] = v;
-  };
-  // breadth-first midpoints of [lo, hi] (sqrt space, or lambda space -> sqrt)
-  auto tree = [&](double lo, double hi, int depth, bool lambda_space) {
-    double los[16], his[16];
-    int cnt = 1;
-    los[0] = lo;
-    his[0] = hi;
-    for (int d = 0; d < depth; ++d) {
-      double nlo[16], nhi[16];
-      int nn = 0;
-      for (int q = 0; q < cnt; ++q) {
-        const double mid = 0.5 * (los[q] + his[q]);
-        push(lambda_space ? sqrt(mid) : mid);
-        if (nn + 2 <= 16) {
-          nlo[nn] = los[q];
-          nhi[nn++] = mid;
-          nlo[nn] = mid;
-          nhi[nn++] = his[q];
-        }
-      }
-      for (int q = 0; q < nn; ++q) {
-        los[q] = nlo[q];
-        his[q] = nhi[q];
-      }
-      cnt = nn;
-    }
-  };
-  if (c.pending()) push(c.s_req);  // the pending request first
   switch (c.phase) {
     case OcCtl::P_WIDEN0:
     case OcCtl::P_WIDEN: {
       double lm = c.lamMax;
-      push(sqrt(lm));
+      out[n++] = sqrt(lm);  // the pending request
       for (int k = 0; k < 3; ++k) {
         lm *= 4.0;
-        push(sqrt(lm));
+        out[n++] = sqrt(lm);
       }
-      push(0.0);
-      if (!c.lambdaSpace) tree(0.0, sqrt(c.lamMax), 3, false);
-      else tree(0.0, c.lamMax, 3, true);
+      out[n++] = 0.0;
+      n += c.lambdaSpace ? oc_tree<L - 1>(0.0, c.lamMax, true, out + n)
+                         : oc_tree<L - 1>(0.0, sqrt(c.lamMax), false, out + n);
       break;
     }
     case OcCtl::P_VLO:
-      push(0.0);
-      if (!c.lambdaSpace) tree(0.0, sqrt(c.lamMax), 4, false);
-      else tree(0.0, c.lamMax, 4, true);
+      out[n++] = 0.0;
+      n += c.lambdaSpace ? oc_tree<L>(0.0, c.lamMax, true, out + n)
+                         : oc_tree<L>(0.0, sqrt(c.lamMax), false, out + n);
       break;
     case OcCtl::P_BIS:
-      tree(c.lo, c.hi, 4, false);
+      n = oc_tree<L>(c.lo, c.hi, false, out);
       break;
     case OcCtl::P_LSBIS:
-      tree(c.lo, c.hi, 4, true);
+      n = oc_tree<L>(c.lo, c.hi, true, out);
       break;
     default:
       break;

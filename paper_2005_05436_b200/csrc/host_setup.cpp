@@ -142,7 +142,8 @@ typedef double (*topo_sfun)(void* user, double s);
 typedef void (*topo_gfun)(void* user, double eta, double* g, double* gp);
 
 // oc.hpp:93-174 replay; V(s) from `vol`. speculative = 1 evaluates requests
-// in the batches the device kernel uses (oc_speculate) and replays them.
+// in the batches the device kernel uses (oc_speculate; 1: 16 requests per
+// batch, 2: 32) and replays them.
 int topo_host_oc_replay(const topo_oc_params* prm, double lamMax, topo_sfun vol, void* user,
                         int speculative, double* lambda, int32_t* bisections,
                         int32_t* evaluations, double* s_final, int32_t* batches) {
@@ -153,9 +154,9 @@ int topo_host_oc_replay(const topo_oc_params* prm, double lamMax, topo_sfun vol,
   if (!speculative) {
     while (c.pending()) c.feed(vol(user, c.s_req));
   } else {
-    double req[16], val[16];
+    double req[32], val[32];
     while (c.pending()) {
-      const int n = topo::oc_speculate<16>(c, req);
+      const int n = speculative >= 2 ? topo::oc_speculate<32>(c, req) : topo::oc_speculate<16>(c, req);
       for (int q = 0; q < n; ++q) val[q] = vol(user, req[q]);
       ++nb;
       while (c.pending()) {

@@ -189,6 +189,13 @@ __device__ __forceinline__ double oc_cand(const double4& r, double s) {
   const double f = s > 0 ? r.z / s : (r.z > 0 ? INFINITY : 0.0);
   return std_min(std_max(f, r.x), r.y);
 }
+// the same candidate with ocP / s taken as ocP * (1 / s) (inv_s = 1 / s for
+// s > 0, else +inf): within one ulp of the division, used only inside the
+// volume sums of the speculative batches (the written xNew uses oc_cand)
+__device__ __forceinline__ double oc_cand_rcp(const double4& r, double s, double inv_s) {
+  const double f = s > 0 ? r.z * inv_s : (r.z > 0 ? INFINITY : 0.0);
+  return std_min(std_max(f, r.x), r.y);
+}
 
 // Tile geometry of one conv launch. Lanes run along i (the fastest memory
 // axis); each thread owns R consecutive outputs along the "run" axis (k in 3D,
@@ -477,16 +484,20 @@ __device__ __forceinline__ void eta_block_eval(const EtaArgs& A, double eta, boo
 // partials in the same order and takes the same Newton decision
 __global__ void __launch_bounds__(kThreads) k_eta_solve(EtaArgs A) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ EtaCtl ctl;
+  EtaCtl ctl;  // replayed by thread 0 of every block (registers, not shared memory)
   __shared__ double scratch[2 * 32];
   __shared__ int cont;
-  if (threadIdx.x == 0) ctl.init(A.eta0);
+  __shared__ double s_eta;
+  if (threadIdx.x == 0) {
+    ctl.init(A.eta0);
+    s_eta = ctl.eta;
+  }
   __syncthreads();
   int buf = 0;
   bool first = true;
   for (;;) {
     double red[2];
-    eta_block_eval(A, ctl.eta, first, red);
+    eta_block_eval(A, s_eta, first, red);
     first = false;
     block_sum<2>(red, scratch);
     double* P = A.partials + (long long)buf * 2 * gridDim.x;
@@ -498,7 +509,10 @@ __global__ void __launch_bounds__(kThreads) k_eta_solve(EtaArgs A) {
     if (threadIdx.x < 32) {
       double s2[2];
       warp_sum_partials<2>(P, gridDim.x, 2, s2);
-      if (threadIdx.x == 0) cont = ctl.feed(s2[0] / A.mtotal, s2[1] / A.mtotal);
+      if (threadIdx.x == 0) {
+        cont = ctl.feed(s2[0] / A.mtotal, s2[1] / A.mtotal);
+        s_eta = ctl.eta;
+      }
     }
     buf ^= 1;
     __syncthreads();
@@ -808,15 +822,23 @@ struct OcArgs {
   double* partials;   // [2][kOcK][gridDim]
   double* xNew;       // full length (passives = x via their records)
   double* result;     // lambda, bisections, evaluations, status, batches, shortcut
+  long long* dbg;     // optional clock64 trace of block 0 (profiling aid)
 };
 
+template <int KK>  // requests per batch: 16 (4 levels) or 32 (5 levels)
 __global__ void __launch_bounds__(kThreads) k_oc_bisect(OcArgs A) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ OcCtl ctl;
-  __shared__ double sreq[kOcK];
-  __shared__ double sval[kOcK];
-  __shared__ int nreq, mode, nbatch;
-  __shared__ double scratch[kOcK * 32];
+  OcCtl ctl;  // replayed by thread 0 of every block (registers, not shared memory)
+  int mode = 0, nbatch = 0;
+  __shared__ double sreq[KK], sinv[KK];
+  __shared__ double sval[KK];
+  __shared__ int nreq;
+  __shared__ double scratch[KK * 32];
+  int ndbg = 0;
+  auto mark = [&]() {
+    if (A.dbg && blockIdx.x == 0 && threadIdx.x == 0 && ndbg < 120) A.dbg[ndbg++] = clock64();
+  };
+  mark();
   if (threadIdx.x < 32) {
     double s[3];
     warp_sum_partials<3>(A.prep_partials, A.n_prep, 3, s);
@@ -848,39 +870,48 @@ __global__ void __launch_bounds__(kThreads) k_oc_bisect(OcArgs A) {
         ctl.check_mono = 0;
         while (ctl.pending()) ctl.feed(mode > 0 ? INFINITY : -INFINITY);
       } else if (ctl.pending()) {
-        nreq = oc_speculate<kOcK>(ctl, sreq);
+        nreq = oc_speculate<KK>(ctl, sreq);
+        for (int q = 0; q < KK; ++q) {  // reciprocals for the batch sums (1/0 = inf)
+          if (q >= nreq) sreq[q] = 1.0;
+          sinv[q] = 1.0 / sreq[q];
+        }
       }
     }
     __syncthreads();
+    mark();
     if (nreq == 0) break;
     const int K = nreq;
-    double acc[kOcK];
+    double acc[KK];
 #pragma unroll
-    for (int q = 0; q < kOcK; ++q) acc[q] = 0.0;
+    for (int q = 0; q < KK; ++q) acc[q] = 0.0;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < A.m;
          e += (long long)gridDim.x * blockDim.x) {
       const double4 r = A.rec[e];
 #pragma unroll
-      for (int q = 0; q < kOcK; ++q)
-        if (q < K) acc[q] = fma(r.w, oc_cand(r, sreq[q]), acc[q]);
+      for (int q = 0; q < KK; ++q)
+        if (q < K) acc[q] = fma(r.w, oc_cand_rcp(r, sreq[q], sinv[q]), acc[q]);
     }
-    block_sum<kOcK>(acc, scratch);
-    double* P = A.partials + (long long)buf * kOcK * gridDim.x;
+    mark();
+    block_sum<KK>(acc, scratch);
+    double* P = A.partials + (long long)buf * KK * gridDim.x;
     if (threadIdx.x == 0)
       for (int q = 0; q < K; ++q) P[(long long)q * gridDim.x + blockIdx.x] = acc[q];
+    mark();
     grid.sync();
+    mark();
     // every block reduces the same partials in the same fixed order: 16
     // threads per request, all requests in parallel
     {
-      const int q = threadIdx.x >> 4, sub = threadIdx.x & 15;
+      constexpr int G = kThreads / KK;  // threads per request (16 or 8)
+      const int q = threadIdx.x / G, sub = threadIdx.x % G;
       double sum = 0.0;
-      if (q < K)
-        for (int i = sub; i < (int)gridDim.x; i += 16) sum += __ldcg(P + (long long)q * gridDim.x + i);
+      if (q < K) sum = strided_sum_l2(P + (long long)q * gridDim.x, gridDim.x, sub, G);
 #pragma unroll
-      for (int off = 8; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+      for (int off = G / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
       if (sub == 0 && q < K) sval[q] = (A.add_const + sum) / A.mtotal;
     }
     __syncthreads();
+    mark();
     if (threadIdx.x == 0) {
       ++nbatch;
       while (ctl.pending()) {
@@ -903,6 +934,7 @@ __global__ void __launch_bounds__(kThreads) k_oc_bisect(OcArgs A) {
     A.result[4] = nbatch;
     A.result[5] = mode;
     A.result[6] = ctl.s_final;
+    if (A.dbg) A.dbg[127] = ndbg;
   }
 }
 
@@ -926,15 +958,19 @@ __global__ void __launch_bounds__(kThreads) k_oc_batch(long long m, const double
   __shared__ double sreq[kOcK];
   if (threadIdx.x < kOcK) sreq[threadIdx.x] = threadIdx.x < K ? s[threadIdx.x] : 0.0;
   __syncthreads();
-  double acc[kOcK];
+  double acc[kOcK], sq[kOcK], iq[kOcK];
 #pragma unroll
-  for (int q = 0; q < kOcK; ++q) acc[q] = 0.0;
+  for (int q = 0; q < kOcK; ++q) {
+    acc[q] = 0.0;
+    sq[q] = q < K ? sreq[q] : 1.0;
+    iq[q] = 1.0 / sq[q];
+  }
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
        e += (long long)gridDim.x * blockDim.x) {
     const double4 r = rec[e];
 #pragma unroll
     for (int q = 0; q < kOcK; ++q)
-      if (q < K) acc[q] = fma(r.w, oc_cand(r, sreq[q]), acc[q]);
+      if (q < K) acc[q] = fma(r.w, oc_cand_rcp(r, sq[q], iq[q]), acc[q]);
   }
   block_sum<kOcK>(acc, scratch);
   if (threadIdx.x == 0)

@@ -140,7 +140,7 @@ def _oc_setup(m, seed, move, volfrac, passives=False):
                                                       (400, 3, 0.1, 0.12, False),
                                                       (400, 4, 0.05, 0.9, False),
                                                       (1000, 5, 0.2, 0.3, True)])
-@pytest.mark.parametrize("speculative", [0, 1])
+@pytest.mark.parametrize("speculative", [0, 1, 2])
 def test_host_oc_replay_matches_oracle(P, lib, oracle_port, m, seed, move, volfrac, pas,
                                        speculative):
     x, dc, dV, state, volume, lam0 = _oc_setup(m, seed, move, volfrac, pas)
@@ -153,7 +153,8 @@ def test_host_oc_replay_matches_oracle(P, lib, oracle_port, m, seed, move, volfr
     assert st == 0
     assert (lam.value, bis.value, ev.value) == (lo, bo, eo)
     if speculative:
-        assert nb.value <= max(2, (bo + 3) // 4 + 2)  # ~4 bisection levels per batch
+        per = 4 if speculative == 1 else 5  # bisection levels per batch
+        assert nb.value <= max(2, (bo + per - 2) // (per - 1) + 2)
 
 
 def test_host_oc_replay_nonmonotone(P, lib):
