@@ -93,6 +93,7 @@ struct topo_ctx {
   int conv_R = 8;              // outputs per thread along the run axis
   int conv_A = 0;              // > 0: small-reach direct variant with half-width bound A
   bool overlap_sk = false;     // run the sK store concurrently with K3a..K6
+  bool fuse_sk = false;        // stream sK from the sensitivity kernel (K3a + K3b)
   int coop_blocks = 148;  // OC bisection grid (cooperative)
   int coop_eta = 148;     // eta Newton grid (cooperative)
   long long launches = 0;
@@ -304,8 +305,8 @@ int conv_blocks(const topo_ctx* ctx) {
 topo_status launch_sk(topo_ctx* ctx, const SkArgs& S, cudaStream_t st) {
   const Geo& G = ctx->G;
   int nb = grid_for(ctx, (G.m + 31) / 32 * 32);
-  if (st == ctx->aux) {  // overlapped: leave SM room for K3a..K6 on the main stream
-    const char* e = getenv("TOPO_SK_BPS");
+  const char* e = getenv("TOPO_SK_BPS");  // blocks per SM (experiments; overlap default 2)
+  if (e || st == ctx->aux) {
     const int bps = e ? atoi(e) : 2;
     nb = std::min(nb, ctx->sm_count * std::max(1, bps));
   }
@@ -734,6 +735,8 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   {
     const char* ov = getenv("TOPO_SK_OVERLAP");
     ctx->overlap_sk = ov && ov[0] == '1';
+    const char* fu = getenv("TOPO_SK_FUSE");
+    ctx->fuse_sk = fu && fu[0] == '1';
   }
 
 #define CKC(x)                                                                          \
@@ -772,13 +775,11 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   CKC(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_eta_solve, kThreads, 0));
   if (occ < 1 || occ2 < 1)
     return bail(fail(ctx, TOPO_ECUDA, "cooperative kernels cannot be resident"));
-  // all blocks resident (cooperative); one per SM in overlap mode, where the
-  // sK stream shares the SMs
+  // all blocks resident (cooperative)
   // (small grids: fewer blocks, cheaper grid-wide barriers)
   const int want = int(std::min<long long>(1LL << 20, (G.m + 1023) / 1024));
   ctx->coop_eta = std::max(1, std::min(ctx->sm_count * occ2, want));
-  ctx->coop_blocks =
-      std::max(1, std::min(ctx->overlap_sk ? ctx->sm_count : ctx->sm_count * occ, want));
+  ctx->coop_blocks = std::max(1, std::min(ctx->sm_count * occ, want));
   const size_t npart = std::max<size_t>(
       {size_t(conv_blocks(ctx)) * 3, size_t(ctx->coop_blocks) * 2 * 32 * 2,
        size_t(ctx->coop_eta) * 2 * 2,
@@ -1326,7 +1327,10 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     S.ke_lower = ctx->d_ke_lower.as<double>();
     S.sK = skp;
   }
-  const bool overlap = want_sk && ctx->overlap_sk && !ctx->comm;
+  // default: sK values streamed by the fused K3a kernel (fuse_sk); else the
+  // separate K3b, overlapped on the aux stream or last on the main stream
+  const bool fuse_sk = want_sk && ctx->fuse_sk;
+  const bool overlap = want_sk && !fuse_sk && ctx->overlap_sk && !ctx->comm;
   if (overlap) {
     CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
     CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
@@ -1353,8 +1357,39 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   E.a1 = ctx->a1_st.as<double>();
   E.a2 = ctx->a2_st.as<double>();
   E.partials = ctx->partials.as<double>() + 0;
-  const int nbe = grid_for(ctx, G.m);
-  TRY(launch_elem(ctx, E, nbe));
+  int nbe = grid_for(ctx, G.m);
+  if (fuse_sk) {
+    tmark(ctx, TOPO_STAGE_SK, 0, ctx->stream);
+    static const int ws = getenv("TOPO_SK_WS") ? atoi(getenv("TOPO_SK_WS")) : 1;
+    if (ws) {  // warp-specialised producer / consumer: 3 blocks per SM
+      constexpr int CW = 5, NB = 4;
+      nbe = int(std::min<long long>((G.m + 32 * CW - 1) / (32 * CW), (long long)ctx->sm_count * 3));
+      if (G.is3d) {
+        KeFull<24> K;
+        memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
+        k_elem_sens_ws<24, 300, CW, NB><<<nbe, kThreads, 0, ctx->stream>>>(G, K, E, S.ke_lower, skp);
+      } else {
+        KeFull<8> K;
+        memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
+        k_elem_sens_ws<8, 36, CW, NB><<<nbe, kThreads, 0, ctx->stream>>>(G, K, E, S.ke_lower, skp);
+      }
+    } else {
+      nbe = grid_for(ctx, (G.m + 31) / 32 * 32);
+      if (G.is3d) {
+        KeFull<24> K;
+        memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
+        k_elem_sens_sk<24, 300><<<nbe, kThreads, 0, ctx->stream>>>(G, K, E, S.ke_lower, skp);
+      } else {
+        KeFull<8> K;
+        memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
+        k_elem_sens_sk<8, 36><<<nbe, kThreads, 0, ctx->stream>>>(G, K, E, S.ke_lower, skp);
+      }
+    }
+    LAUNCHED();
+    tmark(ctx, TOPO_STAGE_SK, 1, ctx->stream);
+  } else {
+    TRY(launch_elem(ctx, E, nbe));
+  }
   k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(E.partials, nbe, 1, res + 4);
   LAUNCHED();
   if (ctx->comm) {
@@ -1379,6 +1414,9 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   TRY((launch_conv<2, CONV_ADJ2_OC>(ctx, G, A4, &nb4)));
   tmark(ctx, TOPO_STAGE_ADJOINT, 1, ctx->stream);
   // K5 + K6
+  // the overlapped sK stream joins before the cooperative OC kernels, whose
+  // blocks must all be resident
+  if (overlap) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
   tmark(ctx, TOPO_STAGE_OC, 0, ctx->stream);
   topo_oc_params oc{prm->move, prm->volfrac, 1e-4, 1e-3, 0, 1e-8, 0.0};  // oc.hpp:14-20 defaults
   double lam = 0;
@@ -1387,9 +1425,7 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   TRY(run_oc(ctx, &oc, vmode, ctx->partials0.as<double>(), nb4, ctx->xnew.as<double>(), &lam,
              &bis, &ev, 0.0, prm->beta, nullptr, nullptr, &oc_deferred));
   tmark(ctx, TOPO_STAGE_OC, 1, ctx->stream);
-  if (overlap) {
-    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
-  } else if (want_sk) {
+  if (want_sk && !fuse_sk && !overlap) {
     tmark(ctx, TOPO_STAGE_SK, 0, ctx->stream);
     TRY(launch_sk(ctx, S, ctx->stream));
     tmark(ctx, TOPO_STAGE_SK, 1, ctx->stream);
