@@ -74,6 +74,10 @@ struct topo_ctx {
   int ncol[3] = {0, 0, 0};
   std::vector<double> wpad;
   DevBuf d_cols, d_wpad;
+  // register-blocked 3D small-reach filter (k_conv3): weights [di][|do|][|dr|]
+  bool conv3 = false;
+  std::vector<double> w3;
+  DevBuf d_w3;
   // element matrices
   std::vector<double> ke_full, ke_lower;
   DevBuf d_ke_lower;
@@ -258,6 +262,81 @@ ConvGeom pick_geom(const topo_ctx* c, const Geo& G) {
   return best;
 }
 
+// k_conv3 (3D, reach 1..4): one warp along i, WR x WO warps of RB x TB
+// outputs; two blocks per SM
+constexpr int kC3R = 4, kC3T = 4;
+ConvGeom conv_geom3(const topo_ctx* c, const Geo& G, int WR, int WO) {
+  ConvGeom T;
+  const int A = c->conv_A;
+  T.WI = 1;
+  T.WR = WR;
+  T.WO = WO;
+  T.TI = 32;
+  T.TR = kC3R * WR;
+  T.TO = kC3T * WO;
+  T.reach = T.reach_o = A;
+  T.EI = T.TI + 2 * A;
+  T.ER = (T.TR + 2 * A) | 1;
+  T.EO = T.TO + 2 * A;
+  T.run_n = G.nz;
+  T.other_n = G.jn;
+  for (int q = 0; q < 3; ++q) T.ncol[q] = c->ncol[q];
+  T.magicEI = unsigned((1ull << 32) / unsigned(T.EI) + 1);
+  return T;
+}
+
+ConvGeom pick_geom3(const topo_ctx* c, const Geo& G) {
+  static const int opts[][2] = {{2, 4}, {4, 2}, {1, 8}, {8, 1}};
+  ConvGeom best{};
+  double best_cost = 1e300;
+  for (auto& o : opts) {
+    ConvGeom T = conv_geom3(c, G, o[0], o[1]);
+    if (conv_smem(T) > 112 * 1024) continue;
+    const double outs = double(T.TI) * T.TR * T.TO;
+    const double fi = std::ceil(double(G.nely) / T.TI) * T.TI / G.nely;
+    const double fr = std::ceil(double(T.run_n) / T.TR) * T.TR / T.run_n;
+    const double fo = std::ceil(double(T.other_n) / T.TO) * T.TO / T.other_n;
+    const double cost = (double(T.EI) * T.ER * T.EO / outs + 64.0) * fi * fr * fo;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = T;
+    }
+  }
+  return best;
+}
+
+// the geometry the filter launches use (k_conv3 when enabled and it fits)
+ConvGeom plan_geom(const topo_ctx* c, const Geo& G, bool* use3) {
+  if (c->conv3 && G.is3d) {
+    ConvGeom T = pick_geom3(c, G);
+    if (T.TI) {
+      *use3 = true;
+      return T;
+    }
+  }
+  *use3 = false;
+  return pick_geom(c, G);
+}
+
+template <int NF, int MODE, int AR>
+topo_status launch_conv3_t(topo_ctx* ctx, const Geo& G, const ConvGeom& T, const ConvArgs& A,
+                           int* nblocks) {
+  dim3 grid((G.nely + T.TI - 1) / T.TI, (T.run_n + T.TR - 1) / T.TR,
+            (T.other_n + T.TO - 1) / T.TO);
+  const size_t smem = conv_smem(T);
+  static bool attr_done = false;  // per instantiation
+  if (!attr_done) {
+    CK(cudaFuncSetAttribute(k_conv3<NF, MODE, AR, kC3R, kC3T>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024 + 4096));
+    attr_done = true;
+  }
+  k_conv3<NF, MODE, AR, kC3R, kC3T><<<grid, kThreads, smem, ctx->stream>>>(
+      G, T, ctx->d_w3.as<double>(), A);
+  LAUNCHED();
+  if (nblocks) *nblocks = int(grid.x * grid.y * grid.z);
+  return TOPO_OK;
+}
+
 template <int NF, int MODE, int R, int AW>
 topo_status launch_conv_t(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* nblocks) {
   const ConvGeom T = pick_geom(ctx, G);
@@ -284,6 +363,16 @@ topo_status launch_conv_t(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* n
 
 template <int NF, int MODE>
 topo_status launch_conv(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* nblocks = nullptr) {
+  bool use3 = false;
+  const ConvGeom T3 = plan_geom(ctx, G, &use3);
+  if (use3) {
+    switch (ctx->conv_A) {
+      case 1: return launch_conv3_t<NF, MODE, 1>(ctx, G, T3, A, nblocks);
+      case 2: return launch_conv3_t<NF, MODE, 2>(ctx, G, T3, A, nblocks);
+      case 3: return launch_conv3_t<NF, MODE, 3>(ctx, G, T3, A, nblocks);
+      default: return launch_conv3_t<NF, MODE, 4>(ctx, G, T3, A, nblocks);
+    }
+  }
   switch (ctx->conv_A) {
     case 1: return launch_conv_t<NF, MODE, 8, 1>(ctx, G, A, nblocks);
     case 2: return launch_conv_t<NF, MODE, 8, 2>(ctx, G, A, nblocks);
@@ -295,7 +384,8 @@ topo_status launch_conv(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* nbl
 
 int conv_blocks(const topo_ctx* ctx) {
   const Geo& G = ctx->G;
-  const ConvGeom T = pick_geom(ctx, G);
+  bool use3 = false;
+  const ConvGeom T = plan_geom(ctx, G, &use3);
   if (T.TI == 0) return 1;
   return ((G.nely + T.TI - 1) / T.TI) * ((T.run_n + T.TR - 1) / T.TR) *
          ((T.other_n + T.TO - 1) / T.TO);
@@ -718,6 +808,16 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
           ++ctx->ncol[group];
         }
     }
+    if (AW > 0) {
+      const char* e3 = getenv("TOPO_CONV3");
+      ctx->conv3 = !(e3 && e3[0] == '0');
+      for (int a = 0; a <= AW; ++a)
+        for (int b = 0; b <= AW; ++b)
+          for (int c = 0; c <= AW; ++c) {
+            const double wv = weight(a, b, c);  // (di, do = dj, dr = dk)
+            ctx->w3.push_back(wv > 0 ? wv : 0.0);
+          }
+    }
   }
   // element matrices
   ctx->ke_full.resize(size_t(G.d * G.d));
@@ -758,6 +858,11 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
                  cudaMemcpyHostToDevice));
   CKC(cudaMemcpy(ctx->d_wpad.p, ctx->wpad.data(), sizeof(double) * ctx->wpad.size(),
                  cudaMemcpyHostToDevice));
+  if (!ctx->w3.empty()) {
+    CKC(ctx->d_w3.ensure(sizeof(double) * ctx->w3.size()));
+    CKC(cudaMemcpy(ctx->d_w3.p, ctx->w3.data(), sizeof(double) * ctx->w3.size(),
+                   cudaMemcpyHostToDevice));
+  }
   CKC(ctx->d_ke_lower.ensure(sizeof(double) * size_t(G.P)));
   CKC(cudaMemcpy(ctx->d_ke_lower.p, ctx->ke_lower.data(), sizeof(double) * size_t(G.P),
                  cudaMemcpyHostToDevice));
@@ -814,7 +919,7 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   if (ctx->device >= 0) cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) comm_destroy(ctx->comm);
-  for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_ke_lower, &ctx->d_state, &ctx->hs, &ctx->hs_st,
+  for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_w3, &ctx->d_ke_lower, &ctx->d_state, &ctx->hs, &ctx->hs_st,
                     &ctx->cw, &ctx->x_st, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
                     &ctx->xnew, &ctx->a1_st, &ctx->a2_st, &ctx->rec, &ctx->u, &ctx->tmp0,
                     &ctx->tmp1, &ctx->tmp_st, &ctx->sK, &ctx->iK, &ctx->jK, &ctx->partials,

@@ -311,25 +311,13 @@ __device__ __forceinline__ void conv_columns_direct(const double* __restrict__ t
   }
 }
 
-template <int NF, int MODE, int R, int AW>
-__global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const ConvCol* __restrict__ cols,
-                                                   int ncols, const double* __restrict__ wts,
-                                                   ConvArgs A) {
-  extern __shared__ double tile[];
-  const int tileN = T.EI * T.ER * T.EO, nlines = T.EO * T.ER;
-  // per tile line (other, run): source offset of its i = 0 element (-1: zero
-  // pad) and its first smem word; per i: folded source i (-1: zero pad)
-  long long* lineSrc = reinterpret_cast<long long*>(tile + tileN);
-  int* lineDst = reinterpret_cast<int*>(lineSrc + nlines);
-  int* mapI = lineDst + nlines;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int wi = warp % T.WI, wr = (warp / T.WI) % T.WR, wo = warp / (T.WI * T.WR);
-  const int bi = blockIdx.x * T.TI, br = blockIdx.y * T.TR, bo = blockIdx.z * T.TO;
-  const int sI = T.ER, sPlane = T.EI * T.ER;
-  // thread base: its first output (r = 0) in tile coordinates
-  const int sb = (wo + T.reach_o) * sPlane + (wi * 32 + lane + T.reach) * sI + (wr * R + T.reach);
-
+// Shared by the conv kernels: per tile line (other, run) the source offset of
+// its i = 0 element (-1: zero line) and its first smem word; per i the folded
+// source i (-1: zero pad).
+__device__ __forceinline__ void conv_tables(const Geo& G, const ConvGeom& T, const ConvArgs& A,
+                                            int bi, int br, int bo, long long* lineSrc,
+                                            int* lineDst, int* mapI) {
+  const int tid = threadIdx.x, nlines = T.EO * T.ER, sPlane = T.EI * T.ER;
   auto fold = [&](int t, int n) {  // mirror (Neumann) or -1 outside (Dirichlet)
     if (t >= 0 && t < n) return t;
     return G.bc == 0 ? reflect_index(t, n) : -1;
@@ -362,6 +350,100 @@ __global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const Conv
     lineSrc[line] = src;
     lineDst[line] = to * sPlane + tr;
   }
+}
+
+// tile load, flat over (line, i): coalesced along i; line = q / EI by a
+// multiply-high with the host-computed magic (exact for q < 2^20)
+template <int MODE>
+__device__ __forceinline__ void conv_fill(const ConvGeom& T, const ConvArgs& A,
+                                          const double* __restrict__ in, double* tile,
+                                          const long long* lineSrc, const int* lineDst,
+                                          const int* mapI) {
+  const int tileN = T.EI * T.ER * T.EO, sI = T.ER;
+  constexpr int U = 8;  // loads in flight per thread
+  for (int q0 = threadIdx.x; q0 < tileN; q0 += U * blockDim.x) {
+    double v[U];
+    int dst[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int q = q0 + u * blockDim.x;
+      v[u] = 0.0;
+      dst[u] = -1;
+      if (q < tileN) {
+        const int line = int(__umulhi(unsigned(q), T.magicEI));
+        const int ti = q - line * T.EI;
+        const long long rb = lineSrc[line];
+        const int ii = mapI[ti];
+        dst[u] = lineDst[line] + ti * sI;
+        if (rb >= 0 && ii >= 0) {
+          const long long src = rb + ii;
+          v[u] = in ? __ldg(in + src) : 1.0;  // null input: the all-ones field (hs)
+          if (MODE == CONV_ADJ_DIV) v[u] = v[u] / __ldg(A.hs_st + src);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (dst[u] >= 0) tile[dst[u]] = v[u];
+  }
+}
+
+// per-output epilogue: (v0, v1) = the filtered field(s) at element e
+template <int NF, int MODE>
+__device__ __forceinline__ void conv_store(const Geo& G, const ConvArgs& A, long long e, double v0,
+                                           double v1, double (&red)[3]) {
+  if (MODE == CONV_PLAIN || MODE == CONV_ADJ_DIV) {
+    A.out0[e] = v0;
+  } else if (MODE == CONV_FWD) {
+    double v = v0 / A.hs[e];  // filter.hpp:121 cwiseQuotient(hs)
+    const int s = elem_state(A.state, e);
+    if (A.pin && s == 1) v = 1.0;  // driver.hpp:130-133
+    if (A.pin && s == 2) v = 0.0;
+    A.out0[e] = v;
+  } else if (MODE == CONV_ADJ2_OC) {
+    const double dc = v0, dV = NF > 1 ? v1 : v0;
+    if (A.out0) A.out0[e] = dc;
+    if (A.out1) A.out1[e] = dV;
+    const bool act = elem_state(A.state, e) == 0;
+    const double4 rec = oc_record(A.x[e], dc, dV, A.cw ? A.cw[e] : 1.0, A.move, act);
+    A.ocrec[e] = rec;
+    if (act) red[0] += rec.z;
+    red[1] += rec.w * oc_cand(rec, 0.0);
+    red[2] += rec.w * std_min(std_max(0.0, rec.x), rec.y);  // V(s -> inf)
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void conv_partials(const ConvArgs& A, double (&red)[3]) {
+  if (MODE == CONV_ADJ2_OC) {
+    __shared__ double scratch[3 * 32];
+    block_sum<3>(red, scratch);
+    const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (threadIdx.x == 0) {
+      A.partials[3 * b] = red[0];
+      A.partials[3 * b + 1] = red[1];
+      A.partials[3 * b + 2] = red[2];
+    }
+  }
+}
+
+template <int NF, int MODE, int R, int AW>
+__global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const ConvCol* __restrict__ cols,
+                                                   int ncols, const double* __restrict__ wts,
+                                                   ConvArgs A) {
+  extern __shared__ double tile[];
+  const int tileN = T.EI * T.ER * T.EO, nlines = T.EO * T.ER;
+  long long* lineSrc = reinterpret_cast<long long*>(tile + tileN);
+  int* lineDst = reinterpret_cast<int*>(lineSrc + nlines);
+  int* mapI = lineDst + nlines;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wi = warp % T.WI, wr = (warp / T.WI) % T.WR, wo = warp / (T.WI * T.WR);
+  const int bi = blockIdx.x * T.TI, br = blockIdx.y * T.TR, bo = blockIdx.z * T.TO;
+  const int sI = T.ER, sPlane = T.EI * T.ER;
+  // thread base: its first output (r = 0) in tile coordinates
+  const int sb = (wo + T.reach_o) * sPlane + (wi * 32 + lane + T.reach) * sI + (wr * R + T.reach);
+  conv_tables(G, T, A, bi, br, bo, lineSrc, lineDst, mapI);
   __syncthreads();
 
   double acc[NF][R];
@@ -372,23 +454,8 @@ __global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const Conv
 
 #pragma unroll
   for (int f = 0; f < NF; ++f) {
-    const double* __restrict__ in = f == 0 ? A.in0 : A.in1;
     if (f > 0) __syncthreads();
-    // tile load, flat over (line, i): coalesced along i; line = q / EI by a
-    // multiply-high with the host-computed magic (exact for q < 2^20)
-    for (int q = tid; q < tileN; q += kThreads) {
-      const int line = int(__umulhi(unsigned(q), T.magicEI));
-      const int ti = q - line * T.EI;
-      const long long rb = lineSrc[line];
-      const int ii = mapI[ti];
-      double v = 0.0;
-      if (rb >= 0 && ii >= 0) {
-        const long long src = rb + ii;
-        v = in ? __ldg(in + src) : 1.0;  // null input: the all-ones field (hs)
-        if (MODE == CONV_ADJ_DIV) v = v / __ldg(A.hs_st + src);
-      }
-      tile[lineDst[line] + ti * sI] = v;
-    }
+    conv_fill<MODE>(T, A, f == 0 ? A.in0 : A.in1, tile, lineSrc, lineDst, mapI);
     __syncthreads();
     if (AW > 0) {
       conv_columns_direct<4, R, AW>(tile, sb, sI, sPlane, cols, 0, T.ncol[0], wts, acc[f]);
@@ -404,7 +471,6 @@ __global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const Conv
     }
   }
 
-  // epilogue
   double red[3] = {0.0, 0.0, 0.0};
   const int gi = bi + wi * 32 + lane, go = bo + wo;
 #pragma unroll
@@ -412,36 +478,101 @@ __global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const Conv
     const int grun = br + wr * R + r;
     if (gi >= G.nely || grun >= T.run_n || go >= T.other_n) continue;
     const long long e = ((long long)go * T.run_n + grun) * G.nely + gi;
-    if (MODE == CONV_PLAIN || MODE == CONV_ADJ_DIV) {
-      A.out0[e] = acc[0][r];
-    } else if (MODE == CONV_FWD) {
-      double v = acc[0][r] / A.hs[e];  // filter.hpp:121 cwiseQuotient(hs)
-      const int s = elem_state(A.state, e);
-      if (A.pin && s == 1) v = 1.0;  // driver.hpp:130-133
-      if (A.pin && s == 2) v = 0.0;
-      A.out0[e] = v;
-    } else if (MODE == CONV_ADJ2_OC) {
-      const double dc = acc[0][r], dV = acc[NF - 1][r];
-      if (A.out0) A.out0[e] = dc;
-      if (A.out1) A.out1[e] = dV;
-      const bool act = elem_state(A.state, e) == 0;
-      const double4 rec = oc_record(A.x[e], dc, dV, A.cw ? A.cw[e] : 1.0, A.move, act);
-      A.ocrec[e] = rec;
-      if (act) red[0] += rec.z;
-      red[1] += rec.w * oc_cand(rec, 0.0);
-      red[2] += rec.w * std_min(std_max(0.0, rec.x), rec.y);  // V(s -> inf)
+    conv_store<NF, MODE>(G, A, e, acc[0][r], acc[NF - 1][r], red);
+  }
+  conv_partials<MODE>(A, red);
+}
+
+// 3D small reach (half-width AR <= 4), register-blocked: every thread owns an
+// RB (run) x TB (other) block of outputs at one i. Taps are folded over +-di
+// only (mirror pairs along i share the weight), so each tile row of the
+// thread's (TB + 2 AR)-row window is loaded once and reused by all TB output
+// rows it reaches: ~(2AR+1)(TB+2AR)(RB+2AR)/(RB TB) shared loads per output
+// instead of ~(#columns)(R+2AR)/R. Weights w3[di][|do|][|dr|] (zero outside
+// the cone) are uniform loads.
+template <int AR, int RB, int TB, bool FOLD>
+__device__ __forceinline__ void conv3_di(const double* __restrict__ base, int di, int sI,
+                                         int sPlane, const double* __restrict__ w3,
+                                         double (&acc)[TB][RB]) {
+  constexpr int NW = AR + 1;
+  double w[NW][NW];
+#pragma unroll
+  for (int a = 0; a < NW; ++a)
+#pragma unroll
+    for (int b = 0; b < NW; ++b) w[a][b] = __ldg(w3 + (di * NW + a) * NW + b);
+  const double* p = base + di * sI;
+  const double* q = base - di * sI;
+#pragma unroll
+  for (int kk = 0; kk < TB + 2 * AR; ++kk) {
+    double v[RB + 2 * AR];
+#pragma unroll
+    for (int j = 0; j < RB + 2 * AR; ++j)
+      v[j] = FOLD ? p[kk * sPlane + j] + q[kk * sPlane + j] : p[kk * sPlane + j];
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      const int dO = kk - t - AR;
+      if (dO < -AR || dO > AR) continue;
+      const int ao = dO < 0 ? -dO : dO;
+#pragma unroll
+      for (int d = 0; d < 2 * AR + 1; ++d) {
+        const double wv = w[ao][d < AR ? AR - d : d - AR];
+#pragma unroll
+        for (int r = 0; r < RB; ++r) acc[t][r] = fma(wv, v[r + d], acc[t][r]);
+      }
     }
   }
-  if (MODE == CONV_ADJ2_OC) {
-    __shared__ double scratch[3 * 32];
-    block_sum<3>(red, scratch);
-    const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    if (tid == 0) {
-      A.partials[3 * b] = red[0];
-      A.partials[3 * b + 1] = red[1];
-      A.partials[3 * b + 2] = red[2];
+}
+
+template <int NF, int MODE, int AR, int RB, int TB>
+__global__ void __launch_bounds__(kThreads, 2) k_conv3(Geo G, ConvGeom T,
+                                                       const double* __restrict__ w3, ConvArgs A) {
+  extern __shared__ double tile[];
+  const int tileN = T.EI * T.ER * T.EO, nlines = T.EO * T.ER;
+  long long* lineSrc = reinterpret_cast<long long*>(tile + tileN);
+  int* lineDst = reinterpret_cast<int*>(lineSrc + nlines);
+  int* mapI = lineDst + nlines;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wr = warp % T.WR, wo = warp / T.WR;  // one warp along i
+  const int bi = blockIdx.x * 32, br = blockIdx.y * T.TR, bo = blockIdx.z * T.TO;
+  const int sI = T.ER, sPlane = T.EI * T.ER;
+  // window origin: tile row wo*TB (halo included), i = lane + AR, run wr*RB
+  const int sb0 = (wo * TB) * sPlane + (lane + AR) * sI + wr * RB;
+  conv_tables(G, T, A, bi, br, bo, lineSrc, lineDst, mapI);
+  __syncthreads();
+  double red[3] = {0.0, 0.0, 0.0};
+  double keep[TB][RB];  // field 0 while field 1 accumulates (NF == 2)
+  const int gi = bi + lane;
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    if (f > 0) __syncthreads();
+    conv_fill<MODE>(T, A, f == 0 ? A.in0 : A.in1, tile, lineSrc, lineDst, mapI);
+    __syncthreads();
+    double acc[TB][RB];
+#pragma unroll
+    for (int t = 0; t < TB; ++t)
+#pragma unroll
+      for (int r = 0; r < RB; ++r) acc[t][r] = 0.0;
+    conv3_di<AR, RB, TB, false>(tile + sb0, 0, sI, sPlane, w3, acc);
+#pragma unroll 1
+    for (int di = 1; di <= AR; ++di) conv3_di<AR, RB, TB, true>(tile + sb0, di, sI, sPlane, w3, acc);
+    if (f + 1 < NF) {
+#pragma unroll
+      for (int t = 0; t < TB; ++t)
+#pragma unroll
+        for (int r = 0; r < RB; ++r) keep[t][r] = acc[t][r];
+      continue;
     }
+#pragma unroll
+    for (int t = 0; t < TB; ++t)
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const int grun = br + wr * RB + r, go = bo + wo * TB + t;
+        if (gi >= G.nely || grun >= T.run_n || go >= T.other_n) continue;
+        const long long e = ((long long)go * T.run_n + grun) * G.nely + gi;
+        conv_store<NF, MODE>(G, A, e, NF > 1 ? keep[t][r] : acc[t][r], acc[t][r], red);
+      }
   }
+  conv_partials<MODE>(A, red);
 }
 
 // ============================================================================
