@@ -76,6 +76,9 @@ struct topo_ctx {
   DevBuf d_cols, d_wpad;
   // register-blocked 3D small-reach filter (k_conv3): weights [di][|do|][|dr|]
   bool conv3 = false;
+  // Walsh-block form of the H8 quadratic form (k_elem_walsh), when Ke allows
+  bool walsh = false;
+  KeWalsh kw{};
   std::vector<double> w3;
   DevBuf d_w3;
   // element matrices
@@ -260,6 +263,59 @@ ConvGeom pick_geom(const topo_ctx* c, const Geo& G) {
     }
   }
   return best;
+}
+
+// Walsh-block coefficients of an H8 Ke (k_elem_walsh): Kt = Wt Ke W / 64 with
+// W[3a + c][(c, S)] = prod_{axis in S} (2 o_axis(a) - 1), o(a) the binary
+// (i, k, j) offsets of local node a (element_dofs order). False when Ke
+// couples modes of different reflection signature beyond rounding.
+bool walsh_blocks(const double* ke, KeWalsh* out) {
+  static const int off[8][3] = {{1, 0, 0}, {1, 0, 1}, {0, 0, 1}, {0, 0, 0},
+                                {1, 1, 0}, {1, 1, 1}, {0, 1, 1}, {0, 1, 0}};
+  long double W[24][24] = {};
+  for (int c = 0; c < 3; ++c)
+    for (int S = 0; S < 8; ++S)
+      for (int a = 0; a < 8; ++a) {
+        long double v = 1;
+        for (int ax = 0; ax < 3; ++ax)
+          if (S >> ax & 1) v *= 2 * off[a][ax] - 1;
+        W[3 * a + c][c * 8 + S] = v;
+      }
+  long double KW[24][24], Kt[24][24];
+  for (int r = 0; r < 24; ++r)
+    for (int q = 0; q < 24; ++q) {
+      long double acc = 0;
+      for (int t = 0; t < 24; ++t) acc += (long double)ke[t * 24 + r] * W[t][q];  // column-major
+      KW[r][q] = acc;
+    }
+  long double mx = 0;
+  for (int p = 0; p < 24; ++p)
+    for (int q = 0; q < 24; ++q) {
+      long double acc = 0;
+      for (int t = 0; t < 24; ++t) acc += W[t][p] * KW[t][q];
+      Kt[p][q] = acc / 64;
+      mx = std::max(mx, fabsl(Kt[p][q]));
+    }
+  auto sig = [](int mode) {  // reflection signature of mode (c, S)
+    const int c = mode / 8, S = mode % 8;
+    return S ^ (1 << walsh_axis(c));
+  };
+  for (int p = 0; p < 24; ++p)
+    for (int q = 0; q < 24; ++q)
+      if (sig(p) != sig(q) && fabsl(Kt[p][q]) > 1e-13L * mx) return false;
+  if (!(mx > 0)) return false;
+  for (int s = 0; s < 8; ++s) {
+    int pm[3];
+    for (int c = 0; c < 3; ++c) pm[c] = c * 8 + (s ^ (1 << walsh_axis(c)));
+    double* k = out->k[s];
+    k[0] = double(Kt[pm[0]][pm[0]]);
+    k[1] = double(2 * Kt[pm[0]][pm[1]]);
+    k[2] = double(2 * Kt[pm[0]][pm[2]]);
+    k[3] = double(Kt[pm[1]][pm[1]]);
+    k[4] = double(2 * Kt[pm[1]][pm[2]]);
+    k[5] = double(Kt[pm[2]][pm[2]]);
+  }
+  return true;
 }
 
 // k_conv3 (3D, reach 1..4): one warp along i, WR x WO warps of RB x TB
@@ -458,12 +514,19 @@ topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
   EtaCtl ctl;
   ctl.init(eta0);
   int first = 1;
+  double sum_t = 0.0, n_act = 0.0;
   for (;;) {
     k_eta_partials<<<ctx->coop_eta, kThreads, 0, ctx->stream>>>(A, ctl.eta, first);
     LAUNCHED();
+    TRY(reduce_to_host<4>(ctx, A.partials, ctx->coop_eta));  // summed over ranks
+    if (first) {
+      sum_t = ctx->h_result[2];
+      n_act = ctx->h_result[3];
+    }
     first = 0;
-    TRY(reduce_to_host<2>(ctx, A.partials, ctx->coop_eta));
-    if (!ctl.feed(ctx->h_result[0] / ctx->m_total, ctx->h_result[1] / ctx->m_total)) break;
+    const double g =
+        eta_mismatch_from_sums(beta, ctl.eta, ctx->h_result[0], sum_t, n_act, ctx->m_total);
+    if (!ctl.feed(g, ctx->h_result[1] / ctx->m_total)) break;
   }
   const double res[3] = {ctl.eta, double(ctl.it), ctl.g};
   CK(cudaMemcpyAsync(eta_dev_out, res, sizeof res, cudaMemcpyHostToDevice, ctx->stream));
@@ -829,6 +892,10 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
     return bail(fail(ctx, TOPO_EINVAL, "element stiffness: Poisson ratio must lie in (-1, 0.5)"));
   }
 
+  if (G.is3d) {
+    const char* ew = getenv("TOPO_ELEM_WALSH");
+    ctx->walsh = !(ew && ew[0] == '0') && walsh_blocks(ctx->ke_full.data(), &ctx->kw);
+  }
   if (pick_geom(ctx, G).TI == 0)
     return bail(fail(ctx, TOPO_EINVAL, "filter: rmin %.3g too large for the shared-memory tile",
                      d->rmin));
@@ -887,7 +954,7 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   ctx->coop_blocks = std::max(1, std::min(ctx->sm_count * occ, want));
   const size_t npart = std::max<size_t>(
       {size_t(conv_blocks(ctx)) * 3, size_t(ctx->coop_blocks) * 2 * 32 * 2,
-       size_t(ctx->coop_eta) * 2 * 2,
+       size_t(ctx->coop_eta) * 2 * 4,
        size_t(ctx->sm_count) * 8 * 4});
   CKC(ctx->partials.ensure(sizeof(double) * npart));
   CKC(ctx->partials0.ensure(sizeof(double) * npart));
@@ -1120,7 +1187,9 @@ topo_status topo_assemble_values(topo_ctx* ctx, const double* sKe, double* vals)
 
 static topo_status launch_elem(topo_ctx* ctx, const ElemArgs& A, int nb) {
   const Geo& G = ctx->G;
-  if (G.is3d) {
+  if (G.is3d && ctx->walsh) {
+    k_elem_walsh<<<nb, kThreads, 0, ctx->stream>>>(G, ctx->kw, A);
+  } else if (G.is3d) {
     KeFull<24> K;
     memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
     static const int ne = getenv("TOPO_ELEM_NE") ? atoi(getenv("TOPO_ELEM_NE")) : 1;

@@ -48,6 +48,15 @@ __device__ __forceinline__ void element_dofs(const Geo& G, int i, int k, int j, 
 }
 
 __device__ __forceinline__ void elem_ijk(const Geo& G, long long e, int& i, int& k, int& j) {
+  if (e <= 0xffffffffLL) {  // 32-bit division (all owned slabs below 2^32 elements)
+    const unsigned u = unsigned(e), ny = unsigned(G.nely), nz = unsigned(G.nz);
+    const unsigned r = u / ny;
+    i = int(u - r * ny);
+    const unsigned jj = r / nz;
+    k = int(r - jj * nz);
+    j = G.j0 + int(jj);
+    return;
+  }
   i = int(e % G.nely);
   const long long r = e / G.nely;
   k = int(r % G.nz);
@@ -589,26 +598,71 @@ struct EtaArgs {
   double* result;           // eta, iterations (as double), g
 };
 
-__device__ __forceinline__ void eta_block_eval(const EtaArgs& A, double eta, bool first,
-                                               double (&red)[2]) {
+// reciprocal: hardware estimate + two Newton steps (within an ulp; finite x > 0)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Partial sums of this thread's active elements (grid-stride, 4 in flight):
+//   [0] sum th, th = tanh(beta (t - eta)) = 1 - 2 / (E + 1), E = E1 exp(-2 beta eta)
+//   [1] sum of the slope terms (filter.hpp:195-199), 1 - th^2 = 4 E / (E + 1)^2
+//   [2] sum t, [3] active count (first evaluation only)
+// with E1 = exp(2 beta t) cached by the first evaluation. The mismatch is then
+// g = ((n a + sum th) / den - sum t) / m (filter.hpp:187-192): one division
+// per evaluation instead of one per element.
+template <bool FIRST>
+__device__ __forceinline__ void eta_block_eval(const EtaArgs& A, double eta, double (&red)[4]) {
   const EtaConsts c = eta_consts(A.beta, eta);
-  red[0] = red[1] = 0.0;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < A.G.m;
-       e += (long long)gridDim.x * blockDim.x) {
-    if (elem_state(A.state, e) != 0) continue;  // active set only (filter.hpp:190)
-    const double t = A.xt[e];
-    double E1;
-    if (first) {
-      E1 = exp(2.0 * A.beta * t);
-      A.e1[e] = E1;
-    } else {
-      E1 = A.e1[e];
+  constexpr int U = 4;
+  const long long S = (long long)gridDim.x * blockDim.x;
+  red[0] = red[1] = red[2] = red[3] = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < A.G.m; e += U * S) {
+    double v[U];
+    bool act[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long q = e + u * S;
+      act[u] = q < A.G.m && elem_state(A.state, q) == 0;  // active set (filter.hpp:190)
+      v[u] = act[u] ? (FIRST ? A.xt[q] : A.e1[q]) : 0.0;
     }
-    double g, gp;
-    eta_terms(c, t, E1, g, gp);
-    red[0] += g;
-    red[1] += gp;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!act[u]) continue;
+      double E1 = v[u];
+      if (FIRST) {
+        red[2] += v[u];
+        red[3] += 1.0;
+        E1 = exp(2.0 * A.beta * v[u]);
+        A.e1[e + u * S] = E1;
+      }
+      const double E = E1 * c.k;
+      double th, w;
+      if (E < INFINITY) {
+        const double r = rcp_nr(E + 1.0);
+        th = fma(-2.0, r, 1.0);
+        w = 4.0 * E * r * r;
+      } else {
+        th = 1.0;
+        w = 0.0;
+      }
+      const double Sv = c.half_coshb - 0.25 * fma(E1, c.emb, c.eb * rcp_nr(E1));
+      red[0] += th;
+      red[1] += c.c0 * w * Sv;
+    }
   }
+}
+
+__host__ __device__ __forceinline__ double eta_mismatch_from_sums(double beta, double eta,
+                                                                  double sum_th, double sum_t,
+                                                                  double n_act, double m) {
+  const double a = tanh(beta * eta);
+  const double den = a + tanh(beta * (1.0 - eta));
+  return ((n_act * a + sum_th) / den - sum_t) / m;
 }
 
 // one (g, g') evaluation per grid-wide step; every block reduces the same
@@ -616,7 +670,7 @@ __device__ __forceinline__ void eta_block_eval(const EtaArgs& A, double eta, boo
 __global__ void __launch_bounds__(kThreads) k_eta_solve(EtaArgs A) {
   cg::grid_group grid = cg::this_grid();
   EtaCtl ctl;  // replayed by thread 0 of every block (registers, not shared memory)
-  __shared__ double scratch[2 * 32];
+  __shared__ double scratch[4 * 32];
   __shared__ int cont;
   __shared__ double s_eta;
   if (threadIdx.x == 0) {
@@ -626,25 +680,36 @@ __global__ void __launch_bounds__(kThreads) k_eta_solve(EtaArgs A) {
   __syncthreads();
   int buf = 0;
   bool first = true;
+  double sum_t = 0.0, n_act = 0.0;  // thread 0: from the first evaluation
   for (;;) {
-    double red[2];
-    eta_block_eval(A, s_eta, first, red);
-    first = false;
-    block_sum<2>(red, scratch);
-    double* P = A.partials + (long long)buf * 2 * gridDim.x;
+    double red[4];
+    if (first)
+      eta_block_eval<true>(A, s_eta, red);
+    else
+      eta_block_eval<false>(A, s_eta, red);
+    block_sum<4>(red, scratch);
+    double* P = A.partials + (long long)buf * 4 * gridDim.x;
     if (threadIdx.x == 0) {
-      P[2 * blockIdx.x] = red[0];
-      P[2 * blockIdx.x + 1] = red[1];
+      P[4 * blockIdx.x] = red[0];
+      P[4 * blockIdx.x + 1] = red[1];
+      P[4 * blockIdx.x + 2] = red[2];
+      P[4 * blockIdx.x + 3] = red[3];
     }
     grid.sync();
     if (threadIdx.x < 32) {
-      double s2[2];
-      warp_sum_partials<2>(P, gridDim.x, 2, s2);
+      double s4[4];
+      warp_sum_partials<4>(P, gridDim.x, 4, s4);
       if (threadIdx.x == 0) {
-        cont = ctl.feed(s2[0] / A.mtotal, s2[1] / A.mtotal);
+        if (first) {
+          sum_t = s4[2];
+          n_act = s4[3];
+        }
+        const double g = eta_mismatch_from_sums(A.beta, s_eta, s4[0], sum_t, n_act, A.mtotal);
+        cont = ctl.feed(g, s4[1] / A.mtotal);
         s_eta = ctl.eta;
       }
     }
+    first = false;
     buf ^= 1;
     __syncthreads();
     if (!cont) break;
@@ -656,16 +721,17 @@ __global__ void __launch_bounds__(kThreads) k_eta_solve(EtaArgs A) {
   }
 }
 
-// plain (g, g') partial sums at one eta: the multi-GPU / host-driven variant
+// plain partial sums at one eta: the multi-GPU / host-driven variant
 __global__ void __launch_bounds__(kThreads) k_eta_partials(EtaArgs A, double eta, int first) {
-  __shared__ double scratch[2 * 32];
-  double red[2];
-  eta_block_eval(A, eta, first != 0, red);
-  block_sum<2>(red, scratch);
-  if (threadIdx.x == 0) {
-    A.partials[2 * blockIdx.x] = red[0];
-    A.partials[2 * blockIdx.x + 1] = red[1];
-  }
+  __shared__ double scratch[4 * 32];
+  double red[4];
+  if (first)
+    eta_block_eval<true>(A, eta, red);
+  else
+    eta_block_eval<false>(A, eta, red);
+  block_sum<4>(red, scratch);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 4; ++q) A.partials[4 * blockIdx.x + q] = red[q];
 }
 
 // ============================================================================
@@ -774,6 +840,99 @@ __global__ void __launch_bounds__(kThreads, 4 - NE) k_elem_sens(Geo G, KeFull<D>
         A.a1[es] = (dH[n] * dcp) * ih;                        // backfilter, filter.hpp:170, :128
         A.a2[es] = (dH[n] * dv0) * ih;
       }
+    }
+  }
+  double red[1] = {csum};
+  block_sum<1>(red, scratch);
+  if (threadIdx.x == 0) A.partials[blockIdx.x] = red[0];
+}
+
+// K3a for hexahedra in Walsh coordinates. Per displacement component the 8
+// nodal values are Walsh-Hadamard transformed over the element's three binary
+// node coordinates (i, k, j); a mirror-symmetric Ke (every H8 Ke of an
+// isotropic cube) couples only the three modes of equal reflection
+// signature, so u' Ke u = sum over 8 signatures of a 3x3 quadratic form:
+// 72 add/sub + 48 FMA instead of the 300-term upper-triangle sum. The host
+// derives the blocks from the given Ke (Wt Ke W / 64) and uses this kernel
+// only when every coupling outside them is negligible (capi.cu, walsh_blocks).
+struct KeWalsh {
+  double k[8][6];  // per signature: k00, 2k01, 2k02, k11, 2k12, k22
+};
+// component c's mode of signature sig has Walsh mask sig ^ (1 << kWalshAxis[c])
+// (component 0 = x flips with j, 1 = y with i, 2 = z with k)
+__host__ __device__ constexpr int walsh_axis(int c) { return c == 0 ? 2 : (c == 1 ? 0 : 1); }
+
+__global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, ElemArgs A) {
+  __shared__ double scratch[32];
+  const double eta = A.input_is_phys ? 0.5 : *A.eta_ptr;
+  const double a = tanh(A.beta * eta);
+  const double denom = a + tanh(A.beta * (1.0 - eta));
+  const double de = A.e0 - A.emin;
+  const long long ny1 = G.nely + 1, pl = ny1 * (G.nelz + 1);
+  double csum = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < G.m;
+       e += (long long)gridDim.x * blockDim.x) {
+    int i, k, j;
+    elem_ijk(G, e, i, k, j);
+    const double t = A.xt[e];
+    double xphys, dH;
+    if (A.input_is_phys) {
+      xphys = t;
+      dH = 0.0;
+    } else {
+      const double th = tanh(A.beta * (t - eta));
+      xphys = (a + th) / denom;               // filter.hpp:142
+      dH = A.beta * (1.0 - th * th) / denom;  // filter.hpp:151
+    }
+    const double xp = simp_xp(xphys, A.penal);
+    const double sK = A.emin + xp * xphys * de;  // fea.hpp:142
+    const double dsK = A.penal * xp * de;        // fea.hpp:143
+    const long long n0 = (long long)(j - G.j0) * pl + (long long)k * ny1 + i;  // node (i, k, j)
+    double h[3][8];  // [component][binary node index oi + 2 ok + 4 oj]
+    {
+      // the element's nodes are 4 (k, j) pairs of 2 consecutive i: 6 doubles each
+      const double* u0 = A.U + 3 * n0;
+      const double* up[4] = {u0, u0 + 3 * ny1, u0 + 3 * pl, u0 + 3 * (pl + ny1)};
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) h[c][b] = __ldg(up[b >> 1] + 3 * (b & 1) + c);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int bit = 1; bit < 8; bit <<= 1)
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          if (!(b & bit)) {
+            const double lo = h[c][b], hi = h[c][b | bit];
+            h[c][b] = hi + lo;
+            h[c][b | bit] = hi - lo;
+          }
+    double q2 = 0.0;  // u' Ke u (fea.hpp:267)
+#pragma unroll
+    for (int sig = 0; sig < 8; ++sig) {
+      const double m0 = h[0][sig ^ (1 << walsh_axis(0))];
+      const double m1 = h[1][sig ^ (1 << walsh_axis(1))];
+      const double m2 = h[2][sig ^ (1 << walsh_axis(2))];
+      const double* kk = K.k[sig];
+      const double r0 = fma(kk[0], m0, fma(kk[1], m1, kk[2] * m2));
+      const double r1 = fma(kk[3], m1, kk[4] * m2);
+      q2 = fma(m0, r0, q2);
+      q2 = fma(m1, r1, q2);
+      q2 = fma(m2, kk[5] * m2, q2);
+    }
+    csum = fma(sK, q2, csum);
+    const int st = elem_state(A.state, e);
+    const double dcp = st == 0 ? -dsK * q2 : 0.0;
+    const double dv0 = st == 0 ? A.inv_m : 0.0;  // driver.hpp:155
+    if (A.xPhys) A.xPhys[e] = xphys;
+    if (A.dcPhys) A.dcPhys[e] = dcp;
+    if (A.a1) {
+      const double ih = 1.0 / A.hs[e];
+      const long long es = e + (long long)(G.j0 - G.sj0) * G.S;
+      A.a1[es] = (dH * dcp) * ih;  // backfilter, filter.hpp:170, :128
+      A.a2[es] = (dH * dv0) * ih;
     }
   }
   double red[1] = {csum};
