@@ -92,6 +92,7 @@ struct topo_ctx {
   double m_total = 0;   // global element count
   // fields
   DevBuf e1;  // exp(2 beta xTilde) for the eta passes
+  OcRecs oc_view{};  // the records run_oc reads (set by their producer)
   DevBuf hs, hs_st, cw, x_st, xt, xphys, dcphys, dc, dV, xnew, a1_st, a2_st, rec, u, tmp0, tmp1,
       tmp_st;
   DevBuf sK, iK, jK;
@@ -546,7 +547,7 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
   if ((mode == TOPO_VOL_MEAN || mode == TOPO_VOL_FILTERED) && !ctx->comm && !force_host) {
     OcArgs A;
     A.m = G.m;
-    A.rec = ctx->rec.as<double4>();
+    A.R = ctx->oc_view;
     double* pre = ctx->result.as<double>() + 32;
     TRY(reduce_on_device<3>(ctx, prep, n_prep, pre));
     A.prep_partials = pre;
@@ -579,7 +580,7 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
       for (int q = 1; q < h[127]; ++q) fprintf(stderr, " %lld", h[q] - h[q - 1]);
       fprintf(stderr, "\n");
     }
-    k_oc_final<<<grid_for(ctx, G.m), kThreads, 0, ctx->stream>>>(G.m, A.rec, A.result, xnew_dev);
+    k_oc_final<<<grid_for(ctx, G.m), kThreads, 0, ctx->stream>>>(G.m, A.R, A.result, xnew_dev);
     LAUNCHED();
     CK(cudaMemcpyAsync(ctx->h_result + 8, A.result, sizeof(double) * 7, cudaMemcpyDeviceToHost,
                        ctx->stream));
@@ -643,7 +644,7 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
   while (ctl.pending()) {
     const double s = ctl.s_req;
     double v = 0;
-    k_oc_candidates<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->rec.as<double4>(), s, xnew_dev);
+    k_oc_candidates<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->oc_view, s, xnew_dev);
     LAUNCHED();
     if (mode == TOPO_VOL_CALLBACK) {
       if (!cb) return fail(ctx, TOPO_EINVAL, "oc: volume callback is null");
@@ -674,7 +675,7 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
   }
   if (ctl.status == OcCtl::ST_NONMONO)
     return fail(ctx, TOPO_ENONMONO, "oc: candidate volume is not monotone in the multiplier");
-  k_oc_candidates<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->rec.as<double4>(), ctl.s_final,
+  k_oc_candidates<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->oc_view, ctl.s_final,
                                                     xnew_dev);
   LAUNCHED();
   *lam = ctl.lam_result;
@@ -937,7 +938,7 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
                     &ctx->xnew, &ctx->tmp0, &ctx->tmp1, &ctx->e1})
     CKC(b->ensure(md));
   for (DevBuf* b : {&ctx->hs_st, &ctx->a1_st, &ctx->a2_st, &ctx->tmp_st}) CKC(b->ensure(sd));
-  CKC(ctx->rec.ensure(sizeof(double4) * size_t(G.m)));
+  CKC(ctx->rec.ensure(sizeof(double) * size_t(G.m)));
   CKC(ctx->u.ensure(sizeof(double) * size_t(ctx->n)));
   if (d->nranks > 1) CKC(ctx->x_st.ensure(sd));
 
@@ -1418,8 +1419,11 @@ topo_status topo_oc_bisect(topo_ctx* ctx, const double* x, const double* dc, con
   k_oc_prep<<<nb, kThreads, 0, ctx->stream>>>(
       G.m, xd, dcd, dVd, ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr,
       volume_mode == TOPO_VOL_FILTERED ? ctx->cw.as<double>() : nullptr, prm->move,
-      ctx->rec.as<double4>(), ctx->partials0.as<double>());
+      ctx->rec.as<double>(), ctx->partials0.as<double>());
   LAUNCHED();
+  ctx->oc_view = OcRecs{xd, ctx->rec.as<double>(),
+                        volume_mode == TOPO_VOL_FILTERED ? ctx->cw.as<double>() : nullptr,
+                        prm->move};
   bool h;
   double* o = out_ptr(ctx, xNew, ctx->xnew, G.m, &h);
   double lam = 0;
@@ -1527,7 +1531,7 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   E.penal = prm->simp.penal;
   E.inv_m = 1.0 / ctx->m_total;
   E.xPhys = ctx->xphys.as<double>();
-  E.dcPhys = ctx->dcphys.as<double>();
+  E.dcPhys = out->dcPhys ? ctx->dcphys.as<double>() : nullptr;  // only when requested
   E.a1 = ctx->a1_st.as<double>();
   E.a2 = ctx->a2_st.as<double>();
   E.partials = ctx->partials.as<double>() + 0;
@@ -1576,13 +1580,14 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   ConvArgs A4{};
   A4.in0 = ctx->a1_st.as<double>();
   A4.in1 = ctx->a2_st.as<double>();
-  A4.out0 = ctx->dc.as<double>();
-  A4.out1 = ctx->dV.as<double>();
+  A4.out0 = out->dc ? ctx->dc.as<double>() : nullptr;  // written only when requested
+  A4.out1 = out->dV ? ctx->dV.as<double>() : nullptr;
   A4.state = state;
   A4.x = xown;
   A4.cw = vmode == TOPO_VOL_FILTERED ? ctx->cw.as<double>() : nullptr;
   A4.move = prm->move;
-  A4.ocrec = ctx->rec.as<double4>();
+  A4.ocp = ctx->rec.as<double>();
+  ctx->oc_view = OcRecs{xown, ctx->rec.as<double>(), A4.cw, prm->move};
   A4.partials = ctx->partials0.as<double>();
   int nb4 = 0;
   TRY((launch_conv<2, CONV_ADJ2_OC>(ctx, G, A4, &nb4)));
@@ -1805,7 +1810,7 @@ topo_status comm_oc_volumes(Comm* c, topo_ctx* ctx, const double* s, int K, doub
   const int nb = grid_for(ctx, G.m);
   double* dreq = ctx->result.as<double>() + 40;  // K <= 16 requests
   CK(cudaMemcpyAsync(dreq, s, sizeof(double) * K, cudaMemcpyHostToDevice, ctx->stream));
-  k_oc_batch<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->rec.as<double4>(), dreq, K,
+  k_oc_batch<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->oc_view, dreq, K,
                                                 ctx->partials.as<double>());
   LAUNCHED();
   double* sums = ctx->partials0.as<double>();

@@ -151,7 +151,7 @@ struct ConvArgs {
   const double* x;   // design (owned)
   const double* cw;  // volume weights (owned)
   double move;
-  double4* ocrec;    // (lb, ub, ocP, cw) per element
+  double* ocp;       // ocP per element, -1 for passives (OcRecs)
 };
 
 // eta pass terms for one filtered value t (filter.hpp:187-201), evaluated
@@ -193,6 +193,21 @@ __device__ __forceinline__ double4 oc_record(double x, double dc, double dV, dou
   const double ocP = x * sqrt(std_max(0.0, -dc / dV));
   return make_double4(std_max(0.0, x - move), std_min(1.0, x + move), ocP, cw);
 }
+// The OC record (lb, ub, ocP, cw) of an element, stored as ocP only: lb and ub
+// follow from the design x (oc.hpp:55-56), cw is the volume-weight field
+// (null: 1), and ocP = -1 marks passives (lb = ub = x, candidate x).
+struct OcRecs {
+  const double* x;
+  const double* ocp;
+  const double* cw;
+  double move;
+  __device__ __forceinline__ double4 get(long long e) const {
+    const double xv = x[e], p = ocp[e], w = cw ? cw[e] : 1.0;
+    if (p < 0.0) return make_double4(xv, xv, 0.0, w);
+    return make_double4(std_max(0.0, xv - move), std_min(1.0, xv + move), p, w);
+  }
+};
+
 // oc.hpp:47-51
 __device__ __forceinline__ double oc_cand(const double4& r, double s) {
   const double f = s > 0 ? r.z / s : (r.z > 0 ? INFINITY : 0.0);
@@ -415,7 +430,7 @@ __device__ __forceinline__ void conv_store(const Geo& G, const ConvArgs& A, long
     if (A.out1) A.out1[e] = dV;
     const bool act = elem_state(A.state, e) == 0;
     const double4 rec = oc_record(A.x[e], dc, dV, A.cw ? A.cw[e] : 1.0, A.move, act);
-    A.ocrec[e] = rec;
+    A.ocp[e] = act ? rec.z : -1.0;
     if (act) red[0] += rec.z;
     red[1] += rec.w * oc_cand(rec, 0.0);
     red[2] += rec.w * std_min(std_max(0.0, rec.x), rec.y);  // V(s -> inf)
@@ -1256,7 +1271,7 @@ __global__ void __launch_bounds__(kThreads) k_oc_prep(long long m, const double*
                                                       const double* __restrict__ dV,
                                                       const uint8_t* __restrict__ state,
                                                       const double* __restrict__ cw, double move,
-                                                      double4* __restrict__ rec,
+                                                      double* __restrict__ ocp,
                                                       double* __restrict__ partials) {
   __shared__ double scratch[3 * 32];
   double red[3] = {0.0, 0.0, 0.0};
@@ -1264,7 +1279,7 @@ __global__ void __launch_bounds__(kThreads) k_oc_prep(long long m, const double*
        e += (long long)gridDim.x * blockDim.x) {
     const bool act = elem_state(state, e) == 0;
     const double4 r = oc_record(x[e], dc[e], dV[e], cw ? cw[e] : 1.0, move, act);
-    rec[e] = r;
+    ocp[e] = act ? r.z : -1.0;
     if (act) red[0] += r.z;
     red[1] += r.w * oc_cand(r, 0.0);
     red[2] += r.w * std_min(std_max(0.0, r.x), r.y);
@@ -1288,7 +1303,7 @@ constexpr int kOcK = 16;
 
 struct OcArgs {
   long long m;
-  const double4* rec;
+  OcRecs R;
   const double* prep_partials;  // stride 3, count n_prep
   int n_prep;
   double volfrac, rel_tol, vol_tol, abs_tol, lambda_max, mtotal, add_const;
@@ -1361,7 +1376,7 @@ __global__ void __launch_bounds__(kThreads) k_oc_bisect(OcArgs A) {
     for (int q = 0; q < KK; ++q) acc[q] = 0.0;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < A.m;
          e += (long long)gridDim.x * blockDim.x) {
-      const double4 r = A.rec[e];
+      const double4 r = A.R.get(e);
 #pragma unroll
       for (int q = 0; q < KK; ++q)
         if (q < K) acc[q] = fma(r.w, oc_cand_rcp(r, sreq[q], sinv[q]), acc[q]);
@@ -1415,18 +1430,18 @@ __global__ void __launch_bounds__(kThreads) k_oc_bisect(OcArgs A) {
 
 // K6: xNew at the final multiplier s = result[6] (oc.hpp:108, :171), skipped
 // when the bisection reported an error (result[3])
-__global__ void __launch_bounds__(kThreads) k_oc_final(long long m, const double4* __restrict__ rec,
+__global__ void __launch_bounds__(kThreads) k_oc_final(long long m, OcRecs R,
                                                        const double* __restrict__ result,
                                                        double* __restrict__ out) {
   if (result[3] != 0.0) return;
   const double s = result[6];
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
        e += (long long)gridDim.x * blockDim.x)
-    out[e] = oc_cand(rec[e], s);
+    out[e] = oc_cand(R.get(e), s);
 }
 
 // K block partial volume sums at the multipliers s[0..K) (multi-GPU OC round)
-__global__ void __launch_bounds__(kThreads) k_oc_batch(long long m, const double4* __restrict__ rec,
+__global__ void __launch_bounds__(kThreads) k_oc_batch(long long m, OcRecs R,
                                                        const double* __restrict__ s, int K,
                                                        double* __restrict__ partials) {
   __shared__ double scratch[kOcK * 32];
@@ -1442,7 +1457,7 @@ __global__ void __launch_bounds__(kThreads) k_oc_batch(long long m, const double
   }
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
        e += (long long)gridDim.x * blockDim.x) {
-    const double4 r = rec[e];
+    const double4 r = R.get(e);
 #pragma unroll
     for (int q = 0; q < kOcK; ++q)
       if (q < K) acc[q] = fma(r.w, oc_cand_rcp(r, sq[q], iq[q]), acc[q]);
@@ -1463,11 +1478,10 @@ __global__ void k_reduce_rows(const double* __restrict__ p, int count, double* _
 }
 
 // candidate at one multiplier (host-driven OC modes and final write)
-__global__ void k_oc_candidates(long long m, const double4* __restrict__ rec, double s,
-                                double* __restrict__ out) {
+__global__ void k_oc_candidates(long long m, OcRecs R, double s, double* __restrict__ out) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
        e += (long long)gridDim.x * blockDim.x)
-    out[e] = oc_cand(rec[e], s);
+    out[e] = oc_cand(R.get(e), s);
 }
 
 // block partial sums of v (optionally projected: mean(H(v)))
