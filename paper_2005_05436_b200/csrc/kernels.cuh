@@ -889,7 +889,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, El
        e += (long long)gridDim.x * blockDim.x) {
     int i, k, j;
     elem_ijk(G, e, i, k, j);
+    // every load of the element first (latency overlap): x~, hs, state, u_e
     const double t = A.xt[e];
+    const double hsv = A.a1 ? A.hs[e] : 1.0;
+    const int st = elem_state(A.state, e);
+    const long long n0 = (long long)(j - G.j0) * pl + (long long)k * ny1 + i;  // node (i, k, j)
+    double h[3][8];  // [component][binary node index oi + 2 ok + 4 oj]
+    {
+      // the element's nodes are 4 (k, j) pairs of 2 consecutive i: 6 doubles each
+      const double* u0 = A.U + 3 * n0;
+      const double* up[4] = {u0, u0 + 3 * ny1, u0 + 3 * pl, u0 + 3 * (pl + ny1)};
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) h[c][b] = __ldg(up[b >> 1] + 3 * (b & 1) + c);
+    }
     double xphys, dH;
     if (A.input_is_phys) {
       xphys = t;
@@ -902,17 +916,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, El
     const double xp = simp_xp(xphys, A.penal);
     const double sK = A.emin + xp * xphys * de;  // fea.hpp:142
     const double dsK = A.penal * xp * de;        // fea.hpp:143
-    const long long n0 = (long long)(j - G.j0) * pl + (long long)k * ny1 + i;  // node (i, k, j)
-    double h[3][8];  // [component][binary node index oi + 2 ok + 4 oj]
-    {
-      // the element's nodes are 4 (k, j) pairs of 2 consecutive i: 6 doubles each
-      const double* u0 = A.U + 3 * n0;
-      const double* up[4] = {u0, u0 + 3 * ny1, u0 + 3 * pl, u0 + 3 * (pl + ny1)};
-#pragma unroll
-      for (int b = 0; b < 8; ++b)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) h[c][b] = __ldg(up[b >> 1] + 3 * (b & 1) + c);
-    }
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -938,13 +941,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, El
       q2 = fma(m2, kk[5] * m2, q2);
     }
     csum = fma(sK, q2, csum);
-    const int st = elem_state(A.state, e);
     const double dcp = st == 0 ? -dsK * q2 : 0.0;
     const double dv0 = st == 0 ? A.inv_m : 0.0;  // driver.hpp:155
     if (A.xPhys) A.xPhys[e] = xphys;
     if (A.dcPhys) A.dcPhys[e] = dcp;
     if (A.a1) {
-      const double ih = 1.0 / A.hs[e];
+      const double ih = 1.0 / hsv;
       const long long es = e + (long long)(G.j0 - G.sj0) * G.S;
       A.a1[es] = (dH * dcp) * ih;  // backfilter, filter.hpp:170, :128
       A.a2[es] = (dH * dv0) * ih;
