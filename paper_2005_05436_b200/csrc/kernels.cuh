@@ -437,6 +437,31 @@ __device__ __forceinline__ void conv_store(const Geo& G, const ConvArgs& A, long
   }
 }
 
+// conv_store with the per-element inputs already loaded: l0 = hs (FWD) or x
+// (ADJ2_OC), l1 = cw (ADJ2_OC), st = element state
+template <int NF, int MODE>
+__device__ __forceinline__ void conv_store_pre(const ConvArgs& A, long long e, double v0, double v1,
+                                               double l0, double l1, int st, double (&red)[3]) {
+  if (MODE == CONV_PLAIN || MODE == CONV_ADJ_DIV) {
+    A.out0[e] = v0;
+  } else if (MODE == CONV_FWD) {
+    double v = v0 / l0;  // filter.hpp:121 cwiseQuotient(hs)
+    if (A.pin && st == 1) v = 1.0;  // driver.hpp:130-133
+    if (A.pin && st == 2) v = 0.0;
+    A.out0[e] = v;
+  } else if (MODE == CONV_ADJ2_OC) {
+    const double dc = v0, dV = NF > 1 ? v1 : v0;
+    if (A.out0) A.out0[e] = dc;
+    if (A.out1) A.out1[e] = dV;
+    const bool act = st == 0;
+    const double4 rec = oc_record(l0, dc, dV, l1, A.move, act);
+    A.ocp[e] = act ? rec.z : -1.0;
+    if (act) red[0] += rec.z;
+    red[1] += rec.w * oc_cand(rec, 0.0);
+    red[2] += rec.w * std_min(std_max(0.0, rec.x), rec.y);  // V(s -> inf)
+  }
+}
+
 template <int MODE>
 __device__ __forceinline__ void conv_partials(const ConvArgs& A, double (&red)[3]) {
   if (MODE == CONV_ADJ2_OC) {
@@ -586,15 +611,48 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv3(Geo G, ConvGeom T,
         for (int r = 0; r < RB; ++r) keep[t][r] = acc[t][r];
       continue;
     }
+    if (MODE != CONV_FWD) {  // (measured: batching the ADJ2_OC loads costs registers)
 #pragma unroll
-    for (int t = 0; t < TB; ++t)
+      for (int t = 0; t < TB; ++t)
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          const int grun = br + wr * RB + r, go = bo + wo * TB + t;
+          if (gi >= G.nely || grun >= T.run_n || go >= T.other_n) continue;
+          const long long e = ((long long)go * T.run_n + grun) * G.nely + gi;
+          conv_store<NF, MODE>(G, A, e, NF > 1 ? keep[t][r] : acc[t][r], acc[t][r], red);
+        }
+      continue;
+    }
+    // FWD epilogue one output row (RB outputs) at a time, its loads issued first
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      const int go = bo + wo * TB + t;
+      long long eo[RB];
+      double l0[RB], l1[RB];
+      int sv[RB];
 #pragma unroll
       for (int r = 0; r < RB; ++r) {
-        const int grun = br + wr * RB + r, go = bo + wo * TB + t;
-        if (gi >= G.nely || grun >= T.run_n || go >= T.other_n) continue;
-        const long long e = ((long long)go * T.run_n + grun) * G.nely + gi;
-        conv_store<NF, MODE>(G, A, e, NF > 1 ? keep[t][r] : acc[t][r], acc[t][r], red);
+        const int grun = br + wr * RB + r;
+        const bool ok = gi < G.nely && grun < T.run_n && go < T.other_n;
+        eo[r] = ok ? ((long long)go * T.run_n + grun) * G.nely + gi : -1;
+        l0[r] = l1[r] = 0.0;
+        sv[r] = 0;
+        if (ok) {
+          if (MODE == CONV_FWD) l0[r] = A.hs[eo[r]];
+          if (MODE == CONV_ADJ2_OC) {
+            l0[r] = A.x[eo[r]];
+            l1[r] = A.cw ? A.cw[eo[r]] : 1.0;
+          }
+          if (MODE == CONV_FWD || MODE == CONV_ADJ2_OC) sv[r] = elem_state(A.state, eo[r]);
+        }
       }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        if (eo[r] < 0) continue;
+        conv_store_pre<NF, MODE>(A, eo[r], NF > 1 ? keep[t][r] : acc[t][r], acc[t][r], l0[r],
+                                 l1[r], sv[r], red);
+      }
+    }
   }
   conv_partials<MODE>(A, red);
 }
