@@ -549,6 +549,14 @@ __device__ __forceinline__ void conv3_di(const double* __restrict__ base, int di
   for (int a = 0; a < NW; ++a)
 #pragma unroll
     for (int b = 0; b < NW; ++b) w[a][b] = __ldg(w3 + (di * NW + a) * NW + b);
+  int hw[NW];  // largest |dr| with a nonzero weight at (di, |do|), -1: none
+#pragma unroll
+  for (int a = 0; a < NW; ++a) {
+    hw[a] = -1;
+#pragma unroll
+    for (int b = 0; b < NW; ++b)
+      if (w[a][b] != 0.0) hw[a] = b;
+  }
   const double* p = base + di * sI;
   const double* q = base - di * sI;
 #pragma unroll
@@ -562,11 +570,20 @@ __device__ __forceinline__ void conv3_di(const double* __restrict__ base, int di
       const int dO = kk - t - AR;
       if (dO < -AR || dO > AR) continue;
       const int ao = dO < 0 ? -dO : dO;
+      // taps outside the cone (zero weight) skipped by uniform branches on the
+      // column's half-width hw[ao] (its weights vanish beyond it)
+      const int hwa = hw[ao];
+      if (hwa < 0) continue;
 #pragma unroll
-      for (int d = 0; d < 2 * AR + 1; ++d) {
-        const double wv = w[ao][d < AR ? AR - d : d - AR];
+      for (int r = 0; r < RB; ++r) acc[t][r] = fma(w[ao][0], v[r + AR], acc[t][r]);
 #pragma unroll
-        for (int r = 0; r < RB; ++r) acc[t][r] = fma(wv, v[r + d], acc[t][r]);
+      for (int ad = 1; ad <= AR; ++ad) {
+        if (hwa < ad) break;
+#pragma unroll
+        for (int r = 0; r < RB; ++r) {
+          acc[t][r] = fma(w[ao][ad], v[r + AR - ad], acc[t][r]);
+          acc[t][r] = fma(w[ao][ad], v[r + AR + ad], acc[t][r]);
+        }
       }
     }
   }
