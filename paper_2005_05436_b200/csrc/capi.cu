@@ -57,9 +57,9 @@ bool is_device_ptr(const void* p) {
 struct topo_ctx {
   std::string err;
   int device = 0;
-  cudaStream_t stream = nullptr, aux = nullptr;
+  cudaStream_t stream = nullptr, aux = nullptr, cstream = nullptr;  // main, sK, copies
   bool own_stream = true;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_x = nullptr, ev_u = nullptr;
   int sm_count = 148;
   Geo G{};
   int rank = 0, nranks = 1;
@@ -449,19 +449,43 @@ int conv_blocks(const topo_ctx* ctx) {
 }
 
 // K3b: grid sized for full occupancy (no shared-memory or barrier limits)
+// K3b. Serial (main stream): grid sized for full occupancy, static split.
+// Overlapped (aux stream, large 3D passes): 2 blocks per SM claiming work
+// dynamically, so the stream keeps its rate while K3a / K4 blocks share the SMs
+// (measured on C5: 6.38 ms per pass against 6.84 ms serial).
 topo_status launch_sk(topo_ctx* ctx, const SkArgs& S, cudaStream_t st) {
   const Geo& G = ctx->G;
   int nb = grid_for(ctx, (G.m + 31) / 32 * 32);
-  const char* e = getenv("TOPO_SK_BPS");  // blocks per SM (experiments; overlap default 2)
-  if (e || st == ctx->aux) {
-    const int bps = e ? atoi(e) : 2;
-    nb = std::min(nb, ctx->sm_count * std::max(1, bps));
+  const bool ov = st == ctx->aux;
+  const char* e = getenv("TOPO_SK_BPS");  // blocks per SM (experiments)
+  if (e || ov) nb = std::min(nb, ctx->sm_count * std::max(1, e ? atoi(e) : 2));
+  SkArgs S2 = S;
+  S2.counter = nullptr;
+  static const char* de = getenv("TOPO_SK_DYN");
+  if (de ? atoi(de) != 0 : ov) {
+    S2.counter = reinterpret_cast<unsigned long long*>(ctx->result.as<double>() + 63);
+    CK(cudaMemsetAsync(S2.counter, 0, sizeof(unsigned long long), st));
   }
   if (G.is3d)
-    k_sk_store<300><<<nb, kThreads, 0, st>>>(G, S);
+    k_sk_store<300><<<nb, kThreads, 0, st>>>(G, S2);
   else
-    k_sk_store<36><<<nb, kThreads, 0, st>>>(G, S);
+    k_sk_store<36><<<nb, kThreads, 0, st>>>(G, S2);
   LAUNCHED();
+  return TOPO_OK;
+}
+
+// The SM's L1 / shared split is fixed while any block is resident. Kernels
+// that co-run with the adjoint filter (k_conv3, ~100 KB per block) prefer the
+// maximum shared carveout, or the filter's blocks wait for the SMs to drain.
+topo_status set_overlap_carveout() {
+  static bool done = false;
+  if (done) return TOPO_OK;
+  for (const void* f : {(const void*)k_sk_store<300>, (const void*)k_sk_store<36>,
+                        (const void*)k_elem_walsh})
+    if (cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             int(cudaSharedmemCarveoutMaxShared)) != cudaSuccess)
+      return TOPO_ECUDA;
+  done = true;
   return TOPO_OK;
 }
 
@@ -477,7 +501,7 @@ topo_status reduce_on_device(topo_ctx* ctx, const double* partials, int count, d
 
 // device scratch layout of ctx->result (64 doubles): [0..5) pass scalars
 // (eta, iterations, g, -, c), [8..15) OC results, [24..36) pre-reductions,
-// [40..56) OC requests, [56..64) reduce_to_host
+// [40..56) OC requests, [56..63) reduce_to_host, [63] sK work counter
 template <int N>
 topo_status reduce_to_host(topo_ctx* ctx, const double* partials, int count) {
   double* dst = ctx->result.as<double>() + 56;
@@ -901,8 +925,10 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
     return bail(fail(ctx, TOPO_EINVAL, "filter: rmin %.3g too large for the shared-memory tile",
                      d->rmin));
   {
+    // sK stream overlapped with K3a + K4 on large single-GPU 3D passes (C5)
     const char* ov = getenv("TOPO_SK_OVERLAP");
-    ctx->overlap_sk = ov && ov[0] == '1';
+    const bool big = G.is3d && double(G.m) * G.P * 8.0 >= 4e9 && d->nranks == 1;
+    ctx->overlap_sk = ov ? ov[0] == '1' : big;
     const char* fu = getenv("TOPO_SK_FUSE");
     ctx->fuse_sk = fu && fu[0] == '1';
   }
@@ -915,6 +941,11 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   } while (0)
   CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   CKC(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+  CKC(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+  CKC(cudaEventCreateWithFlags(&ctx->ev_x, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&ctx->ev_u, cudaEventDisableTiming));
+  if (ctx->overlap_sk && set_overlap_carveout() != TOPO_OK)
+    return bail(fail(ctx, TOPO_ECUDA, "cannot set the shared-memory carveout"));
   CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
   CKC(cudaMallocHost(&ctx->h_result, 64 * sizeof(double)));
@@ -998,7 +1029,10 @@ void topo_ctx_destroy(topo_ctx* ctx) {
     if (ctx->tev[q]) cudaEventDestroy(ctx->tev[q]);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->ev_x) cudaEventDestroy(ctx->ev_x);
+  if (ctx->ev_u) cudaEventDestroy(ctx->ev_u);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
   if (ctx->stream && ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -1456,9 +1490,10 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     return fail(ctx, TOPO_EINVAL, "design pass: volume mode %d not supported in the fused pass",
                 vmode);
   const uint8_t* state = ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr;
-  const double *xs, *ud;
+  const double *xs, *ud = nullptr;
   TRY(stage_field_storage(ctx, x, ctx->x_st.p ? ctx->x_st : ctx->tmp_st, &xs));
-  TRY(stage_in(ctx, U, ctx->n, ctx->u, &ud));
+  if (!U) return fail(ctx, TOPO_EINVAL, "null input array");
+  CK(cudaEventRecord(ctx->ev_x, ctx->stream));  // x staged: a host U may follow on the link
   const double* xown = xs + (long long)(G.j0 - G.sj0) * G.S;
   double* res = ctx->result.as<double>();
 
@@ -1509,13 +1544,29 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   // separate K3b, overlapped on the aux stream or last on the main stream
   const bool fuse_sk = want_sk && ctx->fuse_sk;
   const bool overlap = want_sk && !fuse_sk && ctx->overlap_sk && !ctx->comm;
-  if (overlap) {
+  static const bool fork_late = getenv("TOPO_SK_FORK_LATE") != nullptr;  // experiment
+  auto fork_sk = [&]() -> topo_status {
     CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
     CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
     tmark(ctx, TOPO_STAGE_SK, 0, ctx->aux);
     TRY(launch_sk(ctx, S, ctx->aux));
     tmark(ctx, TOPO_STAGE_SK, 1, ctx->aux);
     CK(cudaEventRecord(ctx->ev_join, ctx->aux));
+    return TOPO_OK;
+  };
+  if (overlap && !fork_late) TRY(fork_sk());
+  // U: a host array is copied on the copy stream behind x, overlapping K1, K2
+  // and the sK stream; K3a waits for it
+  if (is_device_ptr(U)) {
+    ud = U;
+  } else {
+    CK(ctx->u.ensure(sizeof(double) * size_t(ctx->n)));
+    CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_x, 0));
+    CK(cudaMemcpyAsync(ctx->u.p, U, sizeof(double) * size_t(ctx->n), cudaMemcpyHostToDevice,
+                       ctx->cstream));
+    CK(cudaEventRecord(ctx->ev_u, ctx->cstream));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_u, 0));
+    ud = ctx->u.as<double>();
   }
   // K3a
   tmark(ctx, TOPO_STAGE_ELEM, 0, ctx->stream);
@@ -1575,6 +1626,7 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     TRY(comm_halo(ctx->comm, ctx, ctx->a2_st.as<double>()));
   }
   tmark(ctx, TOPO_STAGE_ELEM, 1, ctx->stream);
+  if (overlap && fork_late) TRY(fork_sk());
   // K4
   tmark(ctx, TOPO_STAGE_ADJOINT, 0, ctx->stream);
   ConvArgs A4{};

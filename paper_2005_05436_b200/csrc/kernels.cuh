@@ -1044,6 +1044,7 @@ struct SkArgs {
   const double* eta_ptr;  // device scalar eta
   double beta, e0, emin, penal;
   double* sK;
+  unsigned long long* counter;  // non-null: dynamic work distribution (zeroed before launch)
 };
 
 // 256-bit streaming store (STG.E.EF.ENL2.256 on sm_100a): evict-first, the
@@ -1058,6 +1059,10 @@ __device__ __forceinline__ void st256_cs(double* p, double a, double b, double c
 // element l (one tanh + SIMP), then the warp streams the group's 32*P values
 // as 32-byte vectors (fully coalesced, no block barriers), taking each value's
 // modulus from its owner lane by shuffle and Ke_lower from shared memory.
+#ifndef SKU
+#define SKU 4
+#endif
+constexpr int kSkUnroll = SKU;
 template <int P>
 __global__ void __launch_bounds__(kThreads) k_sk_store(Geo G, SkArgs A) {
   constexpr int PV = P / 4;  // double4 per element
@@ -1074,10 +1079,8 @@ __global__ void __launch_bounds__(kThreads) k_sk_store(Geo G, SkArgs A) {
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   const long long ngroups = (G.m + 31) >> 5;
-  for (long long g = warp0; g < ngroups; g += nwarps) {
+  auto group = [&](long long g) {
     const long long e0 = g << 5;
     const int ne = int(min(32LL, G.m - e0));
     double s = 0.0;
@@ -1092,7 +1095,7 @@ __global__ void __launch_bounds__(kThreads) k_sk_store(Geo G, SkArgs A) {
     }
     double* out = A.sK + e0 * P;
     const int nv = ne * PV;
-#pragma unroll 4
+#pragma unroll kSkUnroll
     for (int base = 0; base < nv; base += 32) {
       const int v = base + lane;
       const int el = min(v / PV, 31);
@@ -1102,7 +1105,24 @@ __global__ void __launch_bounds__(kThreads) k_sk_store(Geo G, SkArgs A) {
         st256_cs(out + 4 * (long long)v, se * k.x, se * k.y, se * k.z, se * k.w);  // fea.hpp:168
       }
     }
+  };
+  if (A.counter) {
+    // dynamic: warps claim runs of GCH groups, so blocks that share an SM with
+    // other kernels simply claim fewer (the static split would wait on them)
+    constexpr int GCH = 4;
+    for (;;) {
+      unsigned long long g0 = 0;
+      if (lane == 0) g0 = atomicAdd(A.counter, (unsigned long long)GCH);
+      g0 = __shfl_sync(0xffffffffu, g0, 0);
+      if ((long long)g0 >= ngroups) break;
+      const long long g1 = min((long long)g0 + GCH, ngroups);
+      for (long long g = (long long)g0; g < g1; ++g) group(g);
+    }
+    return;
   }
+  const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long g = warp0; g < ngroups; g += nwarps) group(g);
 }
 
 // K3a + K3b fused: one warp owns 32 consecutive elements; each lane computes
