@@ -101,7 +101,8 @@ struct topo_ctx {
   int conv_R = 8;              // outputs per thread along the run axis
   int conv_A = 0;              // > 0: small-reach direct variant with half-width bound A
   bool overlap_sk = false;     // run the sK store concurrently with K3a..K6
-  bool fuse_sk = false;        // stream sK from the sensitivity kernel (K3a + K3b)
+  bool fuse_sk = false;
+  int oc_blocks_now = 0;  // > 0: cooperative OC grid for this call (beside the sK stream)        // stream sK from the sensitivity kernel (K3a + K3b)
   int coop_blocks = 148;  // OC bisection grid (cooperative)
   int coop_eta = 148;     // eta Newton grid (cooperative)
   long long launches = 0;
@@ -596,11 +597,12 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
     }
     // 4 bisection levels per grid-wide round (k_oc_bisect<32> does 5 levels;
     // measured slower on C1-C3: 224 registers, one block per SM)
-    TRY(coop_launch(ctx, (const void*)k_oc_bisect<16>, &A, ctx->coop_blocks));
+    const int ocb = ctx->oc_blocks_now > 0 ? ctx->oc_blocks_now : ctx->coop_blocks;
+    TRY(coop_launch(ctx, (const void*)k_oc_bisect<16>, &A, ocb));
     if (prof) {
       long long h[128];
       CK(cudaMemcpy(h, A.dbg, sizeof h, cudaMemcpyDeviceToHost));
-      fprintf(stderr, "[oc profile] blocks %d marks %lld:", ctx->coop_blocks, h[127]);
+      fprintf(stderr, "[oc profile] blocks %d marks %lld:", ocb, h[127]);
       for (int q = 1; q < h[127]; ++q) fprintf(stderr, " %lld", h[q] - h[q - 1]);
       fprintf(stderr, "\n");
     }
@@ -1481,6 +1483,7 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
                              const topo_pass_params* prm, topo_pass_out* out) {
   if (!ctx || !prm || !out) return TOPO_EINVAL;
   ctx->launches = 0;
+  ctx->oc_blocks_now = 0;
   const Geo& G = ctx->G;
   if (ctx->nranks > 1 && !ctx->comm)
     return fail(ctx, TOPO_EINVAL, "multi-rank context: call topo_comm_init_nccl/_host first");
@@ -1644,10 +1647,12 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   int nb4 = 0;
   TRY((launch_conv<2, CONV_ADJ2_OC>(ctx, G, A4, &nb4)));
   tmark(ctx, TOPO_STAGE_ADJOINT, 1, ctx->stream);
-  // K5 + K6
-  // the overlapped sK stream joins before the cooperative OC kernels, whose
-  // blocks must all be resident
-  if (overlap) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+  // K5 + K6: beside the overlapped sK stream, with one cooperative block per
+  // SM (all resident next to its 2 blocks per SM); else after the join
+  static const char* oce = getenv("TOPO_OC_EARLY");
+  const bool oc_early = overlap && (oce ? oce[0] == '1' : true);
+  if (overlap && !oc_early) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+  if (oc_early) ctx->oc_blocks_now = std::min(ctx->coop_blocks, ctx->sm_count);
   tmark(ctx, TOPO_STAGE_OC, 0, ctx->stream);
   topo_oc_params oc{prm->move, prm->volfrac, 1e-4, 1e-3, 0, 1e-8, 0.0};  // oc.hpp:14-20 defaults
   double lam = 0;
@@ -1656,6 +1661,8 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   TRY(run_oc(ctx, &oc, vmode, ctx->partials0.as<double>(), nb4, ctx->xnew.as<double>(), &lam,
              &bis, &ev, 0.0, prm->beta, nullptr, nullptr, &oc_deferred));
   tmark(ctx, TOPO_STAGE_OC, 1, ctx->stream);
+  ctx->oc_blocks_now = 0;
+  if (oc_early) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
   if (want_sk && !fuse_sk && !overlap) {
     tmark(ctx, TOPO_STAGE_SK, 0, ctx->stream);
     TRY(launch_sk(ctx, S, ctx->stream));
