@@ -1,0 +1,96 @@
+"""The design pass's execution variants agree with each other and with the
+oracle: the sK stream overlapped with K3a/K4 (TOPO_SK_OVERLAP, default on large
+3D passes) versus serial, host versus device inputs (the host U copy overlaps
+K1/K2), the register-blocked 3D filter (k_conv3) versus the column kernel,
+and the Walsh-block H8 sensitivity versus the dense quadratic form. Variants
+that run the same arithmetic must agree bit for bit; those that reorder sums
+within 1e-12 (max-normalised), like every GPU/oracle comparison."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from tests.common import rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2005_05436_b200 as P
+    return P
+
+
+def _inputs(cfg, seed=7):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(0.01, 1.0, cfg.m), rng.normal(size=cfg.n)
+
+
+def _pass(P, cfg, x, u, env=None, **kw):
+    old = {k: os.environ.get(k) for k in (env or {})}
+    os.environ.update(env or {})
+    try:
+        with P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu) as ctx:
+            return ctx.design_pass(x, u, beta=cfg.beta, eta0=cfg.eta0, move=cfg.move,
+                                   volfrac=cfg.volfrac, return_sk=True, **kw)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _as_np(a):
+    return a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+
+
+FIELDS = ("xTilde", "xPhys", "dcPhys", "dc", "dV", "xNew", "sK")
+
+
+@pytest.mark.parametrize("grid", [(24, 16, 12), (40, 24, 16)])
+def test_overlapped_sk_stream_is_bitwise_serial(P, grid):
+    from paper_2005_05436_b200.configs import CONFIGS
+    cfg = CONFIGS[5].scaled(*grid)
+    x, u = _inputs(cfg)
+    xd, ud = torch.from_numpy(x).cuda(), torch.from_numpy(u).cuda()
+    a = _pass(P, cfg, xd, ud, {"TOPO_SK_OVERLAP": "0"})
+    b = _pass(P, cfg, xd, ud, {"TOPO_SK_OVERLAP": "1"})
+    for k in FIELDS:
+        np.testing.assert_array_equal(_as_np(getattr(a, k)), _as_np(getattr(b, k)), err_msg=k)
+    assert (a.eta, a.lam, a.bisections, a.c) == (b.eta, b.lam, b.bisections, b.c)
+
+
+@pytest.mark.parametrize("overlap", ["0", "1"])
+def test_host_inputs_match_device_inputs(P, overlap):
+    from paper_2005_05436_b200.configs import CONFIGS
+    cfg = CONFIGS[4].scaled(20, 12, 10)
+    x, u = _inputs(cfg, 3)
+    env = {"TOPO_SK_OVERLAP": overlap}
+    dev = _pass(P, cfg, torch.from_numpy(x).cuda(), torch.from_numpy(u).cuda(), env)
+    host = _pass(P, cfg, x, u, env)  # numpy: host pointers through the C-ABI
+    for k in FIELDS:
+        np.testing.assert_array_equal(_as_np(getattr(dev, k)), _as_np(getattr(host, k)), err_msg=k)
+
+
+@pytest.mark.parametrize("cid,grid", [(4, (20, 14, 12)), (5, (30, 20, 16))])
+def test_conv3_matches_column_kernel(P, cid, grid):
+    from paper_2005_05436_b200.configs import CONFIGS
+    cfg = CONFIGS[cid].scaled(*grid)
+    x, u = _inputs(cfg, 11)
+    a = _pass(P, cfg, x, u, {"TOPO_CONV3": "0"}, eta_override=0.5)
+    b = _pass(P, cfg, x, u, {"TOPO_CONV3": "1"}, eta_override=0.5)
+    for k in ("xTilde", "dc", "dV"):
+        assert rel(_as_np(getattr(b, k)), _as_np(getattr(a, k))) <= 1e-13, k
+
+
+def test_walsh_sensitivity_matches_dense(P):
+    from paper_2005_05436_b200.configs import CONFIGS
+    cfg = CONFIGS[4].scaled(18, 12, 10)
+    x, u = _inputs(cfg, 5)
+    a = _pass(P, cfg, x, u, {"TOPO_ELEM_WALSH": "0"}, eta_override=0.5)
+    b = _pass(P, cfg, x, u, {"TOPO_ELEM_WALSH": "1"}, eta_override=0.5)
+    for k in ("dcPhys", "dc", "xNew"):
+        assert rel(_as_np(getattr(b, k)), _as_np(getattr(a, k))) <= 1e-12, k
+    assert abs(a.c - b.c) <= 1e-12 * abs(a.c)
