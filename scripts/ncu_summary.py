@@ -14,12 +14,14 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
         "smsp__inst_executed.sum", "sm__instruction_throughput.avg.pct_of_peak_sustained_active",
-        "lts__t_bytes.sum"]
+        "lts__t_bytes.sum", "l1tex__throughput.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed.avg.per_cycle_active"]
 
 def main(rep):
     h, units, rows = raw(rep)
     idx = {k: i for i, k in enumerate(h)}
-    stall_cols = [k for k in h if k.startswith("smsp__average_warp_latency_issue_stalled_") and k.endswith(".ratio")]
+    pre, suf = "smsp__average_warps_issue_stalled_", "_per_issue_active.ratio"
+    stall_cols = [k for k in h if k.startswith(pre) and k.endswith(suf)]
     for r in rows:
         name = r[idx["Kernel Name"]][:60]
         print("==", name)
@@ -29,7 +31,7 @@ def main(rep):
         st = []
         for k in stall_cols:
             try:
-                st.append((float(r[idx[k]]), k.replace("smsp__average_warp_latency_issue_stalled_", "").replace(".ratio", "")))
+                st.append((float(r[idx[k]]), k[len(pre):-len(suf)]))
             except ValueError:
                 pass
         st.sort(reverse=True)
