@@ -296,8 +296,14 @@ def run_ours(args, cfg, rank, world, local_rank):
         e2e_ms = float(t.item())
     h2d = 8 * (x.size + u.size) * world
     d2h = (8 * m_local + 8 * 5) * world
+    fp64 = None
+    if rank == 0:  # FP64 DFMA peak of this GPU (the C2/C3 roof)
+        t = C.c_double()
+        if ctx.lib.topo_fp64_peak(local_rank, C.byref(t)) == 0:
+            fp64 = t.value
     return dict(ms=ms, e2e_ms=e2e_ms, stages=stages, launches=launches, clocks=clk.summary(),
-                h2d=h2d, d2h=d2h, r=r, m_local=m_local, flushed=flush is not None)
+                h2d=h2d, d2h=d2h, r=r, m_local=m_local, flushed=flush is not None,
+                ntaps=ctx.ntaps, fp64_peak=fp64)
 
 
 def main():
@@ -355,6 +361,11 @@ def main():
     traffic = load_traffic(cfg.cid)
     b_elem = algorithmic_bytes_per_elem(cfg)
     pass_gbs = m * b_elem / (res["ms"] * 1e-3) / 1e9 / max(1, args.gpus)
+    # FP64 work per element: 3 convolutions x 2 T flops + the
+    # sensitivity (2D 144, 3D 1200 as the dense form counts it)
+    flop_elem = 6 * res["ntaps"] + (1200 if cfg.nelz else 144)
+    fp64_tf = m * flop_elem / (res["ms"] * 1e-3) / 1e12 / max(1, world)
+    workload["taps"] = res["ntaps"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": res["ms"], "higher_is_better": True,
@@ -372,6 +383,10 @@ def main():
                           "achieved": pass_gbs, "peak": peak, "unit": "GB/s",
                           "frac": pass_gbs / peak,
                           "ceiling_melem_s": peak * 1e9 / b_elem / 1e6 * max(1, args.gpus)},
+        "fp64_roofline": {"flop_per_elem": flop_elem, "achieved": fp64_tf,
+                          "peak": res["fp64_peak"], "unit": "TFLOP/s",
+                          "frac": fp64_tf / res["fp64_peak"] if res["fp64_peak"] else None,
+                          "peak_source": "measured DFMA loop (topo_fp64_peak)"},
         "stages_ms": res["stages"],
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": res["h2d"],
                 "d2h_bytes_per_step": res["d2h"], "ms_per_step": res["e2e_ms"]},

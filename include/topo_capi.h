@@ -220,6 +220,12 @@ enum { TOPO_STAGE_FILTER = 0, TOPO_STAGE_ETA, TOPO_STAGE_ELEM, TOPO_STAGE_ADJOIN
 topo_status topo_set_timing(topo_ctx* ctx, int on);
 topo_status topo_stage_times(topo_ctx* ctx, double* times_ms);
 
+/* ---- measurement helper (not part of the reference API) ------------------
+ * FP64 FMA throughput of `device` in TFLOP/s (2 flops per DFMA), measured
+ * with a dependent-chain-free DFMA loop over the whole GPU (SURVEY.md §8(d):
+ * the FP64 roof of the filter-bound configs C2/C3). */
+topo_status topo_fp64_peak(int device, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,8 +7,8 @@ C-ABI in include/topo_capi.h. See DESIGN.md.
 """
 from . import _lib
 from .api import (Context, CudaError, IndexOverflow, InvalidArgument, NonMonotone, OcParams,
-                  PassResult, SimpParams, TopoError, UpdateResult, element_stiffness, generate,
-                  nccl_unique_id, partition_domain, slab_plan)
+                  PassResult, SimpParams, TopoError, UpdateResult, element_stiffness, fp64_peak,
+                  generate, nccl_unique_id, partition_domain, slab_plan)
 from .configs import CONFIGS, Config, make_inputs
 
 BC_NEUMANN, BC_DIRICHLET = _lib.BC_NEUMANN, _lib.BC_DIRICHLET
@@ -19,5 +19,5 @@ _lib.load()  # fail loudly at import if the native library is missing
 
 __all__ = ["Context", "SimpParams", "OcParams", "PassResult", "UpdateResult", "TopoError",
            "InvalidArgument", "IndexOverflow", "NonMonotone", "CudaError", "element_stiffness",
-           "generate", "partition_domain", "CONFIGS", "Config", "make_inputs", "BC_NEUMANN",
+           "generate", "partition_domain", "fp64_peak", "CONFIGS", "Config", "make_inputs", "BC_NEUMANN",
            "BC_DIRICHLET", "VOL_CALLBACK", "VOL_MEAN", "VOL_PROJECTED", "VOL_FILTERED"]

@@ -209,6 +209,16 @@ def slab_plan(nelx: int, nely: int, nelz: int, rmin: float, rank: int, nranks: i
     return plan
 
 
+def fp64_peak(device: int = 0) -> float:
+    """Measured FP64 FMA throughput of `device` in TFLOP/s (DFMA loop)."""
+    lib = L.load()
+    t = C.c_double()
+    st = lib.topo_fp64_peak(device, C.byref(t))
+    if st:
+        _raise(st, "fp64 peak probe failed")
+    return t.value
+
+
 def partition_domain(grid, pasS=(), pasV=()) -> np.ndarray:
     """grid.hpp:155-188 as a per-element state byte array (0 act / 1 solid / 2 void)."""
     nelx, nely, nelz = grid

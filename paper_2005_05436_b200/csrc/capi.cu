@@ -1047,6 +1047,38 @@ topo_status topo_set_timing(topo_ctx* ctx, int on) {
   return TOPO_OK;
 }
 
+topo_status topo_fp64_peak(int device, double* tflops) {
+  if (!tflops) return TOPO_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return TOPO_ECUDA;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess)
+    return TOPO_ECUDA;
+  double* d = nullptr;
+  cudaEvent_t e0, e1;
+  if (cudaMalloc(&d, sizeof(double)) != cudaSuccess) return TOPO_ECUDA;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8, iters = 20000;
+  k_dfma_peak<<<blocks, kThreads>>>(200, 1.0, d);  // warm-up
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    cudaEventRecord(e0);
+    k_dfma_peak<<<blocks, kThreads>>>(iters, 1.0, d);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = std::min(best, ms);
+  }
+  const cudaError_t err = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  if (err != cudaSuccess) return TOPO_ECUDA;
+  *tflops = 2.0 * 8.0 * iters * double(blocks) * kThreads / (best * 1e-3) / 1e12;
+  return TOPO_OK;
+}
+
 topo_status topo_stage_times(topo_ctx* ctx, double* times_ms) {
   if (!ctx || !times_ms) return TOPO_EINVAL;
   for (int q = 0; q < TOPO_NSTAGES; ++q) times_ms[q] = ctx->stage_ms[q];

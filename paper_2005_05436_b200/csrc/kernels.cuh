@@ -1643,4 +1643,19 @@ __global__ void k_oc_compact(long long n, const double* __restrict__ x,
   if (threadIdx.x == 0 && partials) partials[blockIdx.x] = red[0];
 }
 
+// FP64 peak probe: 8 independent FMA chains per thread (topo_fp64_peak)
+__global__ void __launch_bounds__(kThreads) k_dfma_peak(int iters, double seed, double* out) {
+  double a[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) a[q] = seed + threadIdx.x * 1e-9 + q;
+  const double b = 0.999999999, c = 1e-12;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = fma(a[q], b, c);
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += a[q];
+  if (s == 12345.678) out[0] = s;  // keeps the loop alive
+}
+
 }  // namespace topo
