@@ -98,6 +98,9 @@ typedef struct {
   double* sK; /* m*P; NULL keeps the values in the context (topo_device_buffer) */
   double eta, c, lambda;
   int32_t eta_iters, bisections, evaluations;
+  /* duplicate-summed lower-triangle CSC values of K (topo_csc_pattern order,
+   * nnz entries), or NULL; single-rank contexts */
+  double* Kval;
 } topo_pass_out;
 
 /* device buffers owned by the context, for zero-copy consumers (the state
@@ -171,6 +174,15 @@ topo_status topo_simp_interpolate(topo_ctx* ctx, const double* xhat, const topo_
 /* fea.hpp:154-176 assemble_lower, value generation (:162-169): vals[e*P+q] =
  * sK[e] * Ke_lower[q] (duplicates are summed by the consumer) */
 topo_status topo_assemble_values(topo_ctx* ctx, const double* sK, double* vals);
+/* the matrix assemble_lower returns (fea.hpp:154-176): setFromTriplets of the
+ * (iK, jK, vals) triplets, i.e. the n x n lower triangle of K in compressed
+ * column form with ascending rows and duplicates summed in triplet order
+ * (ascending element). topo_csc_pattern: col_ptr n+1 (int64), row_idx nnz;
+ * any pointer may be NULL (query nnz first). topo_csc_values: values[nnz]
+ * from the per-element modulus sK (m), bitwise equal to the reference's sums.
+ * Built on the device without the m*P triplets; single-rank contexts. */
+topo_status topo_csc_pattern(topo_ctx* ctx, int64_t* col_ptr, int32_t* row_idx, int64_t* nnz);
+topo_status topo_csc_values(topo_ctx* ctx, const double* sK, double* values);
 /* fea.hpp:248-272 compliance_and_sensitivity (c is the rank-local partial) */
 topo_status topo_sensitivity(topo_ctx* ctx, const double* U, const double* xhat,
                              const topo_simp* prm, double* c, double* dc);

@@ -181,6 +181,8 @@ class Oracle:
             L.orc_set_threads.argtypes = [C.c_int]
             fn("element_stiffness", C.c_int, C.c_int, C.c_double, f64p, f64p)
             fn("assemble_values", None, C.c_int64, C.c_int, f64p, f64p, f64p)
+            fn("assemble_lower", C.c_int, Grid, C.c_double, f64p, i32p, i32p, f64p,
+               C.POINTER(C.c_int64))
             fn("compliance_sensitivity", C.c_int, Grid, f64p, f64p, f64p, C.c_double,
                C.c_double, C.c_double, u8p, C.POINTER(C.c_double), f64p)
             fn("apply_filter", None, C.c_void_p, f64p, f64p)
@@ -275,17 +277,16 @@ class Oracle:
         return out
 
     def assemble_lower_csc(self, grid, nu, sK):
-        """reference only: duplicate-summed lower CSC from assemble_lower."""
+        """duplicate-summed lower CSC of assemble_lower (fea.hpp:154-176)."""
         sK = _f64(sK)
         nnz = C.c_int64()
-        self._check(self.lib.ref_assemble_lower(Grid(*grid), nu, _p(sK), None, None, None,
-                                                C.byref(nnz)))
+        f = getattr(self.lib, self.pre + "assemble_lower")
+        self._check(f(Grid(*grid), nu, _p(sK), None, None, None, C.byref(nnz)))
         n = _num_dofs(grid)
         cp = np.empty(n + 1, np.int32)
         ri = np.empty(nnz.value, np.int32)
         va = np.empty(nnz.value)
-        self._check(self.lib.ref_assemble_lower(Grid(*grid), nu, _p(sK), _p(cp), _p(ri), _p(va),
-                                                C.byref(nnz)))
+        self._check(f(Grid(*grid), nu, _p(sK), _p(cp), _p(ri), _p(va), C.byref(nnz)))
         return cp, ri, va
 
     def compliance_sensitivity(self, grid, ke_full_or_nu, u, xhat, state=None, e0=1.0,

@@ -300,6 +300,69 @@ void orc_assemble_values(int64_t m, int P, const double* sK, const double* ke_lo
   }
 }
 
+/* fea.hpp:154-176 assemble_lower: the triplets (iK[t], jK[t], sK[e] * Ke_lower[q])
+ * of t = e*P + q through Eigen's setFromTriplets (restated from its published
+ * algorithm, Eigen 3.x SparseMatrix::setFromTriplets): triplets are bucketed
+ * by outer index (column, ColMajor) in input order, duplicates summed in that
+ * order (collapseDuplicates, scalar_sum_op), inner (row) indices ascending.
+ * Two calls: col_ptr/row_idx/values NULL returns nnz only. */
+int orc_assemble_lower(orc_grid g, double nu, const double* sK, int32_t* col_ptr,
+                       int32_t* row_idx, double* values, int64_t* nnz) {
+  const int dim = g.nelz > 0 ? 3 : 2, d = dim == 3 ? 24 : 8, P = d * (d + 1) / 2;
+  const int64_t m = (int64_t)g.nelx * g.nely * (g.nelz > 0 ? g.nelz : 1);
+  const int64_t n = (int64_t)dim * (g.nelx + 1) * (g.nely + 1) * (g.nelz > 0 ? g.nelz + 1 : 1);
+  const int64_t T = m * P;
+  double kf[576], kl[300];
+  if (orc_element_stiffness(dim, nu, kf, kl)) return 1;
+  int32_t* iK = malloc(sizeof(int32_t) * T);
+  int32_t* jK = malloc(sizeof(int32_t) * T);
+  int64_t* start = calloc((size_t)n + 1, sizeof(int64_t));
+  int64_t* order = malloc(sizeof(int64_t) * T);
+  int rc = orc_build_index_pairs(g, iK, jK);
+  if (!rc) {
+    for (int64_t t = 0; t < T; ++t) ++start[jK[t] + 1];
+    for (int64_t c = 0; c < n; ++c) start[c + 1] += start[c];
+    int64_t* fill = malloc(sizeof(int64_t) * n);
+    for (int64_t c = 0; c < n; ++c) fill[c] = start[c];
+    for (int64_t t = 0; t < T; ++t) order[fill[jK[t]]++] = t; /* input order per column */
+    free(fill);
+    /* per column: distinct rows ascending, each summed over its triplets in input order */
+    int64_t k = 0;
+    if (col_ptr) col_ptr[0] = 0;
+    for (int64_t c = 0; c < n; ++c) {
+      const int64_t a = start[c], b = start[c + 1];
+      /* stable insertion sort of this column's triplets by row (input order kept on ties) */
+      for (int64_t i = a + 1; i < b; ++i) {
+        const int64_t v = order[i];
+        int64_t j = i - 1;
+        while (j >= a && iK[order[j]] > iK[v]) {
+          order[j + 1] = order[j];
+          --j;
+        }
+        order[j + 1] = v;
+      }
+      for (int64_t i = a; i < b; ++i) {
+        const int64_t t = order[i];
+        const double v = sK[t / P] * kl[t % P]; /* fea.hpp:168 */
+        if (i == a || iK[t] != iK[order[i - 1]]) {
+          if (row_idx) row_idx[k] = iK[t];
+          if (values) values[k] = v;
+          ++k;
+        } else if (values) {
+          values[k - 1] += v;
+        }
+      }
+      if (col_ptr) col_ptr[c + 1] = (int32_t)k;
+    }
+    *nnz = k;
+  }
+  free(iK);
+  free(jK);
+  free(start);
+  free(order);
+  return rc;
+}
+
 /* fea.hpp:248-272 */
 int orc_compliance_sensitivity(orc_grid g, const double* ke_full, const double* u,
                                const double* xhat, double e0, double emin, double p,

@@ -48,6 +48,8 @@ int orc_element_stiffness(int dim, double nu, double* full, double* lower);
 void orc_simp(int64_t m, const double* xhat, double e0, double emin, double p, double* sK,
               double* dsK);
 void orc_assemble_values(int64_t m, int P, const double* sK, const double* ke_lower, double* vals);
+int orc_assemble_lower(orc_grid g, double nu, const double* sK, int32_t* col_ptr,
+                       int32_t* row_idx, double* values, int64_t* nnz);
 int orc_compliance_sensitivity(orc_grid g, const double* ke_full, const double* u,
                                const double* xhat, double e0, double emin, double p,
                                const uint8_t* state, double* c, double* dc);

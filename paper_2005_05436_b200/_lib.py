@@ -29,6 +29,7 @@ EXPORTS = [
     "topo_oc_candidate", "topo_oc_bisect", "topo_design_pass", "topo_last_launch_count",
     "topo_set_timing", "topo_stage_times", "topo_host_oc_replay", "topo_host_eta_replay",
     "topo_nccl_unique_id", "topo_comm_init_host", "topo_slab_plan", "topo_fp64_peak",
+    "topo_csc_pattern", "topo_csc_values",
 ]
 STAGES = ["filter", "eta", "elem", "adjoint", "oc", "sk_store", "pass"]
 
@@ -61,7 +62,7 @@ class PassOut(C.Structure):
                 ("dc", C.c_void_p), ("dV", C.c_void_p), ("xNew", C.c_void_p),
                 ("sK", C.c_void_p), ("eta", C.c_double), ("c", C.c_double),
                 ("lambda_", C.c_double), ("eta_iters", C.c_int32), ("bisections", C.c_int32),
-                ("evaluations", C.c_int32)]
+                ("evaluations", C.c_int32), ("Kval", C.c_void_p)]
 
 
 VOLUME_FN = C.CFUNCTYPE(C.c_double, C.c_void_p, C.POINTER(C.c_double), C.c_int64)
@@ -128,6 +129,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         "topo_set_timing": (C.c_int, [vp, C.c_int]),
         "topo_stage_times": (C.c_int, [vp, vp]),
         "topo_fp64_peak": (C.c_int, [C.c_int, vp]),
+        "topo_csc_pattern": (C.c_int, [vp, vp, vp, vp]),
+        "topo_csc_values": (C.c_int, [vp, vp, vp]),
         "topo_host_oc_replay": (C.c_int, [p(OcParams), C.c_double, SFUN, vp, C.c_int,
                                           p(C.c_double), p(C.c_int32), p(C.c_int32),
                                           p(C.c_double), p(C.c_int32)]),

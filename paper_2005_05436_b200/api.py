@@ -102,7 +102,7 @@ class _Arr:
 def _empty(n: int, like_device: bool, dtype=np.float64):
     if like_device:
         import torch
-        tdt = {np.float64: torch.float64, np.int32: torch.int32}[dtype]
+        tdt = {np.float64: torch.float64, np.int32: torch.int32, np.int64: torch.int64}[dtype]
         t = torch.empty(n, dtype=tdt, device="cuda")
         return t, t.data_ptr()
     a = np.empty(n, dtype=dtype)
@@ -159,6 +159,7 @@ class PassResult:
     bisections: int
     evaluations: int
     launches: int
+    Kval: object = None  # lower-triangle CSC values of K (return_K=True)
 
 
 # ---------------------------------------------------------- module helpers
@@ -451,6 +452,25 @@ class Context:
         self._check(self.lib.topo_assemble_values(self.h, a.ptr, ptr))
         return out
 
+    def csc_pattern(self, device: bool = False):
+        """Lower-triangle CSC pattern of K (assemble_lower / setFromTriplets,
+        fea.hpp:154-176): (col_ptr int64 n+1, row_idx int32 nnz)."""
+        nnz = C.c_int64()
+        self._check(self.lib.topo_csc_pattern(self.h, None, None, C.byref(nnz)))
+        cp, pc = _empty(self.n + 1, device, np.int64)
+        ri, pr = _empty(nnz.value, device, np.int32)
+        self._check(self.lib.topo_csc_pattern(self.h, pc, pr, None))
+        return cp, ri
+
+    def csc_values(self, sK, device: bool = False):
+        """Duplicate-summed CSC values from the per-element modulus sK (m)."""
+        a = _Arr(sK, n=self.m, name="csc: sK")
+        nnz = C.c_int64()
+        self._check(self.lib.topo_csc_pattern(self.h, None, None, C.byref(nnz)))
+        out, ptr = _empty(nnz.value, device or a.device)
+        self._check(self.lib.topo_csc_values(self.h, a.ptr, ptr))
+        return out
+
     def compliance_and_sensitivity(self, u, xhat, prm: SimpParams = SimpParams()):
         ua = _Arr(u, n=self.n, name="sensitivity: displacement")
         xa = _Arr(xhat, n=self.m, name="sensitivity: field")
@@ -507,7 +527,7 @@ class Context:
                     volfrac: float = 0.5, simp: SimpParams = SimpParams(),
                     eta_override: float = math.nan, volume_mode: int = L.VOL_FILTERED,
                     write_sk: bool = True, return_sk: bool = False, outputs: bool = True,
-                    out_device: Optional[bool] = None) -> PassResult:
+                    out_device: Optional[bool] = None, return_K: bool = False) -> PassResult:
         xa = _Arr(x, n=self.m, name="pass: x")
         ua = _Arr(U, n=self.n, name="pass: U")
         dev = xa.device if out_device is None else out_device
@@ -522,11 +542,17 @@ class Context:
             res["sK"], ptrs["sK"] = _empty(self.m * self.P, dev)
         else:
             res["sK"], ptrs["sK"] = None, None
+        kv, pk = None, None
+        if return_K:
+            nnz = C.c_int64()
+            self._check(self.lib.topo_csc_pattern(self.h, None, None, C.byref(nnz)))
+            kv, pk = _empty(nnz.value, dev)
         pp = L.PassParams(simp.c(), beta, eta0, move, volfrac, eta_override, volume_mode,
                           int(write_sk))
         po = L.PassOut(ptrs["xTilde"], ptrs["xPhys"], ptrs["dcPhys"], ptrs["dc"], ptrs["dV"],
                        ptrs["xNew"], ptrs["sK"])
+        po.Kval = pk
         self._check(self.lib.topo_design_pass(self.h, xa.ptr, ua.ptr, C.byref(pp), C.byref(po)))
         return PassResult(eta=po.eta, c=po.c, lam=po.lambda_, eta_iters=po.eta_iters,
                           bisections=po.bisections, evaluations=po.evaluations,
-                          launches=self.launches, **res)
+                          launches=self.launches, Kval=kv, **res)

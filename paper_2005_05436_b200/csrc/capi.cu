@@ -14,6 +14,7 @@
 #include "../../include/topo_capi.h"
 #include "comm.h"
 #include "kernels.cuh"
+#include <cub/device/device_scan.cuh>
 
 using namespace topo;
 
@@ -102,7 +103,11 @@ struct topo_ctx {
   int conv_A = 0;              // > 0: small-reach direct variant with half-width bound A
   bool overlap_sk = false;     // run the sK store concurrently with K3a..K6
   bool fuse_sk = false;
-  int oc_blocks_now = 0;  // > 0: cooperative OC grid for this call (beside the sK stream)        // stream sK from the sensitivity kernel (K3a + K3b)
+  int oc_blocks_now = 0;
+  // lower-triangle CSC of K (topo_csc_*): pattern built once on first use
+  CscTab csc_tab{};
+  long long csc_nnz = -1;
+  DevBuf d_csc_tab, csc_colptr, csc_rows, csc_E;  // > 0: cooperative OC grid for this call (beside the sK stream)        // stream sK from the sensitivity kernel (K3a + K3b)
   int coop_blocks = 148;  // OC bisection grid (cooperative)
   int coop_eta = 148;     // eta Newton grid (cooperative)
   long long launches = 0;
@@ -1020,6 +1025,7 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   if (ctx->device >= 0) cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) comm_destroy(ctx->comm);
+  for (DevBuf* b : {&ctx->d_csc_tab, &ctx->csc_colptr, &ctx->csc_rows, &ctx->csc_E}) b->release();
   for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_w3, &ctx->d_ke_lower, &ctx->d_state, &ctx->hs, &ctx->hs_st,
                     &ctx->cw, &ctx->x_st, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
                     &ctx->xnew, &ctx->a1_st, &ctx->a2_st, &ctx->rec, &ctx->u, &ctx->tmp0,
@@ -1250,6 +1256,141 @@ topo_status topo_assemble_values(topo_ctx* ctx, const double* sKe, double* vals)
   LAUNCHED();
   if (!dev && vals)
     CK(cudaMemcpyAsync(vals, o, sizeof(double) * size_t(cnt), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+// ------------------------------------------------- CSC
+// Candidate rows of a column (ascending) and the elements both nodes share
+// (ascending), from the element_dofs node order (grid.hpp:105-107, :118-122).
+static void build_csc_tab(bool is3d, CscTab* T) {
+  const int dim = is3d ? 3 : 2, d = is3d ? 24 : 8;
+  auto local = [&](int oi, int ok, int oj) {  // node offsets (y, z, x) -> local node
+    if (!is3d) {
+      static const int t2[2][2] = {{3, 2}, {0, 1}};  // [oi][oj]
+      return t2[oi][oj];
+    }
+    static const int t3[2][2][2] = {{{3, 2}, {7, 6}}, {{0, 1}, {4, 5}}};  // [oi][ok][oj]
+    return t3[oi][ok][oj];
+  };
+  const int zlo = is3d ? -1 : 0, zhi = is3d ? 1 : 0;
+  for (int cc = 0; cc < dim; ++cc) {
+    int n = 0;
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dz = zlo; dz <= zhi; ++dz)
+        for (int dy = -1; dy <= 1; ++dy) {
+          const int lex = dx != 0 ? dx : (dz != 0 ? dz : dy);
+          if (lex < 0) continue;
+          for (int cr = 0; cr < dim; ++cr) {
+            if (lex == 0 && cr < cc) continue;
+            T->cand[cc][n] = (dx + 1) | (dz + 1) << 2 | (dy + 1) << 4 | cr << 6;
+            int k = 0;
+            for (int ex = -1; ex <= 0; ++ex)
+              for (int ez = is3d ? -1 : 0; ez <= 0; ++ez)
+                for (int ey = -1; ey <= 0; ++ey) {
+                  const int rx = dx - ex, rz = dz - ez, ry = dy - ey;
+                  if (rx < 0 || rx > 1 || rz < 0 || rz > 1 || ry < 0 || ry > 1) continue;
+                  const int ac = local(-ey, -ez, -ex), ar = local(ry, rz, rx);
+                  const int la = dim * ar + cr, lb = dim * ac + cc;
+                  const int il = std::max(la, lb), jl = std::min(la, lb);
+                  const int q = jl * d - jl * (jl - 1) / 2 + (il - jl);  // grid.hpp:143-150
+                  T->con[cc][n][k++] = (ex + 1) | (ez + 1) << 1 | (ey + 1) << 2 | q << 3;
+                }
+            T->ncon[cc][n] = k;
+            ++n;
+          }
+        }
+    T->ncand[cc] = n;
+  }
+}
+
+static CscGeo csc_geo(const topo_ctx* ctx) {
+  const Geo& G = ctx->G;
+  CscGeo C;
+  C.dim = G.dim;
+  C.nelx = G.nelx;
+  C.nely = G.nely;
+  C.nz = G.is3d ? G.nelz : 1;
+  C.nz1 = G.is3d ? G.nelz + 1 : 1;
+  C.ny1 = G.nely + 1;
+  C.pl = C.ny1 * C.nz1;
+  C.n = ctx->n;
+  return C;
+}
+
+static topo_status csc_setup(topo_ctx* ctx) {
+  if (ctx->csc_nnz >= 0) return TOPO_OK;
+  if (ctx->nranks > 1) return fail(ctx, TOPO_EINVAL, "csc: single-rank contexts only");
+  const CscGeo C = csc_geo(ctx);
+  build_csc_tab(ctx->G.is3d, &ctx->csc_tab);
+  CK(ctx->d_csc_tab.ensure(sizeof(CscTab)));
+  CK(cudaMemcpyAsync(ctx->d_csc_tab.p, &ctx->csc_tab, sizeof(CscTab), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(ctx->csc_colptr.ensure(sizeof(long long) * size_t(C.n + 1)));
+  long long* cp = ctx->csc_colptr.as<long long>();
+  CK(cudaMemsetAsync(cp, 0, sizeof(long long), ctx->stream));
+  k_csc_count<<<grid_for(ctx, C.n), kThreads, 0, ctx->stream>>>(C, ctx->d_csc_tab.as<CscTab>(),
+                                                               cp + 1);
+  LAUNCHED();
+  size_t tmp = 0;
+  CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, cp + 1, cp + 1, C.n, ctx->stream));
+  DevBuf t;
+  CK(t.ensure(tmp));
+  CK(cub::DeviceScan::InclusiveSum(t.p, tmp, cp + 1, cp + 1, C.n, ctx->stream));
+  long long nnz = 0;
+  CK(cudaMemcpyAsync(&nnz, cp + C.n, sizeof nnz, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  t.release();
+  if (nnz > INT32_MAX)  // Eigen's default StorageIndex (int) holds the reference's pattern
+    return fail(ctx, TOPO_EOVERFLOW, "csc: %lld nonzeros exceed int32 indexing", nnz);
+  CK(ctx->csc_rows.ensure(sizeof(int) * size_t(nnz)));
+  const int nb = int(std::min<long long>((C.n + 7) / 8, (long long)ctx->sm_count * 64));
+  k_csc_fill<true, false><<<nb, kThreads, 0, ctx->stream>>>(
+      C, ctx->d_csc_tab.as<CscTab>(), cp, nullptr, nullptr, ctx->csc_rows.as<int>(), nullptr);
+  LAUNCHED();
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->csc_nnz = nnz;
+  return TOPO_OK;
+}
+
+// values of the CSC slots from the per-element modulus E (device) into vals (device)
+static topo_status csc_values_dev(topo_ctx* ctx, const double* E, double* vals, cudaStream_t st) {
+  const CscGeo C = csc_geo(ctx);
+  const int nb = int(std::min<long long>((C.n + 7) / 8, (long long)ctx->sm_count * 64));
+  k_csc_fill<false, true><<<nb, kThreads, 0, st>>>(C, ctx->d_csc_tab.as<CscTab>(),
+                                                   ctx->csc_colptr.as<long long>(), E,
+                                                   ctx->d_ke_lower.as<double>(), nullptr, vals);
+  LAUNCHED();
+  return TOPO_OK;
+}
+
+topo_status topo_csc_pattern(topo_ctx* ctx, int64_t* col_ptr, int32_t* row_idx, int64_t* nnz) {
+  if (!ctx) return TOPO_EINVAL;
+  ctx->launches = 0;
+  TRY(csc_setup(ctx));
+  if (nnz) *nnz = ctx->csc_nnz;
+  if (col_ptr)
+    CK(cudaMemcpyAsync(col_ptr, ctx->csc_colptr.p, sizeof(int64_t) * size_t(ctx->n + 1),
+                       cudaMemcpyDefault, ctx->stream));
+  if (row_idx)
+    CK(cudaMemcpyAsync(row_idx, ctx->csc_rows.p, sizeof(int32_t) * size_t(ctx->csc_nnz),
+                       cudaMemcpyDefault, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+topo_status topo_csc_values(topo_ctx* ctx, const double* sKe, double* values) {
+  if (!ctx) return TOPO_EINVAL;
+  ctx->launches = 0;
+  TRY(csc_setup(ctx));
+  const Geo& G = ctx->G;
+  const double* s;
+  TRY(stage_in(ctx, sKe, G.m, ctx->tmp0, &s));
+  bool h;
+  double* o = out_ptr(ctx, values, ctx->tmp1, ctx->csc_nnz, &h);
+  if (!o) return fail(ctx, TOPO_ECUDA, "csc: cannot allocate the value buffer");
+  TRY(csc_values_dev(ctx, s, o, ctx->stream));
+  TRY(finish_out(ctx, values, o, ctx->csc_nnz, h));
   CK(cudaStreamSynchronize(ctx->stream));
   return TOPO_OK;
 }
@@ -1553,6 +1694,20 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     CK(cudaMemcpyAsync(res, r, sizeof r, cudaMemcpyHostToDevice, ctx->stream));
   }
   tmark(ctx, TOPO_STAGE_ETA, 1, ctx->stream);
+  // lower-triangle CSC values of K (fea.hpp:154-176), when requested
+  if (out->Kval) {
+    TRY(csc_setup(ctx));
+    CK(ctx->csc_E.ensure(sizeof(double) * size_t(G.m)));
+    k_modulus<<<grid_for(ctx, G.m), kThreads, 0, ctx->stream>>>(
+        G.m, ctx->xt.as<double>(), res, prm->beta, prm->simp.e0, prm->simp.emin, prm->simp.penal,
+        ctx->csc_E.as<double>());
+    LAUNCHED();
+    bool hk;
+    double* ko = out_ptr(ctx, out->Kval, ctx->tmp1, ctx->csc_nnz, &hk);
+    if (!ko) return fail(ctx, TOPO_ECUDA, "csc: cannot allocate the value buffer");
+    TRY(csc_values_dev(ctx, ctx->csc_E.as<double>(), ko, ctx->stream));
+    TRY(finish_out(ctx, out->Kval, ko, ctx->csc_nnz, hk));
+  }
   // K3b: after eta it depends on nothing else; either overlapped on the aux
   // stream with K3a..K6, or last on the main stream
   const bool want_sk = prm->write_sk != 0;

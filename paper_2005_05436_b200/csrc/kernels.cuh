@@ -1643,6 +1643,123 @@ __global__ void k_oc_compact(long long n, const double* __restrict__ x,
   if (threadIdx.x == 0 && partials) partials[blockIdx.x] = red[0];
 }
 
+// ============================================================================
+// Duplicate-summed lower-triangle CSC of K: the
+// matrix assemble_lower builds with setFromTriplets (fea.hpp:154-176), values
+// summed per slot in triplet order (ascending element), no atomics.
+//   Column c = dim * node + cc. Its rows are the lower-triangle DOFs of the
+//   nodes one step away in x, z, y (ascending node order = lexicographic
+//   (dx, dz, dy)); table entry (cc, j) is candidate row j of such a column and
+//   the elements shared by the two nodes, in ascending element order, with
+//   the lower-triangle index q of the pair in each (grid.hpp:143-150).
+// ============================================================================
+struct CscTab {
+  int ncand[3];
+  int cand[3][42];    // (dx + 1) | (dz + 1) << 2 | (dy + 1) << 4 | cr << 6
+  int ncon[3][42];
+  int con[3][42][8];  // (ex + 1) | (ez + 1) << 1 | (ey + 1) << 2 | q << 3
+};
+
+struct CscGeo {
+  int dim, nelx, nely, nz;  // element extents (nz = 1 in 2D)
+  long long ny1, pl;        // node strides: y 1, z ny1, x pl = nz1 * ny1
+  int nz1;                  // node extent along z (1 in 2D)
+  long long n;              // columns
+};
+
+__device__ __forceinline__ void csc_col(const CscGeo& C, long long c, int& cc, long long& nc, int& ix,
+                                        int& iz, int& iy) {
+  nc = c / C.dim;
+  cc = int(c - nc * C.dim);
+  iy = int(nc % C.ny1);
+  const long long t = nc / C.ny1;
+  iz = int(t % C.nz1);
+  ix = int(t / C.nz1);
+}
+
+__device__ __forceinline__ bool csc_valid(const CscGeo& C, int code, int ix, int iz, int iy) {
+  const int dx = (code & 3) - 1, dz = ((code >> 2) & 3) - 1, dy = ((code >> 4) & 3) - 1;
+  return ix + dx >= 0 && ix + dx <= C.nelx && iz + dz >= 0 && iz + dz < C.nz1 && iy + dy >= 0 &&
+         iy + dy <= C.nely;
+}
+
+__global__ void k_csc_count(CscGeo C, const CscTab* __restrict__ T, long long* __restrict__ cnt) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < C.n;
+       c += (long long)gridDim.x * blockDim.x) {
+    int cc, ix, iz, iy;
+    long long nc;
+    csc_col(C, c, cc, nc, ix, iz, iy);
+    int k = 0;
+    for (int j = 0; j < T->ncand[cc]; ++j) k += csc_valid(C, T->cand[cc][j], ix, iz, iy);
+    cnt[c] = k;
+  }
+}
+
+// one warp per column: lanes take candidate rows, a ballot compacts them in
+// order; rows (setup) and/or values (per pass: E = per-element modulus)
+template <bool ROWS, bool VALS>
+__global__ void __launch_bounds__(kThreads) k_csc_fill(CscGeo C, const CscTab* __restrict__ T,
+                                                        const long long* __restrict__ col_ptr,
+                                                        const double* __restrict__ E,
+                                                        const double* __restrict__ kl,
+                                                        int* __restrict__ rows,
+                                                        double* __restrict__ vals) {
+  const int lane = threadIdx.x & 31;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long c = w0; c < C.n; c += nw) {
+    int cc, ix, iz, iy;
+    long long nc;
+    csc_col(C, c, cc, nc, ix, iz, iy);
+    const int nj = T->ncand[cc];
+    long long base = col_ptr[c];
+    for (int j0 = 0; j0 < nj; j0 += 32) {
+      const int j = j0 + lane;
+      const int code = j < nj ? T->cand[cc][j] : 0;
+      const bool ok = j < nj && csc_valid(C, code, ix, iz, iy);
+      const unsigned bal = __ballot_sync(0xffffffffu, ok);
+      if (ok) {
+        const long long slot = base + __popc(bal & ((1u << lane) - 1u));
+        const int dx = (code & 3) - 1, dz = ((code >> 2) & 3) - 1, dy = ((code >> 4) & 3) - 1;
+        if (ROWS) {
+          const long long nr = nc + dx * C.pl + dz * C.ny1 + dy;
+          rows[slot] = int(C.dim * nr + (code >> 6));
+        }
+        if (VALS) {
+          double acc = 0.0;
+          bool first = true;
+          for (int k = 0; k < T->ncon[cc][j]; ++k) {  // ascending element = triplet order
+            const int w = T->con[cc][j][k];
+            const int ex = ix + (w & 1) - 1, ez = iz + ((w >> 1) & 1) - 1,
+                      ey = iy + ((w >> 2) & 1) - 1;
+            if (ex < 0 || ex >= C.nelx || ez < 0 || ez >= C.nz || ey < 0 || ey >= C.nely) continue;
+            const long long e = ((long long)ex * C.nz + ez) * C.nely + ey;
+            const double v = E[e] * kl[w >> 3];  // fea.hpp:168
+            acc = first ? v : acc + v;            // setFromTriplets duplicate sum
+            first = false;
+          }
+          vals[slot] = acc;
+        }
+      }
+      base += __popc(bal);
+    }
+  }
+}
+
+// per-element modulus E(xPhys) from the filtered field and eta (fea.hpp:142)
+__global__ void k_modulus(long long m, const double* __restrict__ xt, const double* __restrict__ eta_ptr,
+                          double beta, double e0, double emin, double penal, double* __restrict__ E) {
+  const double eta = *eta_ptr;
+  const double a = tanh(beta * eta);
+  const double denom = a + tanh(beta * (1.0 - eta));
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double xphys = (a + tanh(beta * (xt[e] - eta))) / denom;  // filter.hpp:142
+    const double xp = simp_xp(xphys, penal);
+    E[e] = emin + xp * xphys * (e0 - emin);
+  }
+}
+
 // FP64 peak probe: 8 independent FMA chains per thread (topo_fp64_peak)
 __global__ void __launch_bounds__(kThreads) k_dfma_peak(int iters, double seed, double* out) {
   double a[8];

@@ -81,6 +81,23 @@ def main():
         taps[name] = {"ntaps": int(f.ntaps), "w_sum": float(w.sum()), "hs0": float(f.hs()[0]),
                       "sha_w": sha(w)}
     meta["taps"] = taps
+    # lower-triangle CSC of assemble_lower (fea.hpp:154-176): small grids in
+    # full, the C1 / C4 patterns and values as checksums
+    csc = {}
+    arrays = {}
+    for name, grid in [("5x4", (5, 4, 0)), ("4x3x2", (4, 3, 2)), ("3x1x2", (3, 1, 2)),
+                       ("C1", (300, 100, 0)), ("C4", (96, 48, 48))]:
+        m = grid[0] * grid[1] * (grid[2] or 1)
+        sK = np.random.default_rng(2005).uniform(0.01, 1.0, m)
+        cp, ri, va = ref.assemble_lower_csc(grid, 0.3, sK)
+        csc[name] = {"grid": grid, "nnz": int(ri.size), "sha_col_ptr": sha(cp.astype(np.int64)),
+                     "sha_row_idx": sha(ri), "sha_values": sha(va),
+                     "sK": "numpy default_rng(2005).uniform(0.01, 1.0, m)"}
+        if m < 100:
+            arrays.update({f"{name}_sK": sK, f"{name}_col_ptr": cp, f"{name}_row_idx": ri,
+                           f"{name}_values": va})
+    np.savez(os.path.join(HERE, "csc.npz"), **arrays)
+    meta["csc"] = csc
     # pass cases
     for name, grid, rmin, beta, move, volfrac, pas, seed in PASS_CASES:
         x, u, state = rand_case(grid, seed, pas)
