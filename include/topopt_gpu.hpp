@@ -129,6 +129,31 @@ inline std::vector<double> assemble_lower_values(const Eigen::VectorXd& sK, Devi
   return vals;
 }
 
+/// fea.hpp:154-176 assemble_lower: the duplicate-summed lower triangle of K
+/// (setFromTriplets order), built on the device from the per-element modulus
+/// without the m*P triplets; filled through Eigen's public compressed-storage
+/// API (resize + resizeNonZeros + outer/inner/value pointers).
+inline SymmetricSparseMatrix assemble_lower(const Eigen::VectorXd& sK, Device& dev) {
+  if (sK.size() != dev.numElements())
+    throw std::invalid_argument("assemble: index pairs do not match element count");
+  std::int64_t nnz = 0, m = 0, n = 0;
+  check(topo_ctx_info(dev.handle(), &m, &n, nullptr, nullptr, nullptr, nullptr, nullptr),
+        dev.handle());
+  check(topo_csc_pattern(dev.handle(), nullptr, nullptr, &nnz), dev.handle());
+  std::vector<std::int64_t> cp(size_t(n + 1));
+  SymmetricSparseMatrix mat;
+  mat.n = n;
+  mat.lower.resize(n, n);
+  mat.lower.resizeNonZeros(nnz);
+  static_assert(sizeof(*mat.lower.innerIndexPtr()) == sizeof(std::int32_t), "int32 rows");
+  check(topo_csc_pattern(dev.handle(), cp.data(),
+                         reinterpret_cast<std::int32_t*>(mat.lower.innerIndexPtr()), nullptr),
+        dev.handle());
+  for (std::int64_t c = 0; c <= n; ++c) mat.lower.outerIndexPtr()[c] = int(cp[size_t(c)]);
+  check(topo_csc_values(dev.handle(), sK.data(), mat.lower.valuePtr()), dev.handle());
+  return mat;
+}
+
 /// fea.hpp:248-272
 inline ComplianceResult compliance_and_sensitivity(const Eigen::VectorXd& u,
                                                    const Eigen::VectorXd& xhat,

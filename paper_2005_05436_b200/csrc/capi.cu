@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "../../include/topo_capi.h"
@@ -107,7 +108,7 @@ struct topo_ctx {
   // lower-triangle CSC of K (topo_csc_*): pattern built once on first use
   CscTab csc_tab{};
   long long csc_nnz = -1;
-  DevBuf d_csc_tab, csc_colptr, csc_rows, csc_E;  // > 0: cooperative OC grid for this call (beside the sK stream)        // stream sK from the sensitivity kernel (K3a + K3b)
+  DevBuf d_csc_tab, d_csc_int, csc_colptr, csc_rows, csc_E;  // > 0: cooperative OC grid for this call (beside the sK stream)        // stream sK from the sensitivity kernel (K3a + K3b)
   int coop_blocks = 148;  // OC bisection grid (cooperative)
   int coop_eta = 148;     // eta Newton grid (cooperative)
   long long launches = 0;
@@ -1025,7 +1026,7 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   if (ctx->device >= 0) cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) comm_destroy(ctx->comm);
-  for (DevBuf* b : {&ctx->d_csc_tab, &ctx->csc_colptr, &ctx->csc_rows, &ctx->csc_E}) b->release();
+  for (DevBuf* b : {&ctx->d_csc_tab, &ctx->d_csc_int, &ctx->csc_colptr, &ctx->csc_rows, &ctx->csc_E}) b->release();
   for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_w3, &ctx->d_ke_lower, &ctx->d_state, &ctx->hs, &ctx->hs_st,
                     &ctx->cw, &ctx->x_st, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
                     &ctx->xnew, &ctx->a1_st, &ctx->a2_st, &ctx->rec, &ctx->u, &ctx->tmp0,
@@ -1304,6 +1305,27 @@ static void build_csc_tab(bool is3d, CscTab* T) {
   }
 }
 
+// the interior-node slot layout (CscInterior) from the candidate tables
+static void build_csc_interior(const CscTab& T, int dim, const double* ke_lower, CscInterior* I) {
+  memset(I, 0, sizeof *I);
+  int s = 0;
+  for (int cc = 0; cc < dim; ++cc)
+    for (int j = 0; j < T.ncand[cc]; ++j, ++s) {
+      I->code[s] = T.cand[cc][j];
+      for (int q = 0; q < T.ncon[cc][j]; ++q) {
+        const int w = T.con[cc][j][q], ec = w & 7;
+        int k = 0;
+        while (csc_ord(k) != ec) ++k;
+        I->pmask[s] |= (unsigned char)(1u << k);
+        I->klt[k][s] = ke_lower[w >> 3];
+      }
+    }
+  I->nslot = s;
+  I->branchless = 1;
+  for (int q = 0; q < (dim == 3 ? 300 : 36); ++q)
+    if (ke_lower[q] == 0.0 && std::signbit(ke_lower[q])) I->branchless = 0;
+}
+
 static CscGeo csc_geo(const topo_ctx* ctx) {
   const Geo& G = ctx->G;
   CscGeo C;
@@ -1326,6 +1348,10 @@ static topo_status csc_setup(topo_ctx* ctx) {
   CK(ctx->d_csc_tab.ensure(sizeof(CscTab)));
   CK(cudaMemcpyAsync(ctx->d_csc_tab.p, &ctx->csc_tab, sizeof(CscTab), cudaMemcpyHostToDevice,
                      ctx->stream));
+  std::unique_ptr<CscInterior> I(new CscInterior);
+  build_csc_interior(ctx->csc_tab, ctx->G.dim, ctx->ke_lower.data(), I.get());
+  CK(ctx->d_csc_int.ensure(sizeof(CscInterior)));
+  CK(cudaMemcpy(ctx->d_csc_int.p, I.get(), sizeof(CscInterior), cudaMemcpyHostToDevice));
   CK(ctx->csc_colptr.ensure(sizeof(long long) * size_t(C.n + 1)));
   long long* cp = ctx->csc_colptr.as<long long>();
   CK(cudaMemsetAsync(cp, 0, sizeof(long long), ctx->stream));
@@ -1344,9 +1370,10 @@ static topo_status csc_setup(topo_ctx* ctx) {
   if (nnz > INT32_MAX)  // Eigen's default StorageIndex (int) holds the reference's pattern
     return fail(ctx, TOPO_EOVERFLOW, "csc: %lld nonzeros exceed int32 indexing", nnz);
   CK(ctx->csc_rows.ensure(sizeof(int) * size_t(nnz)));
-  const int nb = int(std::min<long long>((C.n + 7) / 8, (long long)ctx->sm_count * 64));
+  const int nb = int(std::min<long long>((C.n / C.dim + 7) / 8, (long long)ctx->sm_count * 64));
   k_csc_fill<true, false><<<nb, kThreads, 0, ctx->stream>>>(
-      C, ctx->d_csc_tab.as<CscTab>(), cp, nullptr, nullptr, ctx->csc_rows.as<int>(), nullptr);
+      C, ctx->d_csc_tab.as<CscTab>(), ctx->d_csc_int.as<CscInterior>(), cp, nullptr, nullptr,
+      ctx->csc_rows.as<int>(), nullptr);
   LAUNCHED();
   CK(cudaStreamSynchronize(ctx->stream));
   ctx->csc_nnz = nnz;
@@ -1356,8 +1383,9 @@ static topo_status csc_setup(topo_ctx* ctx) {
 // values of the CSC slots from the per-element modulus E (device) into vals (device)
 static topo_status csc_values_dev(topo_ctx* ctx, const double* E, double* vals, cudaStream_t st) {
   const CscGeo C = csc_geo(ctx);
-  const int nb = int(std::min<long long>((C.n + 7) / 8, (long long)ctx->sm_count * 64));
+  const int nb = int(std::min<long long>((C.n / C.dim + 7) / 8, (long long)ctx->sm_count * 64));
   k_csc_fill<false, true><<<nb, kThreads, 0, st>>>(C, ctx->d_csc_tab.as<CscTab>(),
+                                                   ctx->d_csc_int.as<CscInterior>(),
                                                    ctx->csc_colptr.as<long long>(), E,
                                                    ctx->d_ke_lower.as<double>(), nullptr, vals);
   LAUNCHED();

@@ -1660,6 +1660,22 @@ struct CscTab {
   int con[3][42][8];  // (ex + 1) | (ez + 1) << 1 | (ey + 1) << 2 | q << 3
 };
 
+// Interior nodes (all 8 surrounding elements and all neighbours exist) share
+// one slot layout: slot s of the node's run sums, over the elements in
+// ascending order k (element code kOrd[k]), E_k * klt[k][s] where pmask[s]
+// has bit k set.
+struct CscInterior {
+  int nslot;
+  int branchless;           // no Ke_lower entry is -0: absent terms may add +0 (exact)
+  int code[128];            // candidate code of slot s (cand packing)
+  unsigned char pmask[128];
+  double klt[8][128];
+};
+// ascending element order of the codes (ex + 1) | (ez + 1) << 1 | (ey + 1) << 2
+__host__ __device__ constexpr int csc_ord(int k) {
+  return (k >> 2 & 1) | (k >> 1 & 1) << 1 | (k & 1) << 2;  // ex slowest, then ez, then ey
+}
+
 struct CscGeo {
   int dim, nelx, nely, nz;  // element extents (nz = 1 in 2D)
   long long ny1, pl;        // node strides: y 1, z ny1, x pl = nz1 * ny1
@@ -1695,47 +1711,140 @@ __global__ void k_csc_count(CscGeo C, const CscTab* __restrict__ T, long long* _
   }
 }
 
-// one warp per column: lanes take candidate rows, a ballot compacts them in
-// order; rows (setup) and/or values (per pass: E = per-element modulus)
+// one warp per node: its dim columns are consecutive, so the node's slots are
+// one contiguous run of the value array. Lanes take the node's candidate rows
+// (flattened over (cc, j)); a ballot per round compacts them in slot order.
+// The <= 8 elements around the node (all the elements any of its slots sums
+// over) have their moduli staged once per warp in shared memory; the tables
+// and Ke_lower live in shared memory.
 template <bool ROWS, bool VALS>
 __global__ void __launch_bounds__(kThreads) k_csc_fill(CscGeo C, const CscTab* __restrict__ T,
+                                                        const CscInterior* __restrict__ TI,
                                                         const long long* __restrict__ col_ptr,
                                                         const double* __restrict__ E,
                                                         const double* __restrict__ kl,
                                                         int* __restrict__ rows,
                                                         double* __restrict__ vals) {
-  const int lane = threadIdx.x & 31;
+  __shared__ CscTab st;
+  __shared__ double skl[300];
+  __shared__ double sE[kThreads / 32][8];
+  __shared__ unsigned char sflat[128][2];  // (cc, j) of flattened candidate k
+  __shared__ int snflat;
+  __shared__ CscInterior si;
+  {
+    const int* srci = reinterpret_cast<const int*>(TI);
+    int* dsti = reinterpret_cast<int*>(&si);
+    for (int q = threadIdx.x; q < int(sizeof(CscInterior) / sizeof(int)); q += blockDim.x)
+      dsti[q] = srci[q];
+    const int* src = reinterpret_cast<const int*>(T);
+    int* dst = reinterpret_cast<int*>(&st);
+    for (int q = threadIdx.x; q < int(sizeof(CscTab) / sizeof(int)); q += blockDim.x) dst[q] = src[q];
+    if (VALS)
+      for (int q = threadIdx.x; q < (C.dim == 3 ? 300 : 36); q += blockDim.x) skl[q] = kl[q];
+    if (threadIdx.x == 0) {
+      int k = 0;
+      for (int cc = 0; cc < C.dim; ++cc)
+        for (int j = 0; j < T->ncand[cc]; ++j, ++k) {
+          sflat[k][0] = (unsigned char)cc;
+          sflat[k][1] = (unsigned char)j;
+        }
+      snflat = k;
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long c = w0; c < C.n; c += nw) {
-    int cc, ix, iz, iy;
-    long long nc;
-    csc_col(C, c, cc, nc, ix, iz, iy);
-    const int nj = T->ncand[cc];
-    long long base = col_ptr[c];
-    for (int j0 = 0; j0 < nj; j0 += 32) {
-      const int j = j0 + lane;
-      const int code = j < nj ? T->cand[cc][j] : 0;
-      const bool ok = j < nj && csc_valid(C, code, ix, iz, iy);
+  const long long nnodes = C.n / C.dim;
+  const int nflat = snflat;
+  const bool fast = !VALS || si.branchless;
+  for (long long nc = w0; nc < nnodes; nc += nw) {
+    int iy, iz, ix;
+    if (nc <= 0xffffffffLL) {  // 32-bit division
+      const unsigned u = unsigned(nc), ny1 = unsigned(C.ny1), nz1 = unsigned(C.nz1);
+      const unsigned t = u / ny1;
+      iy = int(u - t * ny1);
+      ix = int(t / nz1);
+      iz = int(t - unsigned(ix) * nz1);
+    } else {
+      iy = int(nc % C.ny1);
+      const long long t = nc / C.ny1;
+      iz = int(t % C.nz1);
+      ix = int(t / C.nz1);
+    }
+    const long long base0 = col_ptr[nc * C.dim];
+    unsigned emask = 0;  // elements (ex, ez, ey) around the node that exist
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int ex = ix + (q & 1) - 1, ez = iz + ((q >> 1) & 1) - 1, ey = iy + ((q >> 2) & 1) - 1;
+      if (ex >= 0 && ex < C.nelx && ez >= 0 && ez < C.nz && ey >= 0 && ey < C.nely)
+        emask |= 1u << q;
+    }
+    if (VALS) {
+      __syncwarp();
+      if (lane < 8 && (emask >> lane & 1u)) {
+        const int ex = ix + (lane & 1) - 1, ez = iz + ((lane >> 1) & 1) - 1,
+                  ey = iy + ((lane >> 2) & 1) - 1;
+        sE[wib][lane] = E[((long long)ex * C.nz + ez) * C.nely + ey];
+      }
+      __syncwarp();
+    }
+    const bool interior = ix >= 1 && ix < C.nelx && iy >= 1 && iy < C.nely &&
+                          (C.nz1 == 1 || (iz >= 1 && iz < C.nz1 - 1));
+    if (interior && fast) {  // fixed layout: every candidate valid, every element present
+      double Ek[8];
+      if (VALS) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          Ek[k] = (emask >> csc_ord(k) & 1u) ? sE[wib][csc_ord(k)] : 0.0;
+      }
+      for (int s0 = 0; s0 < si.nslot; s0 += 32) {
+        const int sl = s0 + lane;
+        if (sl >= si.nslot) continue;
+        if (ROWS) {
+          const int code = si.code[sl];
+          const int dx = (code & 3) - 1, dz = ((code >> 2) & 3) - 1, dy = ((code >> 4) & 3) - 1;
+          rows[base0 + sl] = int(C.dim * (nc + dx * C.pl + dz * C.ny1 + dy) + (code >> 6));
+        }
+        if (VALS) {
+          // absent terms carry weight +0: acc + E * 0 = acc and 0 + v1 = v1, so
+          // the sum is the reference's v1 + v2 + ... bit for bit (no -0 in Ke)
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, __dmul_rn(Ek[k], si.klt[k][sl]));
+          vals[base0 + sl] = acc;
+        }
+      }
+      continue;
+    }
+    long long base = base0;
+    for (int k0 = 0; k0 < nflat; k0 += 32) {
+      const int k = k0 + lane;
+      int cc = 0, j = 0, code = 0;
+      bool ok = false;
+      if (k < nflat) {
+        cc = sflat[k][0];
+        j = sflat[k][1];
+        code = st.cand[cc][j];
+        ok = csc_valid(C, code, ix, iz, iy);
+      }
       const unsigned bal = __ballot_sync(0xffffffffu, ok);
       if (ok) {
         const long long slot = base + __popc(bal & ((1u << lane) - 1u));
-        const int dx = (code & 3) - 1, dz = ((code >> 2) & 3) - 1, dy = ((code >> 4) & 3) - 1;
         if (ROWS) {
+          const int dx = (code & 3) - 1, dz = ((code >> 2) & 3) - 1, dy = ((code >> 4) & 3) - 1;
           const long long nr = nc + dx * C.pl + dz * C.ny1 + dy;
           rows[slot] = int(C.dim * nr + (code >> 6));
         }
         if (VALS) {
           double acc = 0.0;
           bool first = true;
-          for (int k = 0; k < T->ncon[cc][j]; ++k) {  // ascending element = triplet order
-            const int w = T->con[cc][j][k];
-            const int ex = ix + (w & 1) - 1, ez = iz + ((w >> 1) & 1) - 1,
-                      ey = iy + ((w >> 2) & 1) - 1;
-            if (ex < 0 || ex >= C.nelx || ez < 0 || ez >= C.nz || ey < 0 || ey >= C.nely) continue;
-            const long long e = ((long long)ex * C.nz + ez) * C.nely + ey;
-            const double v = E[e] * kl[w >> 3];  // fea.hpp:168
-            acc = first ? v : acc + v;            // setFromTriplets duplicate sum
+          const int ncon = st.ncon[cc][j];
+          for (int q = 0; q < ncon; ++q) {  // ascending element = triplet order
+            const int w = st.con[cc][j][q];
+            if (!(emask >> (w & 7) & 1u)) continue;
+            const double v = sE[wib][w & 7] * skl[w >> 3];  // fea.hpp:168
+            acc = first ? v : acc + v;                       // setFromTriplets duplicate sum
             first = false;
           }
           vals[slot] = acc;

@@ -5,6 +5,8 @@
 // tests/test_gpu_adapter.py. Exit code 0 = all checks passed.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <algorithm>
 #include <random>
 
 #include "topopt/fea.hpp"
@@ -64,6 +66,16 @@ int main() {
     const SimpParams simp{1.0, 1e-9, 3.0};
     const SimpField sr = simp_interpolate(x, simp), sg = gpu::simp_interpolate(x, simp, dev);
     expect(rel(sg.sK, sr.sK) <= 1e-12 && rel(sg.dsK, sr.dsK) <= 1e-12, "simp_interpolate");
+    const SymmetricSparseMatrix Kr = assemble_lower(pr, ke, sr.sK, grid.numDofs());
+    const SymmetricSparseMatrix Kg = gpu::assemble_lower(sr.sK, dev);
+    const auto nz = Kr.lower.nonZeros();
+    expect(Kg.lower.nonZeros() == nz &&
+               std::equal(Kr.lower.outerIndexPtr(), Kr.lower.outerIndexPtr() + grid.numDofs() + 1,
+                          Kg.lower.outerIndexPtr()) &&
+               std::equal(Kr.lower.innerIndexPtr(), Kr.lower.innerIndexPtr() + nz,
+                          Kg.lower.innerIndexPtr()) &&
+               std::memcmp(Kr.lower.valuePtr(), Kg.lower.valuePtr(), sizeof(double) * nz) == 0,
+           "assemble_lower (CSC bit-exact)");
     const ComplianceResult cr = compliance_and_sensitivity(u, build_connectivity(grid), x, simp, ke, part);
     const ComplianceResult cg = gpu::compliance_and_sensitivity(u, x, simp, dev);
     expect(std::abs(cr.c - cg.c) <= 1e-12 * std::abs(cr.c) && rel(cg.dc, cr.dc) <= 1e-12,
