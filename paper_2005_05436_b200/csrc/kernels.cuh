@@ -1773,12 +1773,18 @@ __global__ void __launch_bounds__(kThreads) k_csc_fill(CscGeo C, const CscTab* _
       ix = int(t / C.nz1);
     }
     const long long base0 = col_ptr[nc * C.dim];
+    const bool interior = ix >= 1 && ix < C.nelx && iy >= 1 && iy < C.nely &&
+                          (C.nz1 == 1 || (iz >= 1 && iz < C.nz1 - 1));
     unsigned emask = 0;  // elements (ex, ez, ey) around the node that exist
+    if (interior) {
+      emask = C.nz1 == 1 ? 0xCCu : 0xFFu;  // 2D: only ez = 0 (code bit 1 set)
+    } else {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int ex = ix + (q & 1) - 1, ez = iz + ((q >> 1) & 1) - 1, ey = iy + ((q >> 2) & 1) - 1;
-      if (ex >= 0 && ex < C.nelx && ez >= 0 && ez < C.nz && ey >= 0 && ey < C.nely)
-        emask |= 1u << q;
+      for (int q = 0; q < 8; ++q) {
+        const int ex = ix + (q & 1) - 1, ez = iz + ((q >> 1) & 1) - 1, ey = iy + ((q >> 2) & 1) - 1;
+        if (ex >= 0 && ex < C.nelx && ez >= 0 && ez < C.nz && ey >= 0 && ey < C.nely)
+          emask |= 1u << q;
+      }
     }
     if (VALS) {
       __syncwarp();
@@ -1789,8 +1795,6 @@ __global__ void __launch_bounds__(kThreads) k_csc_fill(CscGeo C, const CscTab* _
       }
       __syncwarp();
     }
-    const bool interior = ix >= 1 && ix < C.nelx && iy >= 1 && iy < C.nely &&
-                          (C.nz1 == 1 || (iz >= 1 && iz < C.nz1 - 1));
     if (interior && fast) {  // fixed layout: every candidate valid, every element present
       double Ek[8];
       if (VALS) {
