@@ -182,6 +182,14 @@ topo_status topo_assemble_values(topo_ctx* ctx, const double* sK, double* vals);
  * from the per-element modulus sK (m), bitwise equal to the reference's sums.
  * Built on the device without the m*P triplets; single-rank contexts. */
 topo_status topo_csc_pattern(topo_ctx* ctx, int64_t* col_ptr, int32_t* row_idx, int64_t* nnz);
+/* reduced mode (EquilibriumSolver, fea.hpp:316-361; solve_equilibrium :206-239):
+ * with the load case's fixed DOFs (host, any order, duplicates allowed), the
+ * CSC covers only the free DOFs, renumbered by detail::free_dof_map
+ * (fea.hpp:186-199); col_ptr then has num_free+1 entries. nfixed = 0 returns
+ * to the full matrix. Values accumulate per slot in triplet order starting
+ * from 0 (fea.hpp:352-361), bitwise equal to the reference's. */
+topo_status topo_csc_set_fixed(topo_ctx* ctx, const int32_t* fixed, int64_t nfixed,
+                               int64_t* num_free);
 topo_status topo_csc_values(topo_ctx* ctx, const double* sK, double* values);
 /* fea.hpp:248-272 compliance_and_sensitivity (c is the rank-local partial) */
 topo_status topo_sensitivity(topo_ctx* ctx, const double* U, const double* xhat,

@@ -452,12 +452,26 @@ class Context:
         self._check(self.lib.topo_assemble_values(self.h, a.ptr, ptr))
         return out
 
+    def csc_set_fixed(self, fixed=None) -> int:
+        """Reduced (free-DOF) CSC mode of EquilibriumSolver (fea.hpp:316-361) for
+        the load case's fixed DOFs; None / empty returns to the full matrix.
+        Returns the number of free DOFs (columns)."""
+        nf = C.c_int64()
+        if fixed is None or len(fixed) == 0:
+            self._check(self.lib.topo_csc_set_fixed(self.h, None, 0, C.byref(nf)))
+        else:
+            f = np.ascontiguousarray(fixed, dtype=np.int32)
+            self._check(self.lib.topo_csc_set_fixed(self.h, f.ctypes.data, f.size, C.byref(nf)))
+        self._csc_cols = nf.value
+        return nf.value
+
     def csc_pattern(self, device: bool = False):
         """Lower-triangle CSC pattern of K (assemble_lower / setFromTriplets,
-        fea.hpp:154-176): (col_ptr int64 n+1, row_idx int32 nnz)."""
+        fea.hpp:154-176): (col_ptr int64 ncols+1, row_idx int32 nnz); ncols = n,
+        or the free-DOF count after csc_set_fixed."""
         nnz = C.c_int64()
         self._check(self.lib.topo_csc_pattern(self.h, None, None, C.byref(nnz)))
-        cp, pc = _empty(self.n + 1, device, np.int64)
+        cp, pc = _empty(getattr(self, "_csc_cols", self.n) + 1, device, np.int64)
         ri, pr = _empty(nnz.value, device, np.int32)
         self._check(self.lib.topo_csc_pattern(self.h, pc, pr, None))
         return cp, ri

@@ -108,7 +108,9 @@ struct topo_ctx {
   // lower-triangle CSC of K (topo_csc_*): pattern built once on first use
   CscTab csc_tab{};
   long long csc_nnz = -1;
-  DevBuf d_csc_tab, d_csc_int, csc_colptr, csc_rows, csc_E;  // > 0: cooperative OC grid for this call (beside the sK stream)        // stream sK from the sensitivity kernel (K3a + K3b)
+  DevBuf d_csc_tab, d_csc_int, csc_colptr, csc_rows, csc_E;
+  long long n_free = -1;  // reduced (free-DOF) mode when >= 0 (topo_csc_set_fixed)
+  DevBuf d_map, d_clean;  // > 0: cooperative OC grid for this call (beside the sK stream)        // stream sK from the sensitivity kernel (K3a + K3b)
   int coop_blocks = 148;  // OC bisection grid (cooperative)
   int coop_eta = 148;     // eta Newton grid (cooperative)
   long long launches = 0;
@@ -1026,6 +1028,7 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   if (ctx->device >= 0) cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) comm_destroy(ctx->comm);
+  for (DevBuf* b : {&ctx->d_map, &ctx->d_clean}) b->release();
   for (DevBuf* b : {&ctx->d_csc_tab, &ctx->d_csc_int, &ctx->csc_colptr, &ctx->csc_rows, &ctx->csc_E}) b->release();
   for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_w3, &ctx->d_ke_lower, &ctx->d_state, &ctx->hs, &ctx->hs_st,
                     &ctx->cw, &ctx->x_st, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
@@ -1337,8 +1340,12 @@ static CscGeo csc_geo(const topo_ctx* ctx) {
   C.ny1 = G.nely + 1;
   C.pl = C.ny1 * C.nz1;
   C.n = ctx->n;
+  C.map = ctx->n_free >= 0 ? ctx->d_map.as<int>() : nullptr;
+  C.clean = ctx->n_free >= 0 ? ctx->d_clean.as<unsigned char>() : nullptr;
   return C;
 }
+
+static long long csc_ncols(const topo_ctx* ctx) { return ctx->n_free >= 0 ? ctx->n_free : ctx->n; }
 
 static topo_status csc_setup(topo_ctx* ctx) {
   if (ctx->csc_nnz >= 0) return TOPO_OK;
@@ -1352,21 +1359,24 @@ static topo_status csc_setup(topo_ctx* ctx) {
   build_csc_interior(ctx->csc_tab, ctx->G.dim, ctx->ke_lower.data(), I.get());
   CK(ctx->d_csc_int.ensure(sizeof(CscInterior)));
   CK(cudaMemcpy(ctx->d_csc_int.p, I.get(), sizeof(CscInterior), cudaMemcpyHostToDevice));
-  CK(ctx->csc_colptr.ensure(sizeof(long long) * size_t(C.n + 1)));
+  const long long ncols = csc_ncols(ctx);
+  CK(ctx->csc_colptr.ensure(sizeof(long long) * size_t(ncols + 1)));
   long long* cp = ctx->csc_colptr.as<long long>();
   CK(cudaMemsetAsync(cp, 0, sizeof(long long), ctx->stream));
   k_csc_count<<<grid_for(ctx, C.n), kThreads, 0, ctx->stream>>>(C, ctx->d_csc_tab.as<CscTab>(),
                                                                cp + 1);
   LAUNCHED();
-  size_t tmp = 0;
-  CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, cp + 1, cp + 1, C.n, ctx->stream));
-  DevBuf t;
-  CK(t.ensure(tmp));
-  CK(cub::DeviceScan::InclusiveSum(t.p, tmp, cp + 1, cp + 1, C.n, ctx->stream));
   long long nnz = 0;
-  CK(cudaMemcpyAsync(&nnz, cp + C.n, sizeof nnz, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  t.release();
+  if (ncols > 0) {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tmp, cp + 1, cp + 1, ncols, ctx->stream));
+    DevBuf t;
+    CK(t.ensure(tmp));
+    CK(cub::DeviceScan::InclusiveSum(t.p, tmp, cp + 1, cp + 1, ncols, ctx->stream));
+    CK(cudaMemcpyAsync(&nnz, cp + ncols, sizeof nnz, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    t.release();
+  }
   if (nnz > INT32_MAX)  // Eigen's default StorageIndex (int) holds the reference's pattern
     return fail(ctx, TOPO_EOVERFLOW, "csc: %lld nonzeros exceed int32 indexing", nnz);
   CK(ctx->csc_rows.ensure(sizeof(int) * size_t(nnz)));
@@ -1398,12 +1408,45 @@ topo_status topo_csc_pattern(topo_ctx* ctx, int64_t* col_ptr, int32_t* row_idx, 
   TRY(csc_setup(ctx));
   if (nnz) *nnz = ctx->csc_nnz;
   if (col_ptr)
-    CK(cudaMemcpyAsync(col_ptr, ctx->csc_colptr.p, sizeof(int64_t) * size_t(ctx->n + 1),
+    CK(cudaMemcpyAsync(col_ptr, ctx->csc_colptr.p, sizeof(int64_t) * size_t(csc_ncols(ctx) + 1),
                        cudaMemcpyDefault, ctx->stream));
   if (row_idx)
     CK(cudaMemcpyAsync(row_idx, ctx->csc_rows.p, sizeof(int32_t) * size_t(ctx->csc_nnz),
                        cudaMemcpyDefault, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
+topo_status topo_csc_set_fixed(topo_ctx* ctx, const int32_t* fixed, int64_t nfixed,
+                               int64_t* num_free) {
+  if (!ctx) return TOPO_EINVAL;
+  if (ctx->nranks > 1) return fail(ctx, TOPO_EINVAL, "csc: single-rank contexts only");
+  ctx->launches = 0;
+  ctx->csc_nnz = -1;  // the pattern follows the new numbering
+  if (!fixed || nfixed <= 0) {
+    ctx->n_free = -1;
+    if (num_free) *num_free = ctx->n;
+    return TOPO_OK;
+  }
+  const long long n = ctx->n;
+  std::vector<int> map(size_t(n), 0);  // detail::free_dof_map (fea.hpp:186-199)
+  for (int64_t q = 0; q < nfixed; ++q) {
+    if (fixed[q] < 0 || fixed[q] >= n)
+      return fail(ctx, TOPO_EINVAL, "load case: fixed DOF out of range");
+    map[size_t(fixed[q])] = -1;
+  }
+  int next = 0;
+  for (long long d = 0; d < n; ++d) map[size_t(d)] = map[size_t(d)] < 0 ? -1 : next++;
+  CK(ctx->d_map.ensure(sizeof(int) * size_t(n)));
+  CK(cudaMemcpy(ctx->d_map.p, map.data(), sizeof(int) * size_t(n), cudaMemcpyHostToDevice));
+  ctx->n_free = next;
+  CK(ctx->d_clean.ensure(size_t(n / ctx->G.dim)));
+  const CscGeo C = csc_geo(ctx);
+  k_csc_clean<<<grid_for(ctx, n / ctx->G.dim), kThreads, 0, ctx->stream>>>(
+      C, ctx->d_clean.as<unsigned char>());
+  LAUNCHED();
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (num_free) *num_free = next;
   return TOPO_OK;
 }
 

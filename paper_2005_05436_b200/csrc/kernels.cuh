@@ -1680,7 +1680,10 @@ struct CscGeo {
   int dim, nelx, nely, nz;  // element extents (nz = 1 in 2D)
   long long ny1, pl;        // node strides: y 1, z ny1, x pl = nz1 * ny1
   int nz1;                  // node extent along z (1 in 2D)
-  long long n;              // columns
+  long long n;              // DOFs (full columns)
+  const int* map;           // reduced mode (EquilibriumSolver, fea.hpp:188-199, :316-336):
+                            // DOF -> free index or -1; null = the full matrix
+  const unsigned char* clean;  // reduced mode: node whose 27-neighbourhood is all free
 };
 
 __device__ __forceinline__ void csc_col(const CscGeo& C, long long c, int& cc, long long& nc, int& ix,
@@ -1699,15 +1702,46 @@ __device__ __forceinline__ bool csc_valid(const CscGeo& C, int code, int ix, int
          iy + dy <= C.nely;
 }
 
+__device__ __forceinline__ long long csc_row(const CscGeo& C, long long nc, int code) {
+  const int dx = (code & 3) - 1, dz = ((code >> 2) & 3) - 1, dy = ((code >> 4) & 3) - 1;
+  return C.dim * (nc + dx * C.pl + dz * C.ny1 + dy) + (code >> 6);
+}
+
+// slots per (free) column; cnt is indexed by the (reduced) column number
 __global__ void k_csc_count(CscGeo C, const CscTab* __restrict__ T, long long* __restrict__ cnt) {
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < C.n;
        c += (long long)gridDim.x * blockDim.x) {
+    if (C.map && C.map[c] < 0) continue;
     int cc, ix, iz, iy;
     long long nc;
     csc_col(C, c, cc, nc, ix, iz, iy);
     int k = 0;
-    for (int j = 0; j < T->ncand[cc]; ++j) k += csc_valid(C, T->cand[cc][j], ix, iz, iy);
-    cnt[c] = k;
+    for (int j = 0; j < T->ncand[cc]; ++j) {
+      const int code = T->cand[cc][j];
+      k += csc_valid(C, code, ix, iz, iy) && (!C.map || C.map[csc_row(C, nc, code)] >= 0);
+    }
+    cnt[C.map ? C.map[c] : c] = k;
+  }
+}
+
+// reduced mode: node flags, 1 when every DOF of its 27-neighbourhood is free
+__global__ void k_csc_clean(CscGeo C, unsigned char* __restrict__ clean) {
+  const long long nn = C.n / C.dim;
+  for (long long nc = blockIdx.x * (long long)blockDim.x + threadIdx.x; nc < nn;
+       nc += (long long)gridDim.x * blockDim.x) {
+    const int iy = int(nc % C.ny1);
+    const long long t = nc / C.ny1;
+    const int iz = int(t % C.nz1), ix = int(t / C.nz1);
+    bool ok = true;
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy) {
+          const int jx = ix + dx, jz = iz + dz, jy = iy + dy;
+          if (jx < 0 || jx > C.nelx || jz < 0 || jz >= C.nz1 || jy < 0 || jy > C.nely) continue;
+          const long long nr = ((long long)jx * C.nz1 + jz) * C.ny1 + jy;
+          for (int c = 0; c < C.dim; ++c) ok = ok && C.map[C.dim * nr + c] >= 0;
+        }
+    clean[nc] = ok;
   }
 }
 
@@ -1772,9 +1806,17 @@ __global__ void __launch_bounds__(kThreads) k_csc_fill(CscGeo C, const CscTab* _
       iz = int(t % C.nz1);
       ix = int(t / C.nz1);
     }
-    const long long base0 = col_ptr[nc * C.dim];
+    // the node's first (free) column and its slot run
+    long long c0 = nc * C.dim;
+    if (C.map) {
+      int q = 0;
+      while (q < C.dim && C.map[c0 + q] < 0) ++q;
+      if (q == C.dim) continue;  // every DOF of the node is fixed: no columns
+      c0 = C.map[c0 + q];
+    }
+    const long long base0 = col_ptr[c0];
     const bool interior = ix >= 1 && ix < C.nelx && iy >= 1 && iy < C.nely &&
-                          (C.nz1 == 1 || (iz >= 1 && iz < C.nz1 - 1));
+                          (C.nz1 == 1 || (iz >= 1 && iz < C.nz1 - 1)) && (!C.map || C.clean[nc]);
     unsigned emask = 0;  // elements (ex, ez, ey) around the node that exist
     if (interior) {
       emask = C.nz1 == 1 ? 0xCCu : 0xFFu;  // 2D: only ez = 0 (code bit 1 set)
@@ -1806,9 +1848,8 @@ __global__ void __launch_bounds__(kThreads) k_csc_fill(CscGeo C, const CscTab* _
         const int sl = s0 + lane;
         if (sl >= si.nslot) continue;
         if (ROWS) {
-          const int code = si.code[sl];
-          const int dx = (code & 3) - 1, dz = ((code >> 2) & 3) - 1, dy = ((code >> 4) & 3) - 1;
-          rows[base0 + sl] = int(C.dim * (nc + dx * C.pl + dz * C.ny1 + dy) + (code >> 6));
+          const long long r = csc_row(C, nc, si.code[sl]);
+          rows[base0 + sl] = C.map ? C.map[r] : int(r);
         }
         if (VALS) {
           // absent terms carry weight +0: acc + E * 0 = acc and 0 + v1 = v1, so
@@ -1830,15 +1871,15 @@ __global__ void __launch_bounds__(kThreads) k_csc_fill(CscGeo C, const CscTab* _
         cc = sflat[k][0];
         j = sflat[k][1];
         code = st.cand[cc][j];
-        ok = csc_valid(C, code, ix, iz, iy);
+        ok = csc_valid(C, code, ix, iz, iy) &&
+             (!C.map || (C.map[nc * C.dim + cc] >= 0 && C.map[csc_row(C, nc, code)] >= 0));
       }
       const unsigned bal = __ballot_sync(0xffffffffu, ok);
       if (ok) {
         const long long slot = base + __popc(bal & ((1u << lane) - 1u));
         if (ROWS) {
-          const int dx = (code & 3) - 1, dz = ((code >> 2) & 3) - 1, dy = ((code >> 4) & 3) - 1;
-          const long long nr = nc + dx * C.pl + dz * C.ny1 + dy;
-          rows[slot] = int(C.dim * nr + (code >> 6));
+          const long long r = csc_row(C, nc, code);
+          rows[slot] = C.map ? C.map[r] : int(r);
         }
         if (VALS) {
           double acc = 0.0;

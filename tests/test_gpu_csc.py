@@ -84,3 +84,41 @@ def test_csc_rejects_multi_rank(P):
     with P.Context(8, 4, 0, rmin=1.5, rank=0, nranks=2) as ctx:
         with pytest.raises(P.InvalidArgument):
             ctx.csc_pattern()
+
+
+def _restrict(cp, ri, va, fixed, n):
+    """the reduced matrix of solve_equilibrium / EquilibriumSolver (fea.hpp:206-239,
+    :316-361): entries with a fixed row or column dropped, free DOFs renumbered."""
+    free = np.ones(n, bool)
+    free[fixed] = False
+    mp = np.cumsum(free) - 1
+    cols = np.repeat(np.arange(n), np.diff(cp))
+    keep = free[ri] & free[cols]
+    rc = mp[cols[keep]]
+    ncols = int(free.sum())
+    cpr = np.zeros(ncols + 1, np.int64)
+    np.add.at(cpr, rc + 1, 1)
+    return np.cumsum(cpr), mp[ri[keep]].astype(np.int32), va[keep]
+
+
+@pytest.mark.parametrize("cid,grid", [(1, (12, 6, 0)), (4, (7, 5, 4)), (5, (9, 6, 5))])
+def test_reduced_csc_matches_reference(P, oracle_ref, cid, grid):
+    from paper_2005_05436_b200.configs import CONFIGS, fixed_dofs
+    cfg = CONFIGS[cid].scaled(*grid)
+    fixed = fixed_dofs(cfg)
+    sK = np.random.default_rng(9).uniform(0.01, 1.0, cfg.m)
+    cp, ri, va = oracle_ref.assemble_lower_csc(cfg.grid, cfg.nu, sK)
+    rcp, rri, rva = _restrict(cp.astype(np.int64), ri, va, fixed, cfg.n)
+    with P.Context(*cfg.grid, rmin=1.0, nu=cfg.nu) as ctx:
+        nf = ctx.csc_set_fixed(fixed)
+        gcp, gri = ctx.csc_pattern()
+        gva = ctx.csc_values(sK)
+        assert nf == rcp.size - 1
+        ctx.csc_set_fixed(None)  # back to the full matrix
+        fcp, _ = ctx.csc_pattern()
+        assert fcp.size == cfg.n + 1
+        with pytest.raises(P.InvalidArgument):
+            ctx.csc_set_fixed([cfg.n])
+    np.testing.assert_array_equal(gcp, rcp)
+    np.testing.assert_array_equal(gri, rri)
+    np.testing.assert_array_equal(gva.view(np.int64), rva.view(np.int64))
