@@ -260,7 +260,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     ms = t_total / args.steps
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms], dtype=torch.float64)  # gloo: host tensor
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     stages = {k: v / args.steps for k, v in stage_acc.items()}
@@ -291,7 +291,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     e2e_ms /= args.steps
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([e2e_ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     h2d = 8 * (x.size + u.size) * world

@@ -98,3 +98,28 @@ def test_nccl_two_gpus(P):
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs (NCCL ranks cannot share a GPU)")
+
+
+def test_nccl_single_rank_clique_matches_plain_pass():
+    """The NCCL communicator path (dlopen'ed libnccl, unique id, halo send/recv
+    groups, allreduces, host-driven eta / OC replays) on a one-rank clique:
+    nothing waits on another GPU, and the pass must equal the plain one."""
+    import numpy as np
+    import paper_2005_05436_b200 as P
+    from paper_2005_05436_b200.configs import CONFIGS
+    from tests.common import rel
+    for cid, grid in ((4, (16, 10, 8)), (2, (60, 20, 0))):
+        cfg = CONFIGS[cid].scaled(*grid)
+        rng = np.random.default_rng(4)
+        x, u = rng.uniform(0.01, 1.0, cfg.m), rng.normal(size=cfg.n)
+        kw = dict(beta=cfg.beta, move=cfg.move, volfrac=cfg.volfrac, return_sk=True)
+        with P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu) as ctx:
+            a = ctx.design_pass(x, u, **kw)
+        with P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu, rank=0, nranks=1) as ctx:
+            ctx.comm_init(P.nccl_unique_id())
+            b0 = ctx.design_pass(x, u, **kw)  # eta over NCCL allreduces
+            b = ctx.design_pass(x, u, eta_override=a.eta, **kw)
+        assert abs(a.eta - b0.eta) <= 5e-8
+        assert a.bisections == b.bisections and abs(a.lam - b.lam) <= 1e-10 * abs(a.lam)
+        for k in ("xTilde", "xPhys", "dc", "dV", "xNew", "sK"):
+            assert rel(getattr(b, k), getattr(a, k)) <= 1e-12, k
