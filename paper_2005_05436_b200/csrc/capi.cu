@@ -935,9 +935,9 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
     return bail(fail(ctx, TOPO_EINVAL, "filter: rmin %.3g too large for the shared-memory tile",
                      d->rmin));
   {
-    // sK stream overlapped with K3a + K4 on large single-GPU 3D passes (C5)
+    // sK stream overlapped with K3a + K4 on large 3D passes (C5, also per slab)
     const char* ov = getenv("TOPO_SK_OVERLAP");
-    const bool big = G.is3d && double(G.m) * G.P * 8.0 >= 4e9 && d->nranks == 1;
+    const bool big = G.is3d && double(G.m) * G.P * 8.0 >= 4e9;
     ctx->overlap_sk = ov ? ov[0] == '1' : big;
     const char* fu = getenv("TOPO_SK_FUSE");
     ctx->fuse_sk = fu && fu[0] == '1';
@@ -1804,7 +1804,7 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   // default: sK values streamed by the fused K3a kernel (fuse_sk); else the
   // separate K3b, overlapped on the aux stream or last on the main stream
   const bool fuse_sk = want_sk && ctx->fuse_sk;
-  const bool overlap = want_sk && !fuse_sk && ctx->overlap_sk && !ctx->comm;
+  const bool overlap = want_sk && !fuse_sk && ctx->overlap_sk;
   static const bool fork_late = getenv("TOPO_SK_FORK_LATE") != nullptr;  // experiment
   auto fork_sk = [&]() -> topo_status {
     CK(cudaEventRecord(ctx->ev_fork, ctx->stream));

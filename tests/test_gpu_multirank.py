@@ -123,3 +123,19 @@ def test_nccl_single_rank_clique_matches_plain_pass():
         assert a.bisections == b.bisections and abs(a.lam - b.lam) <= 1e-10 * abs(a.lam)
         for k in ("xTilde", "xPhys", "dc", "dV", "xNew", "sK"):
             assert rel(getattr(b, k), getattr(a, k)) <= 1e-12, k
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_slab_ranks_with_overlapped_sk_stream(P, nranks, monkeypatch):
+    """Per-slab sK stream on the aux stream beside K3a/K4 and the host-driven
+    OC (the default on large slabs): bitwise equal to the serial schedule."""
+    from paper_2005_05436_b200.configs import CONFIGS, make_inputs
+    cfg = CONFIGS[5].scaled(30, 16, 12)
+    x, u, state = make_inputs(cfg)
+    monkeypatch.setenv("TOPO_SK_OVERLAP", "0")
+    a = run_ranks(P, cfg, x, u, state, nranks)
+    monkeypatch.setenv("TOPO_SK_OVERLAP", "1")
+    b = run_ranks(P, cfg, x, u, state, nranks)
+    for k in ("xTilde", "xPhys", "dc", "dV", "xNew", "sK"):
+        np.testing.assert_array_equal(cat(a, k), cat(b, k), err_msg=k)
+    assert [r.lam for r in a] == [r.lam for r in b]
