@@ -226,6 +226,15 @@ topo_status topo_oc_bisect(topo_ctx* ctx, const double* x, const double* dc, con
                            topo_volume_fn cb, void* user, double* xNew, double* lambda,
                            int32_t* bisections, int32_t* evaluations);
 
+/* oc.hpp:181-241 primal_dual_update (driver.hpp:211-212, ft = 1): explicit
+ * dual-map iteration to |lm' - lm| <= pd_tol (OcParams::pdTol, 1e-10), with
+ * the reference's fallback to bisect_update on the mean volume (*fell_back =
+ * 1; *iterations then counts bisections, as UpdateResult::bisections does) */
+topo_status topo_oc_primal_dual(topo_ctx* ctx, const double* x, const double* dc,
+                                const double* dV, const topo_oc_params* prm, double pd_tol,
+                                double* xNew, double* lambda, int32_t* iterations,
+                                int32_t* fell_back);
+
 /* ---- fused pass: driver.hpp:183-231 (ft = 3) minus the state solve ------ */
 topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
                              const topo_pass_params* prm, topo_pass_out* out);

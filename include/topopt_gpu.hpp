@@ -295,6 +295,25 @@ inline UpdateResult bisect_update(const Eigen::VectorXd& x, const Eigen::VectorX
   return detail::bisect(x, dc, dV, prm, opt, int(mode), prj.eta, prj.beta, nullptr, nullptr, dev);
 }
 
+/// oc.hpp:181-241 primal_dual_update (ft = 1), with the reference's fallback
+/// to the mean-volume bisection
+inline UpdateResult primal_dual_update(const Eigen::VectorXd& x, const Eigen::VectorXd& dc,
+                                       const Eigen::VectorXd& dV, const OcParams& prm,
+                                       Device& dev) {
+  detail::need(x.size(), dev.numElements(), "oc");
+  detail::need(dc.size(), dev.numElements(), "oc");
+  detail::need(dV.size(), dev.numElements(), "oc");
+  topo_oc_params p{prm.move, prm.volfrac, prm.bisectRelTol, prm.volumeTol, 0, 1e-8, 0.0};
+  UpdateResult r;
+  r.xNew.resize(x.size());
+  std::int32_t it = 0, fb = 0;
+  check(topo_oc_primal_dual(dev.handle(), x.data(), dc.data(), dV.data(), &p, prm.pdTol,
+                            r.xNew.data(), &r.lambda, &it, &fb),
+        dev.handle());
+  r.bisections = it;
+  return r;
+}
+
 // ----------------------------------------------------------- fused pass
 /// driver.hpp:183-231 (ft = 3) with the displacement supplied
 struct PassResult {

@@ -196,6 +196,9 @@ class Oracle:
                C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int))
             fn("design_pass", C.c_int, Grid, C.c_void_p, f64p, u8p, f64p, f64p,
                C.POINTER(PassParams), C.POINTER(PassOut))
+            fn("primal_dual_update", C.c_int, C.c_int64, f64p, f64p, f64p, u8p,
+               C.POINTER(OcParams), C.c_double, f64p, C.POINTER(C.c_double),
+               C.POINTER(C.c_int), C.POINTER(C.c_int))
         else:
             L.ref_filter_hs.restype = None
             L.ref_filter_hs.argtypes = [C.c_void_p, f64p]
@@ -213,6 +216,8 @@ class Oracle:
             fn("bisect_update", C.c_int, Grid, f64p, f64p, f64p, u8p, C.POINTER(OcParams),
                C.c_int, C.c_void_p, C.c_double, C.c_double, VOLUME_FN, C.c_void_p, f64p,
                C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int))
+            fn("primal_dual_update", C.c_int, Grid, f64p, f64p, f64p, u8p, C.POINTER(OcParams),
+               C.c_double, f64p, C.POINTER(C.c_double), C.POINTER(C.c_int))
             fn("problem_create", C.c_void_p, Grid, C.c_double, C.c_int, C.c_double, u8p)
             fn("problem_destroy", None, C.c_void_p)
             fn("design_pass", C.c_int, C.c_void_p, f64p, f64p, C.POINTER(PassParams),
@@ -413,6 +418,28 @@ class Oracle:
                                            C.byref(bis), C.byref(ev))
         self._check(r)
         return xNew, lam.value, bis.value, ev.value
+
+    def primal_dual_update(self, x, dc, dV, state=None, move=0.2, volfrac=0.5, rel_tol=1e-4,
+                           vol_tol=1e-3, pd_tol=1e-10, grid=None):
+        """oc.hpp:181-241. Returns (xNew, lambda, iterations, fell_back); the
+        reference does not report a fallback (-1)."""
+        x, dc, dV = _f64(x), _f64(dc), _f64(dV)
+        m = len(x)
+        st = None if state is None else np.ascontiguousarray(state, np.uint8)
+        prm = OcParams(move, volfrac, rel_tol, vol_tol, 0, 1e-8, 0.0)
+        xNew = np.empty_like(x)
+        lam, it, fb = C.c_double(), C.c_int(), C.c_int(-1)
+        if self.kind == "port":
+            r = self.lib.orc_primal_dual_update(m, _p(x), _p(dc), _p(dV), _p(st), C.byref(prm),
+                                                pd_tol, _p(xNew), C.byref(lam), C.byref(it),
+                                                C.byref(fb))
+        else:
+            g = grid if grid is not None else (m, 1, 0)
+            r = self.lib.ref_primal_dual_update(Grid(*g), _p(x), _p(dc), _p(dV), _p(st),
+                                                C.byref(prm), pd_tol, _p(xNew), C.byref(lam),
+                                                C.byref(it))
+        self._check(r)
+        return xNew, lam.value, it.value, fb.value
 
     # ----------------------------------------------------------- driver glue
     def design_pass(self, grid, rmin, x, u, state=None, *, nu=0.3, e0=1.0, emin=1e-9, penal=3.0,

@@ -291,6 +291,28 @@ int ref_bisect_update(ref_grid g, const double* x, const double* dc, const doubl
   });
 }
 
+// oc.hpp:181-241 primal_dual_update (ft = 1); *fell_back is not observable in
+// the reference's result and is reported as -1 here
+int ref_primal_dual_update(ref_grid g, const double* x, const double* dc, const double* dV,
+                           const uint8_t* state, const ref_oc_params* p, double pd_tol,
+                           double* xNew, double* lambda, int* iterations) {
+  return guard([&] {
+    const StructuredGrid grid{g.nelx, g.nely, g.nelz};
+    const int64_t m = grid.numElements();
+    const DomainPartition part = partition_from_state(grid, state);
+    OcParams oc;
+    oc.move = p->move;
+    oc.volfrac = p->volfrac;
+    oc.bisectRelTol = p->bisect_rel_tol;
+    oc.volumeTol = p->volume_tol;
+    oc.pdTol = pd_tol;
+    const UpdateResult r = primal_dual_update(vec(x, m), vec(dc, m), vec(dV, m), part, oc);
+    out(r.xNew, xNew);
+    *lambda = r.lambda;
+    *iterations = r.bisections;
+  });
+}
+
 // ---------------------------------------------------------- pass (driver glue)
 typedef struct {
   double e0, emin, penal, beta, eta0, move, volfrac;

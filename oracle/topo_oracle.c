@@ -731,6 +731,112 @@ static double phys_volume(vol_ctx* v) {
 }
 
 /* oc.hpp:93-174 */
+/* oc.hpp:181-241 primal_dual_update: the clamped resize alternated with the
+ * closed-form dual map over the unclamped set until the multiplier stagnates
+ * (|lm' - lm| <= pdTol); falls back to bisect_update with the mean volume
+ * (oc.hpp:190-193) when the budget, the sums or the map degenerate, or after
+ * 1000 iterations. *fell_back = 1 then, and *iterations is the bisection count. */
+int orc_primal_dual_update(int64_t m, const double* x, const double* dc, const double* dV,
+                           const uint8_t* state, const orc_oc_params* prm, double pd_tol,
+                           double* xNew, double* lambda_out, int* iterations_out,
+                           int* fell_back) {
+  int64_t nact = 0, nS = 0;
+  for (int64_t e = 0; e < m; ++e) {
+    nact += (!state || state[e] == 0);
+    nS += (state && state[e] == 1);
+  }
+  int32_t* act = (int32_t*)malloc(sizeof(int32_t) * (size_t)(nact + 1));
+  double* xAct = (double*)malloc(sizeof(double) * (size_t)(nact + 1));
+  double* dcAct = (double*)malloc(sizeof(double) * (size_t)(nact + 1));
+  double* dVAct = (double*)malloc(sizeof(double) * (size_t)(nact + 1));
+  double* ocP = (double*)malloc(sizeof(double) * (size_t)(nact + 1));
+  double* upper = (double*)malloc(sizeof(double) * (size_t)(nact + 1));
+  double* lower = (double*)malloc(sizeof(double) * (size_t)(nact + 1));
+  {
+    int64_t q = 0;
+    for (int64_t e = 0; e < m; ++e)
+      if (!state || state[e] == 0) act[q++] = (int32_t)e;
+  }
+  for (int64_t q = 0; q < nact; ++q) {
+    xAct[q] = x[act[q]];
+    dcAct[q] = dc[act[q]];
+    dVAct[q] = dV[act[q]];
+  }
+  oc_constant(nact, xAct, dcAct, dVAct, ocP);
+  int fb = 0, it = 0;
+  double lm = 0;
+  const double budget = prm->volfrac * (double)m - (double)nS; /* oc.hpp:195 */
+  if (budget <= 0) fb = 1;
+  if (!fb) {
+    for (int64_t q = 0; q < nact; ++q) {
+      upper[q] = std_min(1.0, xAct[q] + prm->move); /* oc.hpp:199-202 */
+      lower[q] = std_max(0.0, xAct[q] - prm->move);
+    }
+    double s = 0;
+    for (int64_t q = 0; q < nact; ++q) s += ocP[q];
+    lm = s / ((double)m * prm->volfrac); /* oc.hpp:204 */
+    if (!(lm > 0)) fb = 1;
+  }
+  for (; !fb; ++it) {
+    if (it >= 1000) {
+      fb = 1;
+      break;
+    }
+    double sumClamped = 0, sumMid = 0;
+    int64_t numMid = 0;
+    for (int64_t q = 0; q < nact; ++q) {
+      const double f = ocP[q] / lm;
+      if (f > upper[q])
+        sumClamped += upper[q];
+      else if (f < lower[q])
+        sumClamped += lower[q];
+      else {
+        sumMid += ocP[q];
+        ++numMid;
+      }
+    }
+    if (numMid == 0) {
+      fb = 1;
+      break;
+    }
+    const double den = budget - sumClamped;
+    if (den <= 0) {
+      fb = 1;
+      break;
+    }
+    const double lmNext = sumMid / den;
+    if (!(lmNext > 0) || !isfinite(lmNext)) {
+      fb = 1;
+      break;
+    }
+    const int done = fabs(lmNext - lm) <= pd_tol;
+    lm = lmNext;
+    if (done) break;
+  }
+  int rc = ORC_OK;
+  if (fb) {
+    orc_oc_params bp = *prm;
+    int evals = 0;
+    rc = orc_bisect_update(m, x, dc, dV, state, &bp, ORC_VOL_MEAN, NULL, 0.0, 0.0, NULL, NULL, xNew,
+                           lambda_out, iterations_out, &evals);
+  } else {
+    memcpy(xNew, x, sizeof(double) * (size_t)m); /* oc.hpp:233-236 */
+    oc_candidate_into(nact, xAct, ocP, lm, prm->move, upper);
+    for (int64_t q = 0; q < nact; ++q) xNew[act[q]] = upper[q];
+    *lambda_out = lm * lm;
+    *iterations_out = it;
+  }
+  if (fell_back) *fell_back = fb;
+  free(act);
+  free(xAct);
+  free(dcAct);
+  free(dVAct);
+  free(ocP);
+  free(upper);
+  free(lower);
+  return rc;
+}
+
 int orc_bisect_update(int64_t m, const double* x, const double* dc, const double* dV,
                       const uint8_t* state, const orc_oc_params* prm, int volume_mode,
                       const orc_filter* f, double eta, double beta, orc_volume_fn cb, void* user,

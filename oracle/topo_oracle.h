@@ -97,6 +97,9 @@ int orc_bisect_update(int64_t m, const double* x, const double* dc, const double
                       const uint8_t* state, const orc_oc_params* prm, int volume_mode,
                       const orc_filter* f, double eta, double beta, orc_volume_fn cb, void* user,
                       double* xNew, double* lambda, int* bisections, int* evaluations);
+int orc_primal_dual_update(int64_t m, const double* x, const double* dc, const double* dV,
+                           const uint8_t* state, const orc_oc_params* prm, double pd_tol,
+                           double* xNew, double* lambda, int* iterations, int* fell_back);
 
 /* driver.hpp:183-231 (ft = 3 branch) — one design-update pass */
 typedef struct {

@@ -129,6 +129,7 @@ class OcParams:  # oc.hpp:14-20 (+ BisectOptions oc.hpp:81-85)
     lambdaSpace: bool = False
     absTol: float = 1e-8
     lambdaMax: float = 0.0
+    pdTol: float = 1e-10  # primal-dual multiplier stagnation tolerance
 
     def c(self):
         return L.OcParams(self.move, self.volfrac, self.bisectRelTol, self.volumeTol,
@@ -141,6 +142,7 @@ class UpdateResult:  # oc.hpp:22-26
     lam: float
     bisections: int
     evaluations: int = 0
+    fell_back: bool = False  # primal_dual_update: the bisection fallback ran
 
 
 @dataclass
@@ -535,6 +537,20 @@ class Context:
                                             volume_mode, eta, beta, cb, None, ptr, C.byref(lam),
                                             C.byref(bis), C.byref(ev)))
         return UpdateResult(out, lam.value, bis.value, ev.value)
+
+    def primal_dual_update(self, x, dc, dV, prm: OcParams = OcParams()) -> UpdateResult:
+        """oc.hpp:181-241 (ft = 1): dual-map iteration with the reference's
+        fallback to the mean-volume bisection; bisections = iterations."""
+        xa = _Arr(x, n=self.m, name="oc: x")
+        ca = _Arr(dc, n=self.m, name="oc: dc")
+        va = _Arr(dV, n=self.m, name="oc: dV")
+        out, ptr = _empty(self.m, xa.device)
+        lam, it, fb = C.c_double(), C.c_int32(), C.c_int32()
+        op = prm.c()
+        self._check(self.lib.topo_oc_primal_dual(self.h, xa.ptr, ca.ptr, va.ptr, C.byref(op),
+                                                 prm.pdTol, ptr, C.byref(lam), C.byref(it),
+                                                 C.byref(fb)))
+        return UpdateResult(out, lam.value, it.value, 0, bool(fb.value))
 
     # driver.hpp:183-231
     def design_pass(self, x, U, *, beta: float = 2.0, eta0: float = 0.5, move: float = 0.2,

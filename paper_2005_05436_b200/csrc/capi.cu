@@ -1719,6 +1719,87 @@ topo_status topo_oc_bisect(topo_ctx* ctx, const double* x, const double* dc, con
   return TOPO_OK;
 }
 
+// oc.hpp:181-241 primal_dual_update (ft = 1): host-driven, one pass of block
+// sums (allreduced across ranks) per dual-map iteration; the bisection with
+// the mean volume on the reference's fallback conditions
+topo_status topo_oc_primal_dual(topo_ctx* ctx, const double* x, const double* dc,
+                                const double* dV, const topo_oc_params* prm, double pd_tol,
+                                double* xNew, double* lambda, int32_t* iterations,
+                                int32_t* fell_back) {
+  if (!ctx || !prm) return TOPO_EINVAL;
+  ctx->launches = 0;
+  const Geo& G = ctx->G;
+  const double *xd, *dcd, *dVd;
+  DevBuf b0;
+  TRY(stage_in(ctx, x, G.m, ctx->tmp0, &xd));
+  TRY(stage_in(ctx, dc, G.m, ctx->tmp1, &dcd));
+  TRY(stage_in(ctx, dV, G.m, b0, &dVd));
+  const int nb = grid_for(ctx, G.m);
+  k_oc_prep<<<nb, kThreads, 0, ctx->stream>>>(
+      G.m, xd, dcd, dVd, ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr, nullptr,
+      prm->move, ctx->rec.as<double>(), ctx->partials0.as<double>());
+  LAUNCHED();
+  ctx->oc_view = OcRecs{xd, ctx->rec.as<double>(), nullptr, prm->move};
+  bool h;
+  double* o = out_ptr(ctx, xNew, ctx->xnew, G.m, &h);
+  double lam = 0;
+  int32_t it = 0, fb = 0;
+  const double budget = prm->volfrac * ctx->m_total - ctx->nS_total;  // oc.hpp:195
+  double lm = 0;
+  if (budget <= 0) fb = 1;
+  if (!fb) {
+    TRY(reduce_to_host<3>(ctx, ctx->partials0.as<double>(), nb));  // sum ocP (oc.hpp:204)
+    lm = ctx->h_result[0] / (ctx->m_total * prm->volfrac);
+    if (!(lm > 0)) fb = 1;
+  }
+  for (; !fb; ++it) {
+    if (it >= 1000) {
+      fb = 1;
+      break;
+    }
+    k_oc_pd_sums<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->oc_view, lm,
+                                                   ctx->partials.as<double>());
+    LAUNCHED();
+    TRY(reduce_to_host<3>(ctx, ctx->partials.as<double>(), nb));
+    const double sumClamped = ctx->h_result[0], sumMid = ctx->h_result[1];
+    const double numMid = ctx->h_result[2];
+    if (numMid == 0) {
+      fb = 1;
+      break;
+    }
+    const double den = budget - sumClamped;
+    if (den <= 0) {
+      fb = 1;
+      break;
+    }
+    const double lmNext = sumMid / den;
+    if (!(lmNext > 0) || !std::isfinite(lmNext)) {
+      fb = 1;
+      break;
+    }
+    const bool done = std::fabs(lmNext - lm) <= pd_tol;
+    lm = lmNext;
+    if (done) break;
+  }
+  if (fb) {  // bisect_update with the mean volume (oc.hpp:190-193)
+    int32_t bis = 0, ev = 0;
+    TRY(run_oc(ctx, prm, TOPO_VOL_MEAN, ctx->partials0.as<double>(), nb, o, &lam, &bis, &ev, 0.0,
+               1.0, nullptr, nullptr));
+    it = bis;
+  } else {
+    k_oc_candidates<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->oc_view, lm, o);
+    LAUNCHED();
+    lam = lm * lm;
+  }
+  TRY(finish_out(ctx, xNew, o, G.m, h));
+  CK(cudaStreamSynchronize(ctx->stream));
+  b0.release();
+  if (lambda) *lambda = lam;
+  if (iterations) *iterations = it;
+  if (fell_back) *fell_back = fb;
+  return TOPO_OK;
+}
+
 // ------------------------------------------------------------ fused pass
 // driver.hpp:183-231 (ft = 3) with U supplied:
 //   main stream: K1 filter+pin+eta0 terms -> K2 eta -> K3a elem -> K4 adjoint+OC prep -> K5/6 OC

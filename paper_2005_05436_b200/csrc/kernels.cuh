@@ -1564,6 +1564,31 @@ __global__ void __launch_bounds__(kThreads) k_oc_batch(long long m, OcRecs R,
     for (int q = 0; q < K; ++q) partials[(long long)q * gridDim.x + blockIdx.x] = acc[q];
 }
 
+// oc.hpp:209-222: block partial (sumClamped, sumMid, numMid) of the
+// primal-dual iteration at the sqrt multiplier lm, over active elements
+__global__ void __launch_bounds__(kThreads) k_oc_pd_sums(long long m, OcRecs R, double lm,
+                                                         double* __restrict__ partials) {
+  __shared__ double scratch[3 * 32];
+  double red[3] = {0.0, 0.0, 0.0};
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (R.ocp[e] < 0.0) continue;  // passive
+    const double4 r = R.get(e);
+    const double f = r.z / lm;
+    if (f > r.y)
+      red[0] += r.y;
+    else if (f < r.x)
+      red[0] += r.x;
+    else {
+      red[1] += r.z;
+      red[2] += 1.0;
+    }
+  }
+  block_sum<3>(red, scratch);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 3; ++q) partials[3 * blockIdx.x + q] = red[q];
+}
+
 // row q of a [rows][count] partial table summed in a fixed order by block q
 __global__ void k_reduce_rows(const double* __restrict__ p, int count, double* __restrict__ out) {
   __shared__ double scratch[32];

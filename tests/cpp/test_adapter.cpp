@@ -93,6 +93,12 @@ int main() {
     const UpdateResult um = gpu::bisect_update(x, dc, dV, oc, gpu::VolumeMode::Mean, dev);
     expect(um.bisections == ur.bisections && rel(um.xNew, ur.xNew) <= 1e-12,
            "bisect_update (device mean volume)");
+    const UpdateResult pr_ = primal_dual_update(x, dc, dV, part, oc);
+    const UpdateResult pg_ = gpu::primal_dual_update(x, dc, dV, oc, dev);
+    expect(pr_.bisections == pg_.bisections &&
+               std::abs(pr_.lambda - pg_.lambda) <= 1e-10 * pr_.lambda &&
+               rel(pg_.xNew, pr_.xNew) <= 1e-12,
+           "primal_dual_update", pr_.lambda - pg_.lambda);
     // error mapping
     bool threw = false;
     try {

@@ -342,3 +342,48 @@ def test_bisect_filtered_modes(P, oracle_port, grid, rmin, passives, mode):
     assert r.bisections == bo and r.evaluations == eo
     assert abs(r.lam - lo) <= 1e-10 * abs(lo)
     assert rel(r.xNew, xo) <= 1e-12
+
+
+# ------------------------------------------------------------ primal-dual
+@pytest.mark.parametrize("m,seed,move,volfrac,passives", [(400, 1, 0.2, 0.5, False),
+                                                          (1000, 2, 0.05, 0.3, True),
+                                                          (5000, 3, 0.1, 0.12, False),
+                                                          (257, 4, 0.45, 0.5, True)])
+def test_primal_dual_matches_oracle(P, oracle_port, m, seed, move, volfrac, passives):
+    x, dc, dV, state = _oc_instance(m, seed, passives)
+    ro = oracle_port.primal_dual_update(x, dc, dV, state, move=move, volfrac=volfrac)
+    with P.Context(m, 1, 0, rmin=1.0, state=state) as ctx:
+        r = ctx.primal_dual_update(x, dc, dV, P.OcParams(move=move, volfrac=volfrac))
+    assert r.fell_back == bool(ro[3])
+    assert r.bisections == ro[2]
+    assert abs(r.lam - ro[1]) <= 1e-10 * abs(ro[1])
+    assert rel(r.xNew, ro[0]) <= 1e-12
+
+
+def test_primal_dual_reference_known_answers(P):  # test_oc.cpp:195-240
+    rng = np.random.default_rng(5)
+    m = 200
+    x = np.full(m, 0.5)
+    dV = np.full(m, 1.0 / m)
+    dc = -rng.uniform(0.9, 1.1, m) / m
+    with P.Context(m, 1, 0, rmin=1.0) as ctx:
+        # wide box, nothing clamps: <= 3 iterations, lambda = lambda#
+        r = ctx.primal_dual_update(x, dc, dV, P.OcParams(move=0.45, volfrac=0.5))
+        lam_hash = ctx.lambda_upper_estimate(x, dc, dV, 0.5, m)
+        assert r.bisections <= 3 and not r.fell_back
+        assert abs(r.lam - lam_hash) <= 1e-6 * lam_hash
+        # agrees with a tight bisection
+        t = ctx.bisect_update(x, dc, dV, P.OcParams(move=0.2, volfrac=0.5, bisectRelTol=1e-12,
+                                                    volumeTol=1e-9))
+        p2 = ctx.primal_dual_update(x, dc, dV, P.OcParams(move=0.2, volfrac=0.5))
+        assert np.max(np.abs(p2.xNew - t.xNew)) <= 1e-6
+        assert abs(p2.xNew.mean() - 0.5) <= 1e-9
+    # every element clamps: falls back to bisection
+    m = 10
+    x = np.full(m, 0.5)
+    dV = np.full(m, 1.0 / m)
+    dc = np.where(np.arange(m) % 2 == 0, -1e8, -1e-8)
+    with P.Context(m, 1, 0, rmin=1.0) as ctx:
+        r = ctx.primal_dual_update(x, dc, dV, P.OcParams(move=0.01, volfrac=0.5))
+    assert abs(r.xNew.mean() - 0.5) <= 1e-3
+    assert np.all(np.abs(r.xNew - x) <= 0.01 + 1e-14)
