@@ -155,7 +155,9 @@ void topo_generate(uint64_t seed, uint64_t stream, int kind, double a, double b,
 
 /* host replays of the scalar control flow (no device work): oc.hpp:93-174
  * driven by V(s) = vol(user, sqrt-multiplier), optionally in the speculative
- * batches of the device kernel; filter.hpp:182-228 driven by (g, g')(eta) */
+ * batches of the device kernel (speculative 1: 4 levels, 2: 5 levels; -1: the
+ * bound-shortcut replay, vol's first value taken for every evaluation);
+ * filter.hpp:182-228 driven by (g, g')(eta) */
 typedef double (*topo_sfun)(void* user, double s);
 typedef void (*topo_gfun)(void* user, double eta, double* g, double* gp);
 int topo_host_oc_replay(const topo_oc_params* prm, double lamMax, topo_sfun vol, void* user,

@@ -652,8 +652,7 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
     if (Vinf > prm->volfrac + 0.5 * prm->volume_tol + 1e-12) smode = 1;
     if (V0 < prm->volfrac - 0.5 * prm->volume_tol - 1e-12) smode = -1;
     if (smode != 0) {
-      ctl.check_mono = 0;
-      while (ctl.pending()) ctl.feed(smode > 0 ? INFINITY : -INFINITY);
+      ctl.replay_known(smode > 0 ? INFINITY : -INFINITY);
     }
     double req[kOcK], val[kOcK];
     static const bool dbg = getenv("TOPO_DEBUG") != nullptr;

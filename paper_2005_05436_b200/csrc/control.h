@@ -89,6 +89,56 @@ struct OcCtl {
     s_req = sqrt(lamMax);  // oc.hpp:125
   }
   __host__ __device__ bool pending() const { return phase != P_DONE; }
+  // Every evaluation returns vv (+inf or -inf: the bound shortcut, all the
+  // reference's decisions known). The same transitions as feeding vv until
+  // done with check_mono off, but the bisection steps skip the next request
+  // and test the cheap operand of oc.hpp:156-157 first (the same decision).
+  __host__ __device__ void replay_known(double vv) {
+    check_mono = 0;
+    if ((phase == P_WIDEN0 || phase == P_WIDEN) && vv > volfrac && widenings <= 40) {
+      // every remaining widening happens (oc.hpp:127-130): lamMax *= 4 each time,
+      // i.e. an exact power-of-two scaling, then the vLo request
+      const int k = 40 - widenings;
+      evals += k + 1;
+      lamMax = ldexp(lamMax, 2 * k);
+      widenings = 41;
+      vHi = vv;
+      phase = P_VLO;
+      s_req = 0.0;
+    }
+    while (phase == P_WIDEN0 || phase == P_WIDEN || phase == P_VLO) feed(vv);
+    while (phase == P_BIS) {
+      ++evals;
+      v = vv;
+      if (v > volfrac) {
+        lo = mid;
+        vLo = v;
+      } else {
+        hi = mid;
+        vHi = v;
+      }
+      if (++bis >= 500) {
+        finish_bis();
+        break;
+      }
+      const bool far = fabs(v - volfrac) > 0.5 * volTol;
+      if ((far && bis < 200) || (hi - lo) / (hi + lo) > relTol) {
+        const double prev = mid;
+        mid = 0.5 * (lo + hi);
+        s_req = mid;
+        if (mid == prev && far && !((hi - lo) / (hi + lo) > relTol)) {
+          // fixed point (the bracket end moved to mid is mid again): each
+          // remaining step only counts until bis = 200 ends the loop
+          evals += 200 - bis;
+          bis = 200;
+          finish_bis();
+        }
+      } else {
+        finish_bis();
+      }
+    }
+    while (phase == P_LSBIS) feed(vv);
+  }
   // whether the next request depends on the value fed for the current one
   __host__ __device__ bool branching() const { return phase != P_VLO; }
 

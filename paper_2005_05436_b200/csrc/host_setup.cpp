@@ -151,7 +151,9 @@ int topo_host_oc_replay(const topo_oc_params* prm, double lamMax, topo_sfun vol,
   c.init(lamMax, prm->volfrac, prm->bisect_rel_tol, prm->volume_tol, prm->lambda_space,
          prm->abs_tol);
   int nb = 0;
-  if (!speculative) {
+  if (speculative < 0) {  // known outcome: vol's first value (+-inf) for every evaluation
+    c.replay_known(vol(user, c.s_req));
+  } else if (!speculative) {
     while (c.pending()) c.feed(vol(user, c.s_req));
   } else {
     double req[32], val[32];

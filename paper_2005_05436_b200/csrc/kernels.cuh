@@ -1454,8 +1454,7 @@ __global__ void __launch_bounds__(kThreads) k_oc_bisect(OcArgs A) {
     if (threadIdx.x == 0) {
       nreq = 0;
       if (mode != 0) {
-        ctl.check_mono = 0;
-        while (ctl.pending()) ctl.feed(mode > 0 ? INFINITY : -INFINITY);
+        ctl.replay_known(mode > 0 ? INFINITY : -INFINITY);
       } else if (ctl.pending()) {
         nreq = oc_speculate<KK>(ctl, sreq);
         for (int q = 0; q < KK; ++q) {  // reciprocals for the batch sums (1/0 = inf)

@@ -187,3 +187,22 @@ def test_host_eta_replay_matches_oracle(P, lib, oracle_port, beta, seed):
     eta, it = C.c_double(), C.c_int32()
     lib.topo_host_eta_replay(0.5, cb, None, C.byref(eta), C.byref(it))
     assert abs(eta.value - eta_o) <= 1e-15 and it.value == it_o
+
+
+@pytest.mark.parametrize("sign", [1.0, -1.0])
+@pytest.mark.parametrize("lam0,move,volfrac,ls", [(9.3e4, 0.2, 0.5, 0), (2.2e31, 0.1, 0.12, 0),
+                                                  (1.0, 0.05, 0.3, 1), (5e-3, 0.2, 0.9, 0),
+                                                  (1e300, 0.2, 0.5, 0)])
+def test_host_oc_known_outcome_replay(P, lib, sign, lam0, move, volfrac, ls):
+    # the bound-shortcut replay (OcCtl::replay_known, used by the device OC
+    # kernel) ends in the state of feeding +-inf to every evaluation
+    prm = P._lib.OcParams(move, volfrac, 1e-4, 1e-3, ls, 1e-8, 0.0)
+    cb = P._lib.SFUN(lambda _u, s: sign * math.inf)
+    outs = []
+    for spec in (0, -1):
+        lam, bis, ev, sf = C.c_double(), C.c_int32(), C.c_int32(), C.c_double()
+        st = lib.topo_host_oc_replay(C.byref(prm), lam0, cb, None, spec, C.byref(lam),
+                                     C.byref(bis), C.byref(ev), C.byref(sf), None)
+        assert st == 0
+        outs.append((lam.value, bis.value, ev.value, sf.value))
+    assert outs[0] == outs[1]
