@@ -10,7 +10,7 @@ import os
 
 from . import build as _build
 
-LIB_PATH = os.environ.get("TOPO_LIB_OVERRIDE") or _build.LIB  # override: experiments only
+LIB_PATH = _build.LIB
 
 TOPO_OK, TOPO_EINVAL, TOPO_EOVERFLOW, TOPO_ENONMONO, TOPO_ECUDA, TOPO_ENCCL, TOPO_ENOMEM = range(7)
 BC_NEUMANN, BC_DIRICHLET = 0, 1

@@ -103,7 +103,6 @@ struct topo_ctx {
   int conv_R = 8;              // outputs per thread along the run axis
   int conv_A = 0;              // > 0: small-reach direct variant with half-width bound A
   bool overlap_sk = false;     // run the sK store concurrently with K3a..K6
-  bool fuse_sk = false;
   int oc_blocks_now = 0;
   // lower-triangle CSC of K (topo_csc_*): pattern built once on first use
   CscTab csc_tab{};
@@ -938,8 +937,6 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
     const char* ov = getenv("TOPO_SK_OVERLAP");
     const bool big = G.is3d && double(G.m) * G.P * 8.0 >= 4e9;
     ctx->overlap_sk = ov ? ov[0] == '1' : big;
-    const char* fu = getenv("TOPO_SK_FUSE");
-    ctx->fuse_sk = fu && fu[0] == '1';
   }
 
 #define CKC(x)                                                                          \
@@ -1881,11 +1878,9 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     S.ke_lower = ctx->d_ke_lower.as<double>();
     S.sK = skp;
   }
-  // default: sK values streamed by the fused K3a kernel (fuse_sk); else the
-  // separate K3b, overlapped on the aux stream or last on the main stream
-  const bool fuse_sk = want_sk && ctx->fuse_sk;
-  const bool overlap = want_sk && !fuse_sk && ctx->overlap_sk;
-  static const bool fork_late = getenv("TOPO_SK_FORK_LATE") != nullptr;  // experiment
+  // K3b: overlapped on the aux stream with K3a..K6 (large 3D passes), else
+  // last on the main stream
+  const bool overlap = want_sk && ctx->overlap_sk;
   auto fork_sk = [&]() -> topo_status {
     CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
     CK(cudaStreamWaitEvent(ctx->aux, ctx->ev_fork, 0));
@@ -1895,7 +1890,7 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     CK(cudaEventRecord(ctx->ev_join, ctx->aux));
     return TOPO_OK;
   };
-  if (overlap && !fork_late) TRY(fork_sk());
+  if (overlap) TRY(fork_sk());
   // U: a host array is copied on the copy stream behind x, overlapping K1, K2
   // and the sK stream; K3a waits for it
   if (is_device_ptr(U)) {
@@ -1928,38 +1923,8 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   E.a2 = ctx->a2_st.as<double>();
   E.partials = ctx->partials.as<double>() + 0;
   int nbe = grid_for(ctx, G.m);
-  if (fuse_sk) {
-    tmark(ctx, TOPO_STAGE_SK, 0, ctx->stream);
-    static const int ws = getenv("TOPO_SK_WS") ? atoi(getenv("TOPO_SK_WS")) : 1;
-    if (ws) {  // warp-specialised producer / consumer: 3 blocks per SM
-      constexpr int CW = 5, NB = 4;
-      nbe = int(std::min<long long>((G.m + 32 * CW - 1) / (32 * CW), (long long)ctx->sm_count * 3));
-      if (G.is3d) {
-        KeFull<24> K;
-        memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
-        k_elem_sens_ws<24, 300, CW, NB><<<nbe, kThreads, 0, ctx->stream>>>(G, K, E, S.ke_lower, skp);
-      } else {
-        KeFull<8> K;
-        memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
-        k_elem_sens_ws<8, 36, CW, NB><<<nbe, kThreads, 0, ctx->stream>>>(G, K, E, S.ke_lower, skp);
-      }
-    } else {
-      nbe = grid_for(ctx, (G.m + 31) / 32 * 32);
-      if (G.is3d) {
-        KeFull<24> K;
-        memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
-        k_elem_sens_sk<24, 300><<<nbe, kThreads, 0, ctx->stream>>>(G, K, E, S.ke_lower, skp);
-      } else {
-        KeFull<8> K;
-        memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
-        k_elem_sens_sk<8, 36><<<nbe, kThreads, 0, ctx->stream>>>(G, K, E, S.ke_lower, skp);
-      }
-    }
-    LAUNCHED();
-    tmark(ctx, TOPO_STAGE_SK, 1, ctx->stream);
-  } else {
-    TRY(launch_elem(ctx, E, nbe));
-  }
+  TRY(launch_elem(ctx, E, nbe));
+
   k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(E.partials, nbe, 1, res + 4);
   LAUNCHED();
   if (ctx->comm) {
@@ -1967,7 +1932,6 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     TRY(comm_halo(ctx->comm, ctx, ctx->a2_st.as<double>()));
   }
   tmark(ctx, TOPO_STAGE_ELEM, 1, ctx->stream);
-  if (overlap && fork_late) TRY(fork_sk());
   // K4
   tmark(ctx, TOPO_STAGE_ADJOINT, 0, ctx->stream);
   ConvArgs A4{};
@@ -2001,7 +1965,7 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   tmark(ctx, TOPO_STAGE_OC, 1, ctx->stream);
   ctx->oc_blocks_now = 0;
   if (oc_early) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
-  if (want_sk && !fuse_sk && !overlap) {
+  if (want_sk && !overlap) {
     tmark(ctx, TOPO_STAGE_SK, 0, ctx->stream);
     TRY(launch_sk(ctx, S, ctx->stream));
     tmark(ctx, TOPO_STAGE_SK, 1, ctx->stream);

@@ -1059,10 +1059,7 @@ __device__ __forceinline__ void st256_cs(double* p, double a, double b, double c
 // element l (one tanh + SIMP), then the warp streams the group's 32*P values
 // as 32-byte vectors (fully coalesced, no block barriers), taking each value's
 // modulus from its owner lane by shuffle and Ke_lower from shared memory.
-#ifndef SKU
-#define SKU 4
-#endif
-constexpr int kSkUnroll = SKU;
+constexpr int kSkUnroll = 4;
 template <int P>
 __global__ void __launch_bounds__(kThreads) k_sk_store(Geo G, SkArgs A) {
   constexpr int PV = P / 4;  // double4 per element
@@ -1123,191 +1120,6 @@ __global__ void __launch_bounds__(kThreads) k_sk_store(Geo G, SkArgs A) {
   const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long g = warp0; g < ngroups; g += nwarps) group(g);
-}
-
-// K3a + K3b fused: one warp owns 32 consecutive elements; each lane computes
-// its element's projection / SIMP / sensitivity / pre-adjoint fields, then the
-// warp streams the group's 32 * P lower-triangle values (256-bit evict-first
-// stores). The FP64 sensitivity work of one warp overlaps the HBM stores of
-// the others, so the pass pays for the store stream only once.
-template <int D, int P>
-__global__ void __launch_bounds__(kThreads, 3) k_elem_sens_sk(Geo G, KeFull<D> K, ElemArgs A,
-                                                              const double* __restrict__ ke_lower,
-                                                              double* __restrict__ sKout) {
-  constexpr int PV = P / 4;
-  __shared__ double4 kl[PV];
-  __shared__ double scratch[32];
-  for (int q = threadIdx.x; q < PV; q += blockDim.x)
-    kl[q] = make_double4(ke_lower[4 * q], ke_lower[4 * q + 1], ke_lower[4 * q + 2],
-                         ke_lower[4 * q + 3]);
-  const double eta = *A.eta_ptr;
-  const double a = tanh(A.beta * eta);
-  const double denom = a + tanh(A.beta * (1.0 - eta));
-  const double de = A.e0 - A.emin;
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-  const long long ngroups = (G.m + 31) >> 5;
-  double csum = 0.0;
-  for (long long grp = warp0; grp < ngroups; grp += nwarps) {
-    const long long e0 = grp << 5, e = e0 + lane;
-    double smod = 0.0;
-    if (e < G.m) {
-      int i, k, j;
-      elem_ijk(G, e, i, k, j);
-      const double t = A.xt[e];
-      const double th = tanh(A.beta * (t - eta));
-      const double xphys = (a + th) / denom;                 // filter.hpp:142
-      const double dH = A.beta * (1.0 - th * th) / denom;    // filter.hpp:151
-      int dofs[24];
-      element_dofs(G, i, k, j, G.j0, dofs);
-      double ue[D];
-#pragma unroll
-      for (int q = 0; q < D; ++q) ue[q] = __ldg(A.U + dofs[q]);
-      double quad = 0.0;  // ue . (Ke ue) (fea.hpp:267), symmetric upper half
-#pragma unroll
-      for (int r = 0; r < D; ++r) {
-        double sr = 0.5 * K.k[r * D + r] * ue[r];
-#pragma unroll
-        for (int c = r + 1; c < D; ++c) sr = fma(K.k[c * D + r], ue[c], sr);
-        quad = fma(ue[r], sr, quad);
-      }
-      quad = 2.0 * quad;
-      const double xp = simp_xp(xphys, A.penal);
-      smod = A.emin + xp * xphys * de;                      // fea.hpp:142
-      const double dsK = A.penal * xp * de;                 // fea.hpp:143
-      csum = fma(smod, quad, csum);
-      const int st = elem_state(A.state, e);
-      const double dcp = st == 0 ? -dsK * quad : 0.0;
-      const double dv0 = st == 0 ? A.inv_m : 0.0;           // driver.hpp:155
-      if (A.xPhys) A.xPhys[e] = xphys;
-      if (A.dcPhys) A.dcPhys[e] = dcp;
-      const double ih = 1.0 / A.hs[e];
-      const long long es = e + (long long)(G.j0 - G.sj0) * G.S;
-      A.a1[es] = (dH * dcp) * ih;                           // backfilter, filter.hpp:170, :128
-      A.a2[es] = (dH * dv0) * ih;
-    }
-    // fea.hpp:162-169 for the group's elements
-    double* out = sKout + e0 * P;
-    const int nv = int(min(32LL, G.m - e0)) * PV;
-#pragma unroll 4
-    for (int base = 0; base < nv; base += 32) {
-      const int v = base + lane;
-      const int el = min(v / PV, 31);
-      const double se = __shfl_sync(0xffffffffu, smod, el);
-      if (v < nv) {
-        const double4 kk = kl[v - el * PV];
-        st256_cs(out + 4 * (long long)v, se * kk.x, se * kk.y, se * kk.z, se * kk.w);
-      }
-    }
-  }
-  double red[1] = {csum};
-  block_sum<1>(red, scratch);
-  if (threadIdx.x == 0) A.partials[blockIdx.x] = red[0];
-}
-
-// K3a + K3b, warp-specialised producer/consumer: per block, CW "compute"
-// warps evaluate the sensitivity of one element per lane and leave each
-// chunk's moduli in a ring of NB shared-memory slots; the other warps stream
-// the chunks' lower-triangle values to HBM (256-bit evict-first stores).
-// Slots are handed over with named barriers (bar.sync / bar.arrive), so the
-// compute warps run ahead of the store stream by up to NB chunks and the FP64
-// work overlaps the HBM stream inside every SM.
-__device__ __forceinline__ void named_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void named_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-template <int D, int P, int CW, int NB>
-__global__ void __launch_bounds__(kThreads, 3) k_elem_sens_ws(Geo G, KeFull<D> K, ElemArgs A,
-                                                              const double* __restrict__ ke_lower,
-                                                              double* __restrict__ sKout) {
-  constexpr int PV = P / 4, CH = 32 * CW, SW = kThreads / 32 - CW;
-  __shared__ double4 kl[PV];
-  __shared__ double smod[NB][CH];
-  __shared__ double scratch[32];
-  for (int q = threadIdx.x; q < PV; q += blockDim.x)
-    kl[q] = make_double4(ke_lower[4 * q], ke_lower[4 * q + 1], ke_lower[4 * q + 2],
-                         ke_lower[4 * q + 3]);
-  const double eta = *A.eta_ptr;
-  const double a = tanh(A.beta * eta);
-  const double denom = a + tanh(A.beta * (1.0 - eta));
-  const double de = A.e0 - A.emin;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long nch = (G.m + CH - 1) / CH;
-  const long long iters = blockIdx.x < nch ? (nch - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  double csum = 0.0;
-  __syncthreads();
-  // barrier ids: 1 + b = slot b full, 1 + NB + b = slot b empty (all 256 threads)
-  if (warp < CW) {
-    for (long long it = 0; it < iters; ++it) {
-      const int b = int(it % NB);
-      if (it >= NB) named_sync(1 + NB + b, kThreads);  // wait until slot b was drained
-      const long long e = (blockIdx.x + it * gridDim.x) * CH + warp * 32 + lane;
-      double smodv = 0.0;
-      if (e < G.m) {
-        int i, k, j;
-        elem_ijk(G, e, i, k, j);
-        const double t = A.xt[e];
-        const double th = tanh(A.beta * (t - eta));
-        const double xphys = (a + th) / denom;               // filter.hpp:142
-        const double dH = A.beta * (1.0 - th * th) / denom;  // filter.hpp:151
-        int dofs[24];
-        element_dofs(G, i, k, j, G.j0, dofs);
-        double ue[D];
-#pragma unroll
-        for (int q = 0; q < D; ++q) ue[q] = __ldg(A.U + dofs[q]);
-        double quad = 0.0;  // ue . (Ke ue) (fea.hpp:267), symmetric upper half
-#pragma unroll
-        for (int r = 0; r < D; ++r) {
-          double sr = 0.5 * K.k[r * D + r] * ue[r];
-#pragma unroll
-          for (int cc = r + 1; cc < D; ++cc) sr = fma(K.k[cc * D + r], ue[cc], sr);
-          quad = fma(ue[r], sr, quad);
-        }
-        quad = 2.0 * quad;
-        const double xp = simp_xp(xphys, A.penal);
-        smodv = A.emin + xp * xphys * de;                    // fea.hpp:142
-        const double dsK = A.penal * xp * de;                // fea.hpp:143
-        csum = fma(smodv, quad, csum);
-        const int st = elem_state(A.state, e);
-        const double dcp = st == 0 ? -dsK * quad : 0.0;
-        const double dv0 = st == 0 ? A.inv_m : 0.0;          // driver.hpp:155
-        if (A.xPhys) A.xPhys[e] = xphys;
-        if (A.dcPhys) A.dcPhys[e] = dcp;
-        const double ih = 1.0 / A.hs[e];
-        const long long es = e + (long long)(G.j0 - G.sj0) * G.S;
-        A.a1[es] = (dH * dcp) * ih;                          // backfilter, filter.hpp:170
-        A.a2[es] = (dH * dv0) * ih;
-      }
-      smod[b][warp * 32 + lane] = smodv;
-      named_arrive(1 + b, kThreads);  // slot b full
-    }
-  } else {
-    for (long long it = 0; it < iters; ++it) {
-      const int b = int(it % NB);
-      named_sync(1 + b, kThreads);  // wait until slot b is full
-      const long long e0 = (blockIdx.x + it * gridDim.x) * CH;
-      const int nv = int(min((long long)CH, G.m - e0)) * PV;
-      double* out = sKout + e0 * P;  // fea.hpp:162-169
-      const double* sm = smod[b];
-#pragma unroll 4
-      for (int v = (warp - CW) * 32 + lane; v < nv; v += 32 * SW) {
-        const int el = v / PV;
-        const double se = sm[el];
-        const double4 kk = kl[v - el * PV];
-        st256_cs(out + 4 * (long long)v, se * kk.x, se * kk.y, se * kk.z, se * kk.w);
-      }
-      if (it + NB < iters) named_arrive(1 + NB + b, kThreads);  // slot b empty
-    }
-  }
-  __syncthreads();
-  double red[1] = {csum};
-  block_sum<1>(red, scratch);
-  if (threadIdx.x == 0) A.partials[blockIdx.x] = red[0];
 }
 
 // ============================================================================
