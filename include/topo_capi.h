@@ -237,6 +237,15 @@ topo_status topo_oc_primal_dual(topo_ctx* ctx, const double* x, const double* dc
                                 double* xNew, double* lambda, int32_t* iterations,
                                 int32_t* fell_back);
 
+/* ---- state solve: fea.hpp:205-239 solve_equilibrium
+ * K(sK) u = f on the free DOFs (u = 0 on `fixed`, LoadCase, fea.hpp:178-182),
+ * matrix-free Jacobi-preconditioned CG on the structured grid to
+ * ||r|| <= rtol ||f|| (the reference factorises; solutions agree to the solver
+ * tolerance). sK: per-element modulus (m); f, u: n. Single-rank contexts. */
+topo_status topo_solve_state(topo_ctx* ctx, const double* sK, const double* f,
+                             const int32_t* fixed, int64_t nfixed, double rtol, int32_t maxit,
+                             double* u, int32_t* iterations, double* relres);
+
 /* ---- fused pass: driver.hpp:183-231 (ft = 3) minus the state solve ------ */
 topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
                              const topo_pass_params* prm, topo_pass_out* out);

@@ -218,6 +218,7 @@ class Oracle:
                C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int))
             fn("primal_dual_update", C.c_int, Grid, f64p, f64p, f64p, u8p, C.POINTER(OcParams),
                C.c_double, f64p, C.POINTER(C.c_double), C.POINTER(C.c_int))
+            fn("solve_state", C.c_int, Grid, C.c_double, f64p, f64p, i32p, C.c_int64, f64p)
             fn("problem_create", C.c_void_p, Grid, C.c_double, C.c_int, C.c_double, u8p)
             fn("problem_destroy", None, C.c_void_p)
             fn("design_pass", C.c_int, C.c_void_p, f64p, f64p, C.POINTER(PassParams),
@@ -440,6 +441,16 @@ class Oracle:
                                                 C.byref(it))
         self._check(r)
         return xNew, lam.value, it.value, fb.value
+
+    def solve_state(self, grid, nu, sK, f, fixed):
+        """reference only: fea.hpp:205-239 solve_equilibrium (dense Cholesky of
+        the Eigen shim: small grids)."""
+        sK, f = _f64(sK), _f64(f)
+        fx = np.ascontiguousarray(fixed, np.int32)
+        u = np.empty_like(f)
+        self._check(self.lib.ref_solve_state(Grid(*grid), nu, _p(sK), _p(f), _p(fx), fx.size,
+                                             _p(u)))
+        return u
 
     # ----------------------------------------------------------- driver glue
     def design_pass(self, grid, rmin, x, u, state=None, *, nu=0.3, e0=1.0, emin=1e-9, penal=3.0,

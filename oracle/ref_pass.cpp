@@ -12,6 +12,7 @@
 // bench.py (--impl reference, cpu_baseline.kind = "reference").
 #include <cmath>
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <functional>
@@ -310,6 +311,24 @@ int ref_primal_dual_update(ref_grid g, const double* x, const double* dc, const 
     out(r.xNew, xNew);
     *lambda = r.lambda;
     *iterations = r.bisections;
+  });
+}
+
+// fea.hpp:205-239 solve_equilibrium(assemble_lower(...), LoadCase{f, fixed})
+int ref_solve_state(ref_grid g, double nu, const double* sK, const double* f,
+                    const int32_t* fixed, int64_t nfixed, double* u) {
+  return guard([&] {
+    const StructuredGrid grid{g.nelx, g.nely, g.nelz};
+    const ElementStiffness ke = grid.is3d() ? element_stiffness_h8(nu) : element_stiffness_q4(nu);
+    const IndexPairs pairs = build_symmetric_index_pairs(build_connectivity(grid));
+    const SymmetricSparseMatrix K =
+        assemble_lower(pairs, ke, vec(sK, grid.numElements()), grid.numDofs());
+    LoadCase load;
+    load.f = vec(f, grid.numDofs());
+    load.fixed.assign(fixed, fixed + nfixed);
+    std::sort(load.fixed.begin(), load.fixed.end());
+    load.fixed.erase(std::unique(load.fixed.begin(), load.fixed.end()), load.fixed.end());
+    out(solve_equilibrium(K, load), u);
   });
 }
 

@@ -136,6 +136,20 @@ def fixed_dofs(cfg: Config) -> np.ndarray:
     return np.sort(np.concatenate([3 * nodes, 3 * nodes + 1, 3 * nodes + 2]))
 
 
+def load_vector(cfg: Config) -> np.ndarray:
+    """The presets' unit loads: MBB downward at the top-left node (driver.hpp:
+    289-290); cantilever downward along the x = nelx, y = nely edge (:353-354)."""
+    nelx, nely, nelz = cfg.grid
+    f = np.zeros(cfg.n)
+    if not cfg.is3d:
+        f[2 * 0 + 1] = -1.0  # node(0, 0)
+        return f
+    for k in range(nelz + 1):
+        node = (nelx * (nelz + 1) + k) * (nely + 1) + nely
+        f[3 * node + 1] = -1.0
+    return f
+
+
 def displacement(cfg: Config) -> np.ndarray:
     u = _gen("normal", cfg.seed, STREAM_U, 0.0, 1.0, cfg.n)
     u[fixed_dofs(cfg)] = 0.0

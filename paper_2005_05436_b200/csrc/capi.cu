@@ -85,7 +85,7 @@ struct topo_ctx {
   DevBuf d_w3;
   // element matrices
   std::vector<double> ke_full, ke_lower;
-  DevBuf d_ke_lower;
+  DevBuf d_ke_lower, d_ke_full;
   // partition
   DevBuf d_state;
   bool has_state = false;
@@ -968,6 +968,9 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
     CKC(cudaMemcpy(ctx->d_w3.p, ctx->w3.data(), sizeof(double) * ctx->w3.size(),
                    cudaMemcpyHostToDevice));
   }
+  CKC(ctx->d_ke_full.ensure(sizeof(double) * size_t(G.d * G.d)));
+  CKC(cudaMemcpy(ctx->d_ke_full.p, ctx->ke_full.data(), sizeof(double) * size_t(G.d * G.d),
+                 cudaMemcpyHostToDevice));
   CKC(ctx->d_ke_lower.ensure(sizeof(double) * size_t(G.P)));
   CKC(cudaMemcpy(ctx->d_ke_lower.p, ctx->ke_lower.data(), sizeof(double) * size_t(G.P),
                  cudaMemcpyHostToDevice));
@@ -1026,7 +1029,7 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   if (ctx->comm) comm_destroy(ctx->comm);
   for (DevBuf* b : {&ctx->d_map, &ctx->d_clean}) b->release();
   for (DevBuf* b : {&ctx->d_csc_tab, &ctx->d_csc_int, &ctx->csc_colptr, &ctx->csc_rows, &ctx->csc_E}) b->release();
-  for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_w3, &ctx->d_ke_lower, &ctx->d_state, &ctx->hs, &ctx->hs_st,
+  for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_w3, &ctx->d_ke_lower, &ctx->d_ke_full, &ctx->d_state, &ctx->hs, &ctx->hs_st,
                     &ctx->cw, &ctx->x_st, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
                     &ctx->xnew, &ctx->a1_st, &ctx->a2_st, &ctx->rec, &ctx->u, &ctx->tmp0,
                     &ctx->tmp1, &ctx->tmp_st, &ctx->sK, &ctx->iK, &ctx->jK, &ctx->partials,
@@ -1793,6 +1796,106 @@ topo_status topo_oc_primal_dual(topo_ctx* ctx, const double* x, const double* dc
   if (lambda) *lambda = lam;
   if (iterations) *iterations = it;
   if (fell_back) *fell_back = fb;
+  return TOPO_OK;
+}
+
+// ------------------------------------------------ state solve (§8(f) row 2)
+// fea.hpp:205-239 solve_equilibrium: K(E) u = f on the free DOFs, u = 0 on the
+// fixed ones. Matrix-free Jacobi-preconditioned CG (the reference factorises;
+// the solutions agree to the solver tolerance). One host read of r.r per
+// iteration for the stopping test; every reduction in a fixed order.
+topo_status topo_solve_state(topo_ctx* ctx, const double* sK, const double* f,
+                             const int32_t* fixed, int64_t nfixed, double rtol, int32_t maxit,
+                             double* u, int32_t* iterations, double* relres) {
+  if (!ctx) return TOPO_EINVAL;
+  if (ctx->nranks > 1) return fail(ctx, TOPO_EINVAL, "solve: single-rank contexts only");
+  if (!(rtol > 0) || maxit < 0) return fail(ctx, TOPO_EINVAL, "solve: rtol > 0, maxit >= 0");
+  ctx->launches = 0;
+  const Geo& G = ctx->G;
+  const long long n = ctx->n;
+  std::vector<unsigned char> fx(size_t(n), 0);
+  for (int64_t q = 0; q < nfixed; ++q) {
+    if (!fixed || fixed[q] < 0 || fixed[q] >= n)
+      return fail(ctx, TOPO_EINVAL, "load case: fixed DOF out of range");
+    fx[size_t(fixed[q])] = 1;
+  }
+  const double *E, *fd;
+  TRY(stage_in(ctx, sK, G.m, ctx->tmp0, &E));
+  DevBuf fb, mask, vec, part, sc;
+  struct Release {  // scratch freed on every return path
+    std::initializer_list<DevBuf*> bufs;
+    ~Release() {
+      for (DevBuf* b : bufs) b->release();
+    }
+  } release_scratch{{&fb, &mask, &vec, &part, &sc}};
+  TRY(stage_in(ctx, f, n, fb, &fd));
+  CK(mask.ensure(size_t(n)));
+  CK(cudaMemcpyAsync(mask.p, fx.data(), size_t(n), cudaMemcpyHostToDevice, ctx->stream));
+  CK(vec.ensure(sizeof(double) * size_t(n) * 6));
+  double* diag = vec.as<double>();
+  double *r = diag + n, *z = r + n, *p = z + n, *qv = p + n, *ud = qv + n;
+  StateGeo S;
+  S.dim = G.dim;
+  S.nelx = G.nelx;
+  S.nely = G.nely;
+  S.nz = G.is3d ? G.nelz : 1;
+  S.nz1 = G.is3d ? G.nelz + 1 : 1;
+  S.ny1 = G.nely + 1;
+  S.pl = S.ny1 * S.nz1;
+  S.nn = n / G.dim;
+  S.E = E;
+  S.fixed = mask.as<unsigned char>();
+  const int nbn = grid_for(ctx, S.nn), nbd = grid_for(ctx, n);
+  CK(part.ensure(sizeof(double) * 2 * size_t(std::max(nbn, nbd))));
+  CK(sc.ensure(sizeof(double) * 8));
+  double* scd = sc.as<double>();
+  double* pp = part.as<double>();
+  const double* ke = ctx->d_ke_full.as<double>();
+  if (G.is3d)
+    k_state_diag<3><<<nbn, kThreads, 0, ctx->stream>>>(S, ke, diag);
+  else
+    k_state_diag<2><<<nbn, kThreads, 0, ctx->stream>>>(S, ke, diag);
+  LAUNCHED();
+  k_cg_init<<<nbd, kThreads, 0, ctx->stream>>>(n, fd, S.fixed, diag, ud, r, z, p, pp);
+  LAUNCHED();
+  k_reduce_partials<2><<<1, 32, 0, ctx->stream>>>(pp, nbd, 2, scd + 5);
+  LAUNCHED();
+  k_copy_scalar<<<1, 32, 0, ctx->stream>>>(scd + 5, scd + 0);
+  LAUNCHED();
+  double hs[2];
+  CK(cudaMemcpyAsync(hs, scd + 5, sizeof hs, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const double ff = hs[1];
+  double rel = ff > 0 ? 1.0 : 0.0;
+  int it = 0;
+  while (ff > 0 && rel > rtol && it < maxit) {
+    if (G.is3d)
+      k_state_matvec<3><<<nbn, kThreads, 0, ctx->stream>>>(S, ke, p, qv, pp);
+    else
+      k_state_matvec<2><<<nbn, kThreads, 0, ctx->stream>>>(S, ke, p, qv, pp);
+    LAUNCHED();
+    k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(pp, nbn, 1, scd + 1);
+    LAUNCHED();
+    k_cg_update<<<nbd, kThreads, 0, ctx->stream>>>(n, scd, p, qv, diag, ud, r, z, pp);
+    LAUNCHED();
+    k_reduce_partials<2><<<1, 32, 0, ctx->stream>>>(pp, nbd, 2, scd + 2);
+    LAUNCHED();
+    k_cg_direction<<<nbd, kThreads, 0, ctx->stream>>>(n, scd, z, p);
+    LAUNCHED();
+    k_copy_scalar<<<1, 32, 0, ctx->stream>>>(scd + 3, scd + 0);
+    LAUNCHED();
+    double rr = 0;
+    CK(cudaMemcpyAsync(&rr, scd + 2, sizeof rr, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ++it;
+    rel = std::sqrt(rr / ff);
+    if (!std::isfinite(rel))
+      return fail(ctx, TOPO_ENONMONO, "solve: CG broke down (operator not positive definite?)");
+  }
+  if (u) CK(cudaMemcpyAsync(u, ud, sizeof(double) * size_t(n), cudaMemcpyDefault, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (iterations) *iterations = it;
+  if (relres) *relres = rel;
   return TOPO_OK;
 }
 

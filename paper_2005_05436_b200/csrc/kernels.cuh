@@ -1750,6 +1750,193 @@ __global__ void k_modulus(long long m, const double* __restrict__ xt, const doub
   }
 }
 
+// ============================================================================
+// State solve K u = f (fea.hpp:205-239 solve_equilibrium
+// on the free DOFs): matrix-free Jacobi-preconditioned conjugate gradients on
+// the structured grid. K x is gathered per node (no atomics, fixed order):
+// y[dof] = sum over the elements around the node of E_e (Ke x_e)[local dof].
+// ============================================================================
+struct StateGeo {
+  int dim, nelx, nely, nz, nz1;  // elements along x, y, z (nz = 1 in 2D); node layers nz1
+  long long ny1, pl, nn;          // node strides, node count
+  const double* E;                // per-element modulus
+  const unsigned char* fixed;     // per DOF: 1 = fixed (u = 0)
+};
+
+// local node index of binary offsets (oi, ok, oj) in the element_dofs order
+__device__ __forceinline__ int local_node(int dim, int oi, int ok, int oj) {
+  return dim == 3 ? ((ok << 2) | (oi ? (oj ? 1 : 0) : (oj ? 2 : 3)))
+                  : (oi ? (oj ? 1 : 0) : (oj ? 2 : 3));
+}
+
+__device__ __forceinline__ void node_xyz(const StateGeo& S, long long nd, int& ix, int& iz, int& iy) {
+  const long long t = nd / S.ny1;
+  iy = int(nd - t * S.ny1);
+  ix = int(t / S.nz1);
+  iz = int(t - (long long)ix * S.nz1);
+}
+
+// y = K x over the free DOFs (fixed rows zeroed; x is zero on fixed DOFs) and
+// block partials of x . y; Ke (full, column-major) staged in shared memory
+template <int DIM>
+__global__ void __launch_bounds__(kThreads) k_state_matvec(StateGeo S, const double* __restrict__ ke,
+                                                           const double* __restrict__ x,
+                                                           double* __restrict__ y,
+                                                           double* __restrict__ partials) {
+  constexpr int D = 4 * (DIM == 3 ? 2 : 1) * DIM;  // 8 or 24 element DOFs
+  __shared__ double sk[D * D];
+  __shared__ double scratch[32];
+  for (int q = threadIdx.x; q < D * D; q += blockDim.x) sk[q] = ke[q];
+  __syncthreads();
+  double dot = 0.0;
+  for (long long nd = blockIdx.x * (long long)blockDim.x + threadIdx.x; nd < S.nn;
+       nd += (long long)gridDim.x * blockDim.x) {
+    int ix, iz, iy;
+    node_xyz(S, nd, ix, iz, iy);
+    double acc[DIM];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
+#pragma unroll
+    for (int q = 0; q < (DIM == 3 ? 8 : 4); ++q) {  // elements around the node, ascending
+      const int ex = ix - 1 + (q >> (DIM == 3 ? 2 : 1) & 1);
+      const int ez = DIM == 3 ? iz - 1 + (q >> 1 & 1) : 0;
+      const int ey = iy - 1 + (q & 1);
+      if (ex < 0 || ex >= S.nelx || ez < 0 || ez >= S.nz || ey < 0 || ey >= S.nely) continue;
+      const double Ee = S.E[((long long)ex * S.nz + ez) * S.nely + ey];
+      const int a = local_node(DIM, iy - ey, iz - ez, ix - ex);
+      const long long n0 = ((long long)ex * S.nz1 + ez) * S.ny1 + ey;  // element corner node
+      double part[DIM];
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) part[c] = 0.0;
+#pragma unroll
+      for (int b = 0; b < (DIM == 3 ? 8 : 4); ++b) {
+        // local node b's binary offsets (inverse of local_node)
+        const int oi = (b & 3) == 0 || (b & 3) == 1 ? 1 : 0;
+        const int oj = (b & 3) == 1 || (b & 3) == 2 ? 1 : 0;
+        const int ok = DIM == 3 ? (b >> 2) : 0;
+        const long long nb = n0 + oi + (long long)ok * S.ny1 + (long long)oj * S.pl;
+#pragma unroll
+        for (int cc = 0; cc < DIM; ++cc) {
+          const double xv = x[DIM * nb + cc];
+#pragma unroll
+          for (int c = 0; c < DIM; ++c)
+            part[c] = fma(sk[(DIM * b + cc) * D + DIM * a + c], xv, part[c]);  // Ke(row, col)
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) acc[c] = fma(Ee, part[c], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+      const long long d = DIM * nd + c;
+      const double v = S.fixed[d] ? 0.0 : acc[c];
+      y[d] = v;
+      dot = fma(x[d], v, dot);
+    }
+  }
+  double red[1] = {dot};
+  block_sum<1>(red, scratch);
+  if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
+}
+
+// Jacobi diagonal of K (1 on fixed DOFs)
+template <int DIM>
+__global__ void k_state_diag(StateGeo S, const double* __restrict__ ke, double* __restrict__ diag) {
+  constexpr int D = 4 * (DIM == 3 ? 2 : 1) * DIM;
+  for (long long nd = blockIdx.x * (long long)blockDim.x + threadIdx.x; nd < S.nn;
+       nd += (long long)gridDim.x * blockDim.x) {
+    int ix, iz, iy;
+    node_xyz(S, nd, ix, iz, iy);
+    double acc[DIM];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
+    for (int q = 0; q < (DIM == 3 ? 8 : 4); ++q) {
+      const int ex = ix - 1 + (q >> (DIM == 3 ? 2 : 1) & 1);
+      const int ez = DIM == 3 ? iz - 1 + (q >> 1 & 1) : 0;
+      const int ey = iy - 1 + (q & 1);
+      if (ex < 0 || ex >= S.nelx || ez < 0 || ez >= S.nz || ey < 0 || ey >= S.nely) continue;
+      const double Ee = S.E[((long long)ex * S.nz + ez) * S.nely + ey];
+      const int a = local_node(DIM, iy - ey, iz - ez, ix - ex);
+#pragma unroll
+      for (int c = 0; c < DIM; ++c) acc[c] = fma(Ee, ke[(DIM * a + c) * D + DIM * a + c], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+      const long long d = DIM * nd + c;
+      diag[d] = S.fixed[d] ? 1.0 : acc[c];
+    }
+  }
+}
+
+// CG scalars (device): [0] rz, [1] pq, [2] rr, [3] rz_new, [5] rz0, [6] ff
+// u += a p, r -= a q, z = r / diag; partials (r.r, r.z); a = rz / pq
+__global__ void __launch_bounds__(kThreads) k_cg_update(long long n, const double* __restrict__ sc,
+                                                        const double* __restrict__ p,
+                                                        const double* __restrict__ q,
+                                                        const double* __restrict__ diag,
+                                                        double* __restrict__ u, double* __restrict__ r,
+                                                        double* __restrict__ z,
+                                                        double* __restrict__ partials) {
+  __shared__ double scratch[2 * 32];
+  const double a = sc[0] / sc[1];
+  double red[2] = {0.0, 0.0};
+  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n;
+       d += (long long)gridDim.x * blockDim.x) {
+    u[d] = fma(a, p[d], u[d]);
+    const double rv = fma(-a, q[d], r[d]);
+    r[d] = rv;
+    const double zv = rv / diag[d];
+    z[d] = zv;
+    red[0] = fma(rv, rv, red[0]);
+    red[1] = fma(rv, zv, red[1]);
+  }
+  block_sum<2>(red, scratch);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = red[0];
+    partials[2 * blockIdx.x + 1] = red[1];
+  }
+}
+
+// p = z + (rz_new / rz) p; then rz = rz_new (one thread, after the grid)
+__global__ void k_cg_direction(long long n, const double* __restrict__ sc, const double* __restrict__ z,
+                               double* __restrict__ p) {
+  const double b = sc[3] / sc[0];
+  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n;
+       d += (long long)gridDim.x * blockDim.x)
+    p[d] = fma(b, p[d], z[d]);
+}
+
+// initial residual: r = f (0 on fixed), z = r / diag, p = z, u = 0; partials (r.z, f.f)
+__global__ void __launch_bounds__(kThreads) k_cg_init(long long n, const double* __restrict__ f,
+                                                      const unsigned char* __restrict__ fixed,
+                                                      const double* __restrict__ diag,
+                                                      double* __restrict__ u, double* __restrict__ r,
+                                                      double* __restrict__ z, double* __restrict__ p,
+                                                      double* __restrict__ partials) {
+  __shared__ double scratch[2 * 32];
+  double red[2] = {0.0, 0.0};
+  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n;
+       d += (long long)gridDim.x * blockDim.x) {
+    const double rv = fixed[d] ? 0.0 : f[d];
+    const double zv = rv / diag[d];
+    u[d] = 0.0;
+    r[d] = rv;
+    z[d] = zv;
+    p[d] = zv;
+    red[0] = fma(rv, zv, red[0]);
+    red[1] = fma(rv, rv, red[1]);
+  }
+  block_sum<2>(red, scratch);
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = red[0];
+    partials[2 * blockIdx.x + 1] = red[1];
+  }
+}
+
+__global__ void k_copy_scalar(const double* __restrict__ src, double* __restrict__ dst) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *dst = *src;
+}
+
 // FP64 peak probe: 8 independent FMA chains per thread (topo_fp64_peak)
 __global__ void __launch_bounds__(kThreads) k_dfma_peak(int iters, double seed, double* out) {
   double a[8];

@@ -1,0 +1,42 @@
+"""Device state solve: K(sK) u = f on the free DOFs,
+matrix-free Jacobi-PCG, against the reference's solve_equilibrium
+(fea.hpp:205-239, a Cholesky factorisation) on small grids. The solutions
+agree to the solver tolerance, not bitwise (direct vs iterative)."""
+import numpy as np
+import pytest
+
+from tests.common import rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2005_05436_b200 as P
+    return P
+
+
+@pytest.mark.parametrize("cid,grid,lo", [(1, (12, 6, 0), 0.3), (1, (20, 9, 0), 0.05),
+                                         (4, (6, 4, 4), 0.3), (5, (8, 5, 4), 0.1)])
+def test_solve_matches_reference(P, oracle_ref, cid, grid, lo):
+    from paper_2005_05436_b200.configs import CONFIGS, fixed_dofs, load_vector
+    cfg = CONFIGS[cid].scaled(*grid)
+    sK = 1e-9 + np.random.default_rng(2).uniform(lo, 1.0, cfg.m) ** 3  # SIMP moduli
+    f, fixed = load_vector(cfg), fixed_dofs(cfg)
+    ur = oracle_ref.solve_state(cfg.grid, cfg.nu, sK, f, fixed)
+    with P.Context(*cfg.grid, rmin=1.0, nu=cfg.nu) as ctx:
+        u, it, rr = ctx.solve_state(sK, f, fixed, rtol=1e-13)
+    assert rr <= 1e-13 and it > 0
+    assert np.all(u[fixed] == 0.0)
+    assert rel(u, ur) <= 1e-8, rel(u, ur)
+
+
+def test_solve_edge_cases(P):
+    from paper_2005_05436_b200.configs import CONFIGS, fixed_dofs
+    cfg = CONFIGS[4].scaled(4, 3, 3)
+    sK = np.ones(cfg.m)
+    with P.Context(*cfg.grid, rmin=1.0) as ctx:
+        u, it, rr = ctx.solve_state(sK, np.zeros(cfg.n), fixed_dofs(cfg))
+        assert it == 0 and np.all(u == 0)
+        with pytest.raises(P.InvalidArgument):
+            ctx.solve_state(sK, np.ones(cfg.n), [cfg.n])
