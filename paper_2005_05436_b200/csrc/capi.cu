@@ -62,6 +62,8 @@ struct topo_ctx {
   cudaStream_t stream = nullptr, aux = nullptr, cstream = nullptr;  // main, sK, copies
   bool own_stream = true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_x = nullptr, ev_u = nullptr;
+  static constexpr int kUChunks = 8;  // host U copied in x-chunks, K3a per chunk
+  cudaEvent_t ev_uc[kUChunks] = {};
   int sm_count = 148;
   Geo G{};
   int rank = 0, nranks = 1;
@@ -950,6 +952,7 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   CKC(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
   CKC(cudaEventCreateWithFlags(&ctx->ev_x, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_u, cudaEventDisableTiming));
+  for (auto& e : ctx->ev_uc) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   if (ctx->overlap_sk && set_overlap_carveout() != TOPO_OK)
     return bail(fail(ctx, TOPO_ECUDA, "cannot set the shared-memory carveout"));
   CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
@@ -1042,6 +1045,8 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->ev_x) cudaEventDestroy(ctx->ev_x);
   if (ctx->ev_u) cudaEventDestroy(ctx->ev_u);
+  for (auto& e : ctx->ev_uc)
+    if (e) cudaEventDestroy(e);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
   if (ctx->stream && ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -1918,6 +1923,8 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
                 vmode);
   const uint8_t* state = ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr;
   const double *xs, *ud = nullptr;
+  CK(ctx->partials.ensure(std::max(ctx->partials.bytes,
+                                   sizeof(double) * size_t(grid_for(ctx, G.m)) * 8)));
   TRY(stage_field_storage(ctx, x, ctx->x_st.p ? ctx->x_st : ctx->tmp_st, &xs));
   if (!U) return fail(ctx, TOPO_EINVAL, "null input array");
   CK(cudaEventRecord(ctx->ev_x, ctx->stream));  // x staged: a host U may follow on the link
@@ -1994,17 +2001,27 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     return TOPO_OK;
   };
   if (overlap) TRY(fork_sk());
-  // U: a host array is copied on the copy stream behind x, overlapping K1, K2
-  // and the sK stream; K3a waits for it
-  if (is_device_ptr(U)) {
+  // U: a host array is copied on the copy stream behind x in x-chunks of node
+  // planes, overlapping K1, K2 and the sK stream; K3a runs per element chunk
+  // (full grid each) as soon as the planes it touches have arrived. Device U:
+  // one K3a launch.
+  const bool hostU = !is_device_ptr(U);
+  const int nch =
+      (hostU && G.m >= (1LL << 20) && G.jn >= topo_ctx::kUChunks) ? topo_ctx::kUChunks : 1;
+  auto col0 = [&](int k) { return int((long long)k * G.jn / nch); };  // chunk k's first column
+  const long long plane = ctx->n / (G.jn + 1);                        // doubles per node plane
+  if (!hostU) {
     ud = U;
   } else {
     CK(ctx->u.ensure(sizeof(double) * size_t(ctx->n)));
     CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_x, 0));
-    CK(cudaMemcpyAsync(ctx->u.p, U, sizeof(double) * size_t(ctx->n), cudaMemcpyHostToDevice,
-                       ctx->cstream));
-    CK(cudaEventRecord(ctx->ev_u, ctx->cstream));
-    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_u, 0));
+    for (int k = 0; k < nch; ++k) {
+      const long long p0 = col0(k), p1 = k + 1 < nch ? col0(k + 1) : G.jn + 1;
+      CK(cudaMemcpyAsync(ctx->u.as<double>() + p0 * plane, U + p0 * plane,
+                         sizeof(double) * size_t((p1 - p0) * plane), cudaMemcpyHostToDevice,
+                         ctx->cstream));
+      CK(cudaEventRecord(ctx->ev_uc[k], ctx->cstream));
+    }
     ud = ctx->u.as<double>();
   }
   // K3a
@@ -2024,10 +2041,16 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   E.dcPhys = out->dcPhys ? ctx->dcphys.as<double>() : nullptr;  // only when requested
   E.a1 = ctx->a1_st.as<double>();
   E.a2 = ctx->a2_st.as<double>();
-  E.partials = ctx->partials.as<double>() + 0;
-  int nbe = grid_for(ctx, G.m);
-  TRY(launch_elem(ctx, E, nbe));
-
+  const int nbc = grid_for(ctx, (G.m + nch - 1) / nch);  // blocks per chunk
+  const int nbe = nbc * nch;
+  for (int k = 0; k < nch; ++k) {
+    if (hostU) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_uc[std::min(k + 1, nch - 1)], 0));
+    E.e_begin = (long long)col0(k) * G.S;
+    E.e_end = k + 1 < nch ? (long long)col0(k + 1) * G.S : G.m;
+    E.partials = ctx->partials.as<double>() + (long long)k * nbc;
+    TRY(launch_elem(ctx, E, nbc));
+  }
+  E.partials = ctx->partials.as<double>();
   k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(E.partials, nbe, 1, res + 4);
   LAUNCHED();
   if (ctx->comm) {

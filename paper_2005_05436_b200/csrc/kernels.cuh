@@ -847,6 +847,7 @@ struct ElemArgs {
   double* a1;            // storage-indexed pre-adjoint fields (dH dcPhys / hs, dH dV0 / hs)
   double* a2;
   double* partials;      // per block: compliance partial
+  long long e_begin, e_end;  // element range of this launch (e_end 0: all)
 };
 
 __device__ __forceinline__ double simp_xp(double x, double p) {
@@ -863,7 +864,8 @@ __global__ void __launch_bounds__(kThreads, 4 - NE) k_elem_sens(Geo G, KeFull<D>
   const double a = tanh(A.beta * eta);
   const double denom = a + tanh(A.beta * (1.0 - eta));
   const double de = A.e0 - A.emin;
-  const long long H = (G.m + NE - 1) / NE;  // element stride between a thread's elements
+  const long long eb = A.e_begin, ee = A.e_end > 0 ? A.e_end : G.m;
+  const long long H = (ee - eb + NE - 1) / NE;  // element stride between a thread's elements
   double csum = 0.0;
   for (long long e0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; e0 < H;
        e0 += (long long)gridDim.x * blockDim.x) {
@@ -872,9 +874,9 @@ __global__ void __launch_bounds__(kThreads, 4 - NE) k_elem_sens(Geo G, KeFull<D>
     bool ok[NE];
 #pragma unroll
     for (int n = 0; n < NE; ++n) {
-      const long long e = e0 + n * H;
-      ok[n] = e < G.m;
-      const long long ec = ok[n] ? e : e0;
+      const long long e = eb + e0 + n * H;
+      ok[n] = e < ee;
+      const long long ec = ok[n] ? e : eb + e0;
       int i, k, j;
       elem_ijk(G, ec, i, k, j);
       const double t = A.xt[ec];
@@ -913,7 +915,7 @@ __global__ void __launch_bounds__(kThreads, 4 - NE) k_elem_sens(Geo G, KeFull<D>
 #pragma unroll
     for (int n = 0; n < NE; ++n) {
       if (!ok[n]) continue;
-      const long long e = e0 + n * H;
+      const long long e = eb + e0 + n * H;
       const double q2 = 2.0 * quad[n];
       const double xp = simp_xp(xphys[n], A.penal);
       const double sK = A.emin + xp * xphys[n] * de;          // fea.hpp:142
@@ -959,8 +961,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, El
   const double denom = a + tanh(A.beta * (1.0 - eta));
   const double de = A.e0 - A.emin;
   const long long ny1 = G.nely + 1, pl = ny1 * (G.nelz + 1);
+  const long long ee = A.e_end > 0 ? A.e_end : G.m;
   double csum = 0.0;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < G.m;
+  for (long long e = A.e_begin + blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ee;
        e += (long long)gridDim.x * blockDim.x) {
     int i, k, j;
     elem_ijk(G, e, i, k, j);
