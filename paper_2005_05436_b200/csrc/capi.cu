@@ -243,6 +243,7 @@ ConvGeom conv_geom(const topo_ctx* c, const Geo& G, int WI, int WR, int WO) {
   T.other_n = G.is3d ? G.jn : 1;
   for (int q = 0; q < 3; ++q) T.ncol[q] = c->ncol[q];
   T.magicEI = unsigned((1ull << 32) / unsigned(T.EI) + 1);
+  T.zb = 0;
   return T;
 }
 
@@ -349,6 +350,7 @@ ConvGeom conv_geom3(const topo_ctx* c, const Geo& G, int WR, int WO) {
   T.other_n = G.jn;
   for (int q = 0; q < 3; ++q) T.ncol[q] = c->ncol[q];
   T.magicEI = unsigned((1ull << 32) / unsigned(T.EI) + 1);
+  T.zb = 0;
   return T;
 }
 
@@ -386,10 +388,12 @@ ConvGeom plan_geom(const topo_ctx* c, const Geo& G, bool* use3) {
 }
 
 template <int NF, int MODE, int AR>
-topo_status launch_conv3_t(topo_ctx* ctx, const Geo& G, const ConvGeom& T, const ConvArgs& A,
-                           int* nblocks) {
-  dim3 grid((G.nely + T.TI - 1) / T.TI, (T.run_n + T.TR - 1) / T.TR,
-            (T.other_n + T.TO - 1) / T.TO);
+topo_status launch_conv3_t(topo_ctx* ctx, const Geo& G, ConvGeom T, const ConvArgs& A,
+                           int* nblocks, int z0 = 0, int z1 = -1) {
+  const int ztiles = (T.other_n + T.TO - 1) / T.TO;
+  if (z1 < 0) z1 = ztiles;
+  T.zb = z0;
+  dim3 grid((G.nely + T.TI - 1) / T.TI, (T.run_n + T.TR - 1) / T.TR, z1 - z0);
   const size_t smem = conv_smem(T);
   static bool attr_done = false;  // per instantiation
   if (!attr_done) {
@@ -400,8 +404,24 @@ topo_status launch_conv3_t(topo_ctx* ctx, const Geo& G, const ConvGeom& T, const
   k_conv3<NF, MODE, AR, kC3R, kC3T><<<grid, kThreads, smem, ctx->stream>>>(
       G, T, ctx->d_w3.as<double>(), A);
   LAUNCHED();
-  if (nblocks) *nblocks = int(grid.x * grid.y * grid.z);
+  if (nblocks) *nblocks = int(grid.x * grid.y * ztiles);  // the whole grid's partials
   return TOPO_OK;
+}
+
+// tile range [z0, z1) along "other" of a k_conv3 launch (chunked K4); returns
+// false when the filter does not use k_conv3
+template <int NF, int MODE>
+topo_status launch_conv3_range(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int z0, int z1,
+                               int* nblocks) {
+  bool use3 = false;
+  const ConvGeom T3 = plan_geom(ctx, G, &use3);
+  if (!use3) return fail(ctx, TOPO_EINVAL, "internal: chunked filter needs k_conv3");
+  switch (ctx->conv_A) {
+    case 1: return launch_conv3_t<NF, MODE, 1>(ctx, G, T3, A, nblocks, z0, z1);
+    case 2: return launch_conv3_t<NF, MODE, 2>(ctx, G, T3, A, nblocks, z0, z1);
+    case 3: return launch_conv3_t<NF, MODE, 3>(ctx, G, T3, A, nblocks, z0, z1);
+    default: return launch_conv3_t<NF, MODE, 4>(ctx, G, T3, A, nblocks, z0, z1);
+  }
 }
 
 template <int NF, int MODE, int R, int AW>
@@ -2043,23 +2063,7 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   E.a2 = ctx->a2_st.as<double>();
   const int nbc = grid_for(ctx, (G.m + nch - 1) / nch);  // blocks per chunk
   const int nbe = nbc * nch;
-  for (int k = 0; k < nch; ++k) {
-    if (hostU) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_uc[std::min(k + 1, nch - 1)], 0));
-    E.e_begin = (long long)col0(k) * G.S;
-    E.e_end = k + 1 < nch ? (long long)col0(k + 1) * G.S : G.m;
-    E.partials = ctx->partials.as<double>() + (long long)k * nbc;
-    TRY(launch_elem(ctx, E, nbc));
-  }
-  E.partials = ctx->partials.as<double>();
-  k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(E.partials, nbe, 1, res + 4);
-  LAUNCHED();
-  if (ctx->comm) {
-    TRY(comm_halo(ctx->comm, ctx, ctx->a1_st.as<double>()));
-    TRY(comm_halo(ctx->comm, ctx, ctx->a2_st.as<double>()));
-  }
-  tmark(ctx, TOPO_STAGE_ELEM, 1, ctx->stream);
-  // K4
-  tmark(ctx, TOPO_STAGE_ADJOINT, 0, ctx->stream);
+  // K4 arguments (dual-field adjoint + OC records)
   ConvArgs A4{};
   A4.in0 = ctx->a1_st.as<double>();
   A4.in1 = ctx->a2_st.as<double>();
@@ -2073,7 +2077,53 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   ctx->oc_view = OcRecs{xown, ctx->rec.as<double>(), A4.cw, prm->move};
   A4.partials = ctx->partials0.as<double>();
   int nb4 = 0;
-  TRY((launch_conv<2, CONV_ADJ2_OC>(ctx, G, A4, &nb4)));
+  // chunked K4 (host U, single rank, k_conv3): tile range a of K4 runs as soon
+  // as the K3a chunks covering its columns plus the filter reach are done;
+  // the per-block partials keep the layout of one launch (same results)
+  bool use3 = false;
+  const ConvGeom T4 = plan_geom(ctx, G, &use3);
+  const bool k4chunks = nch > 1 && use3 && !ctx->comm;
+  const int ztiles = use3 ? (T4.other_n + T4.TO - 1) / T4.TO : 0;
+  auto ztile0 = [&](int a) { return int((long long)a * ztiles / nch); };
+  auto elem_chunk_of = [&](int col) {  // K3a chunk holding local column col
+    int k = 0;
+    while (k + 1 < nch && col0(k + 1) <= col) ++k;
+    return k;
+  };
+  int next_a = 0;
+  for (int k = 0; k < nch; ++k) {
+    if (hostU) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_uc[std::min(k + 1, nch - 1)], 0));
+    E.e_begin = (long long)col0(k) * G.S;
+    E.e_end = k + 1 < nch ? (long long)col0(k + 1) * G.S : G.m;
+    E.partials = ctx->partials.as<double>() + (long long)k * nbc;
+    TRY(launch_elem(ctx, E, nbc));
+    while (k4chunks && next_a < nch) {
+      const int z0 = ztile0(next_a), z1 = ztile0(next_a + 1);
+      const int last_col = std::min(G.jn, z1 * T4.TO + ctx->reach) - 1;
+      if (elem_chunk_of(last_col) > k) break;
+      if (z1 > z0) TRY((launch_conv3_range<2, CONV_ADJ2_OC>(ctx, G, A4, z0, z1, &nb4)));
+      ++next_a;
+    }
+  }
+  E.partials = ctx->partials.as<double>();
+  k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(E.partials, nbe, 1, res + 4);
+  LAUNCHED();
+  if (ctx->comm) {
+    TRY(comm_halo(ctx->comm, ctx, ctx->a1_st.as<double>()));
+    TRY(comm_halo(ctx->comm, ctx, ctx->a2_st.as<double>()));
+  }
+  tmark(ctx, TOPO_STAGE_ELEM, 1, ctx->stream);
+  // K4
+  tmark(ctx, TOPO_STAGE_ADJOINT, 0, ctx->stream);
+  if (k4chunks) {
+    while (next_a < nch) {  // (none left normally)
+      const int z0 = ztile0(next_a), z1 = ztile0(next_a + 1);
+      if (z1 > z0) TRY((launch_conv3_range<2, CONV_ADJ2_OC>(ctx, G, A4, z0, z1, &nb4)));
+      ++next_a;
+    }
+  } else {
+    TRY((launch_conv<2, CONV_ADJ2_OC>(ctx, G, A4, &nb4)));
+  }
   tmark(ctx, TOPO_STAGE_ADJOINT, 1, ctx->stream);
   // K5 + K6: beside the overlapped sK stream, with one cooperative block per
   // SM (all resident next to its 2 blocks per SM); else after the join

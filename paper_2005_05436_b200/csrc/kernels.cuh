@@ -237,6 +237,7 @@ struct ConvGeom {
   int reach, reach_o;  // halo along i and run / along other (0 in 2D)
   int run_n, other_n;  // owned extents of the run / other axes
   int ncol[3];         // canonical columns with 4, 2, 1 mirrors (stored in that order)
+  int zb;              // k_conv3: first tile along other of this launch (chunked grids)
   unsigned magicEI;    // floor(2^32 / EI) + 1: q / EI == umulhi(q, magicEI) for q < 2^20
 };
 
@@ -463,11 +464,11 @@ __device__ __forceinline__ void conv_store_pre(const ConvArgs& A, long long e, d
 }
 
 template <int MODE>
-__device__ __forceinline__ void conv_partials(const ConvArgs& A, double (&red)[3]) {
+__device__ __forceinline__ void conv_partials(const ConvArgs& A, double (&red)[3], int zb = 0) {
   if (MODE == CONV_ADJ2_OC) {
     __shared__ double scratch[3 * 32];
     block_sum<3>(red, scratch);
-    const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int b = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * (zb + blockIdx.z));
     if (threadIdx.x == 0) {
       A.partials[3 * b] = red[0];
       A.partials[3 * b + 1] = red[1];
@@ -599,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv3(Geo G, ConvGeom T,
   int* mapI = lineDst + nlines;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wr = warp % T.WR, wo = warp / T.WR;  // one warp along i
-  const int bi = blockIdx.x * 32, br = blockIdx.y * T.TR, bo = blockIdx.z * T.TO;
+  const int bi = blockIdx.x * 32, br = blockIdx.y * T.TR, bo = (T.zb + blockIdx.z) * T.TO;
   const int sI = T.ER, sPlane = T.EI * T.ER;
   // window origin: tile row wo*TB (halo included), i = lane + AR, run wr*RB
   const int sb0 = (wo * TB) * sPlane + (lane + AR) * sI + wr * RB;
@@ -671,7 +672,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv3(Geo G, ConvGeom T,
       }
     }
   }
-  conv_partials<MODE>(A, red);
+  conv_partials<MODE>(A, red, T.zb);
 }
 
 // ============================================================================

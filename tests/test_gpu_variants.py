@@ -94,3 +94,19 @@ def test_walsh_sensitivity_matches_dense(P):
     for k in ("dcPhys", "dc", "xNew"):
         assert rel(_as_np(getattr(b, k)), _as_np(getattr(a, k))) <= 1e-12, k
     assert abs(a.c - b.c) <= 1e-12 * abs(a.c)
+
+
+def test_chunked_host_pass_matches_device_pass(P):
+    # host U on a grid large enough for the chunked U copy / K3a / K4 pipeline
+    from paper_2005_05436_b200.configs import CONFIGS
+    cfg = CONFIGS[5].scaled(64, 128, 128)
+    assert cfg.m >= 1 << 20
+    x, u = _inputs(cfg, 21)
+    kw = dict(beta=cfg.beta, eta0=cfg.eta0, move=cfg.move, volfrac=cfg.volfrac)
+    with P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu) as ctx:
+        dev = ctx.design_pass(torch.from_numpy(x).cuda(), torch.from_numpy(u).cuda(), **kw)
+        host = ctx.design_pass(x, u, **kw)
+    for k in ("xTilde", "xPhys", "dcPhys", "dc", "dV", "xNew"):
+        np.testing.assert_array_equal(_as_np(getattr(dev, k)), _as_np(getattr(host, k)), err_msg=k)
+    assert (dev.eta, dev.lam, dev.bisections) == (host.eta, host.lam, host.bisections)
+    assert abs(dev.c - host.c) <= 1e-13 * abs(dev.c)  # K3a partials regrouped by chunk
