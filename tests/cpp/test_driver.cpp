@@ -5,6 +5,7 @@
 // device iterates CG to 1e-12, so histories agree to ~1e-9, not bitwise.
 #include <cmath>
 #include <cstdio>
+#include <string>
 
 #include "topopt/driver.hpp"
 #include "topopt_gpu.hpp"
@@ -39,7 +40,8 @@ static void compare(const char* name, const RunConfig& cfg, const Problem& prob)
   expect(same && dx <= 1e-6, what, dx);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  const bool frame = argc > 1 && std::string(argv[1]) == "--frame";  // slow: dense shim Cholesky
   {  // ft = 3 volume-preserving projection, MBB (top99neo defaults)
     RunConfig cfg;
     cfg.nelx = 30, cfg.nely = 10, cfg.rmin = 2.4, cfg.ft = 3, cfg.maxit = 8;
@@ -66,6 +68,13 @@ int main() {
     cfg.nelx = 20, cfg.nely = 10, cfg.rmin = 1.8, cfg.ft = 2, cfg.maxit = 6;
     cfg.penalCont = ContinuationSchedule{1, 4.0, 2, 0.5};
     compare("MBB 20x10 ft=2 + penal continuation", cfg, preset_mbb_2d(20, 10));
+  }
+  if (frame) {  // frame reinforcement preset: passive frame and void opening (driver.hpp:306-341);
+                // ~12 min, the shim factorises 5202 DOFs densely (measured: 1.3e-8 / 9.3e-9)
+    RunConfig cfg;
+    cfg.nelx = 50, cfg.nely = 50, cfg.rmin = 2.5, cfg.ft = 3, cfg.maxit = 3;
+    cfg.volfrac = 0.4;
+    compare("frame 50x50 ft=3 (passives)", cfg, preset_frame_2d(50, 50, 1));
   }
   std::printf("%d failure(s)\n", failures);
   return failures ? 1 : 0;
