@@ -245,6 +245,14 @@ topo_status topo_oc_primal_dual(topo_ctx* ctx, const double* x, const double* dc
 topo_status topo_solve_state(topo_ctx* ctx, const double* sK, const double* f,
                              const int32_t* fixed, int64_t nfixed, double rtol, int32_t maxit,
                              double* u, int32_t* iterations, double* relres);
+/* the same solve with a geometric multigrid V-cycle as the preconditioner
+ * (the MGCG variant of top3D125): Galerkin element matrices on grids halved
+ * per axis while every element count stays even, damped-Jacobi smoothing,
+ * Jacobi sweeps on the coarsest grid; the Jacobi-PCG solve when the grid
+ * cannot be coarsened */
+topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f,
+                                const int32_t* fixed, int64_t nfixed, double rtol, int32_t maxit,
+                                double* u, int32_t* iterations, double* relres);
 
 /* ---- fused pass: driver.hpp:183-231 (ft = 3) minus the state solve ------ */
 topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,

@@ -552,16 +552,19 @@ class Context:
                                                  C.byref(fb)))
         return UpdateResult(out, lam.value, it.value, 0, bool(fb.value))
 
-    def solve_state(self, sK, f, fixed, rtol: float = 1e-10, maxit: int = 100000):
+    def solve_state(self, sK, f, fixed, rtol: float = 1e-10, maxit: int = 100000,
+                    multigrid: bool = False):
         """fea.hpp:205-239 solve_equilibrium on the device: K(sK) u = f with u = 0
-        on `fixed`; matrix-free Jacobi-PCG. Returns (u, iterations, relres)."""
+        on `fixed`; matrix-free PCG, Jacobi or geometric-multigrid (V-cycle)
+        preconditioned. Returns (u, iterations, relres)."""
         sa = _Arr(sK, n=self.m, name="solve: sK")
         fa = _Arr(f, n=self.n, name="solve: load vector")
         fx = np.ascontiguousarray(fixed if fixed is not None else [], dtype=np.int32)
         out, ptr = _empty(self.n, fa.device)
         it, rr = C.c_int32(), C.c_double()
-        self._check(self.lib.topo_solve_state(self.h, sa.ptr, fa.ptr, fx.ctypes.data, fx.size,
-                                              rtol, maxit, ptr, C.byref(it), C.byref(rr)))
+        fn = self.lib.topo_solve_state_mg if multigrid else self.lib.topo_solve_state
+        self._check(fn(self.h, sa.ptr, fa.ptr, fx.ctypes.data, fx.size, rtol, maxit, ptr,
+                       C.byref(it), C.byref(rr)))
         return out, it.value, rr.value
 
     # driver.hpp:183-231

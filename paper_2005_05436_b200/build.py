@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-fopenmp", "-Xcompiler", "-Wall"]
 SOURCES = ["capi.cu", "host_setup.cpp"]
-HEADERS = ["kernels.cuh", "common.cuh", "control.h", "comm.h"]
+HEADERS = ["kernels.cuh", "common.cuh", "control.h", "comm.h", "mg.cuh"]
 
 
 def _nvcc() -> str:

@@ -9,12 +9,14 @@
 
 #include <algorithm>
 #include <string>
+#include <functional>
 #include <memory>
 #include <vector>
 
 #include "../../include/topo_capi.h"
 #include "comm.h"
 #include "kernels.cuh"
+#include "mg.cuh"
 #include <cub/device/device_scan.cuh>
 
 using namespace topo;
@@ -1904,6 +1906,346 @@ topo_status topo_solve_state(topo_ctx* ctx, const double* sK, const double* f,
     k_cg_update<<<nbd, kThreads, 0, ctx->stream>>>(n, scd, p, qv, diag, ud, r, z, pp);
     LAUNCHED();
     k_reduce_partials<2><<<1, 32, 0, ctx->stream>>>(pp, nbd, 2, scd + 2);
+    LAUNCHED();
+    k_cg_direction<<<nbd, kThreads, 0, ctx->stream>>>(n, scd, z, p);
+    LAUNCHED();
+    k_copy_scalar<<<1, 32, 0, ctx->stream>>>(scd + 3, scd + 0);
+    LAUNCHED();
+    double rr = 0;
+    CK(cudaMemcpyAsync(&rr, scd + 2, sizeof rr, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ++it;
+    rel = std::sqrt(rr / ff);
+    if (!std::isfinite(rel))
+      return fail(ctx, TOPO_ENONMONO, "solve: CG broke down (operator not positive definite?)");
+  }
+  if (u) CK(cudaMemcpyAsync(u, ud, sizeof(double) * size_t(n), cudaMemcpyDefault, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (iterations) *iterations = it;
+  if (relres) *relres = rel;
+  return TOPO_OK;
+}
+
+// ------------------------------------------- multigrid-preconditioned solve
+namespace {
+struct MgLevel {
+  MgGeo g{};
+  DevBuf fixed, K, diag, x, b, r, y;
+  double omega = 0.6;  // damped-Jacobi weight, 1.2 / lambda_max(D^-1 A)
+};
+
+// interpolation Q_p (D x D, column-major): coarse element DOF j -> DOF k of
+// child p, trilinear weights on the 3^dim node lattice of the coarse element
+static void mg_interp(int dim, std::vector<double>& Q) {
+  const int NN = dim == 3 ? 8 : 4, D = NN * dim;
+  Q.assign(size_t(NN) * D * D, 0.0);
+  for (int p = 0; p < NN; ++p) {
+    int pi, pk, pj;
+    mg_offsets(p, pi, pk, pj);
+    for (int a = 0; a < NN; ++a) {  // child node
+      int oi, ok, oj;
+      mg_offsets(a, oi, ok, oj);
+      const double ti = 0.5 * (pi + oi), tk = 0.5 * (pk + ok), tj = 0.5 * (pj + oj);
+      for (int b = 0; b < NN; ++b) {  // coarse node
+        int ci, ck, cj;
+        mg_offsets(b, ci, ck, cj);
+        double w = (ci ? ti : 1.0 - ti) * (cj ? tj : 1.0 - tj);
+        if (dim == 3) w *= ck ? tk : 1.0 - tk;
+        for (int c = 0; c < dim; ++c) Q[size_t(p) * D * D + size_t(dim * b + c) * D + dim * a + c] = w;
+      }
+    }
+  }
+}
+}  // namespace
+
+topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f,
+                                const int32_t* fixed, int64_t nfixed, double rtol, int32_t maxit,
+                                double* u, int32_t* iterations, double* relres) {
+  if (!ctx) return TOPO_EINVAL;
+  if (ctx->nranks > 1) return fail(ctx, TOPO_EINVAL, "solve: single-rank contexts only");
+  if (!(rtol > 0) || maxit < 0) return fail(ctx, TOPO_EINVAL, "solve: rtol > 0, maxit >= 0");
+  const Geo& G = ctx->G;
+  const int dim = G.dim;
+  // levels: halve while every element count is even and the level is not tiny
+  std::vector<MgLevel> lv(1);
+  auto geo = [&](int nx, int ny, int nz3) {
+    MgGeo g{};
+    g.nelx = nx;
+    g.nely = ny;
+    g.nz = dim == 3 ? nz3 : 1;
+    g.nz1 = dim == 3 ? nz3 + 1 : 1;
+    g.ny1 = ny + 1;
+    g.pl = g.ny1 * g.nz1;
+    g.nn = (long long)(nx + 1) * g.pl;
+    g.n = dim * g.nn;
+    g.m = (long long)nx * ny * g.nz;
+    return g;
+  };
+  lv[0].g = geo(G.nelx, G.nely, G.nelz);
+  for (;;) {
+    const MgGeo c = lv.back().g;  // (copy: emplace_back below may reallocate)
+    const bool even = c.nelx % 2 == 0 && c.nely % 2 == 0 && (dim == 2 || c.nz % 2 == 0);
+    static const long long min_dofs =
+        getenv("TOPO_MG_MIN_DOFS") ? atoll(getenv("TOPO_MG_MIN_DOFS")) : 20000;  // tests
+    if (!even || c.n <= min_dofs || lv.size() >= 8) break;
+    lv.emplace_back();
+    lv.back().g = geo(c.nelx / 2, c.nely / 2, dim == 3 ? c.nz / 2 : 0);
+  }
+  if (lv.size() < 2)  // nothing to coarsen: the Jacobi-preconditioned solve
+    return topo_solve_state(ctx, sK, f, fixed, nfixed, rtol, maxit, u, iterations, relres);
+  ctx->launches = 0;
+  const long long n = ctx->n;
+  std::vector<unsigned char> fx(size_t(n), 0);
+  for (int64_t q = 0; q < nfixed; ++q) {
+    if (!fixed || fixed[q] < 0 || fixed[q] >= n)
+      return fail(ctx, TOPO_EINVAL, "load case: fixed DOF out of range");
+    fx[size_t(fixed[q])] = 1;
+  }
+  const double *E, *fd;
+  TRY(stage_in(ctx, sK, G.m, ctx->tmp0, &E));
+  DevBuf fb, cg, part, sc, dQ, dKp;
+  struct Release {
+    std::vector<MgLevel>* lv;
+    std::initializer_list<DevBuf*> bufs;
+    ~Release() {
+      for (DevBuf* b : bufs) b->release();
+      for (auto& L : *lv)
+        for (DevBuf* b : {&L.fixed, &L.K, &L.diag, &L.x, &L.b, &L.r, &L.y}) b->release();
+    }
+  } release_all{&lv, {&fb, &cg, &part, &sc, &dQ, &dKp}};
+  TRY(stage_in(ctx, f, n, fb, &fd));
+  const int D = (dim == 3 ? 8 : 4) * dim, DD = D * D, NN = dim == 3 ? 8 : 4;
+  // interpolation and the level-1 combinations Kp = Qp' Ke Qp (host)
+  std::vector<double> Q, Kp(size_t(NN) * DD, 0.0);
+  mg_interp(dim, Q);
+  const std::vector<double>& Ke = ctx->ke_full;
+  for (int p = 0; p < NN; ++p) {
+    const double* Qp = Q.data() + size_t(p) * DD;
+    std::vector<double> T(size_t(DD), 0.0);
+    for (int j = 0; j < D; ++j)
+      for (int i = 0; i < D; ++i) {
+        double s2 = 0;
+        for (int k = 0; k < D; ++k) s2 += Ke[size_t(k) * D + i] * Qp[size_t(j) * D + k];
+        T[size_t(j) * D + i] = s2;
+      }
+    for (int j = 0; j < D; ++j)
+      for (int i = 0; i < D; ++i) {
+        double s2 = 0;
+        for (int k = 0; k < D; ++k) s2 += Qp[size_t(i) * D + k] * T[size_t(j) * D + k];
+        Kp[size_t(p) * DD + size_t(j) * D + i] = s2;
+      }
+  }
+  CK(dQ.ensure(sizeof(double) * Q.size()));
+  CK(dKp.ensure(sizeof(double) * Kp.size()));
+  CK(cudaMemcpyAsync(dQ.p, Q.data(), sizeof(double) * Q.size(), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dKp.p, Kp.data(), sizeof(double) * Kp.size(), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  // per-level storage, fixed masks, Galerkin matrices, diagonals
+  for (size_t l = 0; l < lv.size(); ++l) {
+    MgLevel& L = lv[l];
+    CK(L.fixed.ensure(size_t(L.g.n)));
+    for (DevBuf* b : {&L.diag, &L.x, &L.b, &L.r, &L.y}) CK(b->ensure(sizeof(double) * size_t(L.g.n)));
+    L.g.fixed = L.fixed.as<unsigned char>();
+    if (l == 0) {
+      CK(cudaMemcpyAsync(L.fixed.p, fx.data(), size_t(n), cudaMemcpyHostToDevice, ctx->stream));
+      continue;
+    }
+    CK(L.K.ensure(sizeof(double) * size_t(L.g.m) * DD));
+    const MgLevel& F = lv[l - 1];
+    const int nbn = grid_for(ctx, L.g.nn);
+    if (dim == 3) {
+      k_mg_fixed<3><<<nbn, kThreads, 0, ctx->stream>>>(L.g, F.g, F.fixed.as<unsigned char>(),
+                                                       L.fixed.as<unsigned char>());
+      if (l == 1)
+        k_mg_galerkin1<3><<<grid_for(ctx, L.g.m * DD), kThreads, 0, ctx->stream>>>(
+            L.g, F.g, E, dKp.as<double>(), L.K.as<double>());
+      else
+        k_mg_galerkin<3><<<int(std::min<long long>(L.g.m, 1LL << 20)), 256, 0, ctx->stream>>>(
+            L.g, F.g, F.K.as<double>(), dQ.as<double>(), L.K.as<double>());
+    } else {
+      k_mg_fixed<2><<<nbn, kThreads, 0, ctx->stream>>>(L.g, F.g, F.fixed.as<unsigned char>(),
+                                                       L.fixed.as<unsigned char>());
+      if (l == 1)
+        k_mg_galerkin1<2><<<grid_for(ctx, L.g.m * DD), kThreads, 0, ctx->stream>>>(
+            L.g, F.g, E, dKp.as<double>(), L.K.as<double>());
+      else
+        k_mg_galerkin<2><<<int(std::min<long long>(L.g.m, 1LL << 20)), 256, 0, ctx->stream>>>(
+            L.g, F.g, F.K.as<double>(), dQ.as<double>(), L.K.as<double>());
+    }
+    LAUNCHED();
+  }
+  const double* dKe = ctx->d_ke_full.as<double>();
+  for (size_t l = 0; l < lv.size(); ++l) {
+    MgLevel& L = lv[l];
+    const int nbn = grid_for(ctx, L.g.nn);
+    if (dim == 3) {
+      if (l == 0)
+        k_mg_diag<3, true><<<nbn, kThreads, 0, ctx->stream>>>(L.g, dKe, E, L.diag.as<double>());
+      else
+        k_mg_diag<3, false><<<nbn, kThreads, 0, ctx->stream>>>(L.g, L.K.as<double>(), nullptr,
+                                                               L.diag.as<double>());
+    } else {
+      if (l == 0)
+        k_mg_diag<2, true><<<nbn, kThreads, 0, ctx->stream>>>(L.g, dKe, E, L.diag.as<double>());
+      else
+        k_mg_diag<2, false><<<nbn, kThreads, 0, ctx->stream>>>(L.g, L.K.as<double>(), nullptr,
+                                                               L.diag.as<double>());
+    }
+    LAUNCHED();
+  }
+  // y = A_l x (elements by colour: no two of a colour share a node)
+  auto apply = [&](size_t l, const double* xin, double* yout) -> topo_status {
+    MgLevel& L = lv[l];
+    CK(cudaMemsetAsync(yout, 0, sizeof(double) * size_t(L.g.n), ctx->stream));
+    const int nb = grid_for(ctx, std::max<long long>(1, L.g.m / 8));
+    for (int color = 0; color < (dim == 3 ? 8 : 8); ++color) {
+      if (dim == 2 && (color & 2)) continue;  // no z parity in 2D
+      if (dim == 3) {
+        if (l == 0)
+          k_mg_apply<3, true><<<nb, 256, 0, ctx->stream>>>(L.g, dKe, E, color, xin, yout);
+        else
+          k_mg_apply<3, false><<<nb, 256, 0, ctx->stream>>>(L.g, L.K.as<double>(), nullptr, color,
+                                                            xin, yout);
+      } else {
+        if (l == 0)
+          k_mg_apply<2, true><<<nb, 256, 0, ctx->stream>>>(L.g, dKe, E, color, xin, yout);
+        else
+          k_mg_apply<2, false><<<nb, 256, 0, ctx->stream>>>(L.g, L.K.as<double>(), nullptr, color,
+                                                            xin, yout);
+      }
+      LAUNCHED();
+    }
+    return TOPO_OK;
+  };
+  // smoother weights: lambda_max(D^-1 A) by 12 power iterations per level,
+  // omega = 1.2 / lambda_max keeps every Jacobi sweep convergent
+  CK(part.ensure(sizeof(double) * 2 * size_t(grid_for(ctx, n))));
+  CK(sc.ensure(sizeof(double) * 8));
+  for (size_t l = 0; l < lv.size(); ++l) {
+    MgLevel& L = lv[l];
+    const long long nl = L.g.n;
+    const int nbd = grid_for(ctx, nl);
+    const unsigned char* fm = L.fixed.as<unsigned char>();
+    double *x = L.x.as<double>(), *y = L.y.as<double>(), *wv = L.r.as<double>();
+    k_mg_scale<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, 1, 0.0, nullptr, x);
+    LAUNCHED();
+    double lam = 1.0;
+    for (int itp = 0; itp < 12; ++itp) {
+      TRY(apply(l, x, y));
+      k_mg_dinv<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, y, L.diag.as<double>(), wv);
+      LAUNCHED();
+      k_dot<<<nbd, kThreads, 0, ctx->stream>>>(nl, wv, wv, part.as<double>());
+      k_dot<<<nbd, kThreads, 0, ctx->stream>>>(nl, x, x, part.as<double>() + nbd);
+      k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(part.as<double>(), nbd, 1, sc.as<double>());
+      k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(part.as<double>() + nbd, nbd, 1,
+                                                       sc.as<double>() + 1);
+      double h2[2];
+      CK(cudaMemcpyAsync(h2, sc.p, sizeof h2, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      if (!(h2[0] > 0) || !(h2[1] > 0)) break;
+      lam = std::sqrt(h2[0] / h2[1]);
+      k_mg_scale<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, 0, 1.0 / std::sqrt(h2[0]), wv, x);
+      LAUNCHED();
+    }
+    L.omega = 1.2 / std::max(lam, 1e-30);
+  }
+  const int nu = 2, ncoarse = 40;
+  // V-cycle: lv[l].x <- approx A_l^{-1} lv[l].b
+  std::function<topo_status(size_t)> vcycle = [&](size_t l) -> topo_status {
+    MgLevel& L = lv[l];
+    const long long nl = L.g.n;
+    const int nbd = grid_for(ctx, nl);
+    const unsigned char* fm = L.fixed.as<unsigned char>();
+    double *x = L.x.as<double>(), *b = L.b.as<double>(), *y = L.y.as<double>(),
+           *dg = L.diag.as<double>();
+    const bool last = l + 1 == lv.size();
+    const int sweeps = last ? ncoarse : nu;
+    const double w = L.omega;
+    k_mg_jacobi<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, b, nullptr, dg, w, x);
+    LAUNCHED();
+    for (int s2 = 1; s2 < sweeps; ++s2) {
+      TRY(apply(l, x, y));
+      k_mg_jacobi<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, b, y, dg, w, x);
+      LAUNCHED();
+    }
+    if (last) return TOPO_OK;
+    MgLevel& Cl = lv[l + 1];
+    TRY(apply(l, x, y));
+    k_mg_residual<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, b, y, L.r.as<double>());
+    LAUNCHED();
+    const int nbc = grid_for(ctx, Cl.g.nn), nbf = grid_for(ctx, L.g.nn);
+    if (dim == 3)
+      k_mg_restrict<3><<<nbc, kThreads, 0, ctx->stream>>>(Cl.g, L.g, L.r.as<double>(), Cl.b.as<double>());
+    else
+      k_mg_restrict<2><<<nbc, kThreads, 0, ctx->stream>>>(Cl.g, L.g, L.r.as<double>(), Cl.b.as<double>());
+    LAUNCHED();
+    TRY(vcycle(l + 1));
+    if (dim == 3)
+      k_mg_prolong_add<3><<<nbf, kThreads, 0, ctx->stream>>>(Cl.g, L.g, Cl.x.as<double>(), x);
+    else
+      k_mg_prolong_add<2><<<nbf, kThreads, 0, ctx->stream>>>(Cl.g, L.g, Cl.x.as<double>(), x);
+    LAUNCHED();
+    for (int s2 = 0; s2 < nu; ++s2) {
+      TRY(apply(l, x, y));
+      k_mg_jacobi<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, b, y, dg, w, x);
+      LAUNCHED();
+    }
+    return TOPO_OK;
+  };
+  // PCG: r = f (0 on fixed), z = V(r), p = z
+  StateGeo S;
+  S.dim = dim;
+  S.nelx = G.nelx;
+  S.nely = G.nely;
+  S.nz = G.is3d ? G.nelz : 1;
+  S.nz1 = G.is3d ? G.nelz + 1 : 1;
+  S.ny1 = G.nely + 1;
+  S.pl = S.ny1 * S.nz1;
+  S.nn = n / dim;
+  S.E = E;
+  S.fixed = lv[0].fixed.as<unsigned char>();
+  const int nbn = grid_for(ctx, S.nn), nbd = grid_for(ctx, n);
+  CK(cg.ensure(sizeof(double) * size_t(n) * 3));
+  double *ud = cg.as<double>(), *p = ud + n, *qv = p + n;
+  double* r = lv[0].b.as<double>();  // the V-cycle reads its right-hand side from level 0's b
+  double* z = lv[0].x.as<double>();
+  CK(part.ensure(sizeof(double) * 2 * size_t(std::max(nbn, nbd))));
+  CK(sc.ensure(sizeof(double) * 8));
+  double* scd = sc.as<double>();
+  double* pp = part.as<double>();
+  k_cg_init<<<nbd, kThreads, 0, ctx->stream>>>(n, fd, S.fixed, lv[0].diag.as<double>(), ud, r, z,
+                                               p, pp);  // (z, p overwritten below)
+  LAUNCHED();
+  k_reduce_partials<2><<<1, 32, 0, ctx->stream>>>(pp, nbd, 2, scd + 5);  // [6] = f.f
+  LAUNCHED();
+  TRY(vcycle(0));
+  CK(cudaMemcpyAsync(p, z, sizeof(double) * size_t(n), cudaMemcpyDeviceToDevice, ctx->stream));
+  k_dot<<<nbd, kThreads, 0, ctx->stream>>>(n, r, z, pp);
+  LAUNCHED();
+  k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(pp, nbd, 1, scd + 0);
+  LAUNCHED();
+  double hs[2];
+  CK(cudaMemcpyAsync(hs, scd + 5, sizeof hs, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const double ff = hs[1];
+  double rel = ff > 0 ? 1.0 : 0.0;
+  int it = 0;
+  while (ff > 0 && rel > rtol && it < maxit) {
+    if (G.is3d)
+      k_state_matvec<3><<<nbn, kThreads, 0, ctx->stream>>>(S, dKe, p, qv, pp);
+    else
+      k_state_matvec<2><<<nbn, kThreads, 0, ctx->stream>>>(S, dKe, p, qv, pp);
+    LAUNCHED();
+    k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(pp, nbn, 1, scd + 1);  // p.q
+    LAUNCHED();
+    k_cg_update_ur<<<nbd, kThreads, 0, ctx->stream>>>(n, scd, p, qv, ud, r, pp);
+    LAUNCHED();
+    k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(pp, nbd, 1, scd + 2);  // r.r
+    LAUNCHED();
+    TRY(vcycle(0));  // z = V(r)
+    k_dot<<<nbd, kThreads, 0, ctx->stream>>>(n, r, z, pp);
+    LAUNCHED();
+    k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(pp, nbd, 1, scd + 3);  // rz_new
     LAUNCHED();
     k_cg_direction<<<nbd, kThreads, 0, ctx->stream>>>(n, scd, z, p);
     LAUNCHED();

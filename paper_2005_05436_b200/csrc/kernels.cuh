@@ -1937,6 +1937,40 @@ __global__ void __launch_bounds__(kThreads) k_cg_init(long long n, const double*
   }
 }
 
+// u += a p, r -= a q (a = rz / pq); partials of r.r (PCG with an external preconditioner)
+__global__ void __launch_bounds__(kThreads) k_cg_update_ur(long long n, const double* __restrict__ sc,
+                                                           const double* __restrict__ p,
+                                                           const double* __restrict__ q,
+                                                           double* __restrict__ u,
+                                                           double* __restrict__ r,
+                                                           double* __restrict__ partials) {
+  __shared__ double scratch[32];
+  const double a = sc[0] / sc[1];
+  double red[1] = {0.0};
+  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n;
+       d += (long long)gridDim.x * blockDim.x) {
+    u[d] = fma(a, p[d], u[d]);
+    const double rv = fma(-a, q[d], r[d]);
+    r[d] = rv;
+    red[0] = fma(rv, rv, red[0]);
+  }
+  block_sum<1>(red, scratch);
+  if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
+}
+
+// block partials of a . b
+__global__ void __launch_bounds__(kThreads) k_dot(long long n, const double* __restrict__ a,
+                                                  const double* __restrict__ b,
+                                                  double* __restrict__ partials) {
+  __shared__ double scratch[32];
+  double red[1] = {0.0};
+  for (long long d = blockIdx.x * (long long)blockDim.x + threadIdx.x; d < n;
+       d += (long long)gridDim.x * blockDim.x)
+    red[0] = fma(a[d], b[d], red[0]);
+  block_sum<1>(red, scratch);
+  if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
+}
+
 __global__ void k_copy_scalar(const double* __restrict__ src, double* __restrict__ dst) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *dst = *src;
 }

@@ -40,3 +40,20 @@ def test_solve_edge_cases(P):
         assert it == 0 and np.all(u == 0)
         with pytest.raises(P.InvalidArgument):
             ctx.solve_state(sK, np.ones(cfg.n), [cfg.n])
+
+
+@pytest.mark.parametrize("cid,grid,lo", [(1, (16, 8, 0), 0.3), (1, (32, 16, 0), 0.05),
+                                         (4, (8, 4, 4), 0.3), (5, (16, 8, 8), 0.1)])
+def test_multigrid_solve_matches_reference(P, oracle_ref, cid, grid, lo, monkeypatch):
+    from paper_2005_05436_b200.configs import CONFIGS, fixed_dofs, load_vector
+    monkeypatch.setenv("TOPO_MG_MIN_DOFS", "50")  # coarsen these small grids
+    cfg = CONFIGS[cid].scaled(*grid)
+    sK = 1e-9 + np.random.default_rng(3).uniform(lo, 1.0, cfg.m) ** 3
+    f, fixed = load_vector(cfg), fixed_dofs(cfg)
+    ur = oracle_ref.solve_state(cfg.grid, cfg.nu, sK, f, fixed)
+    with P.Context(*cfg.grid, rmin=1.0, nu=cfg.nu) as ctx:
+        u, it, rr = ctx.solve_state(sK, f, fixed, rtol=1e-13, multigrid=True)
+        uj, itj, _ = ctx.solve_state(sK, f, fixed, rtol=1e-13)
+    assert rr <= 1e-13 and 0 < it < itj  # the V-cycle cuts the iteration count
+    assert np.all(u[fixed] == 0.0)
+    assert rel(u, ur) <= 1e-8, rel(u, ur)
