@@ -2098,20 +2098,19 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     MgLevel& L = lv[l];
     CK(cudaMemsetAsync(yout, 0, sizeof(double) * size_t(L.g.n), ctx->stream));
     const int nb = grid_for(ctx, std::max<long long>(1, L.g.m / 8));
+    const int nbw = grid_for(ctx, std::max<long long>(1, L.g.m / 8) * 32);  // warp per element
     for (int color = 0; color < (dim == 3 ? 8 : 8); ++color) {
       if (dim == 2 && (color & 2)) continue;  // no z parity in 2D
       if (dim == 3) {
         if (l == 0)
           k_mg_apply<3, true><<<nb, 256, 0, ctx->stream>>>(L.g, dKe, E, color, xin, yout);
         else
-          k_mg_apply<3, false><<<nb, 256, 0, ctx->stream>>>(L.g, L.K.as<double>(), nullptr, color,
-                                                            xin, yout);
+          k_mg_apply_warp<3><<<nbw, 256, 0, ctx->stream>>>(L.g, L.K.as<double>(), color, xin, yout);
       } else {
         if (l == 0)
           k_mg_apply<2, true><<<nb, 256, 0, ctx->stream>>>(L.g, dKe, E, color, xin, yout);
         else
-          k_mg_apply<2, false><<<nb, 256, 0, ctx->stream>>>(L.g, L.K.as<double>(), nullptr, color,
-                                                            xin, yout);
+          k_mg_apply_warp<2><<<nbw, 256, 0, ctx->stream>>>(L.g, L.K.as<double>(), color, xin, yout);
       }
       LAUNCHED();
     }

@@ -170,6 +170,42 @@ __global__ void __launch_bounds__(256) k_mg_apply(MgGeo L, const double* __restr
   }
 }
 
+// y += K x over the elements of one colour, stored element matrices: one
+// warp per element, lane i computes row i (the matrix column j is read by the
+// lanes contiguously), x_e broadcast by shuffles
+template <int DIM>
+__global__ void __launch_bounds__(256) k_mg_apply_warp(MgGeo L, const double* __restrict__ K, int color,
+                                                       const double* __restrict__ x,
+                                                       double* __restrict__ y) {
+  constexpr int D = MgT<DIM>::D;
+  const int lane = threadIdx.x & 31;
+  const int cx = color & 1, cz = (color >> 1) & 1, cy = (color >> 2) & 1;
+  const long long hx = (L.nelx - cx + 1) / 2, hz = (L.nz - cz + 1) / 2, hy = (L.nely - cy + 1) / 2;
+  const long long tot = hx * hz * hy;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long t = w0; t < tot; t += nw) {
+    const int ey = cy + 2 * int(t % hy);
+    const long long u = t / hy;
+    const int ez = cz + 2 * int(u % hz), ex = cx + 2 * int(u / hz);
+    const long long e = ((long long)ex * L.nz + ez) * L.nely + ey;
+    long long dof = 0;
+    double xv = 0.0;
+    if (lane < D) {
+      dof = mg_dof<DIM>(L, ex, ez, ey, lane);
+      xv = x[dof];
+    }
+    const double* Km = K + e * (long long)(D * D);
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double xj = __shfl_sync(0xffffffffu, xv, j);
+      if (lane < D) acc = fma(Km[j * D + lane], xj, acc);
+    }
+    if (lane < D) y[dof] += acc;
+  }
+}
+
 // Jacobi diagonal (fixed DOFs: 1), node-centric
 template <int DIM, bool FINE>
 __global__ void k_mg_diag(MgGeo L, const double* __restrict__ K, const double* __restrict__ E,
