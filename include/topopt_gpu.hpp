@@ -156,8 +156,9 @@ inline SymmetricSparseMatrix assemble_lower(const Eigen::VectorXd& sK, Device& d
 
 /// fea.hpp:205-239 solve_equilibrium with the modulus field instead of the
 /// assembled matrix: K(sK) u = f on the free DOFs, u = 0 on load.fixed, by
-/// the device's matrix-free Jacobi-PCG to ||r|| <= rtol ||f|| (the reference
-/// factorises; the two agree to the solver tolerance)
+/// the device's matrix-free PCG (geometric-multigrid V-cycle preconditioner,
+/// Jacobi when the grid cannot be coarsened) to ||r|| <= rtol ||f|| (the
+/// reference factorises; the two agree to the solver tolerance)
 inline Eigen::VectorXd solve_state(const Eigen::VectorXd& sK, const LoadCase& load, Device& dev,
                                    double rtol = 1e-12, int maxit = 1000000) {
   detail::need(sK.size(), dev.numElements(), "solve");
@@ -166,8 +167,8 @@ inline Eigen::VectorXd solve_state(const Eigen::VectorXd& sK, const LoadCase& lo
   Eigen::VectorXd u(dev.numDofs());
   std::int32_t it = 0;
   double rr = 0;
-  check(topo_solve_state(dev.handle(), sK.data(), load.f.data(), load.fixed.data(),
-                         std::int64_t(load.fixed.size()), rtol, maxit, u.data(), &it, &rr),
+  check(topo_solve_state_mg(dev.handle(), sK.data(), load.f.data(), load.fixed.data(),
+                            std::int64_t(load.fixed.size()), rtol, maxit, u.data(), &it, &rr),
         dev.handle());
   if (!(rr <= rtol)) throw std::runtime_error("solve: CG did not reach the tolerance");
   return u;

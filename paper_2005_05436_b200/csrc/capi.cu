@@ -2093,6 +2093,24 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     }
     LAUNCHED();
   }
+  // fine level in Walsh form when Ke allows (plain symmetric block entries)
+  DevBuf dkwb;
+  const double* dkw = nullptr;
+  if (dim == 3 && ctx->walsh) {
+    double kwp[48];
+    for (int sg = 0; sg < 8; ++sg) {
+      const double* k = ctx->kw.k[sg];  // k00, 2k01, 2k02, k11, 2k12, k22
+      const double v[6] = {k[0], 0.5 * k[1], 0.5 * k[2], k[3], 0.5 * k[4], k[5]};
+      for (int q = 0; q < 6; ++q) kwp[6 * sg + q] = v[q];
+    }
+    CK(dkwb.ensure(sizeof kwp));
+    CK(cudaMemcpy(dkwb.p, kwp, sizeof kwp, cudaMemcpyHostToDevice));
+    dkw = dkwb.as<double>();
+  }
+  struct FreeKw {
+    DevBuf* b;
+    ~FreeKw() { b->release(); }
+  } free_kw{&dkwb};
   // y = A_l x (elements by colour: no two of a colour share a node)
   auto apply = [&](size_t l, const double* xin, double* yout) -> topo_status {
     MgLevel& L = lv[l];
@@ -2102,7 +2120,9 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     for (int color = 0; color < (dim == 3 ? 8 : 8); ++color) {
       if (dim == 2 && (color & 2)) continue;  // no z parity in 2D
       if (dim == 3) {
-        if (l == 0)
+        if (l == 0 && dkw)
+          k_mg_apply_walsh<<<nb, 256, 0, ctx->stream>>>(L.g, dkw, E, color, xin, yout);
+        else if (l == 0)
           k_mg_apply<3, true><<<nb, 256, 0, ctx->stream>>>(L.g, dKe, E, color, xin, yout);
         else
           k_mg_apply_warp<3><<<nbw, 256, 0, ctx->stream>>>(L.g, L.K.as<double>(), color, xin, yout);

@@ -13,6 +13,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "kernels.cuh"
 
 namespace topo {
 
@@ -203,6 +204,85 @@ __global__ void __launch_bounds__(256) k_mg_apply_warp(MgGeo L, const double* __
       if (lane < D) acc = fma(Km[j * D + lane], xj, acc);
     }
     if (lane < D) y[dof] += acc;
+  }
+}
+
+// y += E_e Ke x_e over one colour for hexahedra in Walsh coordinates
+// (Ke = W Kt W', the blocks of k_elem_walsh): per component an 8-point
+// Walsh-Hadamard transform of x_e, the 8 signature blocks (3x3), the inverse
+// transform; 216 flops per element instead of 576. kw: per signature k00,
+// k01, k02, k11, k12, k22 (plain, not doubled).
+__global__ void __launch_bounds__(256) k_mg_apply_walsh(MgGeo L, const double* __restrict__ kw,
+                                                        const double* __restrict__ E, int color,
+                                                        const double* __restrict__ x,
+                                                        double* __restrict__ y) {
+  __shared__ double sk[48];
+  if (threadIdx.x < 48) sk[threadIdx.x] = kw[threadIdx.x];
+  __syncthreads();
+  const int cx = color & 1, cz = (color >> 1) & 1, cy = (color >> 2) & 1;
+  const long long hx = (L.nelx - cx + 1) / 2, hz = (L.nz - cz + 1) / 2, hy = (L.nely - cy + 1) / 2;
+  const long long tot = hx * hz * hy;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int ey = cy + 2 * int(t % hy);
+    const long long u = t / hy;
+    const int ez = cz + 2 * int(u % hz), ex = cx + 2 * int(u / hz);
+    const long long e = ((long long)ex * L.nz + ez) * L.nely + ey;
+    const long long n0 = ((long long)ex * L.nz1 + ez) * L.ny1 + ey;  // node (ey, ez, ex)
+    double h[3][8];  // [component][binary node index oi + 2 ok + 4 oj]
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const long long nd = n0 + (b & 1) + ((b >> 1) & 1) * L.ny1 + ((b >> 2) & 1) * L.pl;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) h[c][b] = x[3 * nd + c];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int bit = 1; bit < 8; bit <<= 1)
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          if (!(b & bit)) {
+            const double lo = h[c][b], hi = h[c][b | bit];
+            h[c][b] = hi + lo;
+            h[c][b | bit] = hi - lo;
+          }
+    const double Ee = E[e];
+#pragma unroll
+    for (int sig = 0; sig < 8; ++sig) {
+      const int i0 = sig ^ (1 << walsh_axis(0)), i1 = sig ^ (1 << walsh_axis(1)),
+                i2 = sig ^ (1 << walsh_axis(2));
+      const double m0 = h[0][i0], m1 = h[1][i1], m2 = h[2][i2];
+      const double* k = sk + 6 * sig;
+      h[0][i0] = Ee * fma(k[0], m0, fma(k[1], m1, k[2] * m2));
+      h[1][i1] = Ee * fma(k[1], m0, fma(k[3], m1, k[4] * m2));
+      h[2][i2] = Ee * fma(k[2], m0, fma(k[4], m1, k[5] * m2));
+    }
+    // W g = D B(D g): the butterfly B is W' = D H (H symmetric Sylvester,
+    // D = (-1)^popcount on the index), so the inverse needs the sign flips
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (__popc(b) & 1) h[c][b] = -h[c][b];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int bit = 1; bit < 8; bit <<= 1)
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          if (!(b & bit)) {
+            const double lo = h[c][b], hi = h[c][b | bit];
+            h[c][b] = hi + lo;
+            h[c][b | bit] = hi - lo;
+          }
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const long long nd = n0 + (b & 1) + ((b >> 1) & 1) * L.ny1 + ((b >> 2) & 1) * L.pl;
+      const double sg = (__popc(b) & 1) ? -1.0 : 1.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) y[3 * nd + c] += sg * h[c][b];
+    }
   }
 }
 
