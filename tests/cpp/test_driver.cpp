@@ -5,6 +5,7 @@
 // device iterates CG to 1e-12, so histories agree to ~1e-9, not bitwise.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "topopt/driver.hpp"
@@ -40,7 +41,24 @@ static void compare(const char* name, const RunConfig& cfg, const Problem& prob)
   expect(same && dx <= 1e-6, what, dx);
 }
 
+// --bench nelx nely nelz maxit: the device loop alone on the 3D cantilever
+// preset (top3D125 defaults: ft = 3, rmin = 1.5), per-iteration records
+static int bench(int nelx, int nely, int nelz, int maxit) {
+  RunConfig cfg;
+  cfg.nelx = nelx, cfg.nely = nely, cfg.nelz = nelz, cfg.maxit = maxit;
+  cfg.ft = 3, cfg.rmin = 1.5, cfg.volfrac = 0.12, cfg.move = 0.1;
+  const RunResult g = gpu::run_optimization(
+      cfg, preset_cantilever_3d(nelx, nely, nelz), [](const IterationRecord& r) {
+        std::printf("it %3d  c %.6e  v %.4f  ch %.3e  eta %.6f  bis %3d  %.3f s\n", r.loop, r.c,
+                    r.v, r.resnorm, r.eta, r.bisections, r.seconds);
+      }, {}, 1e-6);
+  std::printf("total %.2f s for %zu iterations\n", g.wallSeconds, g.history.size());
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc == 6 && std::string(argv[1]) == "--bench")
+    return bench(std::atoi(argv[2]), std::atoi(argv[3]), std::atoi(argv[4]), std::atoi(argv[5]));
   const bool frame = argc > 1 && std::string(argv[1]) == "--frame";  // slow: dense shim Cholesky
   {  // ft = 3 volume-preserving projection, MBB (top99neo defaults)
     RunConfig cfg;
