@@ -254,6 +254,14 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
                                 const int32_t* fixed, int64_t nfixed, double rtol, int32_t maxit,
                                 double* u, int32_t* iterations, double* relres);
 
+/* y = K(sK) x, the matrix-free stiffness operator of the solves (no fixed
+ * DOFs; K = sum_e sK_e Ke over the grid, fea.hpp:162-174 assembled in full).
+ * variant 0: the solver's default (one-launch Walsh-form node tiles for H8,
+ * else the node-centric gather); 1: per-colour element launches (H8, Walsh);
+ * 2: node-centric gather with the dense Ke. 0 and 1 are bitwise equal. */
+topo_status topo_apply_stiffness(topo_ctx* ctx, const double* sK, const double* x, double* y,
+                                 int32_t variant);
+
 /* ---- fused pass: driver.hpp:183-231 (ft = 3) minus the state solve ------ */
 topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
                              const topo_pass_params* prm, topo_pass_out* out);

@@ -30,7 +30,7 @@ EXPORTS = [
     "topo_set_timing", "topo_stage_times", "topo_host_oc_replay", "topo_host_eta_replay",
     "topo_nccl_unique_id", "topo_comm_init_host", "topo_slab_plan", "topo_fp64_peak",
     "topo_csc_pattern", "topo_csc_values", "topo_csc_set_fixed", "topo_oc_primal_dual",
-    "topo_solve_state", "topo_solve_state_mg",
+    "topo_solve_state", "topo_solve_state_mg", "topo_apply_stiffness",
 ]
 STAGES = ["filter", "eta", "elem", "adjoint", "oc", "sk_store", "pass"]
 
@@ -138,6 +138,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
                                        vp]),
         "topo_solve_state_mg": (C.c_int, [vp, vp, vp, vp, C.c_int64, C.c_double, C.c_int32, vp,
                                           vp, vp]),
+        "topo_apply_stiffness": (C.c_int, [vp, vp, vp, vp, C.c_int32]),
         "topo_host_oc_replay": (C.c_int, [p(OcParams), C.c_double, SFUN, vp, C.c_int,
                                           p(C.c_double), p(C.c_int32), p(C.c_int32),
                                           p(C.c_double), p(C.c_int32)]),

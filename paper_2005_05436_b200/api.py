@@ -567,6 +567,14 @@ class Context:
                        C.byref(it), C.byref(rr)))
         return out, it.value, rr.value
 
+    def apply_stiffness(self, sK, x, variant: int = 0):
+        """y = K(sK) x, the solves' matrix-free operator (no fixed DOFs)."""
+        sa = _Arr(sK, n=self.m, name="apply: sK")
+        xa = _Arr(x, n=self.n, name="apply: x")
+        out, ptr = _empty(self.n, xa.device)
+        self._check(self.lib.topo_apply_stiffness(self.h, sa.ptr, xa.ptr, ptr, variant))
+        return out
+
     # driver.hpp:183-231
     def design_pass(self, x, U, *, beta: float = 2.0, eta0: float = 0.5, move: float = 0.2,
                     volfrac: float = 0.5, simp: SimpParams = SimpParams(),

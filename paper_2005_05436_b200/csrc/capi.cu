@@ -102,6 +102,7 @@ struct topo_ctx {
   DevBuf hs, hs_st, cw, x_st, xt, xphys, dcphys, dc, dV, xnew, a1_st, a2_st, rec, u, tmp0, tmp1,
       tmp_st;
   DevBuf sK, iK, jK;
+  DevBuf d_kwp;  // Walsh blocks, plain (k00 k01 k02 k11 k12 k22 per signature), for k_mg_apply_tile
   DevBuf partials, partials0, result;
   double* h_result = nullptr;  // pinned
   int conv_R = 8;              // outputs per thread along the run axis
@@ -1831,6 +1832,138 @@ topo_status topo_oc_primal_dual(topo_ctx* ctx, const double* x, const double* dc
 // fixed ones. Matrix-free Jacobi-preconditioned CG (the reference factorises;
 // the solutions agree to the solver tolerance). One host read of r.r per
 // iteration for the stopping test; every reduction in a fixed order.
+// One-launch H8 operator y = K x in Walsh form (k_mg_apply_tile), used for the
+// fine multigrid level and the CG matvec when Ke has the Walsh-block form.
+// Tiles of kTY x kTZ nodes; the x extent is split so the grid fills ~2 waves of
+// 2 blocks per SM, with chunks of >= 8 node layers (each chunk recomputes one
+// element layer).
+static bool use_tile_op(const topo_ctx* ctx) {
+  static const char* e = getenv("TOPO_MG_TILE");
+  return ctx->G.is3d && ctx->walsh && !(e && e[0] == '0');
+}
+
+static int tile_blocks(const topo_ctx* ctx, const MgGeo& L, int* xchunk) {
+  const int nyz = tile_ny(L) * tile_nz(L), nx1 = L.nelx + 1;
+  const int target = 4 * ctx->sm_count;
+  int chunks = std::max(1, (target + nyz - 1) / nyz);
+  chunks = std::min(chunks, std::max(1, nx1 / 8));
+  *xchunk = (nx1 + chunks - 1) / chunks;
+  return nyz * ((nx1 + *xchunk - 1) / *xchunk);
+}
+
+static topo_status launch_tile_op(topo_ctx* ctx, const MgGeo& L, const double* E, const double* x,
+                                  double* y, double* partials, int* nblocks = nullptr,
+                                  bool c1 = false) {
+  static bool attr = false;
+  if (!attr) {
+    for (const void* f : {(const void*)k_mg_apply_tile<false>, (const void*)k_mg_apply_tile<true>,
+                          (const void*)k_mg_apply_tile<false, true>})
+      CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
+    attr = true;
+  }
+  if (!ctx->d_kwp.p) {
+    double kwp[48];
+    for (int sg = 0; sg < 8; ++sg) {
+      const double* k = ctx->kw.k[sg];  // k00, 2k01, 2k02, k11, 2k12, k22
+      const double v[6] = {k[0], 0.5 * k[1], 0.5 * k[2], k[3], 0.5 * k[4], k[5]};
+      for (int q = 0; q < 6; ++q) kwp[6 * sg + q] = v[q];
+    }
+    CK(ctx->d_kwp.ensure(sizeof kwp));
+    CK(cudaMemcpy(ctx->d_kwp.p, kwp, sizeof kwp, cudaMemcpyHostToDevice));
+  }
+  int xc = 0;
+  const int nb = tile_blocks(ctx, L, &xc);
+  if (nblocks) *nblocks = nb;
+  if (c1)
+    k_mg_apply_tile<false, true><<<nb, 256, kTileSmem, ctx->stream>>>(
+        L, ctx->d_kwp.as<double>(), E, x, y, xc, nullptr);
+  else if (partials)
+    k_mg_apply_tile<true><<<nb, 256, kTileSmem, ctx->stream>>>(L, ctx->d_kwp.as<double>(), E, x,
+                                                               y, xc, partials);
+  else
+    k_mg_apply_tile<false><<<nb, 256, kTileSmem, ctx->stream>>>(L, ctx->d_kwp.as<double>(), E, x,
+                                                                y, xc, nullptr);
+  LAUNCHED();
+  return TOPO_OK;
+}
+
+static MgGeo state_mg_geo(const StateGeo& S, long long m) {
+  MgGeo g{};
+  g.nelx = S.nelx;
+  g.nely = S.nely;
+  g.nz = S.nz;
+  g.nz1 = S.nz1;
+  g.ny1 = S.ny1;
+  g.pl = S.pl;
+  g.nn = S.nn;
+  g.n = S.dim * S.nn;
+  g.m = m;
+  g.fixed = S.fixed;
+  return g;
+}
+
+topo_status topo_apply_stiffness(topo_ctx* ctx, const double* sK, const double* x, double* y,
+                                 int32_t variant) {
+  if (!ctx) return TOPO_EINVAL;
+  if (ctx->nranks > 1) return fail(ctx, TOPO_EINVAL, "apply: single-rank contexts only");
+  if (variant < 0 || variant > 2) return fail(ctx, TOPO_EINVAL, "apply: variant must be 0, 1 or 2");
+  if (variant == 1 && !(ctx->G.is3d && ctx->walsh))
+    return fail(ctx, TOPO_EINVAL, "apply: the colour variant needs the Walsh-block H8 form");
+  ctx->launches = 0;
+  const Geo& G = ctx->G;
+  const long long n = ctx->n;
+  const double *E, *xd;
+  TRY(stage_in(ctx, sK, G.m, ctx->tmp0, &E));
+  DevBuf xb, yb, mask, part;
+  struct Release {
+    std::initializer_list<DevBuf*> bufs;
+    ~Release() {
+      for (DevBuf* b : bufs) b->release();
+    }
+  } release_scratch{{&xb, &yb, &mask, &part}};
+  TRY(stage_in(ctx, x, n, xb, &xd));
+  bool hy;
+  double* yd = out_ptr(ctx, y, yb, n, &hy);
+  if (!yd) return fail(ctx, TOPO_ECUDA, "apply: cannot allocate the output");
+  CK(mask.ensure(size_t(n)));
+  CK(cudaMemsetAsync(mask.p, 0, size_t(n), ctx->stream));
+  StateGeo S;
+  S.dim = G.dim;
+  S.nelx = G.nelx;
+  S.nely = G.nely;
+  S.nz = G.is3d ? G.nelz : 1;
+  S.nz1 = G.is3d ? G.nelz + 1 : 1;
+  S.ny1 = G.nely + 1;
+  S.pl = S.ny1 * S.nz1;
+  S.nn = n / G.dim;
+  S.E = E;
+  S.fixed = mask.as<unsigned char>();
+  const MgGeo L0 = state_mg_geo(S, G.m);
+  const int nbn = grid_for(ctx, S.nn);
+  CK(part.ensure(sizeof(double) * size_t(std::max(nbn, 1 << 16))));
+  if (variant == 0 && use_tile_op(ctx)) {
+    TRY(launch_tile_op(ctx, L0, E, xd, yd, nullptr));
+  } else if (variant == 1) {
+    TRY(launch_tile_op(ctx, L0, E, xd, yd, nullptr));  // (builds d_kwp)
+    CK(cudaMemsetAsync(yd, 0, sizeof(double) * size_t(n), ctx->stream));
+    const int nb = grid_for(ctx, std::max<long long>(1, G.m / 8));
+    for (int color = 0; color < 8; ++color) {
+      k_mg_apply_walsh<<<nb, 256, 0, ctx->stream>>>(L0, ctx->d_kwp.as<double>(), E, color, xd, yd);
+      LAUNCHED();
+    }
+  } else {
+    const double* ke = ctx->d_ke_full.as<double>();
+    if (G.is3d)
+      k_state_matvec<3><<<nbn, kThreads, 0, ctx->stream>>>(S, ke, xd, yd, part.as<double>());
+    else
+      k_state_matvec<2><<<nbn, kThreads, 0, ctx->stream>>>(S, ke, xd, yd, part.as<double>());
+    LAUNCHED();
+  }
+  TRY(finish_out(ctx, y, yd, n, hy));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
 topo_status topo_solve_state(topo_ctx* ctx, const double* sK, const double* f,
                              const int32_t* fixed, int64_t nfixed, double rtol, int32_t maxit,
                              double* u, int32_t* iterations, double* relres) {
@@ -1872,8 +2005,13 @@ topo_status topo_solve_state(topo_ctx* ctx, const double* sK, const double* f,
   S.nn = n / G.dim;
   S.E = E;
   S.fixed = mask.as<unsigned char>();
-  const int nbn = grid_for(ctx, S.nn), nbd = grid_for(ctx, n);
-  CK(part.ensure(sizeof(double) * 2 * size_t(std::max(nbn, nbd))));
+  int nbn = grid_for(ctx, S.nn);
+  const int nbd = grid_for(ctx, n);
+  const bool tile = use_tile_op(ctx);
+  const MgGeo L0 = state_mg_geo(S, G.m);
+  int xc = 0;
+  const int nbt = tile ? tile_blocks(ctx, L0, &xc) : 0;
+  CK(part.ensure(sizeof(double) * 2 * size_t(std::max({nbn, nbd, nbt}))));
   CK(sc.ensure(sizeof(double) * 8));
   double* scd = sc.as<double>();
   double* pp = part.as<double>();
@@ -1896,11 +2034,15 @@ topo_status topo_solve_state(topo_ctx* ctx, const double* sK, const double* f,
   double rel = ff > 0 ? 1.0 : 0.0;
   int it = 0;
   while (ff > 0 && rel > rtol && it < maxit) {
-    if (G.is3d)
-      k_state_matvec<3><<<nbn, kThreads, 0, ctx->stream>>>(S, ke, p, qv, pp);
-    else
-      k_state_matvec<2><<<nbn, kThreads, 0, ctx->stream>>>(S, ke, p, qv, pp);
-    LAUNCHED();
+    if (tile) {
+      TRY(launch_tile_op(ctx, L0, E, p, qv, pp, &nbn));
+    } else {
+      if (G.is3d)
+        k_state_matvec<3><<<nbn, kThreads, 0, ctx->stream>>>(S, ke, p, qv, pp);
+      else
+        k_state_matvec<2><<<nbn, kThreads, 0, ctx->stream>>>(S, ke, p, qv, pp);
+      LAUNCHED();
+    }
     k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(pp, nbn, 1, scd + 1);
     LAUNCHED();
     k_cg_update<<<nbd, kThreads, 0, ctx->stream>>>(n, scd, p, qv, diag, ud, r, z, pp);
@@ -2040,6 +2182,14 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   CK(cudaMemcpyAsync(dQ.p, Q.data(), sizeof(double) * Q.size(), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaMemcpyAsync(dKp.p, Kp.data(), sizeof(double) * Kp.size(), cudaMemcpyHostToDevice,
                      ctx->stream));
+  // stored levels use node-centric kernels (one launch per apply / sweep /
+  // residual); level 1 is applied on the fly from the fine moduli (H8 Walsh
+  // form, k_mg_apply_tile<C1>) when a stored level 2 follows it
+  static const char* mgn = getenv("TOPO_MG_NODE");
+  const bool node_ops = !(mgn && mgn[0] == '0');
+  static const char* mf1e = getenv("TOPO_MG_MF1");
+  const bool mf1 = dim == 3 && ctx->walsh && use_tile_op(ctx) && node_ops && lv.size() >= 3 &&
+                   !(mf1e && mf1e[0] == '0');
   // per-level storage, fixed masks, Galerkin matrices, diagonals
   for (size_t l = 0; l < lv.size(); ++l) {
     MgLevel& L = lv[l];
@@ -2050,13 +2200,18 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
       CK(cudaMemcpyAsync(L.fixed.p, fx.data(), size_t(n), cudaMemcpyHostToDevice, ctx->stream));
       continue;
     }
-    CK(L.K.ensure(sizeof(double) * size_t(L.g.m) * DD));
+    if (!(mf1 && l == 1)) CK(L.K.ensure(sizeof(double) * size_t(L.g.m) * DD));
     const MgLevel& F = lv[l - 1];
     const int nbn = grid_for(ctx, L.g.nn);
     if (dim == 3) {
       k_mg_fixed<3><<<nbn, kThreads, 0, ctx->stream>>>(L.g, F.g, F.fixed.as<unsigned char>(),
                                                        L.fixed.as<unsigned char>());
-      if (l == 1)
+      if (mf1 && l == 1) {
+        // (no stored matrices)
+      } else if (mf1 && l == 2)
+        k_mg_galerkin<3, true><<<int(std::min<long long>(L.g.m, 1LL << 20)), 256, 0, ctx->stream>>>(
+            L.g, F.g, E, dQ.as<double>(), L.K.as<double>(), dKp.as<double>());
+      else if (l == 1)
         k_mg_galerkin1<3><<<grid_for(ctx, L.g.m * DD), kThreads, 0, ctx->stream>>>(
             L.g, F.g, E, dKp.as<double>(), L.K.as<double>());
       else
@@ -2081,6 +2236,9 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     if (dim == 3) {
       if (l == 0)
         k_mg_diag<3, true><<<nbn, kThreads, 0, ctx->stream>>>(L.g, dKe, E, L.diag.as<double>());
+      else if (mf1 && l == 1)
+        k_mg_diag_c1<3><<<nbn, kThreads, 0, ctx->stream>>>(L.g, dKp.as<double>(), E,
+                                                           L.diag.as<double>());
       else
         k_mg_diag<3, false><<<nbn, kThreads, 0, ctx->stream>>>(L.g, L.K.as<double>(), nullptr,
                                                                L.diag.as<double>());
@@ -2112,8 +2270,26 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     ~FreeKw() { b->release(); }
   } free_kw{&dkwb};
   // y = A_l x (elements by colour: no two of a colour share a node)
+  auto node_op = [&](size_t l, int mode, const double* xin, double* yout) -> topo_status {
+    MgLevel& L = lv[l];
+    const int nbn = grid_for(ctx, L.g.nn);
+    const double *K = L.K.as<double>(), *b = L.b.as<double>(), *dg = L.diag.as<double>();
+    const double w = L.omega;
+#define MG_NODE(D, M) k_mg_node<D, M><<<nbn, 256, 0, ctx->stream>>>(L.g, K, xin, b, dg, w, yout)
+    if (dim == 3) {
+      if (mode == 0) MG_NODE(3, 0); else if (mode == 1) MG_NODE(3, 1); else MG_NODE(3, 2);
+    } else {
+      if (mode == 0) MG_NODE(2, 0); else if (mode == 1) MG_NODE(2, 1); else MG_NODE(2, 2);
+    }
+#undef MG_NODE
+    LAUNCHED();
+    return TOPO_OK;
+  };
   auto apply = [&](size_t l, const double* xin, double* yout) -> topo_status {
     MgLevel& L = lv[l];
+    if (l == 0 && dkw && use_tile_op(ctx)) return launch_tile_op(ctx, L.g, E, xin, yout, nullptr);
+    if (l == 1 && mf1) return launch_tile_op(ctx, L.g, E, xin, yout, nullptr, nullptr, true);
+    if (l > 0 && node_ops) return node_op(l, 0, xin, yout);
     CK(cudaMemsetAsync(yout, 0, sizeof(double) * size_t(L.g.n), ctx->stream));
     const int nb = grid_for(ctx, std::max<long long>(1, L.g.m / 8));
     const int nbw = grid_for(ctx, std::max<long long>(1, L.g.m / 8) * 32);  // warp per element
@@ -2169,29 +2345,64 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     L.omega = 1.2 / std::max(lam, 1e-30);
   }
   const int nu = 2, ncoarse = 40;
+  int coarse_grid = 0;  // resident blocks of the cooperative coarsest-level kernel
+  {
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &occ, dim == 3 ? (const void*)k_mg_coarse_sweeps<3> : (const void*)k_mg_coarse_sweeps<2>,
+        256, 0));
+    coarse_grid = std::max(1, occ) * ctx->sm_count;
+  }
   // V-cycle: lv[l].x <- approx A_l^{-1} lv[l].b
   std::function<topo_status(size_t)> vcycle = [&](size_t l) -> topo_status {
     MgLevel& L = lv[l];
     const long long nl = L.g.n;
     const int nbd = grid_for(ctx, nl);
     const unsigned char* fm = L.fixed.as<unsigned char>();
-    double *x = L.x.as<double>(), *b = L.b.as<double>(), *y = L.y.as<double>(),
-           *dg = L.diag.as<double>();
     const bool last = l + 1 == lv.size();
     const int sweeps = last ? ncoarse : nu;
     const double w = L.omega;
-    k_mg_jacobi<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, b, nullptr, dg, w, x);
+    const bool nodes = l > 0 && node_ops && !(l == 1 && mf1);
+    if (nodes && last) {  // coarsest level: all sweeps in one cooperative launch
+      const int nbn = std::max(1, std::min(grid_for(ctx, L.g.n), coarse_grid));
+      MgGeo g = L.g;
+      const double *K = L.K.as<double>(), *b = L.b.as<double>(), *dg = L.diag.as<double>();
+      double *x = L.x.as<double>(), *y = L.y.as<double>();
+      int sw = sweeps;
+      void* args[] = {&g, &K, &b, &dg, (void*)&w, &x, &y, &sw};
+      CK(cudaLaunchCooperativeKernel(dim == 3 ? (const void*)k_mg_coarse_sweeps<3>
+                                              : (const void*)k_mg_coarse_sweeps<2>,
+                                     nbn, 256, args, 0, ctx->stream));
+      LAUNCHED();
+      return TOPO_OK;
+    }
+    // one damped-Jacobi sweep from x (node kernels: into y, then the buffers swap)
+    auto sweep = [&]() -> topo_status {
+      if (nodes) {
+        TRY(node_op(l, 1, L.x.as<double>(), L.y.as<double>()));
+        std::swap(L.x.p, L.y.p);
+        return TOPO_OK;
+      }
+      TRY(apply(l, L.x.as<double>(), L.y.as<double>()));
+      k_mg_jacobi<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, L.b.as<double>(), L.y.as<double>(),
+                                                      L.diag.as<double>(), w, L.x.as<double>());
+      LAUNCHED();
+      return TOPO_OK;
+    };
+    k_mg_jacobi<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, L.b.as<double>(), nullptr,
+                                                    L.diag.as<double>(), w, L.x.as<double>());
     LAUNCHED();
-    for (int s2 = 1; s2 < sweeps; ++s2) {
-      TRY(apply(l, x, y));
-      k_mg_jacobi<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, b, y, dg, w, x);
+    for (int s2 = 1; s2 < sweeps; ++s2) TRY(sweep());
+    if (last) return TOPO_OK;
+    if (nodes) {
+      TRY(node_op(l, 2, L.x.as<double>(), L.r.as<double>()));
+    } else {
+      TRY(apply(l, L.x.as<double>(), L.y.as<double>()));
+      k_mg_residual<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, L.b.as<double>(),
+                                                        L.y.as<double>(), L.r.as<double>());
       LAUNCHED();
     }
-    if (last) return TOPO_OK;
     MgLevel& Cl = lv[l + 1];
-    TRY(apply(l, x, y));
-    k_mg_residual<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, b, y, L.r.as<double>());
-    LAUNCHED();
     const int nbc = grid_for(ctx, Cl.g.nn), nbf = grid_for(ctx, L.g.nn);
     if (dim == 3)
       k_mg_restrict<3><<<nbc, kThreads, 0, ctx->stream>>>(Cl.g, L.g, L.r.as<double>(), Cl.b.as<double>());
@@ -2200,15 +2411,13 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     LAUNCHED();
     TRY(vcycle(l + 1));
     if (dim == 3)
-      k_mg_prolong_add<3><<<nbf, kThreads, 0, ctx->stream>>>(Cl.g, L.g, Cl.x.as<double>(), x);
+      k_mg_prolong_add<3><<<nbf, kThreads, 0, ctx->stream>>>(Cl.g, L.g, Cl.x.as<double>(),
+                                                              L.x.as<double>());
     else
-      k_mg_prolong_add<2><<<nbf, kThreads, 0, ctx->stream>>>(Cl.g, L.g, Cl.x.as<double>(), x);
+      k_mg_prolong_add<2><<<nbf, kThreads, 0, ctx->stream>>>(Cl.g, L.g, Cl.x.as<double>(),
+                                                              L.x.as<double>());
     LAUNCHED();
-    for (int s2 = 0; s2 < nu; ++s2) {
-      TRY(apply(l, x, y));
-      k_mg_jacobi<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, b, y, dg, w, x);
-      LAUNCHED();
-    }
+    for (int s2 = 0; s2 < nu; ++s2) TRY(sweep());
     return TOPO_OK;
   };
   // PCG: r = f (0 on fixed), z = V(r), p = z
@@ -2223,12 +2432,17 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   S.nn = n / dim;
   S.E = E;
   S.fixed = lv[0].fixed.as<unsigned char>();
-  const int nbn = grid_for(ctx, S.nn), nbd = grid_for(ctx, n);
+  int nbn = grid_for(ctx, S.nn);
+  const int nbd = grid_for(ctx, n);
+  const bool tile = use_tile_op(ctx);
+  const MgGeo L0 = state_mg_geo(S, G.m);
+  int xc = 0;
+  const int nbt = tile ? tile_blocks(ctx, L0, &xc) : 0;
   CK(cg.ensure(sizeof(double) * size_t(n) * 3));
   double *ud = cg.as<double>(), *p = ud + n, *qv = p + n;
   double* r = lv[0].b.as<double>();  // the V-cycle reads its right-hand side from level 0's b
   double* z = lv[0].x.as<double>();
-  CK(part.ensure(sizeof(double) * 2 * size_t(std::max(nbn, nbd))));
+  CK(part.ensure(sizeof(double) * 2 * size_t(std::max({nbn, nbd, nbt}))));
   CK(sc.ensure(sizeof(double) * 8));
   double* scd = sc.as<double>();
   double* pp = part.as<double>();
@@ -2250,11 +2464,15 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   double rel = ff > 0 ? 1.0 : 0.0;
   int it = 0;
   while (ff > 0 && rel > rtol && it < maxit) {
-    if (G.is3d)
-      k_state_matvec<3><<<nbn, kThreads, 0, ctx->stream>>>(S, dKe, p, qv, pp);
-    else
-      k_state_matvec<2><<<nbn, kThreads, 0, ctx->stream>>>(S, dKe, p, qv, pp);
-    LAUNCHED();
+    if (tile) {
+      TRY(launch_tile_op(ctx, L0, E, p, qv, pp, &nbn));
+    } else {
+      if (G.is3d)
+        k_state_matvec<3><<<nbn, kThreads, 0, ctx->stream>>>(S, dKe, p, qv, pp);
+      else
+        k_state_matvec<2><<<nbn, kThreads, 0, ctx->stream>>>(S, dKe, p, qv, pp);
+      LAUNCHED();
+    }
     k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(pp, nbn, 1, scd + 1);  // p.q
     LAUNCHED();
     k_cg_update_ur<<<nbd, kThreads, 0, ctx->stream>>>(n, scd, p, qv, ud, r, pp);

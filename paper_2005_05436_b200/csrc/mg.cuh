@@ -68,7 +68,8 @@ __global__ void k_mg_galerkin1(MgGeo C, MgGeo F, const double* __restrict__ E,
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
        t += (long long)gridDim.x * blockDim.x) {
     const long long e = t / DD;
-    const int q = int(t - e * DD);
+    int q = int(t - e * DD);
+    if (q % D < q / D) q = (q % D) * D + q / D;  // exactly symmetric: (i < j) takes (j, i)
     int ex, ez, ey;
     mg_elem(C, e, ex, ez, ey);
     double acc = 0.0;
@@ -84,10 +85,13 @@ __global__ void k_mg_galerkin1(MgGeo C, MgGeo F, const double* __restrict__ E,
 }
 
 // Kc[e] = sum_p Qp' Kf[child p] Qp (levels >= 2); one block per coarse element
-template <int DIM>
+// FROM_E: the children's matrices are level-1 Galerkin matrices built on the
+// fly, K_child = sum_p' E(grandchild p') Kp[p'] (Kf = fine E, Kp: the 8 Qp' Ke Qp)
+template <int DIM, bool FROM_E = false>
 __global__ void __launch_bounds__(256) k_mg_galerkin(MgGeo C, MgGeo F, const double* __restrict__ Kf,
                                                      const double* __restrict__ Q,
-                                                     double* __restrict__ Kc) {
+                                                     double* __restrict__ Kc,
+                                                     const double* __restrict__ Kp = nullptr) {
   constexpr int NN = MgT<DIM>::NN, D = MgT<DIM>::D, DD = D * D;
   __shared__ double sK[DD], sT[DD], sQ[DD];
   for (long long e = blockIdx.x; e < C.m; e += gridDim.x) {
@@ -102,7 +106,24 @@ __global__ void __launch_bounds__(256) k_mg_galerkin(MgGeo C, MgGeo F, const dou
       const long long ef = ((long long)(2 * ex + pj) * F.nz + (2 * ez + pk)) * F.nely + (2 * ey + pi);
       __syncthreads();
       for (int q = threadIdx.x; q < DD; q += blockDim.x) {
-        sK[q] = Kf[ef * DD + q];
+        if (FROM_E) {
+          // child ef = (fx, fz, fy) of level F; its children on the finest grid
+          const int fy = 2 * ey + pi, fz = 2 * ez + pk, fx = 2 * ex + pj;
+          const int qs = q % D < q / D ? (q % D) * D + q / D : q;  // symmetric (as galerkin1)
+          double acc1 = 0.0;
+#pragma unroll
+          for (int p2 = 0; p2 < NN; ++p2) {
+            int qi, qk, qj;
+            mg_offsets(p2, qi, qk, qj);
+            const long long eg =
+                ((long long)(2 * fx + qj) * (DIM == 3 ? 2 * F.nz : 1) + (DIM == 3 ? 2 * fz + qk : 0)) *
+                    (2 * F.nely) + (2 * fy + qi);
+            acc1 = fma(Kf[eg], Kp[p2 * DD + qs], acc1);
+          }
+          sK[q] = acc1;
+        } else {
+          sK[q] = Kf[ef * DD + q];
+        }
         sQ[q] = Q[p * DD + q];
       }
       __syncthreads();
@@ -123,12 +144,18 @@ __global__ void __launch_bounds__(256) k_mg_galerkin(MgGeo C, MgGeo F, const dou
         acc[r] += s;
       }
     }
+    // stored exactly symmetric: entry (i, j) with i < j takes (j, i)'s value
+    __syncthreads();
 #pragma unroll
     for (int r = 0; r < (DD + 255) / 256; ++r) {
       const int q = threadIdx.x + 256 * r;
-      if (q < DD) Kc[e * DD + q] = acc[r];
+      if (q < DD) sT[q] = acc[r];
     }
     __syncthreads();
+    for (int q = threadIdx.x; q < DD; q += blockDim.x) {
+      const int i = q % D, j = q / D;
+      Kc[e * DD + q] = i >= j ? sT[q] : sT[i * D + j];
+    }
   }
 }
 
@@ -207,11 +234,60 @@ __global__ void __launch_bounds__(256) k_mg_apply_warp(MgGeo L, const double* __
   }
 }
 
-// y += E_e Ke x_e over one colour for hexahedra in Walsh coordinates
-// (Ke = W Kt W', the blocks of k_elem_walsh): per component an 8-point
-// Walsh-Hadamard transform of x_e, the 8 signature blocks (3x3), the inverse
-// transform; 216 flops per element instead of 576. kw: per signature k00,
+// E_e Ke x_e for one hexahedron in Walsh coordinates (Ke = W Kt W', the
+// blocks of k_elem_walsh): per component an 8-point Walsh-Hadamard transform
+// of x_e, the 8 signature blocks (3x3), the inverse transform; 216 flops per
+// element instead of 576. h holds x_e on entry ([component][binary node index
+// oi + 2 ok + 4 oj]) and the element's output on exit. sk: per signature k00,
 // k01, k02, k11, k12, k22 (plain, not doubled).
+__device__ __forceinline__ void walsh_elem_apply(const double* sk, double Ee, double (&h)[3][8]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int bit = 1; bit < 8; bit <<= 1)
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (!(b & bit)) {
+          const double lo = h[c][b], hi = h[c][b | bit];
+          h[c][b] = hi + lo;
+          h[c][b | bit] = hi - lo;
+        }
+#pragma unroll
+  for (int sig = 0; sig < 8; ++sig) {
+    const int i0 = sig ^ (1 << walsh_axis(0)), i1 = sig ^ (1 << walsh_axis(1)),
+              i2 = sig ^ (1 << walsh_axis(2));
+    const double m0 = h[0][i0], m1 = h[1][i1], m2 = h[2][i2];
+    const double* k = sk + 6 * sig;
+    h[0][i0] = Ee * fma(k[0], m0, fma(k[1], m1, k[2] * m2));
+    h[1][i1] = Ee * fma(k[1], m0, fma(k[3], m1, k[4] * m2));
+    h[2][i2] = Ee * fma(k[2], m0, fma(k[4], m1, k[5] * m2));
+  }
+  // W g = D B(D g): the butterfly B is W' = D H (H symmetric Sylvester,
+  // D = (-1)^popcount on the index), so the inverse needs the sign flips
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (__popc(b) & 1) h[c][b] = -h[c][b];
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int bit = 1; bit < 8; bit <<= 1)
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (!(b & bit)) {
+          const double lo = h[c][b], hi = h[c][b | bit];
+          h[c][b] = hi + lo;
+          h[c][b | bit] = hi - lo;
+        }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (__popc(b) & 1) h[c][b] = -h[c][b];
+}
+
+// y += E_e Ke x_e over one colour for hexahedra in Walsh coordinates
 __global__ void __launch_bounds__(256) k_mg_apply_walsh(MgGeo L, const double* __restrict__ kw,
                                                         const double* __restrict__ E, int color,
                                                         const double* __restrict__ x,
@@ -236,52 +312,394 @@ __global__ void __launch_bounds__(256) k_mg_apply_walsh(MgGeo L, const double* _
 #pragma unroll
       for (int c = 0; c < 3; ++c) h[c][b] = x[3 * nd + c];
     }
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int bit = 1; bit < 8; bit <<= 1)
-#pragma unroll
-        for (int b = 0; b < 8; ++b)
-          if (!(b & bit)) {
-            const double lo = h[c][b], hi = h[c][b | bit];
-            h[c][b] = hi + lo;
-            h[c][b | bit] = hi - lo;
-          }
-    const double Ee = E[e];
-#pragma unroll
-    for (int sig = 0; sig < 8; ++sig) {
-      const int i0 = sig ^ (1 << walsh_axis(0)), i1 = sig ^ (1 << walsh_axis(1)),
-                i2 = sig ^ (1 << walsh_axis(2));
-      const double m0 = h[0][i0], m1 = h[1][i1], m2 = h[2][i2];
-      const double* k = sk + 6 * sig;
-      h[0][i0] = Ee * fma(k[0], m0, fma(k[1], m1, k[2] * m2));
-      h[1][i1] = Ee * fma(k[1], m0, fma(k[3], m1, k[4] * m2));
-      h[2][i2] = Ee * fma(k[2], m0, fma(k[4], m1, k[5] * m2));
-    }
-    // W g = D B(D g): the butterfly B is W' = D H (H symmetric Sylvester,
-    // D = (-1)^popcount on the index), so the inverse needs the sign flips
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int b = 0; b < 8; ++b)
-        if (__popc(b) & 1) h[c][b] = -h[c][b];
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-      for (int bit = 1; bit < 8; bit <<= 1)
-#pragma unroll
-        for (int b = 0; b < 8; ++b)
-          if (!(b & bit)) {
-            const double lo = h[c][b], hi = h[c][b | bit];
-            h[c][b] = hi + lo;
-            h[c][b | bit] = hi - lo;
-          }
+    walsh_elem_apply(sk, E[e], h);
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
       const long long nd = n0 + (b & 1) + ((b >> 1) & 1) * L.ny1 + ((b >> 2) & 1) * L.pl;
-      const double sg = (__popc(b) & 1) ? -1.0 : 1.0;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) y[3 * nd + c] += sg * h[c][b];
+      for (int c = 0; c < 3; ++c) y[3 * nd + c] += h[c][b];
+    }
+  }
+}
+
+// y = K x for hexahedra in Walsh form, one launch, node-centric output: a block
+// owns a tile of kTY x kTZ nodes in (y, z) and marches along x over a range
+// of node layers. Per step it stages the next node layer of x in shared
+// memory, computes one element layer (kTY+1 x kTZ+1 = 256 elements, one per
+// thread), keeps the element outputs in shared memory, and gathers node layer
+// ex from the element layers ex - 1 and ex. Every node sums its (up to) 8
+// element contributions in colour order, exactly as the 8 colour launches of
+// k_mg_apply_walsh do from y = 0, so the result is bitwise the same, with x and
+// y touched once (the colour launches read and rewrite y 8 times).
+// CG: y = 0 on fixed DOFs and per-block partials of x . y (k_state_matvec's
+// contract).
+// Level-1 Galerkin element operator applied on the fly (H8): Kc x_c =
+// sum_p Q_p' (E_p Ke) Q_p x_c over the 8 children p of the coarse element, Q_p
+// the trilinear interpolation from the coarse corners to child p's nodes
+// (the fine lattice position of child node b' is (pi + oi, pk + ok, pj + oj)
+// in {0, 1, 2}^3; per axis the weight of coarse corner 0 is 1, 1/2, 0 and of
+// corner 1 is 0, 1/2, 1). Algebraically the stored Kc = sum_p E_p Kp, without
+// the 4.6 KB per coarse element.
+__host__ __device__ constexpr double mg_w1(int pos, int corner) {
+  return pos == 1 ? 0.5 : (pos == 0 ? (corner == 0 ? 1.0 : 0.0) : (corner == 1 ? 1.0 : 0.0));
+}
+// Eb: the modulus of child (0, 0, 0), children at + (p & 1) + ((p >> 1) & 1) sz
+// + (p >> 2) sx (null: an element outside the grid, all moduli 0)
+// The output accumulates in shared memory (register budget): out[c][b] at
+// o0[(b * 3 + c) * 256] for b < 4 and o1[((b - 4) * 3 + c) * 256] (the tile's
+// c0 / c1 layout), zeroed here first.
+// The coarse nodal values are read from the staged node layers (xa: layer
+// ex, xb: ex + 1; node (b & 1, (b >> 1) & 1) of the element at offset o +
+// ((b >> 1) & 1) * ny3 + (b & 1) * 3), again per child (register budget).
+template <int NY3>
+__device__ __forceinline__ void mg_c1_elem(const double* sk, const double* __restrict__ Eb,
+                                           long long sz, long long sx, const double* xa,
+                                           const double* xb, int o, double* o0, double* o1) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) (b < 4 ? o0 : o1)[((b & 3) * 3 + c) * 256] = 0.0;
+#pragma unroll 1
+  for (int p = 0; p < 8; ++p) {
+    // per-axis weights w[o][corner] of child node offset o (axes: y = bit 0, z = bit 1, x = bit 2)
+    double w[3][2][2];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int o = 0; o < 2; ++o)
+#pragma unroll
+        for (int cr = 0; cr < 2; ++cr) {
+          const int pos = ((p >> a) & 1) + o;
+          w[a][o][cr] = pos == 1 ? 0.5 : (pos == 2 * cr ? 1.0 : 0.0);
+        }
+    const double Ep = Eb ? Eb[(p & 1) + ((p >> 1) & 1) * sz + (p >> 2) * sx] : 0.0;
+    // t = Q_p h, separably (one axis at a time)
+    double t[3][8];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double u[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {  // axis y: bit 0 of b becomes the child offset
+        const int oo = b & 1, r = b & 6;
+        const double* src = (r & 4) ? xb : xa;
+        const int q = o + ((r >> 1) & 1) * NY3 + c;
+        t[c][b] = fma(w[0][oo][0], src[q], w[0][oo][1] * src[q + 3]);
+      }
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {  // axis z
+        const int o = (b >> 1) & 1, r = b & 5;
+        u[b] = fma(w[1][o][0], t[c][r], w[1][o][1] * t[c][r | 2]);
+      }
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {  // axis x
+        const int o = b >> 2, r = b & 3;
+        t[c][b] = fma(w[2][o][0], u[r], w[2][o][1] * u[r | 4]);
+      }
+    }
+    walsh_elem_apply(sk, Ep, t);
+    // out += Q_p' t (the transposed steps in reverse order)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double u[8], v[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {  // axis x: corner bit 2 from the offsets
+        const int cr = b >> 2, r = b & 3;
+        u[b] = fma(w[2][0][cr], t[c][r], w[2][1][cr] * t[c][r | 4]);
+      }
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {  // axis z
+        const int cr = (b >> 1) & 1, r = b & 5;
+        v[b] = fma(w[1][0][cr], u[r], w[1][1][cr] * u[r | 2]);
+      }
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {  // axis y
+        const int cr = b & 1, r = b & 6;
+        (b < 4 ? o0 : o1)[((b & 3) * 3 + c) * 256] += fma(w[0][0][cr], v[r], w[0][1][cr] * v[r | 1]);
+      }
+    }
+  }
+}
+
+constexpr int kTY = 31, kTZ = 7;             // owned nodes per tile
+constexpr int kEY = kTY + 1, kEZ = kTZ + 1;  // elements per layer (256)
+constexpr int kNY = kTY + 2, kNZ = kTZ + 2;  // element nodes per layer
+constexpr int kLX = kNY * kNZ * 3;           // doubles per staged node layer
+constexpr int kTileSmem = (2 * kLX + 3 * 12 * kEY * kEZ) * int(sizeof(double));
+
+__host__ __device__ inline int tile_ny(const MgGeo& L) { return int((L.ny1 + kTY - 1) / kTY); }
+__host__ __device__ inline int tile_nz(const MgGeo& L) { return (L.nz1 + kTZ - 1) / kTZ; }
+
+// C1: level 1 of the hierarchy, elements by mg_c1_elem from the fine moduli E
+template <bool CG, bool C1 = false>
+__global__ void __launch_bounds__(256, C1 ? 1 : 2) k_mg_apply_tile(MgGeo L, const double* __restrict__ kw,
+                                                          const double* __restrict__ E,
+                                                          const double* __restrict__ x,
+                                                          double* __restrict__ y, int xchunk,
+                                                          double* __restrict__ partials) {
+  static_assert(kEY * kEZ == 256, "one element per thread");
+  extern __shared__ double smem[];
+  double* xs = smem;             // [2][kLX] node layers (parity of the layer index)
+  double* c0 = xs + 2 * kLX;     // [12][256] oj = 0 outputs of the current element layer
+  double* c1 = c0 + 12 * 256;    // [2][12][256] oj = 1 outputs (parity of the element layer)
+  __shared__ double sk[48];
+  __shared__ double scratch[32];
+  if (threadIdx.x < 48) sk[threadIdx.x] = kw[threadIdx.x];
+  const int nty = tile_ny(L), ntz = tile_nz(L);
+  const int by = blockIdx.x % nty, bz = (blockIdx.x / nty) % ntz, bx = blockIdx.x / (nty * ntz);
+  const int y0 = by * kTY, z0 = bz * kTZ;
+  const int nx1 = L.nelx + 1;
+  const int ix0 = bx * xchunk, ix1 = min(nx1, ix0 + xchunk);
+  const int t = threadIdx.x;
+  // node layers are staged through registers one step ahead (the global loads
+  // of layer ex + 2 are in flight while element layer ex + 1 is computed)
+  constexpr int kPer = (kLX + 255) / 256;
+  double pre[kPer];
+  auto fetch = [&](int lx) {
+    const bool okx = lx >= 0 && lx < nx1;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = t + 256 * j;
+      const int row = i / (3 * kNY), k = i - row * (3 * kNY);
+      const int iz = z0 - 1 + row, iy = y0 - 1 + k / 3;
+      double v = 0.0;
+      if (i < kLX && okx && iz >= 0 && iz < L.nz1 && iy >= 0 && iy < L.ny1)
+        v = x[3 * (((long long)lx * L.nz1 + iz) * L.ny1 + (y0 - 1)) + k];
+      pre[j] = v;
+    }
+  };
+  auto commit = [&](int lx) {
+    double* dst = xs + (lx & 1) * kLX;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if (t + 256 * j < kLX) dst[t + 256 * j] = pre[j];
+  };
+  const int ly = t % kEY, lz = t / kEY;  // this thread's element in the layer
+  const int ey = y0 - 1 + ly, ez = z0 - 1 + lz;
+  const bool okyz = ey >= 0 && ey < L.nely && ez >= 0 && ez < L.nz;
+  auto fetchE = [&](int ex) {
+    return okyz && ex >= 0 && ex < L.nelx ? E[((long long)ex * L.nz + ez) * L.nely + ey] : 0.0;
+  };
+  const int ony = t % kTY, onz = t / kTY;  // this thread's node (t < kTY * kTZ)
+  const int iy = y0 + ony, iz = z0 + onz;
+  const bool own = t < kTY * kTZ && iy < L.ny1 && iz < L.nz1;
+  double dot = 0.0;
+  fetch(ix0 - 1);
+  commit(ix0 - 1);
+  fetch(ix0);
+  commit(ix0);
+  fetch(ix0 + 1);
+  double Enext = C1 ? 0.0 : fetchE(ix0 - 1);
+  for (int ex = ix0 - 1; ex < ix1; ++ex) {
+    __syncthreads();
+    {  // element layer ex
+      double h[3][8];
+      const double* xa = xs + (ex & 1) * kLX;
+      const double* xb = xs + ((ex + 1) & 1) * kLX;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        if (C1) break;
+        const double* src = (b & 4) ? xb : xa;
+        const int o = ((lz + ((b >> 1) & 1)) * kNY + ly + (b & 1)) * 3;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) h[c][b] = src[o + c];
+      }
+      const bool ok = okyz && ex >= 0 && ex < L.nelx;
+      if (C1) {
+        const long long fny = 2 * L.nely, fnz = 2 * L.nz;
+        const double* Eb = ok ? E + ((long long)(2 * ex) * fnz + 2 * ez) * fny + 2 * ey : nullptr;
+        mg_c1_elem<3 * kNY>(sk, Eb, fny, fnz * fny, xa, xb, (lz * kNY + ly) * 3, c0 + t,
+                            c1 + (ex & 1) * 12 * 256 + t);
+      } else {
+        const double Ee = Enext;
+        Enext = fetchE(ex + 1);
+        walsh_elem_apply(sk, Ee, h);
+      }
+      double* h1 = c1 + (ex & 1) * 12 * 256;
+      if (!C1) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            c0[(r * 3 + c) * 256 + t] = ok ? h[c][r] : 0.0;
+            h1[(r * 3 + c) * 256 + t] = ok ? h[c][r + 4] : 0.0;
+          }
+      }
+    }
+    __syncthreads();
+    if (ex >= ix0 && own) {  // node layer ix = ex
+      const int ix = ex;
+      const double* h1p = c1 + ((ex - 1) & 1) * 12 * 256;
+      double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int col = 0; col < 8; ++col) {
+        const int cx = col & 1, cz = (col >> 1) & 1, cy = (col >> 2) & 1;
+        const int oj = ((ix - 1) & 1) == cx ? 1 : 0;  // element layer ix - oj
+        const int ok = ((iz - 1) & 1) == cz ? 1 : 0;
+        const int oi = ((iy - 1) & 1) == cy ? 1 : 0;
+        const int le = (onz + 1 - ok) * kEY + (ony + 1 - oi);  // element (ly, lz) in the tile
+        const double* src = oj ? h1p : c0;
+        const int r = oi + 2 * ok;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] += src[(r * 3 + c) * 256 + le];
+      }
+      const long long nd = ((long long)ix * L.nz1 + iz) * L.ny1 + iy;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const long long d = 3 * nd + c;
+        if (CG) {
+          const double v = L.fixed[d] ? 0.0 : acc[c];
+          y[d] = v;
+          dot = fma(x[d], v, dot);
+        } else {
+          y[d] = acc[c];
+        }
+      }
+    }
+    commit(ex + 2);  // (layer ex's buffer: read by the compute above, before the barrier)
+    fetch(ex + 3);
+  }
+  if (CG) {
+    double red[1] = {dot};
+    block_sum<1>(red, scratch);
+    if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
+  }
+}
+
+// Node-centric operator on a level with stored (symmetric) element matrices,
+// one launch instead of 8 colour launches: each node gathers its rows of the
+// (up to 2^dim) elements around it, in ascending element order, so every
+// matrix entry is read once per apply and y is written once. Rows are read as
+// columns (the Galerkin matrices are stored exactly symmetric), contiguous.
+// MODE 0: y = A x. MODE 1: damped Jacobi, y = x + w (b - A x) / diag (0 on
+// fixed DOFs; y must not alias x). MODE 2: y = b - A x (0 on fixed DOFs).
+// ROWS = DIM: all rows of node nd; ROWS = 1: row c0 only (small levels: 3x
+// the threads, shorter dependency chains)
+template <int DIM, int MODE, int ROWS = DIM>
+__device__ __forceinline__ void mg_node_rows(const MgGeo& L, const double* __restrict__ K,
+                                             const double* __restrict__ x,
+                                             const double* __restrict__ b,
+                                             const double* __restrict__ diag, double w,
+                                             double* __restrict__ y, long long nd, int c0 = 0) {
+  constexpr int NN = MgT<DIM>::NN, D = MgT<DIM>::D;
+  const int iy = int(nd % L.ny1);
+  const long long t = nd / L.ny1;
+  const int iz = int(t % L.nz1), ix = int(t / L.nz1);
+  double acc[ROWS];
+#pragma unroll
+  for (int c = 0; c < ROWS; ++c) acc[c] = 0.0;
+#pragma unroll 1
+  for (int q = 0; q < NN; ++q) {  // elements around the node, ascending
+    const int ex = ix - 1 + (q >> (DIM == 3 ? 2 : 1) & 1);
+    const int ez = DIM == 3 ? iz - 1 + (q >> 1 & 1) : 0;
+    const int ey = iy - 1 + (q & 1);
+    if (ex < 0 || ex >= L.nelx || ez < 0 || ez >= L.nz || ey < 0 || ey >= L.nely) continue;
+    const long long e = ((long long)ex * L.nz + ez) * L.nely + ey;
+    const int a = mg_local(DIM, iy - ey, iz - ez, ix - ex);
+    double xe[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) xe[j] = __ldg(x + mg_dof<DIM>(L, ex, ez, ey, j));
+#pragma unroll
+    for (int c = 0; c < ROWS; ++c) {
+      const double2* row = reinterpret_cast<const double2*>(K + e * (long long)(D * D) +
+                                                            (DIM * a + c + c0) * D);
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < D / 2; ++j) {
+        const double2 k = __ldg(row + j);
+        s = fma(k.x, xe[2 * j], s);
+        s = fma(k.y, xe[2 * j + 1], s);
+      }
+      acc[c] += s;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < ROWS; ++c) {
+    const long long d = DIM * nd + c + c0;
+    if (MODE == 0) {
+      y[d] = acc[c];
+    } else if (MODE == 1) {
+      y[d] = L.fixed[d] ? 0.0 : x[d] + w * (b[d] - acc[c]) / diag[d];
+    } else {
+      y[d] = L.fixed[d] ? 0.0 : b[d] - acc[c];
+    }
+  }
+}
+
+template <int DIM, int MODE>
+__global__ void __launch_bounds__(256) k_mg_node(MgGeo L, const double* __restrict__ K,
+                                                 const double* __restrict__ x,
+                                                 const double* __restrict__ b,
+                                                 const double* __restrict__ diag, double w,
+                                                 double* __restrict__ y) {
+  for (long long nd = blockIdx.x * (long long)blockDim.x + threadIdx.x; nd < L.nn;
+       nd += (long long)gridDim.x * blockDim.x)
+    mg_node_rows<DIM, MODE>(L, K, x, b, diag, w, y, nd);
+}
+
+// The coarsest level's Jacobi sweeps in one cooperative launch: x = w b / diag,
+// then sweeps - 1 damped-Jacobi sweeps ping-ponging x <-> y with a grid
+// barrier between sweeps; the result ends in x.
+template <int DIM>
+__global__ void __launch_bounds__(256) k_mg_coarse_sweeps(MgGeo L, const double* __restrict__ K,
+                                                          const double* __restrict__ b,
+                                                          const double* __restrict__ diag, double w,
+                                                          double* __restrict__ x,
+                                                          double* __restrict__ y, int sweeps) {
+  cg::grid_group grid = cg::this_grid();
+  const long long S = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (long long d = t0; d < L.n; d += S) x[d] = L.fixed[d] ? 0.0 : w * b[d] / diag[d];
+  double *src = x, *dst = y;
+  for (int s = 1; s < sweeps; ++s) {
+    grid.sync();
+    for (long long d = t0; d < L.n; d += S)
+      mg_node_rows<DIM, 1, 1>(L, K, src, b, diag, w, dst, d / DIM, int(d % DIM));
+    double* tmp = src;
+    src = dst;
+    dst = tmp;
+  }
+  if (src != x) {
+    grid.sync();
+    for (long long d = t0; d < L.n; d += S) x[d] = src[d];
+  }
+}
+
+// level-1 Jacobi diagonal from the fine moduli: sum_p E_p Kp[p](l, l)
+template <int DIM>
+__global__ void k_mg_diag_c1(MgGeo L, const double* __restrict__ Kp, const double* __restrict__ E,
+                             double* __restrict__ diag) {
+  constexpr int NN = MgT<DIM>::NN, D = MgT<DIM>::D;
+  for (long long nd = blockIdx.x * (long long)blockDim.x + threadIdx.x; nd < L.nn;
+       nd += (long long)gridDim.x * blockDim.x) {
+    const int iy = int(nd % L.ny1);
+    const long long t = nd / L.ny1;
+    const int iz = int(t % L.nz1), ix = int(t / L.nz1);
+    double acc[DIM];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) acc[c] = 0.0;
+    for (int q = 0; q < NN; ++q) {
+      const int ex = ix - 1 + (q >> (DIM == 3 ? 2 : 1) & 1);
+      const int ez = DIM == 3 ? iz - 1 + (q >> 1 & 1) : 0;
+      const int ey = iy - 1 + (q & 1);
+      if (ex < 0 || ex >= L.nelx || ez < 0 || ez >= L.nz || ey < 0 || ey >= L.nely) continue;
+      const int a = mg_local(DIM, iy - ey, iz - ez, ix - ex);
+      for (int c = 0; c < DIM; ++c) {
+        const int l = DIM * a + c;
+        double s = 0.0;
+        for (int p = 0; p < NN; ++p) {
+          int pi, pk, pj;
+          mg_offsets(p, pi, pk, pj);
+          const long long ef =
+              ((long long)(2 * ex + pj) * (DIM == 3 ? 2 * L.nz : 1) + (DIM == 3 ? 2 * ez + pk : 0)) *
+                  (2 * L.nely) + (2 * ey + pi);
+          s = fma(E[ef], Kp[p * D * D + l * D + l], s);
+        }
+        acc[c] += s;
+      }
+    }
+    for (int c = 0; c < DIM; ++c) {
+      const long long d = DIM * nd + c;
+      diag[d] = L.fixed[d] ? 1.0 : acc[c];
     }
   }
 }

@@ -57,3 +57,33 @@ def test_multigrid_solve_matches_reference(P, oracle_ref, cid, grid, lo, monkeyp
     assert rr <= 1e-13 and 0 < it < itj  # the V-cycle cuts the iteration count
     assert np.all(u[fixed] == 0.0)
     assert rel(u, ur) <= 1e-8, rel(u, ur)
+
+
+def _numpy_apply(P, cfg, sK, x):
+    """y = sum_e sK_e Ke x_e over the element DOF table (fea.hpp:162-174)."""
+    Ke, _ = P.element_stiffness(3, cfg.nu)
+    with P.Context(*cfg.grid, rmin=1.0, nu=cfg.nu) as ctx:
+        dofs = np.asarray(ctx.build_connectivity()).reshape(cfg.m, -1).astype(np.int64)
+    y = np.zeros(cfg.n)
+    np.add.at(y, dofs.ravel(), (sK[:, None] * (x[dofs] @ Ke.T)).ravel())
+    return y
+
+
+# grids around the tile shape (31 x 7 nodes in y, z; x split in chunks)
+@pytest.mark.parametrize("grid", [(3, 2, 2), (7, 5, 9), (12, 30, 6), (17, 31, 7), (40, 33, 17),
+                                  (96, 48, 48)])
+def test_stiffness_operator_variants(P, grid):
+    from paper_2005_05436_b200.configs import CONFIGS
+    cfg = CONFIGS[4].scaled(*grid)
+    rng = np.random.default_rng(11)
+    sK = 1e-9 + rng.uniform(0.01, 1.0, cfg.m) ** 3
+    x = rng.standard_normal(cfg.n)
+    with P.Context(*cfg.grid, rmin=1.0, nu=cfg.nu) as ctx:
+        y0 = ctx.apply_stiffness(sK, x, 0)
+        y1 = ctx.apply_stiffness(sK, x, 1)
+        y2 = ctx.apply_stiffness(sK, x, 2)
+    assert np.array_equal(y0, y1)  # one-launch tiles == colour launches, bit for bit
+    assert rel(y0, y2) <= 1e-13, rel(y0, y2)
+    if cfg.m <= 20000:
+        yr = _numpy_apply(P, cfg, sK, x)
+        assert rel(y0, yr) <= 1e-13, rel(y0, yr)
