@@ -58,6 +58,9 @@ bool is_device_ptr(const void* p) {
 
 }  // namespace
 
+struct MgState;
+void mg_state_free(MgState*);
+
 struct topo_ctx {
   std::string err;
   int device = 0;
@@ -102,6 +105,8 @@ struct topo_ctx {
   DevBuf hs, hs_st, cw, x_st, xt, xphys, dcphys, dc, dV, xnew, a1_st, a2_st, rec, u, tmp0, tmp1,
       tmp_st;
   DevBuf sK, iK, jK;
+  struct MgState* mg = nullptr;  // multigrid levels and scratch, kept between solves
+  double kwp_host[48] = {};
   DevBuf d_kwp;  // Walsh blocks, plain (k00 k01 k02 k11 k12 k22 per signature), for k_mg_apply_tile
   DevBuf partials, partials0, result;
   double* h_result = nullptr;  // pinned
@@ -1053,6 +1058,9 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   if (ctx->device >= 0) cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) comm_destroy(ctx->comm);
+  mg_state_free(ctx->mg);
+  ctx->mg = nullptr;
+  ctx->d_kwp.release();
   for (DevBuf* b : {&ctx->d_map, &ctx->d_clean}) b->release();
   for (DevBuf* b : {&ctx->d_csc_tab, &ctx->d_csc_int, &ctx->csc_colptr, &ctx->csc_rows, &ctx->csc_E}) b->release();
   for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_w3, &ctx->d_ke_lower, &ctx->d_ke_full, &ctx->d_state, &ctx->hs, &ctx->hs_st,
@@ -1853,12 +1861,18 @@ static int tile_blocks(const topo_ctx* ctx, const MgGeo& L, int* xchunk) {
 
 static topo_status launch_tile_op(topo_ctx* ctx, const MgGeo& L, const double* E, const double* x,
                                   double* y, double* partials, int* nblocks = nullptr,
-                                  bool c1 = false) {
+                                  bool c1 = false, int epi = -1, const double* b = nullptr,
+                                  const double* diag = nullptr, double w = 0.0) {
+#define TILE_KERNELS(X)                                                                    \
+  X(kEpiApply, false) X(kEpiCG, false) X(kEpiJacobi, false) X(kEpiResidual, false)          \
+  X(kEpiApply, true) X(kEpiJacobi, true) X(kEpiResidual, true)
   static bool attr = false;
   if (!attr) {
-    for (const void* f : {(const void*)k_mg_apply_tile<false>, (const void*)k_mg_apply_tile<true>,
-                          (const void*)k_mg_apply_tile<false, true>})
-      CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
+#define TILE_ATTR(E_, C_)                                                               \
+  CK(cudaFuncSetAttribute((const void*)k_mg_apply_tile<E_, C_>,                          \
+                          cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
+    TILE_KERNELS(TILE_ATTR)
+#undef TILE_ATTR
     attr = true;
   }
   if (!ctx->d_kwp.p) {
@@ -1870,19 +1884,25 @@ static topo_status launch_tile_op(topo_ctx* ctx, const MgGeo& L, const double* E
     }
     CK(ctx->d_kwp.ensure(sizeof kwp));
     CK(cudaMemcpy(ctx->d_kwp.p, kwp, sizeof kwp, cudaMemcpyHostToDevice));
+    memcpy(ctx->kwp_host, kwp, sizeof kwp);
   }
   int xc = 0;
   const int nb = tile_blocks(ctx, L, &xc);
   if (nblocks) *nblocks = nb;
-  if (c1)
-    k_mg_apply_tile<false, true><<<nb, 256, kTileSmem, ctx->stream>>>(
-        L, ctx->d_kwp.as<double>(), E, x, y, xc, nullptr);
-  else if (partials)
-    k_mg_apply_tile<true><<<nb, 256, kTileSmem, ctx->stream>>>(L, ctx->d_kwp.as<double>(), E, x,
-                                                               y, xc, partials);
-  else
-    k_mg_apply_tile<false><<<nb, 256, kTileSmem, ctx->stream>>>(L, ctx->d_kwp.as<double>(), E, x,
-                                                                y, xc, nullptr);
+  if (epi < 0) epi = partials ? kEpiCG : kEpiApply;
+  const TileEpi ep{b, diag, w, partials};
+
+  bool launched = false;
+#define TILE_LAUNCH(E_, C_)                                                              \
+  if (!launched && epi == E_ && c1 == C_) {                                              \
+    k_mg_apply_tile<E_, C_><<<nb, 256, kTileSmem, ctx->stream>>>(L, ctx->d_kwp.as<double>(),  \
+                                                                 E, x, y, xc, ep);       \
+    launched = true;                                                                     \
+  }
+  TILE_KERNELS(TILE_LAUNCH)
+#undef TILE_LAUNCH
+#undef TILE_KERNELS
+  if (!launched) return fail(ctx, TOPO_EINVAL, "tile operator: unsupported epilogue");
   LAUNCHED();
   return TOPO_OK;
 }
@@ -2100,6 +2120,26 @@ static void mg_interp(int dim, std::vector<double>& Q) {
 }
 }  // namespace
 
+// multigrid levels and scratch of a context, kept between solves (the device
+// redesign loop solves on the same grid every iteration)
+struct MgState {
+  std::vector<MgLevel> lv;
+  DevBuf fb, cg, part, sc, dQ, dKp, dM;
+  void release() {
+    for (DevBuf* b : {&fb, &cg, &part, &sc, &dQ, &dKp, &dM}) b->release();
+    for (auto& L : lv)
+      for (DevBuf* b : {&L.fixed, &L.K, &L.diag, &L.x, &L.b, &L.r, &L.y}) b->release();
+    lv.clear();
+  }
+};
+}  // extern "C" (a C++ helper between the entry points)
+void mg_state_free(MgState* s) {
+  if (!s) return;
+  s->release();
+  delete s;
+}
+extern "C" {
+
 topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f,
                                 const int32_t* fixed, int64_t nfixed, double rtol, int32_t maxit,
                                 double* u, int32_t* iterations, double* relres) {
@@ -2109,7 +2149,7 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   const Geo& G = ctx->G;
   const int dim = G.dim;
   // levels: halve while every element count is even and the level is not tiny
-  std::vector<MgLevel> lv(1);
+  std::vector<MgLevel> lvg(1);  // (geometry only; the storage lives in ctx->mg)
   auto geo = [&](int nx, int ny, int nz3) {
     MgGeo g{};
     g.nelx = nx;
@@ -2123,17 +2163,17 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     g.m = (long long)nx * ny * g.nz;
     return g;
   };
-  lv[0].g = geo(G.nelx, G.nely, G.nelz);
+  lvg[0].g = geo(G.nelx, G.nely, G.nelz);
   for (;;) {
-    const MgGeo c = lv.back().g;  // (copy: emplace_back below may reallocate)
+    const MgGeo c = lvg.back().g;  // (copy: emplace_back below may reallocate)
     const bool even = c.nelx % 2 == 0 && c.nely % 2 == 0 && (dim == 2 || c.nz % 2 == 0);
     static const long long min_dofs =
         getenv("TOPO_MG_MIN_DOFS") ? atoll(getenv("TOPO_MG_MIN_DOFS")) : 20000;  // tests
-    if (!even || c.n <= min_dofs || lv.size() >= 8) break;
-    lv.emplace_back();
-    lv.back().g = geo(c.nelx / 2, c.nely / 2, dim == 3 ? c.nz / 2 : 0);
+    if (!even || c.n <= min_dofs || lvg.size() >= 8) break;
+    lvg.emplace_back();
+    lvg.back().g = geo(c.nelx / 2, c.nely / 2, dim == 3 ? c.nz / 2 : 0);
   }
-  if (lv.size() < 2)  // nothing to coarsen: the Jacobi-preconditioned solve
+  if (lvg.size() < 2)  // nothing to coarsen: the Jacobi-preconditioned solve
     return topo_solve_state(ctx, sK, f, fixed, nfixed, rtol, maxit, u, iterations, relres);
   ctx->launches = 0;
   const long long n = ctx->n;
@@ -2145,16 +2185,19 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   }
   const double *E, *fd;
   TRY(stage_in(ctx, sK, G.m, ctx->tmp0, &E));
-  DevBuf fb, cg, part, sc, dQ, dKp;
-  struct Release {
-    std::vector<MgLevel>* lv;
-    std::initializer_list<DevBuf*> bufs;
-    ~Release() {
-      for (DevBuf* b : bufs) b->release();
-      for (auto& L : *lv)
-        for (DevBuf* b : {&L.fixed, &L.K, &L.diag, &L.x, &L.b, &L.r, &L.y}) b->release();
-    }
-  } release_all{&lv, {&fb, &cg, &part, &sc, &dQ, &dKp}};
+  if (!ctx->mg) ctx->mg = new MgState;
+  MgState& ms = *ctx->mg;
+  if (ms.lv.size() != lvg.size()) {
+    ms.release();
+    ms.lv.resize(lvg.size());
+  }
+  for (size_t l = 0; l < lvg.size(); ++l) {
+    ms.lv[l].g = lvg[l].g;
+    ms.lv[l].omega = 0.6;
+  }
+  std::vector<MgLevel>& lv = ms.lv;
+  DevBuf &fb = ms.fb, &cg = ms.cg, &part = ms.part, &sc = ms.sc, &dQ = ms.dQ, &dKp = ms.dKp,
+         &dM = ms.dM;
   TRY(stage_in(ctx, f, n, fb, &fd));
   const int D = (dim == 3 ? 8 : 4) * dim, DD = D * D, NN = dim == 3 ? 8 : 4;
   // interpolation and the level-1 combinations Kp = Qp' Ke Qp (host)
@@ -2208,9 +2251,45 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
                                                        L.fixed.as<unsigned char>());
       if (mf1 && l == 1) {
         // (no stored matrices)
-      } else if (mf1 && l == 2)
-        k_mg_galerkin<3, true><<<int(std::min<long long>(L.g.m, 1LL << 20)), 256, 0, ctx->stream>>>(
-            L.g, F.g, E, dQ.as<double>(), L.K.as<double>(), dKp.as<double>());
+      } else if (mf1 && l == 2) {
+        // M[p1 * NN + p2] = Qc' Ke Qc, Qc = Q_p2 Q_p1 (exactly symmetric; Ke is fixed per
+        // context, so M is built on the first solve only)
+        const size_t msize = size_t(NN) * NN * DD;
+        std::vector<double> M(dM.bytes == sizeof(double) * msize ? 0 : msize);
+        std::vector<double> Qc(static_cast<size_t>(DD)), T(static_cast<size_t>(DD));
+        for (int p1 = 0; p1 < NN && !M.empty(); ++p1)
+          for (int p2 = 0; p2 < NN; ++p2) {
+            const double *Q1 = Q.data() + size_t(p1) * DD, *Q2 = Q.data() + size_t(p2) * DD;
+            for (int j = 0; j < D; ++j)
+              for (int i = 0; i < D; ++i) {
+                double a = 0;
+                for (int k = 0; k < D; ++k) a += Q2[size_t(k) * D + i] * Q1[size_t(j) * D + k];
+                Qc[size_t(j) * D + i] = a;
+              }
+            for (int j = 0; j < D; ++j)
+              for (int i = 0; i < D; ++i) {
+                double a = 0;
+                for (int k = 0; k < D; ++k) a += Ke[size_t(k) * D + i] * Qc[size_t(j) * D + k];
+                T[size_t(j) * D + i] = a;
+              }
+            double* Mg = M.data() + size_t(p1 * NN + p2) * DD;
+            for (int j = 0; j < D; ++j)
+              for (int i = j; i < D; ++i) {
+                double a = 0;
+                for (int k = 0; k < D; ++k) a += Qc[size_t(i) * D + k] * T[size_t(j) * D + k];
+                Mg[size_t(j) * D + i] = a;
+                Mg[size_t(i) * D + j] = a;
+              }
+          }
+        if (!M.empty()) {
+          CK(dM.ensure(sizeof(double) * M.size()));
+          CK(cudaMemcpyAsync(dM.p, M.data(), sizeof(double) * M.size(), cudaMemcpyHostToDevice,
+                             ctx->stream));
+          CK(cudaStreamSynchronize(ctx->stream));  // (M is a host temporary)
+        }
+        k_mg_galerkin2e<3, 16><<<int(std::min<long long>((L.g.m + 15) / 16, 1LL << 20)), 192, 0,
+                                 ctx->stream>>>(L.g, E, dM.as<double>(), L.K.as<double>());
+      }
       else if (l == 1)
         k_mg_galerkin1<3><<<grid_for(ctx, L.g.m * DD), kThreads, 0, ctx->stream>>>(
             L.g, F.g, E, dKp.as<double>(), L.K.as<double>());
@@ -2364,7 +2443,7 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     const double w = L.omega;
     const bool nodes = l > 0 && node_ops && !(l == 1 && mf1);
     if (nodes && last) {  // coarsest level: all sweeps in one cooperative launch
-      const int nbn = std::max(1, std::min(grid_for(ctx, L.g.n), coarse_grid));
+      const int nbn = std::max(1, std::min(grid_for(ctx, L.g.n * (dim == 3 ? 8 : 4)), coarse_grid));
       MgGeo g = L.g;
       const double *K = L.K.as<double>(), *b = L.b.as<double>(), *dg = L.diag.as<double>();
       double *x = L.x.as<double>(), *y = L.y.as<double>();
@@ -2377,9 +2456,20 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
       return TOPO_OK;
     }
     // one damped-Jacobi sweep from x (node kernels: into y, then the buffers swap)
+    // tile-operator levels (fine Walsh level, on-the-fly level 1): fused epilogues
+    // (off by default: measured 3% slower on C5 than the apply + elementwise
+    // sweep, the epilogue's extra loads sit in the latency-bound tile loop)
+    static const char* fz = getenv("TOPO_MG_FUSE");
+    const bool tiled = (fz && fz[0] == '1') && ((l == 0 && dkw && use_tile_op(ctx)) || (l == 1 && mf1));
     auto sweep = [&]() -> topo_status {
       if (nodes) {
         TRY(node_op(l, 1, L.x.as<double>(), L.y.as<double>()));
+        std::swap(L.x.p, L.y.p);
+        return TOPO_OK;
+      }
+      if (tiled) {
+        TRY(launch_tile_op(ctx, L.g, E, L.x.as<double>(), L.y.as<double>(), nullptr, nullptr,
+                           l == 1, kEpiJacobi, L.b.as<double>(), L.diag.as<double>(), w));
         std::swap(L.x.p, L.y.p);
         return TOPO_OK;
       }
@@ -2396,6 +2486,9 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     if (last) return TOPO_OK;
     if (nodes) {
       TRY(node_op(l, 2, L.x.as<double>(), L.r.as<double>()));
+    } else if (tiled) {
+      TRY(launch_tile_op(ctx, L.g, E, L.x.as<double>(), L.r.as<double>(), nullptr, nullptr, l == 1,
+                         kEpiResidual, L.b.as<double>(), L.diag.as<double>(), w));
     } else {
       TRY(apply(l, L.x.as<double>(), L.y.as<double>()));
       k_mg_residual<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, L.b.as<double>(),
@@ -2452,6 +2545,7 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   k_reduce_partials<2><<<1, 32, 0, ctx->stream>>>(pp, nbd, 2, scd + 5);  // [6] = f.f
   LAUNCHED();
   TRY(vcycle(0));
+  z = lv[0].x.as<double>();  // (the sweeps may have swapped level 0's x and y)
   CK(cudaMemcpyAsync(p, z, sizeof(double) * size_t(n), cudaMemcpyDeviceToDevice, ctx->stream));
   k_dot<<<nbd, kThreads, 0, ctx->stream>>>(n, r, z, pp);
   LAUNCHED();
@@ -2480,6 +2574,7 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(pp, nbd, 1, scd + 2);  // r.r
     LAUNCHED();
     TRY(vcycle(0));  // z = V(r)
+    z = lv[0].x.as<double>();
     k_dot<<<nbd, kThreads, 0, ctx->stream>>>(n, r, z, pp);
     LAUNCHED();
     k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(pp, nbd, 1, scd + 3);  // rz_new

@@ -84,6 +84,54 @@ __global__ void k_mg_galerkin1(MgGeo C, MgGeo F, const double* __restrict__ E,
   }
 }
 
+// Level-2 Galerkin matrices straight from the fine moduli (level 1 is not
+// stored): Kc[e] = sum over the (2^dim)^2 fine grandchildren g = p1 * NN + p2 of
+// E_g M[g], M[g] = (Q_p2 Q_p1)' Ke (Q_p2 Q_p1) precomputed (exactly symmetric).
+// A block takes NE coarse elements: their E in shared memory, each M entry
+// read once per block and used NE times.
+template <int DIM, int NE>
+__global__ void __launch_bounds__(192) k_mg_galerkin2e(MgGeo C, const double* __restrict__ E,
+                                                       const double* __restrict__ M,
+                                                       double* __restrict__ Kc) {
+  constexpr int NN = MgT<DIM>::NN, D = MgT<DIM>::D, DD = D * D, NG = NN * NN;
+  __shared__ double sE[NE][NG];
+  const long long fny = 4LL * C.nely, fnz = DIM == 3 ? 4LL * C.nz : 1;
+  for (long long e0 = (long long)blockIdx.x * NE; e0 < C.m; e0 += (long long)gridDim.x * NE) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < NE * NG; i += blockDim.x) {
+      const int n = i / NG, g = i - n * NG;
+      const long long e = e0 + n;
+      double v = 0.0;
+      if (e < C.m) {
+        int ex, ez, ey;
+        mg_elem(C, e, ex, ez, ey);
+        int i1, k1, j1, i2, k2, j2;
+        mg_offsets(g / NN, i1, k1, j1);
+        mg_offsets(g % NN, i2, k2, j2);
+        const long long fx = 4LL * ex + 2 * j1 + j2, fy = 4LL * ey + 2 * i1 + i2;
+        const long long fz = DIM == 3 ? 4LL * ez + 2 * k1 + k2 : 0;
+        v = E[(fx * fnz + fz) * fny + fy];
+      }
+      sE[n][g] = v;
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < DD; q += blockDim.x) {
+      double acc[NE];
+#pragma unroll
+      for (int n = 0; n < NE; ++n) acc[n] = 0.0;
+#pragma unroll 4
+      for (int g = 0; g < NG; ++g) {
+        const double m = __ldg(M + (long long)g * DD + q);
+#pragma unroll
+        for (int n = 0; n < NE; ++n) acc[n] = fma(sE[n][g], m, acc[n]);
+      }
+#pragma unroll
+      for (int n = 0; n < NE; ++n)
+        if (e0 + n < C.m) Kc[(e0 + n) * DD + q] = acc[n];
+    }
+  }
+}
+
 // Kc[e] = sum_p Qp' Kf[child p] Qp (levels >= 2); one block per coarse element
 // FROM_E: the children's matrices are level-1 Galerkin matrices built on the
 // fly, K_child = sum_p' E(grandchild p') Kp[p'] (Kf = fine E, Kp: the 8 Qp' Ke Qp)
@@ -240,7 +288,8 @@ __global__ void __launch_bounds__(256) k_mg_apply_warp(MgGeo L, const double* __
 // element instead of 576. h holds x_e on entry ([component][binary node index
 // oi + 2 ok + 4 oj]) and the element's output on exit. sk: per signature k00,
 // k01, k02, k11, k12, k22 (plain, not doubled).
-__device__ __forceinline__ void walsh_elem_apply(const double* sk, double Ee, double (&h)[3][8]) {
+// h <- H h per component (H[m][b] = prod over the axes a in m of (bit a of b ? 1 : -1))
+__device__ __forceinline__ void wh_butterfly(double (&h)[3][8]) {
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -252,6 +301,17 @@ __device__ __forceinline__ void walsh_elem_apply(const double* sk, double Ee, do
           h[c][b] = hi + lo;
           h[c][b | bit] = hi - lo;
         }
+}
+// h <- S h, S = diag((-1)^popcount(b))
+__device__ __forceinline__ void wh_signs(double (&h)[3][8]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (__popc(b) & 1) h[c][b] = -h[c][b];
+}
+// the 8 signature blocks (3 x 3) times Ee, on Walsh coefficients
+__device__ __forceinline__ void wh_blocks(const double* sk, double Ee, double (&h)[3][8]) {
 #pragma unroll
   for (int sig = 0; sig < 8; ++sig) {
     const int i0 = sig ^ (1 << walsh_axis(0)), i1 = sig ^ (1 << walsh_axis(1)),
@@ -262,29 +322,20 @@ __device__ __forceinline__ void walsh_elem_apply(const double* sk, double Ee, do
     h[1][i1] = Ee * fma(k[1], m0, fma(k[3], m1, k[4] * m2));
     h[2][i2] = Ee * fma(k[2], m0, fma(k[4], m1, k[5] * m2));
   }
-  // W g = D B(D g): the butterfly B is W' = D H (H symmetric Sylvester,
-  // D = (-1)^popcount on the index), so the inverse needs the sign flips
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int b = 0; b < 8; ++b)
-      if (__popc(b) & 1) h[c][b] = -h[c][b];
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int bit = 1; bit < 8; bit <<= 1)
-#pragma unroll
-      for (int b = 0; b < 8; ++b)
-        if (!(b & bit)) {
-          const double lo = h[c][b], hi = h[c][b | bit];
-          h[c][b] = hi + lo;
-          h[c][b | bit] = hi - lo;
-        }
-#pragma unroll
-  for (int c = 0; c < 3; ++c)
-#pragma unroll
-    for (int b = 0; b < 8; ++b)
-      if (__popc(b) & 1) h[c][b] = -h[c][b];
+}
+
+// E_e Ke x_e for one hexahedron in Walsh coordinates (Ke = W Kt W', the
+// blocks of k_elem_walsh): per component an 8-point Walsh-Hadamard transform
+// of x_e, the 8 signature blocks (3x3), the inverse transform (S H S = H',
+// H H' = 8 I); 216 flops per element instead of 576. h holds x_e on entry
+// ([component][binary node index oi + 2 ok + 4 oj]) and the element's output
+// on exit. sk: per signature k00, k01, k02, k11, k12, k22 (plain, not doubled).
+__device__ __forceinline__ void walsh_elem_apply(const double* sk, double Ee, double (&h)[3][8]) {
+  wh_butterfly(h);
+  wh_blocks(sk, Ee, h);
+  wh_signs(h);
+  wh_butterfly(h);
+  wh_signs(h);
 }
 
 // y += E_e Ke x_e over one colour for hexahedra in Walsh coordinates
@@ -335,89 +386,68 @@ __global__ void __launch_bounds__(256) k_mg_apply_walsh(MgGeo L, const double* _
 // contract).
 // Level-1 Galerkin element operator applied on the fly (H8): Kc x_c =
 // sum_p Q_p' (E_p Ke) Q_p x_c over the 8 children p of the coarse element, Q_p
-// the trilinear interpolation from the coarse corners to child p's nodes
-// (the fine lattice position of child node b' is (pi + oi, pk + ok, pj + oj)
-// in {0, 1, 2}^3; per axis the weight of coarse corner 0 is 1, 1/2, 0 and of
-// corner 1 is 0, 1/2, 1). Algebraically the stored Kc = sum_p E_p Kp, without
-// the 4.6 KB per coarse element.
-__host__ __device__ constexpr double mg_w1(int pos, int corner) {
-  return pos == 1 ? 0.5 : (pos == 0 ? (corner == 0 ? 1.0 : 0.0) : (corner == 1 ? 1.0 : 0.0));
-}
-// Eb: the modulus of child (0, 0, 0), children at + (p & 1) + ((p >> 1) & 1) sz
-// + (p >> 2) sx (null: an element outside the grid, all moduli 0)
-// The output accumulates in shared memory (register budget): out[c][b] at
-// o0[(b * 3 + c) * 256] for b < 4 and o1[((b - 4) * 3 + c) * 256] (the tile's
-// c0 / c1 layout), zeroed here first.
-// The coarse nodal values are read from the staged node layers (xa: layer
-// ex, xb: ex + 1; node (b & 1, (b >> 1) & 1) of the element at offset o +
-// ((b >> 1) & 1) * ny3 + (b & 1) * 3), again per child (register budget).
-template <int NY3>
+// the trilinear interpolation to child p's nodes. Everything stays in Walsh
+// coefficients: with h^ = H x_c, Q_p = H' T_p H / 8 where T_p is, per axis a,
+// the pair map (u0, u1) -> (u0 + c_a u1, u1 / 2), c_a = +-1/2 the child's
+// offset (a linear coarse mode restricted to a half cell); Ke = H' Kt H / 8
+// gives Kc x_c = H' sum_p T_p' (E_p Kt T_p h^): one transform in and one out
+// per coarse element, 72 + 105 + 72 flops per child. Algebraically the stored
+// Kc = sum_p E_p Kp, without its 4.6 KB per coarse element. h: x_c in, Kc x_c
+// out. Eb: the modulus of child (0, 0, 0), children at + (p & 1) + ((p >> 1) & 1)
+// sz + (p >> 2) sx (null: an element outside the grid, all moduli 0).
 __device__ __forceinline__ void mg_c1_elem(const double* sk, const double* __restrict__ Eb,
-                                           long long sz, long long sx, const double* xa,
-                                           const double* xb, int o, double* o0, double* o1) {
+                                           long long sz, long long sx, double (&h)[3][8]) {
+  wh_butterfly(h);
+  double acc[3][8];
 #pragma unroll
   for (int c = 0; c < 3; ++c)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) (b < 4 ? o0 : o1)[((b & 3) * 3 + c) * 256] = 0.0;
+    for (int b = 0; b < 8; ++b) acc[c][b] = 0.0;
 #pragma unroll 1
   for (int p = 0; p < 8; ++p) {
-    // per-axis weights w[o][corner] of child node offset o (axes: y = bit 0, z = bit 1, x = bit 2)
-    double w[3][2][2];
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int o = 0; o < 2; ++o)
-#pragma unroll
-        for (int cr = 0; cr < 2; ++cr) {
-          const int pos = ((p >> a) & 1) + o;
-          w[a][o][cr] = pos == 1 ? 0.5 : (pos == 2 * cr ? 1.0 : 0.0);
-        }
+    const double* skp = sk;
+    asm volatile("" : "+l"(skp));  // re-read the blocks per child: no 48 registers held
     const double Ep = Eb ? Eb[(p & 1) + ((p >> 1) & 1) * sz + (p >> 2) * sx] : 0.0;
-    // t = Q_p h, separably (one axis at a time)
-    double t[3][8];
+    double g[3][8];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      double u[8];
+    for (int c = 0; c < 3; ++c)
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {  // axis y: bit 0 of b becomes the child offset
-        const int oo = b & 1, r = b & 6;
-        const double* src = (r & 4) ? xb : xa;
-        const int q = o + ((r >> 1) & 1) * NY3 + c;
-        t[c][b] = fma(w[0][oo][0], src[q], w[0][oo][1] * src[q + 3]);
-      }
+      for (int b = 0; b < 8; ++b) g[c][b] = h[c][b];
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {  // axis z
-        const int o = (b >> 1) & 1, r = b & 5;
-        u[b] = fma(w[1][o][0], t[c][r], w[1][o][1] * t[c][r | 2]);
-      }
+    for (int a = 0; a < 3; ++a) {
+      const double ca = ((p >> a) & 1) ? 0.5 : -0.5;
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {  // axis x
-        const int o = b >> 2, r = b & 3;
-        t[c][b] = fma(w[2][o][0], u[r], w[2][o][1] * u[r | 4]);
-      }
+      for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          if (!(b & (1 << a))) {
+            const double u1 = g[c][b | (1 << a)];
+            g[c][b] = fma(ca, u1, g[c][b]);
+            g[c][b | (1 << a)] = 0.5 * u1;
+          }
     }
-    walsh_elem_apply(sk, Ep, t);
-    // out += Q_p' t (the transposed steps in reverse order)
+    wh_blocks(skp, Ep, g);
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      double u[8], v[8];
+    for (int a = 0; a < 3; ++a) {
+      const double ca = ((p >> a) & 1) ? 0.5 : -0.5;
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {  // axis x: corner bit 2 from the offsets
-        const int cr = b >> 2, r = b & 3;
-        u[b] = fma(w[2][0][cr], t[c][r], w[2][1][cr] * t[c][r | 4]);
-      }
+      for (int c = 0; c < 3; ++c)
 #pragma unroll
-      for (int b = 0; b < 8; ++b) {  // axis z
-        const int cr = (b >> 1) & 1, r = b & 5;
-        v[b] = fma(w[1][0][cr], u[r], w[1][1][cr] * u[r | 2]);
-      }
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {  // axis y
-        const int cr = b & 1, r = b & 6;
-        (b < 4 ? o0 : o1)[((b & 3) * 3 + c) * 256] += fma(w[0][0][cr], v[r], w[0][1][cr] * v[r | 1]);
-      }
+        for (int b = 0; b < 8; ++b)
+          if (!(b & (1 << a))) g[c][b | (1 << a)] = fma(ca, g[c][b], 0.5 * g[c][b | (1 << a)]);
     }
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) acc[c][b] += g[c][b];
   }
+  wh_signs(acc);
+  wh_butterfly(acc);
+  wh_signs(acc);
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) h[c][b] = acc[c][b];
 }
 
 constexpr int kTY = 31, kTZ = 7;             // owned nodes per tile
@@ -430,12 +460,24 @@ __host__ __device__ inline int tile_ny(const MgGeo& L) { return int((L.ny1 + kTY
 __host__ __device__ inline int tile_nz(const MgGeo& L) { return (L.nz1 + kTZ - 1) / kTZ; }
 
 // C1: level 1 of the hierarchy, elements by mg_c1_elem from the fine moduli E
-template <bool CG, bool C1 = false>
+// Epilogues (EPI): y = A x; CG: y = A x masked + dot partials; JACOBI: y = x +
+// w (b - A x) / diag (0 on fixed; y must not alias x); RESIDUAL: y = b - A x
+// (0 on fixed).
+enum { kEpiApply = 0, kEpiCG = 1, kEpiJacobi = 2, kEpiResidual = 3 };
+struct TileEpi {
+  const double* b;
+  const double* diag;
+  double w;
+  double* partials;
+};
+
+template <int EPI, bool C1 = false>
 __global__ void __launch_bounds__(256, C1 ? 1 : 2) k_mg_apply_tile(MgGeo L, const double* __restrict__ kw,
                                                           const double* __restrict__ E,
                                                           const double* __restrict__ x,
                                                           double* __restrict__ y, int xchunk,
-                                                          double* __restrict__ partials) {
+                                                          TileEpi ep) {
+  constexpr bool CG = EPI == kEpiCG;
   static_assert(kEY * kEZ == 256, "one element per thread");
   extern __shared__ double smem[];
   double* xs = smem;             // [2][kLX] node layers (parity of the layer index)
@@ -497,7 +539,6 @@ __global__ void __launch_bounds__(256, C1 ? 1 : 2) k_mg_apply_tile(MgGeo L, cons
       const double* xb = xs + ((ex + 1) & 1) * kLX;
 #pragma unroll
       for (int b = 0; b < 8; ++b) {
-        if (C1) break;
         const double* src = (b & 4) ? xb : xa;
         const int o = ((lz + ((b >> 1) & 1)) * kNY + ly + (b & 1)) * 3;
 #pragma unroll
@@ -507,23 +548,20 @@ __global__ void __launch_bounds__(256, C1 ? 1 : 2) k_mg_apply_tile(MgGeo L, cons
       if (C1) {
         const long long fny = 2 * L.nely, fnz = 2 * L.nz;
         const double* Eb = ok ? E + ((long long)(2 * ex) * fnz + 2 * ez) * fny + 2 * ey : nullptr;
-        mg_c1_elem<3 * kNY>(sk, Eb, fny, fnz * fny, xa, xb, (lz * kNY + ly) * 3, c0 + t,
-                            c1 + (ex & 1) * 12 * 256 + t);
+        mg_c1_elem(sk, Eb, fny, fnz * fny, h);
       } else {
         const double Ee = Enext;
         Enext = fetchE(ex + 1);
         walsh_elem_apply(sk, Ee, h);
       }
       double* h1 = c1 + (ex & 1) * 12 * 256;
-      if (!C1) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+      for (int r = 0; r < 4; ++r)
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            c0[(r * 3 + c) * 256 + t] = ok ? h[c][r] : 0.0;
-            h1[(r * 3 + c) * 256 + t] = ok ? h[c][r + 4] : 0.0;
-          }
-      }
+        for (int c = 0; c < 3; ++c) {
+          c0[(r * 3 + c) * 256 + t] = ok ? h[c][r] : 0.0;
+          h1[(r * 3 + c) * 256 + t] = ok ? h[c][r + 4] : 0.0;
+        }
     }
     __syncthreads();
     if (ex >= ix0 && own) {  // node layer ix = ex
@@ -550,6 +588,10 @@ __global__ void __launch_bounds__(256, C1 ? 1 : 2) k_mg_apply_tile(MgGeo L, cons
           const double v = L.fixed[d] ? 0.0 : acc[c];
           y[d] = v;
           dot = fma(x[d], v, dot);
+        } else if (EPI == kEpiJacobi) {
+          y[d] = L.fixed[d] ? 0.0 : x[d] + ep.w * (ep.b[d] - acc[c]) / ep.diag[d];
+        } else if (EPI == kEpiResidual) {
+          y[d] = L.fixed[d] ? 0.0 : ep.b[d] - acc[c];
         } else {
           y[d] = acc[c];
         }
@@ -561,7 +603,7 @@ __global__ void __launch_bounds__(256, C1 ? 1 : 2) k_mg_apply_tile(MgGeo L, cons
   if (CG) {
     double red[1] = {dot};
     block_sum<1>(red, scratch);
-    if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
+    if (threadIdx.x == 0) ep.partials[blockIdx.x] = red[0];
   }
 }
 
@@ -636,6 +678,38 @@ __global__ void __launch_bounds__(256) k_mg_node(MgGeo L, const double* __restri
     mg_node_rows<DIM, MODE>(L, K, x, b, diag, w, y, nd);
 }
 
+// One damped-Jacobi row of a small stored level by NN lanes (lane q takes the
+// q-th element around the node; a fixed shuffle tree sums them): short
+// dependency chains for the latency-bound coarsest level. All lanes of the
+// group must call it (the shuffles); returns the new value on lane 0.
+template <int DIM>
+__device__ __forceinline__ double mg_row_lanes(const MgGeo& L, const double* __restrict__ K,
+                                               const double* __restrict__ x, long long d, int q,
+                                               bool valid) {
+  constexpr int NN = MgT<DIM>::NN, D = MgT<DIM>::D;
+  double s = 0.0;
+  if (valid) {
+    const long long nd = d / DIM;
+    const int c = int(d - nd * DIM);
+    const int iy = int(nd % L.ny1);
+    const long long t = nd / L.ny1;
+    const int iz = int(t % L.nz1), ix = int(t / L.nz1);
+    const int ex = ix - 1 + (q >> (DIM == 3 ? 2 : 1) & 1);
+    const int ez = DIM == 3 ? iz - 1 + (q >> 1 & 1) : 0;
+    const int ey = iy - 1 + (q & 1);
+    if (ex >= 0 && ex < L.nelx && ez >= 0 && ez < L.nz && ey >= 0 && ey < L.nely) {
+      const long long e = ((long long)ex * L.nz + ez) * L.nely + ey;
+      const int a = mg_local(DIM, iy - ey, iz - ez, ix - ex);
+      const double* row = K + e * (long long)(D * D) + (DIM * a + c) * D;
+#pragma unroll
+      for (int j = 0; j < D; ++j) s = fma(__ldg(row + j), __ldg(x + mg_dof<DIM>(L, ex, ez, ey, j)), s);
+    }
+  }
+#pragma unroll
+  for (int o = NN / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, NN);
+  return s;
+}
+
 // The coarsest level's Jacobi sweeps in one cooperative launch: x = w b / diag,
 // then sweeps - 1 damped-Jacobi sweeps ping-ponging x <-> y with a grid
 // barrier between sweeps; the result ends in x.
@@ -650,10 +724,18 @@ __global__ void __launch_bounds__(256) k_mg_coarse_sweeps(MgGeo L, const double*
   const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   for (long long d = t0; d < L.n; d += S) x[d] = L.fixed[d] ? 0.0 : w * b[d] / diag[d];
   double *src = x, *dst = y;
+  constexpr int NN = MgT<DIM>::NN;
+  const int q = threadIdx.x % NN;
+  const long long ng = S / NN;  // lane groups in the grid (blockDim is a multiple of NN)
+  const long long nrounds = (L.n + ng - 1) / ng;
   for (int s = 1; s < sweeps; ++s) {
     grid.sync();
-    for (long long d = t0; d < L.n; d += S)
-      mg_node_rows<DIM, 1, 1>(L, K, src, b, diag, w, dst, d / DIM, int(d % DIM));
+    for (long long r = 0; r < nrounds; ++r) {  // uniform trip count: the shuffles need all lanes
+      const long long d = r * ng + t0 / NN;
+      const bool valid = d < L.n;
+      const double ax = mg_row_lanes<DIM>(L, K, src, d, q, valid);
+      if (valid && q == 0) dst[d] = L.fixed[d] ? 0.0 : src[d] + w * (b[d] - ax) / diag[d];
+    }
     double* tmp = src;
     src = dst;
     dst = tmp;
