@@ -1850,12 +1850,23 @@ static bool use_tile_op(const topo_ctx* ctx) {
   return ctx->G.is3d && ctx->walsh && !(e && e[0] == '0');
 }
 
-static int tile_blocks(const topo_ctx* ctx, const MgGeo& L, int* xchunk) {
+static int tile_blocks(const topo_ctx* ctx, const MgGeo& L, int* xchunk, int per_sm = 2) {
+  // pick the x split with the best (full waves) x (layers / (layers + 1)) score:
+  // every chunk recomputes one element layer, a partial last wave idles SMs
   const int nyz = tile_ny(L) * tile_nz(L), nx1 = L.nelx + 1;
-  const int target = 4 * ctx->sm_count;
-  int chunks = std::max(1, (target + nyz - 1) / nyz);
-  chunks = std::min(chunks, std::max(1, nx1 / 8));
-  *xchunk = (nx1 + chunks - 1) / chunks;
+  const int wave = per_sm * ctx->sm_count;
+  int best = 1;
+  double best_s = -1.0;
+  for (int ch = 1; ch <= std::max(1, nx1 / 4); ++ch) {
+    const int xc = (nx1 + ch - 1) / ch, nb = nyz * ((nx1 + xc - 1) / xc);
+    const int waves = (nb + wave - 1) / wave;
+    const double s = double(nb) / (double(waves) * wave) * double(xc) / (xc + 1);
+    if (s > best_s + 1e-9) {
+      best_s = s;
+      best = ch;
+    }
+  }
+  *xchunk = (nx1 + best - 1) / best;
   return nyz * ((nx1 + *xchunk - 1) / *xchunk);
 }
 
@@ -1887,7 +1898,7 @@ static topo_status launch_tile_op(topo_ctx* ctx, const MgGeo& L, const double* E
     memcpy(ctx->kwp_host, kwp, sizeof kwp);
   }
   int xc = 0;
-  const int nb = tile_blocks(ctx, L, &xc);
+  const int nb = tile_blocks(ctx, L, &xc, c1 ? 1 : 2);
   if (nblocks) *nblocks = nb;
   if (epi < 0) epi = partials ? kEpiCG : kEpiApply;
   const TileEpi ep{b, diag, w, partials};

@@ -454,7 +454,8 @@ constexpr int kTY = 31, kTZ = 7;             // owned nodes per tile
 constexpr int kEY = kTY + 1, kEZ = kTZ + 1;  // elements per layer (256)
 constexpr int kNY = kTY + 2, kNZ = kTZ + 2;  // element nodes per layer
 constexpr int kLX = kNY * kNZ * 3;           // doubles per staged node layer
-constexpr int kTileSmem = (2 * kLX + 3 * 12 * kEY * kEZ) * int(sizeof(double));
+constexpr int kCS = kEY * kEZ + 4;  // contribution row stride: rows r*3+c land 8 banks apart
+constexpr int kTileSmem = (2 * kLX + 3 * 12 * kCS) * int(sizeof(double));
 
 __host__ __device__ inline int tile_ny(const MgGeo& L) { return int((L.ny1 + kTY - 1) / kTY); }
 __host__ __device__ inline int tile_nz(const MgGeo& L) { return (L.nz1 + kTZ - 1) / kTZ; }
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(256, C1 ? 1 : 2) k_mg_apply_tile(MgGeo L, cons
   extern __shared__ double smem[];
   double* xs = smem;             // [2][kLX] node layers (parity of the layer index)
   double* c0 = xs + 2 * kLX;     // [12][256] oj = 0 outputs of the current element layer
-  double* c1 = c0 + 12 * 256;    // [2][12][256] oj = 1 outputs (parity of the element layer)
+  double* c1 = c0 + 12 * kCS;    // [2][12][kCS] oj = 1 outputs (parity of the element layer)
   __shared__ double sk[48];
   __shared__ double scratch[32];
   if (threadIdx.x < 48) sk[threadIdx.x] = kw[threadIdx.x];
@@ -554,19 +555,19 @@ __global__ void __launch_bounds__(256, C1 ? 1 : 2) k_mg_apply_tile(MgGeo L, cons
         Enext = fetchE(ex + 1);
         walsh_elem_apply(sk, Ee, h);
       }
-      double* h1 = c1 + (ex & 1) * 12 * 256;
+      double* h1 = c1 + (ex & 1) * 12 * kCS;
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          c0[(r * 3 + c) * 256 + t] = ok ? h[c][r] : 0.0;
-          h1[(r * 3 + c) * 256 + t] = ok ? h[c][r + 4] : 0.0;
+          c0[(r * 3 + c) * kCS + t] = ok ? h[c][r] : 0.0;
+          h1[(r * 3 + c) * kCS + t] = ok ? h[c][r + 4] : 0.0;
         }
     }
     __syncthreads();
     if (ex >= ix0 && own) {  // node layer ix = ex
       const int ix = ex;
-      const double* h1p = c1 + ((ex - 1) & 1) * 12 * 256;
+      const double* h1p = c1 + ((ex - 1) & 1) * 12 * kCS;
       double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
       for (int col = 0; col < 8; ++col) {
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(256, C1 ? 1 : 2) k_mg_apply_tile(MgGeo L, cons
         const double* src = oj ? h1p : c0;
         const int r = oi + 2 * ok;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) acc[c] += src[(r * 3 + c) * 256 + le];
+        for (int c = 0; c < 3; ++c) acc[c] += src[(r * 3 + c) * kCS + le];
       }
       const long long nd = ((long long)ix * L.nz1 + iz) * L.ny1 + iy;
 #pragma unroll
