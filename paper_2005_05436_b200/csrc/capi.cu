@@ -105,6 +105,7 @@ struct topo_ctx {
   DevBuf hs, hs_st, cw, x_st, xt, xphys, dcphys, dc, dV, xnew, a1_st, a2_st, rec, u, tmp0, tmp1,
       tmp_st;
   DevBuf sK, iK, jK;
+  DevBuf eta_dev;  // EtaDev: multi-GPU Newton state
   struct MgState* mg = nullptr;  // multigrid levels and scratch, kept between solves
   double kwp_host[48] = {};
   DevBuf d_kwp;  // Walsh blocks, plain (k00 k01 k02 k11 k12 k22 per signature), for k_mg_apply_tile
@@ -573,28 +574,33 @@ topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
   A.partials = ctx->partials.as<double>();
   A.result = eta_dev_out;
   if (!ctx->comm) return coop_launch(ctx, (const void*)k_eta_solve, &A, ctx->coop_eta);
-  // multi-GPU: host-driven replay, one allreduce of (g, g') per evaluation
-  EtaCtl ctl;
-  ctl.init(eta0);
+  // multi-GPU: the Newton replay on the device, one allreduce of the four sums
+  // per evaluation on the stream; evaluations are issued in batches of 4 and
+  // the host reads the `done` flag once per batch (no-ops after convergence)
+  CK(ctx->eta_dev.ensure(sizeof(EtaDev)));
+  EtaDev* st = ctx->eta_dev.as<EtaDev>();
+  double* sums = ctx->result.as<double>() + 56;
+  k_eta_dev_init<<<1, 1, 0, ctx->stream>>>(st, eta0);
+  LAUNCHED();
+  constexpr int kBatch = 4;
   int first = 1;
-  double sum_t = 0.0, n_act = 0.0;
-  for (;;) {
-    k_eta_partials<<<ctx->coop_eta, kThreads, 0, ctx->stream>>>(A, ctl.eta, first);
-    LAUNCHED();
-    TRY(reduce_to_host<4>(ctx, A.partials, ctx->coop_eta));  // summed over ranks
-    if (first) {
-      sum_t = ctx->h_result[2];
-      n_act = ctx->h_result[3];
+  for (int round = 0; round < 64; round += kBatch) {  // filter.hpp:213: at most 50 iterations
+    for (int q = 0; q < kBatch; ++q) {
+      k_eta_partials_dev<<<ctx->coop_eta, kThreads, 0, ctx->stream>>>(A, st, first);
+      LAUNCHED();
+      k_reduce_partials<4><<<1, 32, 0, ctx->stream>>>(A.partials, ctx->coop_eta, 4, sums);
+      LAUNCHED();
+      TRY(comm_allreduce(ctx->comm, ctx, sums, 4));
+      k_eta_dev_step<<<1, 1, 0, ctx->stream>>>(st, sums, first, beta, ctx->m_total, eta_dev_out);
+      LAUNCHED();
+      first = 0;
     }
-    first = 0;
-    const double g =
-        eta_mismatch_from_sums(beta, ctl.eta, ctx->h_result[0], sum_t, n_act, ctx->m_total);
-    if (!ctl.feed(g, ctx->h_result[1] / ctx->m_total)) break;
+    int done = 0;
+    CK(cudaMemcpyAsync(&done, &st->ctl.done, sizeof done, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (done) return TOPO_OK;
   }
-  const double res[3] = {ctl.eta, double(ctl.it), ctl.g};
-  CK(cudaMemcpyAsync(eta_dev_out, res, sizeof res, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  return TOPO_OK;
+  return fail(ctx, TOPO_ENONMONO, "eta solve did not terminate");
 }
 
 // ------------------------------------------------------------------- OC
@@ -1061,7 +1067,7 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   mg_state_free(ctx->mg);
   ctx->mg = nullptr;
   ctx->d_kwp.release();
-  for (DevBuf* b : {&ctx->d_map, &ctx->d_clean}) b->release();
+  for (DevBuf* b : {&ctx->d_map, &ctx->d_clean, &ctx->eta_dev}) b->release();
   for (DevBuf* b : {&ctx->d_csc_tab, &ctx->d_csc_int, &ctx->csc_colptr, &ctx->csc_rows, &ctx->csc_E}) b->release();
   for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_w3, &ctx->d_ke_lower, &ctx->d_ke_full, &ctx->d_state, &ctx->hs, &ctx->hs_st,
                     &ctx->cw, &ctx->x_st, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,

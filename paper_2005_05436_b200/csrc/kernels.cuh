@@ -825,6 +825,49 @@ __global__ void __launch_bounds__(kThreads) k_eta_partials(EtaArgs A, double eta
     for (int q = 0; q < 4; ++q) A.partials[4 * blockIdx.x + q] = red[q];
 }
 
+// Multi-GPU eta without host round trips: the Newton state lives on the
+// device; per evaluation partials -> on-device sum -> allreduce (NCCL, on the
+// stream) -> one-thread Newton step. Evaluations after convergence are no-ops,
+// so the host launches them in batches and checks `done` once per batch.
+struct EtaDev {
+  EtaCtl ctl;
+  double sum_t, n_act;
+};
+
+__global__ void k_eta_dev_init(EtaDev* st, double eta0) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) st->ctl.init(eta0);
+}
+
+__global__ void __launch_bounds__(kThreads) k_eta_partials_dev(EtaArgs A, const EtaDev* st,
+                                                               int first) {
+  if (st->ctl.done) return;
+  __shared__ double scratch[4 * 32];
+  double red[4];
+  const double eta = st->ctl.eta;
+  if (first)
+    eta_block_eval<true>(A, eta, red);
+  else
+    eta_block_eval<false>(A, eta, red);
+  block_sum<4>(red, scratch);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 4; ++q) A.partials[4 * blockIdx.x + q] = red[q];
+}
+
+// sums: the allreduced (sum th, sum slope, sum t, active count) at ctl.eta
+__global__ void k_eta_dev_step(EtaDev* st, const double* __restrict__ sums, int first, double beta,
+                               double mtotal, double* __restrict__ result) {
+  if (threadIdx.x != 0 || blockIdx.x != 0 || st->ctl.done) return;
+  if (first) {
+    st->sum_t = sums[2];
+    st->n_act = sums[3];
+  }
+  const double g = eta_mismatch_from_sums(beta, st->ctl.eta, sums[0], st->sum_t, st->n_act, mtotal);
+  st->ctl.feed(g, sums[1] / mtotal);
+  result[0] = st->ctl.eta;
+  result[1] = double(st->ctl.it);
+  result[2] = st->ctl.g;
+}
+
 // ============================================================================
 // K3a: projection + SIMP + sensitivity + pre-adjoint fields (one element/thread)
 //   filter.hpp:137-154, fea.hpp:135-146, fea.hpp:248-272, filter.hpp:170

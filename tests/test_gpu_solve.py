@@ -87,3 +87,40 @@ def test_stiffness_operator_variants(P, grid):
     if cfg.m <= 20000:
         yr = _numpy_apply(P, cfg, sK, x)
         assert rel(y0, yr) <= 1e-13, rel(y0, yr)
+
+
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2005_05436_b200 as P
+from paper_2005_05436_b200.configs import CONFIGS, fixed_dofs, load_vector
+cfg = CONFIGS[5].scaled(32, 16, 16)
+sK = 1e-9 + np.random.default_rng(7).uniform(0.05, 1.0, cfg.m) ** 3
+with P.Context(*cfg.grid, rmin=1.0, nu=cfg.nu) as ctx:
+    u, it, rr = ctx.solve_state(sK, load_vector(cfg), fixed_dofs(cfg), rtol=1e-12, multigrid=True)
+np.save(sys.argv[2], u)
+print(it, rr)
+"""
+
+
+# the multigrid's alternative code paths (env switches, read once per process):
+# each must solve to the same answer
+@pytest.mark.parametrize("env", [{}, {"TOPO_MG_FUSE": "1"}, {"TOPO_MG_MF1": "0"},
+                                 {"TOPO_MG_NODE": "0"}, {"TOPO_MG_TILE": "0"}])
+def test_multigrid_variants_agree(P, tmp_path, env):
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "u.npy"
+    e = dict(os.environ, TOPO_MG_MIN_DOFS="500", **env)
+    r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root, str(out)], env=e,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    it, rr = r.stdout.split()
+    assert float(rr) <= 1e-12 and 0 < int(it) < 200
+    u = np.load(out)
+    from paper_2005_05436_b200.configs import CONFIGS, fixed_dofs, load_vector
+    cfg = CONFIGS[5].scaled(32, 16, 16)
+    sK = 1e-9 + np.random.default_rng(7).uniform(0.05, 1.0, cfg.m) ** 3
+    with P.Context(*cfg.grid, rmin=1.0, nu=cfg.nu) as ctx:
+        uj, _, _ = ctx.solve_state(sK, load_vector(cfg), fixed_dofs(cfg), rtol=1e-12)
+    assert rel(u, uj) <= 1e-9, rel(u, uj)
