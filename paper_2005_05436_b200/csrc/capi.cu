@@ -2799,6 +2799,7 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   E.partials = ctx->partials.as<double>();
   k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(E.partials, nbe, 1, res + 4);
   LAUNCHED();
+  if (ctx->comm) TRY(comm_allreduce(ctx->comm, ctx, res + 4, 1));  // c, on the stream
   if (ctx->comm) {
     TRY(comm_halo(ctx->comm, ctx, ctx->a1_st.as<double>()));
     TRY(comm_halo(ctx->comm, ctx, ctx->a2_st.as<double>()));
@@ -2862,7 +2863,6 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     bis = int32_t(r[1]);
     ev = int32_t(r[2]);
   }
-  if (ctx->comm) TRY(comm_allreduce_host(ctx->comm, ctx, &c, 1));
   if (ctx->timing) {
     for (int q = 0; q < TOPO_NSTAGES; ++q) {
       float ms = 0.f;
