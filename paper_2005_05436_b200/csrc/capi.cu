@@ -2185,7 +2185,8 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     const MgGeo c = lvg.back().g;  // (copy: emplace_back below may reallocate)
     const bool even = c.nelx % 2 == 0 && c.nely % 2 == 0 && (dim == 2 || c.nz % 2 == 0);
     static const long long min_dofs =
-        getenv("TOPO_MG_MIN_DOFS") ? atoll(getenv("TOPO_MG_MIN_DOFS")) : 20000;  // tests
+        getenv("TOPO_MG_MIN_DOFS") ? atoll(getenv("TOPO_MG_MIN_DOFS")) : 500;  // (measured:
+    // C5 to 1e-6 in 32 MGCG iterations with a ~300-DOF coarsest grid, 59 with ~13k)
     if (!even || c.n <= min_dofs || lvg.size() >= 8) break;
     lvg.emplace_back();
     lvg.back().g = geo(c.nelx / 2, c.nely / 2, dim == 3 ? c.nz / 2 : 0);
@@ -2371,7 +2372,18 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     const int nbn = grid_for(ctx, L.g.nn);
     const double *K = L.K.as<double>(), *b = L.b.as<double>(), *dg = L.diag.as<double>();
     const double w = L.omega;
-#define MG_NODE(D, M) k_mg_node<D, M><<<nbn, 256, 0, ctx->stream>>>(L.g, K, xin, b, dg, w, yout)
+    // node-per-thread on big levels, 2^dim lanes per row on small ones (latency)
+    static const char* nl = getenv("TOPO_MG_LANES_MAX");  // rows up to which lanes are used
+    const long long lanes_max = nl ? atoll(nl) : (1LL << 62);
+    const bool lanes = L.g.n <= lanes_max;
+    const int nbl = grid_for(ctx, L.g.n * (dim == 3 ? 8 : 4));
+#define MG_NODE(D, M)                                                                         \
+  do {                                                                                        \
+    if (lanes)                                                                                \
+      k_mg_node_lanes<D, M><<<nbl, 256, 0, ctx->stream>>>(L.g, K, xin, b, dg, w, yout);        \
+    else                                                                                      \
+      k_mg_node<D, M><<<nbn, 256, 0, ctx->stream>>>(L.g, K, xin, b, dg, w, yout);              \
+  } while (0)
     if (dim == 3) {
       if (mode == 0) MG_NODE(3, 0); else if (mode == 1) MG_NODE(3, 1); else MG_NODE(3, 2);
     } else {

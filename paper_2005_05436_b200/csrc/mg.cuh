@@ -701,14 +701,45 @@ __device__ __forceinline__ double mg_row_lanes(const MgGeo& L, const double* __r
     if (ex >= 0 && ex < L.nelx && ez >= 0 && ez < L.nz && ey >= 0 && ey < L.nely) {
       const long long e = ((long long)ex * L.nz + ez) * L.nely + ey;
       const int a = mg_local(DIM, iy - ey, iz - ez, ix - ex);
-      const double* row = K + e * (long long)(D * D) + (DIM * a + c) * D;
+      const double2* row =
+          reinterpret_cast<const double2*>(K + e * (long long)(D * D) + (DIM * a + c) * D);
 #pragma unroll
-      for (int j = 0; j < D; ++j) s = fma(__ldg(row + j), __ldg(x + mg_dof<DIM>(L, ex, ez, ey, j)), s);
+      for (int j = 0; j < D / 2; ++j) {
+        const double2 k = __ldg(row + j);
+        s = fma(k.x, __ldg(x + mg_dof<DIM>(L, ex, ez, ey, 2 * j)), s);
+        s = fma(k.y, __ldg(x + mg_dof<DIM>(L, ex, ez, ey, 2 * j + 1)), s);
+      }
     }
   }
 #pragma unroll
   for (int o = NN / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, NN);
   return s;
+}
+
+// k_mg_node with NN lanes per row (stored levels: short dependency chains,
+// NN x the threads). MODE as k_mg_node.
+template <int DIM, int MODE>
+__global__ void __launch_bounds__(256) k_mg_node_lanes(MgGeo L, const double* __restrict__ K,
+                                                       const double* __restrict__ x,
+                                                       const double* __restrict__ b,
+                                                       const double* __restrict__ diag, double w,
+                                                       double* __restrict__ y) {
+  constexpr int NN = MgT<DIM>::NN;
+  const int q = threadIdx.x % NN;
+  const long long S = (long long)gridDim.x * blockDim.x / NN;
+  const long long nrounds = (L.n + S - 1) / S;
+  for (long long r = 0; r < nrounds; ++r) {  // uniform trip count: the shuffles need all lanes
+    const long long d = r * S + (blockIdx.x * (long long)blockDim.x + threadIdx.x) / NN;
+    const bool valid = d < L.n;
+    const double ax = mg_row_lanes<DIM>(L, K, x, d, q, valid);
+    if (!valid || q != 0) continue;
+    if (MODE == 0)
+      y[d] = ax;
+    else if (MODE == 1)
+      y[d] = L.fixed[d] ? 0.0 : x[d] + w * (b[d] - ax) / diag[d];
+    else
+      y[d] = L.fixed[d] ? 0.0 : b[d] - ax;
+  }
 }
 
 // The coarsest level's Jacobi sweeps in one cooperative launch: x = w b / diag,
