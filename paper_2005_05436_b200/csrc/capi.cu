@@ -2141,9 +2141,9 @@ static void mg_interp(int dim, std::vector<double>& Q) {
 // redesign loop solves on the same grid every iteration)
 struct MgState {
   std::vector<MgLevel> lv;
-  DevBuf fb, cg, part, sc, dQ, dKp, dM;
+  DevBuf fb, cg, part, sc, dQ, dKp, dM, dAc;
   void release() {
-    for (DevBuf* b : {&fb, &cg, &part, &sc, &dQ, &dKp, &dM}) b->release();
+    for (DevBuf* b : {&fb, &cg, &part, &sc, &dQ, &dKp, &dM, &dAc}) b->release();
     for (auto& L : lv)
       for (DevBuf* b : {&L.fixed, &L.K, &L.diag, &L.x, &L.b, &L.r, &L.y}) b->release();
     lv.clear();
@@ -2348,6 +2348,36 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     }
     LAUNCHED();
   }
+  // exact coarsest solve when the coarsest stored level is small: its dense
+  // matrix gathered and inverted once per solve (Gauss-Jordan, one block)
+  static const char* dce = getenv("TOPO_MG_DENSE_COARSE");
+  const MgLevel& Lc = lv.back();
+  const bool dense_coarse = node_ops && lv.size() >= 2 && Lc.g.n <= kCoarseDenseMax &&
+                            !(mf1 && lv.size() == 2) && !(dce && dce[0] == '0');
+  if (dense_coarse) {
+    const long long nc = Lc.g.n;
+    CK(ms.dAc.ensure(sizeof(double) * size_t(nc * nc + 4 * nc)));
+    if (dim == 3)
+      k_mg_dense_gather<3><<<grid_for(ctx, nc * nc), kThreads, 0, ctx->stream>>>(
+          Lc.g, Lc.K.as<double>(), ms.dAc.as<double>());
+    else
+      k_mg_dense_gather<2><<<grid_for(ctx, nc * nc), kThreads, 0, ctx->stream>>>(
+          Lc.g, Lc.K.as<double>(), ms.dAc.as<double>());
+    LAUNCHED();
+    {
+      int occ = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_dense_inverse, 256, 0));
+      const int nb = std::max(1, std::min(occ * ctx->sm_count,
+                                          int(std::min<long long>(ctx->sm_count, (nc * nc + 255) / 256))));
+      int ni = int(nc);
+      double* Ad = ms.dAc.as<double>();
+      double* rbuf = Ad + nc * nc;
+      double* cbuf = rbuf + 2 * nc;
+      void* args[] = {&ni, &Ad, &rbuf, &cbuf};
+      CK(cudaLaunchCooperativeKernel((const void*)k_dense_inverse, nb, 256, args, 0, ctx->stream));
+      LAUNCHED();
+    }
+  }
   // fine level in Walsh form when Ke allows (plain symmetric block entries)
   DevBuf dkwb;
   const double* dkw = nullptr;
@@ -2425,6 +2455,7 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   CK(part.ensure(sizeof(double) * 2 * size_t(grid_for(ctx, n))));
   CK(sc.ensure(sizeof(double) * 8));
   for (size_t l = 0; l < lv.size(); ++l) {
+    if (dense_coarse && l + 1 == lv.size()) break;  // (solved exactly: no smoother)
     MgLevel& L = lv[l];
     const long long nl = L.g.n;
     const int nbd = grid_for(ctx, nl);
@@ -2471,6 +2502,12 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     const int sweeps = last ? ncoarse : nu;
     const double w = L.omega;
     const bool nodes = l > 0 && node_ops && !(l == 1 && mf1);
+    if (nodes && last && dense_coarse) {  // exact coarsest solve: x = A^-1 b
+      k_dense_matvec<<<std::max(1, int((L.g.n * 32 + 255) / 256)), 256, 0, ctx->stream>>>(
+          int(L.g.n), ms.dAc.as<double>(), L.b.as<double>(), L.x.as<double>());
+      LAUNCHED();
+      return TOPO_OK;
+    }
     if (nodes && last) {  // coarsest level: all sweeps in one cooperative launch
       const int nbn = std::max(1, std::min(grid_for(ctx, L.g.n * (dim == 3 ? 8 : 4)), coarse_grid));
       MgGeo g = L.g;

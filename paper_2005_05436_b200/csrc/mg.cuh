@@ -706,8 +706,9 @@ __device__ __forceinline__ double mg_row_lanes(const MgGeo& L, const double* __r
 #pragma unroll
       for (int j = 0; j < D / 2; ++j) {
         const double2 k = __ldg(row + j);
-        s = fma(k.x, __ldg(x + mg_dof<DIM>(L, ex, ez, ey, 2 * j)), s);
-        s = fma(k.y, __ldg(x + mg_dof<DIM>(L, ex, ez, ey, 2 * j + 1)), s);
+        const long long d0 = mg_dof<DIM>(L, ex, ez, ey, 2 * j), d1 = mg_dof<DIM>(L, ex, ez, ey, 2 * j + 1);
+        s = fma(k.x, __ldg(x + d0), s);
+        s = fma(k.y, __ldg(x + d1), s);
       }
     }
   }
@@ -739,6 +740,93 @@ __global__ void __launch_bounds__(256) k_mg_node_lanes(MgGeo L, const double* __
       y[d] = L.fixed[d] ? 0.0 : x[d] + w * (b[d] - ax) / diag[d];
     else
       y[d] = L.fixed[d] ? 0.0 : b[d] - ax;
+  }
+}
+
+// Exact solve on a small coarsest level (n <= kCoarseDenseMax): the dense
+// matrix is gathered from the element matrices (fixed DOFs: identity rows and
+// columns), inverted once per solve by Gauss-Jordan in one block (SPD, no
+// pivoting), and each V-cycle applies x = A^-1 b with one warp per row.
+constexpr int kCoarseDenseMax = 1024;
+
+// A[i][j] = sum over the elements holding both DOFs (ascending) of K_e(li, lj)
+template <int DIM>
+__global__ void k_mg_dense_gather(MgGeo L, const double* __restrict__ K, double* __restrict__ A) {
+  constexpr int NN = MgT<DIM>::NN, D = MgT<DIM>::D;
+  const long long n = L.n;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n * n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long i = t / n, j = t - i * n;
+    if (L.fixed[i] || L.fixed[j]) {
+      A[t] = i == j ? 1.0 : 0.0;
+      continue;
+    }
+    const long long ni = i / DIM, nj = j / DIM;
+    const int ci = int(i - ni * DIM), cj = int(j - nj * DIM);
+    const int iy = int(ni % L.ny1), iz = int((ni / L.ny1) % L.nz1), ix = int(ni / L.pl);
+    const int jy = int(nj % L.ny1), jz = int((nj / L.ny1) % L.nz1), jx = int(nj / L.pl);
+    double a = 0.0;
+    for (int q = 0; q < NN; ++q) {  // elements around node i, ascending
+      const int ex = ix - 1 + (q >> (DIM == 3 ? 2 : 1) & 1);
+      const int ez = DIM == 3 ? iz - 1 + (q >> 1 & 1) : 0;
+      const int ey = iy - 1 + (q & 1);
+      if (ex < 0 || ex >= L.nelx || ez < 0 || ez >= L.nz || ey < 0 || ey >= L.nely) continue;
+      const int oj = jx - ex, ok = jz - ez, oi = jy - ey;  // node j inside this element?
+      if (oj < 0 || oj > 1 || oi < 0 || oi > 1 || ok < 0 || ok > (DIM == 3 ? 1 : 0)) continue;
+      const long long e = ((long long)ex * L.nz + ez) * L.nely + ey;
+      const int li = DIM * mg_local(DIM, iy - ey, iz - ez, ix - ex) + ci;
+      const int lj = DIM * mg_local(DIM, oi, ok, oj) + cj;
+      a += K[e * (long long)(D * D) + (long long)lj * D + li];
+    }
+    A[t] = a;
+  }
+}
+
+// in-place Gauss-Jordan inverse of an SPD n x n matrix (row-major, no
+// pivoting), cooperative: one grid barrier per pivot. Step k reads the pivot
+// row and column as they were at its start from double buffers (rb, cb: 2 x n
+// each), which the same step refills for pivot k + 1.
+__global__ void __launch_bounds__(256) k_dense_inverse(int n, double* __restrict__ A,
+                                                       double* __restrict__ rb,
+                                                       double* __restrict__ cb) {
+  cg::grid_group grid = cg::this_grid();
+  const long long nn = (long long)n * n;
+  const long long S = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (long long t = t0; t < n; t += S) {
+    rb[t] = A[t];                  // row 0
+    cb[t] = A[t * n];              // column 0
+  }
+  for (int k = 0; k < n; ++k) {
+    grid.sync();
+    const double* r = rb + (k & 1) * n;
+    const double* c = cb + (k & 1) * n;
+    double* r1 = rb + ((k + 1) & 1) * n;
+    double* c1 = cb + ((k + 1) & 1) * n;
+    const double inv = 1.0 / r[k];
+    for (long long t = t0; t < nn; t += S) {
+      const int i = int(t / n), j = int(t - (long long)i * n);
+      const double rk = (j == k ? 1.0 : r[j]) * inv;  // the scaled pivot row
+      const double v = i == k ? rk : fma(-c[i], rk, j == k ? 0.0 : A[t]);
+      A[t] = v;
+      if (j == k + 1) c1[i] = v;
+      if (i == k + 1) r1[j] = v;
+    }
+  }
+}
+
+// x = A^-1 b, one warp per row (fixed-order lane sums + shuffle tree)
+__global__ void k_dense_matvec(int n, const double* __restrict__ Ainv, const double* __restrict__ b,
+                               double* __restrict__ x) {
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n;
+       i += (gridDim.x * blockDim.x) >> 5) {
+    const double* r = Ainv + (long long)i * n;
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s = fma(__ldg(r + j), __ldg(b + j), s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) x[i] = s;
   }
 }
 
