@@ -11,6 +11,7 @@
 // and link libtopo_b200.so. See INTEGRATION.md.
 #pragma once
 
+#include <chrono>
 #include <cstring>
 #include <functional>
 #include <limits>
@@ -159,6 +160,17 @@ inline SymmetricSparseMatrix assemble_lower(const Eigen::VectorXd& sK, Device& d
 /// the device's matrix-free PCG (geometric-multigrid V-cycle preconditioner,
 /// Jacobi when the grid cannot be coarsened) to ||r|| <= rtol ||f|| (the
 /// reference factorises; the two agree to the solver tolerance)
+/// per-thread totals of solve_state calls (wall seconds incl. host copies,
+/// PCG iterations); reset by the caller
+struct SolveStats {
+  double seconds = 0.0;
+  long long iterations = 0, calls = 0;
+};
+inline SolveStats& solve_stats() {
+  static thread_local SolveStats s;
+  return s;
+}
+
 inline Eigen::VectorXd solve_state(const Eigen::VectorXd& sK, const LoadCase& load, Device& dev,
                                    double rtol = 1e-12, int maxit = 1000000) {
   detail::need(sK.size(), dev.numElements(), "solve");
@@ -167,9 +179,14 @@ inline Eigen::VectorXd solve_state(const Eigen::VectorXd& sK, const LoadCase& lo
   Eigen::VectorXd u(dev.numDofs());
   std::int32_t it = 0;
   double rr = 0;
+  const auto t0 = std::chrono::steady_clock::now();
   check(topo_solve_state_mg(dev.handle(), sK.data(), load.f.data(), load.fixed.data(),
                             std::int64_t(load.fixed.size()), rtol, maxit, u.data(), &it, &rr),
         dev.handle());
+  SolveStats& st = solve_stats();
+  st.seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  st.iterations += it;
+  ++st.calls;
   if (!(rr <= rtol)) throw std::runtime_error("solve: CG did not reach the tolerance");
   return u;
 }

@@ -49,8 +49,12 @@ static int bench(int nelx, int nely, int nelz, int maxit) {
   cfg.ft = 3, cfg.rmin = 1.5, cfg.volfrac = 0.12, cfg.move = 0.1;
   const RunResult g = gpu::run_optimization(
       cfg, preset_cantilever_3d(nelx, nely, nelz), [](const IterationRecord& r) {
-        std::printf("it %3d  c %.6e  v %.4f  ch %.3e  eta %.6f  bis %3d  %.3f s\n", r.loop, r.c,
-                    r.v, r.resnorm, r.eta, r.bisections, r.seconds);
+        gpu::SolveStats& st = gpu::solve_stats();
+        std::printf("it %3d  c %.6e  v %.4f  ch %.3e  eta %.6f  bis %3d  %.3f s  (solve %.3f s, "
+                    "%lld MGCG its)\n",
+                    r.loop, r.c, r.v, r.resnorm, r.eta, r.bisections, r.seconds, st.seconds,
+                    st.iterations);
+        st = gpu::SolveStats{};
       }, {}, 1e-6);
   std::printf("total %.2f s for %zu iterations\n", g.wallSeconds, g.history.size());
   return 0;
