@@ -120,6 +120,13 @@ const char* topo_last_error(const topo_ctx* ctx);
 topo_status topo_set_stream(topo_ctx* ctx, void* cuda_stream);
 topo_status topo_sync(topo_ctx* ctx);
 topo_status topo_device_buffer(topo_ctx* ctx, int which, void** ptr, int64_t* count);
+/* device memory for callers without a CUDA runtime of their own (the C++
+ * adapter's device-resident redesign loop): allocate / free on the context's
+ * device, and a copy in any direction ordered on the context stream
+ * (synchronous at return) */
+topo_status topo_device_alloc(topo_ctx* ctx, int64_t bytes, void** ptr);
+topo_status topo_device_free(topo_ctx* ctx, void* ptr);
+topo_status topo_copy(topo_ctx* ctx, void* dst, const void* src, int64_t bytes);
 /* sizes: m (local elements), n (local DOFs), P (pairs/element), ntaps, reach,
  * j0, j1 */
 topo_status topo_ctx_info(const topo_ctx* ctx, int64_t* m, int64_t* n, int32_t* P,

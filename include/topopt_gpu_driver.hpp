@@ -9,9 +9,109 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 
 namespace topopt {
 namespace gpu {
+
+namespace detail {
+// device buffer through the C-ABI (the header has no CUDA runtime of its own)
+struct DevVec {
+  topo_ctx* h = nullptr;
+  double* p = nullptr;
+  DevVec(topo_ctx* ctx, std::int64_t n) : h(ctx) {
+    void* q = nullptr;
+    check(topo_device_alloc(h, std::int64_t(sizeof(double)) * n, &q), h);
+    p = static_cast<double*>(q);
+  }
+  ~DevVec() { topo_device_free(h, p); }
+  DevVec(const DevVec&) = delete;
+  DevVec& operator=(const DevVec&) = delete;
+};
+}  // namespace detail
+
+/// The device-resident form of the loop below for the top3D125 default (ft = 3,
+/// OC bisection, no Anderson extrapolation, no probe): design, filtered and
+/// physical fields, moduli, displacements and the updated design stay in
+/// device memory; per iteration only xPhys (residual, volume) and the new
+/// design (nondiscreteness) come back to the host. Stages: filter + pin, eta
+/// solve, projection, SIMP moduli, multigrid solve, then the fused pass with
+/// the solved eta (sensitivity, back-filters, OC) -- the same kernels as the
+/// stage-by-stage loop.
+inline void run_loop_device(const RunConfig& cfg, const Problem& prob, Device& dev,
+                            Eigen::VectorXd& x, double& penal, double& beta, double& eta,
+                            double& ch, Eigen::VectorXd& xPrevPhys, RunResult& result,
+                            const RecordSink& sink, double solve_rtol) {
+  topo_ctx* h = dev.handle();
+  const std::int64_t m = dev.numElements(), n = dev.numDofs();
+  detail::DevVec x_d(h, m), xn_d(h, m), xt_d(h, m), xp_d(h, m), e_d(h, m), f_d(h, n), u_d(h, n);
+  check(topo_copy(h, x_d.p, x.data(), std::int64_t(sizeof(double)) * m), h);
+  check(topo_copy(h, f_d.p, prob.load.f.data(), std::int64_t(sizeof(double)) * n), h);
+  double* xcur = x_d.p;
+  double* xnext = xn_d.p;
+  Eigen::VectorXd xPhys(m);
+  for (int loop = 1; loop <= cfg.maxit && ch > cfg.tol; ++loop) {
+    const auto iterStart = std::chrono::steady_clock::now();
+    // RL.1 physical density field
+    check(topo_filter(h, xcur, xt_d.p, 1), h);
+    double etaNew = eta;
+    std::int32_t etaIts = 0;
+    check(topo_solve_eta(h, xt_d.p, beta, eta, &etaNew, &etaIts), h);
+    eta = etaNew;
+    check(topo_project(h, xt_d.p, eta, beta, xp_d.p), h);
+    check(topo_copy(h, xPhys.data(), xp_d.p, std::int64_t(sizeof(double)) * m), h);
+    ch = (xPhys - xPrevPhys).norm() / std::sqrt(double(m));
+    xPrevPhys = xPhys;
+    // RL.2 equilibrium
+    const topo_simp simp{cfg.e0, cfg.eMin, penal};
+    check(topo_simp_interpolate(h, xp_d.p, &simp, e_d.p, nullptr), h);
+    std::int32_t its = 0;
+    double rr = 0.0;
+    const auto t0 = std::chrono::steady_clock::now();
+    check(topo_solve_state_mg(h, e_d.p, f_d.p, prob.load.fixed.data(),
+                              std::int64_t(prob.load.fixed.size()), solve_rtol, 1000000, u_d.p,
+                              &its, &rr),
+          h);
+    if (!(rr <= solve_rtol)) throw std::runtime_error("solve: CG did not reach the tolerance");
+    SolveStats& st = solve_stats();
+    st.seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    st.iterations += its;
+    ++st.calls;
+    // RL.3 + RL.4 sensitivities, back-filters and the OC update in one pass at this eta
+    topo_pass_params pp{};
+    pp.simp = simp;
+    pp.beta = beta;
+    pp.eta0 = eta;
+    pp.move = cfg.move;
+    pp.volfrac = cfg.volfrac;
+    pp.eta_override = eta;
+    pp.volume_mode = TOPO_VOL_FILTERED;
+    pp.write_sk = 0;
+    topo_pass_out po{};
+    po.xNew = xnext;
+    check(topo_design_pass(h, xcur, u_d.p, &pp, &po), h);
+    std::swap(xcur, xnext);
+    check(topo_copy(h, x.data(), xcur, std::int64_t(sizeof(double)) * m), h);
+    const double penalUsed = penal, betaUsed = beta;
+    if (cfg.penalCont) penal = apply_continuation(penal, *cfg.penalCont, loop);
+    if (cfg.betaCont) beta = apply_continuation(beta, *cfg.betaCont, loop);
+    // RL.5 record
+    IterationRecord rec;
+    rec.loop = loop;
+    rec.c = po.c;
+    rec.v = xPhys.mean();
+    rec.resnorm = ch;
+    rec.mnd = nondiscreteness(x);
+    rec.penal = penalUsed;
+    rec.beta = betaUsed;
+    rec.eta = eta;
+    rec.bisections = po.bisections;
+    rec.seconds =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - iterStart).count();
+    if (sink) sink(rec);
+    result.history.push_back(rec);
+  }
+}
 
 /// driver.hpp:137-265 with the equilibrium solved by solve_state (rtol
 /// solve_rtol) instead of the Cholesky factorisation.
@@ -53,7 +153,12 @@ inline RunResult run_optimization(const RunConfig& cfg, const Problem& prob,
                            : cfg.ft == 2 ? VolumeMode::Projected
                                          : VolumeMode::Filtered;
 
-  for (int loop = 1; loop <= cfg.maxit && ch > cfg.tol; ++loop) {
+  const char* dl = std::getenv("TOPO_LOOP_DEVICE");
+  const bool device_loop = cfg.ft == 3 && cfg.update != UpdateStrategy::PrimalDual &&
+                           !cfg.accel.enabled && !probe && !(dl && dl[0] == '0');
+  if (device_loop)
+    run_loop_device(cfg, prob, dev, x, penal, beta, eta, ch, xPrevPhys, result, sink, solve_rtol);
+  for (int loop = 1; !device_loop && loop <= cfg.maxit && ch > cfg.tol; ++loop) {
     const auto iterStart = std::chrono::steady_clock::now();
     // RL.1 physical density field
     Eigen::VectorXd xTilde = apply_filter(x, dev);

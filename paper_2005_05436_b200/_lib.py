@@ -31,6 +31,7 @@ EXPORTS = [
     "topo_nccl_unique_id", "topo_comm_init_host", "topo_slab_plan", "topo_fp64_peak",
     "topo_csc_pattern", "topo_csc_values", "topo_csc_set_fixed", "topo_oc_primal_dual",
     "topo_solve_state", "topo_solve_state_mg", "topo_apply_stiffness",
+    "topo_device_alloc", "topo_device_free", "topo_copy",
 ]
 STAGES = ["filter", "eta", "elem", "adjoint", "oc", "sk_store", "pass"]
 
@@ -139,6 +140,9 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         "topo_solve_state_mg": (C.c_int, [vp, vp, vp, vp, C.c_int64, C.c_double, C.c_int32, vp,
                                           vp, vp]),
         "topo_apply_stiffness": (C.c_int, [vp, vp, vp, vp, C.c_int32]),
+        "topo_device_alloc": (C.c_int, [vp, C.c_int64, vp]),
+        "topo_device_free": (C.c_int, [vp, vp]),
+        "topo_copy": (C.c_int, [vp, vp, vp, C.c_int64]),
         "topo_host_oc_replay": (C.c_int, [p(OcParams), C.c_double, SFUN, vp, C.c_int,
                                           p(C.c_double), p(C.c_int32), p(C.c_int32),
                                           p(C.c_double), p(C.c_int32)]),

@@ -1182,6 +1182,27 @@ topo_status topo_device_buffer(topo_ctx* ctx, int which, void** ptr, int64_t* co
   return TOPO_OK;
 }
 
+topo_status topo_device_alloc(topo_ctx* ctx, int64_t bytes, void** ptr) {
+  if (!ctx || !ptr || bytes < 0) return TOPO_EINVAL;
+  *ptr = nullptr;
+  CK(cudaMalloc(ptr, size_t(bytes > 0 ? bytes : 16)));
+  return TOPO_OK;
+}
+
+topo_status topo_device_free(topo_ctx* ctx, void* ptr) {
+  if (!ctx) return TOPO_EINVAL;
+  if (ptr) CK(cudaFree(ptr));
+  return TOPO_OK;
+}
+
+topo_status topo_copy(topo_ctx* ctx, void* dst, const void* src, int64_t bytes) {
+  if (!ctx || bytes < 0 || (bytes > 0 && (!dst || !src))) return TOPO_EINVAL;
+  if (bytes == 0) return TOPO_OK;
+  CK(cudaMemcpyAsync(dst, src, size_t(bytes), cudaMemcpyDefault, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return TOPO_OK;
+}
+
 topo_status topo_filter_taps(topo_ctx* ctx, int32_t* di, int32_t* dj, int32_t* dk, double* w) {
   if (!ctx) return TOPO_EINVAL;
   for (size_t t = 0; t < ctx->w.size(); ++t) {
