@@ -2373,7 +2373,9 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   // matrix gathered and inverted once per solve (Gauss-Jordan, one block)
   static const char* dce = getenv("TOPO_MG_DENSE_COARSE");
   const MgLevel& Lc = lv.back();
-  const bool dense_coarse = node_ops && lv.size() >= 2 && Lc.g.n <= kCoarseDenseMax &&
+  static const char* dmx = getenv("TOPO_MG_DENSE_MAX");  // experiments
+  const long long dense_max = dmx ? atoll(dmx) : kCoarseDenseMax;
+  const bool dense_coarse = node_ops && lv.size() >= 2 && Lc.g.n <= dense_max &&
                             !(mf1 && lv.size() == 2) && !(dce && dce[0] == '0');
   if (dense_coarse) {
     const long long nc = Lc.g.n;
