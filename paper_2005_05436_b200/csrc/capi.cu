@@ -60,6 +60,7 @@ bool is_device_ptr(const void* p) {
 
 struct MgState;
 void mg_state_free(MgState*);
+void solver_destroy(void*);
 
 struct topo_ctx {
   std::string err;
@@ -107,6 +108,7 @@ struct topo_ctx {
   DevBuf sK, iK, jK;
   DevBuf eta_dev;  // EtaDev: multi-GPU Newton state
   struct MgState* mg = nullptr;  // multigrid levels and scratch, kept between solves
+  void* cusolver = nullptr;      // cusolverDn handle (coarsest-grid inverse), lazily created
   double kwp_host[48] = {};
   DevBuf d_kwp;  // Walsh blocks, plain (k00 k01 k02 k11 k12 k22 per signature), for k_mg_apply_tile
   DevBuf partials, partials0, result;
@@ -1066,6 +1068,8 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   if (ctx->comm) comm_destroy(ctx->comm);
   mg_state_free(ctx->mg);
   ctx->mg = nullptr;
+  solver_destroy(ctx->cusolver);
+  ctx->cusolver = nullptr;
   ctx->d_kwp.release();
   for (DevBuf* b : {&ctx->d_map, &ctx->d_clean, &ctx->eta_dev}) b->release();
   for (DevBuf* b : {&ctx->d_csc_tab, &ctx->d_csc_int, &ctx->csc_colptr, &ctx->csc_rows, &ctx->csc_E}) b->release();
@@ -2127,6 +2131,54 @@ topo_status topo_solve_state(topo_ctx* ctx, const double* sK, const double* f,
 }
 
 // ------------------------------------------- multigrid-preconditioned solve
+// cuSOLVER (dlopen'ed; the library is used only for the coarsest grid's dense
+// Cholesky inverse at solve setup): potrf + potri on the device
+#include <dlfcn.h>
+namespace {
+struct SolverApi {
+  void* h = nullptr;
+  bool tried = false;
+  typedef int (*Create_t)(void**);
+  typedef int (*SetStream_t)(void*, cudaStream_t);
+  typedef int (*Buf_t)(void*, int, int, double*, int, int*);
+  typedef int (*Potrf_t)(void*, int, int, double*, int, double*, int, int*);
+  Create_t Create = nullptr;
+  SetStream_t SetStream = nullptr;
+  Buf_t PotrfBuf = nullptr, PotriBuf = nullptr;
+  Potrf_t Potrf = nullptr, Potri = nullptr;
+  typedef int (*Destroy_t)(void*);
+  Destroy_t Destroy = nullptr;
+  bool load() {
+    if (tried) return h != nullptr;
+    tried = true;
+    for (const char* name : {"libcusolver.so.11", "libcusolver.so",
+                             "/usr/local/cuda/lib64/libcusolver.so.11"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    Create = (Create_t)dlsym(h, "cusolverDnCreate");
+    SetStream = (SetStream_t)dlsym(h, "cusolverDnSetStream");
+    PotrfBuf = (Buf_t)dlsym(h, "cusolverDnDpotrf_bufferSize");
+    PotriBuf = (Buf_t)dlsym(h, "cusolverDnDpotri_bufferSize");
+    Potrf = (Potrf_t)dlsym(h, "cusolverDnDpotrf");
+    Potri = (Potrf_t)dlsym(h, "cusolverDnDpotri");
+    Destroy = (Destroy_t)dlsym(h, "cusolverDnDestroy");
+    if (!Create || !SetStream || !PotrfBuf || !PotriBuf || !Potrf || !Potri) {
+      dlclose(h);
+      h = nullptr;
+    }
+    return h != nullptr;
+  }
+};
+SolverApi g_solver;
+}  // namespace
+}  // extern "C" (a C++ helper between the entry points)
+void solver_destroy(void* hnd) {
+  if (hnd && g_solver.Destroy) g_solver.Destroy(hnd);
+}
+extern "C" {
+
 namespace {
 struct MgLevel {
   MgGeo g{};
@@ -2162,9 +2214,9 @@ static void mg_interp(int dim, std::vector<double>& Q) {
 // redesign loop solves on the same grid every iteration)
 struct MgState {
   std::vector<MgLevel> lv;
-  DevBuf fb, cg, part, sc, dQ, dKp, dM, dAc;
+  DevBuf fb, cg, part, sc, dQ, dKp, dM, dAc, dWork;
   void release() {
-    for (DevBuf* b : {&fb, &cg, &part, &sc, &dQ, &dKp, &dM, &dAc}) b->release();
+    for (DevBuf* b : {&fb, &cg, &part, &sc, &dQ, &dKp, &dM, &dAc, &dWork}) b->release();
     for (auto& L : lv)
       for (DevBuf* b : {&L.fixed, &L.K, &L.diag, &L.x, &L.b, &L.r, &L.y}) b->release();
     lv.clear();
@@ -2206,8 +2258,9 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     const MgGeo c = lvg.back().g;  // (copy: emplace_back below may reallocate)
     const bool even = c.nelx % 2 == 0 && c.nely % 2 == 0 && (dim == 2 || c.nz % 2 == 0);
     static const long long min_dofs =
-        getenv("TOPO_MG_MIN_DOFS") ? atoll(getenv("TOPO_MG_MIN_DOFS")) : 500;  // (measured:
-    // C5 to 1e-6 in 32 MGCG iterations with a ~300-DOF coarsest grid, 59 with ~13k)
+        getenv("TOPO_MG_MIN_DOFS") ? atoll(getenv("TOPO_MG_MIN_DOFS")) : 2000;  // (measured:
+    // coarsest ~2k DOFs solved exactly: C5 25 MGCG iterations, a sharpening 96x48x48
+    // design 44 instead of 81 with ~300 DOFs; Jacobi sweeps on ~13k DOFs: C5 59)
     if (!even || c.n <= min_dofs || lvg.size() >= 8) break;
     lvg.emplace_back();
     lvg.back().g = geo(c.nelx / 2, c.nely / 2, dim == 3 ? c.nz / 2 : 0);
@@ -2374,7 +2427,9 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   static const char* dce = getenv("TOPO_MG_DENSE_COARSE");
   const MgLevel& Lc = lv.back();
   static const char* dmx = getenv("TOPO_MG_DENSE_MAX");  // experiments
-  const long long dense_max = dmx ? atoll(dmx) : kCoarseDenseMax;
+  // cuSOLVER's Cholesky inverse takes ~2 ms for 2k DOFs; the one-pivot-per-
+  // barrier Gauss-Jordan fallback only pays below ~1k
+  const long long dense_max = dmx ? atoll(dmx) : (g_solver.load() ? 2048 : kCoarseDenseMax);
   const bool dense_coarse = node_ops && lv.size() >= 2 && Lc.g.n <= dense_max &&
                             !(mf1 && lv.size() == 2) && !(dce && dce[0] == '0');
   if (dense_coarse) {
@@ -2387,7 +2442,33 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
       k_mg_dense_gather<2><<<grid_for(ctx, nc * nc), kThreads, 0, ctx->stream>>>(
           Lc.g, Lc.K.as<double>(), ms.dAc.as<double>());
     LAUNCHED();
-    {
+    static const char* gje = getenv("TOPO_MG_GJ");  // force the Gauss-Jordan kernel
+    bool inverted = false;
+    if (!(gje && gje[0] == '1') && g_solver.load()) {
+      // Cholesky (potrf) + inverse from it (potri, lower triangle), then mirror;
+      // the dense matrix is symmetric, so row- and column-major coincide
+      if (!ctx->cusolver) {
+        if (g_solver.Create(&ctx->cusolver) != 0) return fail(ctx, TOPO_ECUDA, "cusolverDnCreate");
+      }
+      if (g_solver.SetStream(ctx->cusolver, ctx->stream) != 0)
+        return fail(ctx, TOPO_ECUDA, "cusolverDnSetStream");
+      double* Ad = ms.dAc.as<double>();
+      const int ni = int(nc);
+      int l1 = 0, l2 = 0;
+      if (g_solver.PotrfBuf(ctx->cusolver, 0 /*lower*/, ni, Ad, ni, &l1) != 0 ||
+          g_solver.PotriBuf(ctx->cusolver, 0, ni, Ad, ni, &l2) != 0)
+        return fail(ctx, TOPO_ECUDA, "cusolver workspace query");
+      CK(ms.dWork.ensure(sizeof(double) * size_t(std::max(l1, l2) + 2)));
+      double* work = ms.dWork.as<double>();
+      int* info = reinterpret_cast<int*>(work + std::max(l1, l2));
+      if (g_solver.Potrf(ctx->cusolver, 0, ni, Ad, ni, work, l1, info) != 0 ||
+          g_solver.Potri(ctx->cusolver, 0, ni, Ad, ni, work, l2, info) != 0)
+        return fail(ctx, TOPO_ECUDA, "cusolver potrf/potri");
+      k_mirror_lower<<<grid_for(ctx, nc * nc), kThreads, 0, ctx->stream>>>(ni, Ad);
+      LAUNCHED();
+      inverted = true;
+    }
+    if (!inverted) {
       int occ = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_dense_inverse, 256, 0));
       const int nb = std::max(1, std::min(occ * ctx->sm_count,

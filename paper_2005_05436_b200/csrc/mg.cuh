@@ -815,6 +815,16 @@ __global__ void __launch_bounds__(256) k_dense_inverse(int n, double* __restrict
   }
 }
 
+// column-major lower triangle (cuSOLVER potri output) -> full symmetric matrix
+__global__ void k_mirror_lower(int n, double* __restrict__ A) {
+  const long long nn = (long long)n * n;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int j = int(t / n), i = int(t - (long long)j * n);  // column-major (i, j)
+    if (i < j) A[t] = A[(long long)i * n + j];                  // upper <- lower (j, i)
+  }
+}
+
 // x = A^-1 b, one warp per row (fixed-order lane sums + shuffle tree)
 __global__ void k_dense_matvec(int n, const double* __restrict__ Ainv, const double* __restrict__ b,
                                double* __restrict__ x) {
