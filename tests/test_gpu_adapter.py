@@ -28,3 +28,31 @@ def test_cpp_device_loop_matches_reference_driver():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failure(s)" in r.stdout
+
+
+def test_cpp_stage_loop_matches_reference_driver():
+    # the same driver tests with the device-resident ft = 3 loop switched off
+    if not os.path.exists(DRV):
+        pytest.skip("driver test binary not built (needs the reference headers at build time)")
+    r = subprocess.run([DRV], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, TOPO_LOOP_DEVICE="0"))
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failure(s)" in r.stdout
+
+
+def test_device_alloc_copy_roundtrip():
+    import ctypes as C
+    import numpy as np
+    import paper_2005_05436_b200 as P
+    with P.Context(4, 3, 2, rmin=1.5) as ctx:
+        lib = ctx.lib
+        a = np.arange(1000, dtype=np.float64)
+        b = np.zeros_like(a)
+        p = C.c_void_p()
+        assert lib.topo_device_alloc(ctx.h, a.nbytes, C.byref(p)) == 0 and p.value
+        assert lib.topo_copy(ctx.h, p, a.ctypes.data, a.nbytes) == 0
+        assert lib.topo_copy(ctx.h, b.ctypes.data, p, a.nbytes) == 0
+        assert np.array_equal(a, b)
+        assert lib.topo_copy(ctx.h, None, p, 8) != 0  # null destination: invalid argument
+        assert lib.topo_device_free(ctx.h, p) == 0
