@@ -2587,7 +2587,8 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     }
     L.omega = 1.2 / std::max(lam, 1e-30);
   }
-  const int nu = 2, ncoarse = 40;
+  static const char* nue = getenv("TOPO_MG_NU");  // experiments: sweeps per side
+  const int nu = nue ? std::max(1, atoi(nue)) : 2, ncoarse = 40;
   int coarse_grid = 0;  // resident blocks of the cooperative coarsest-level kernel
   {
     int occ = 0;
