@@ -1888,7 +1888,7 @@ static int tile_blocks(const topo_ctx* ctx, const MgGeo& L, int* xchunk, int per
   const int wave = per_sm * ctx->sm_count;
   int best = 1;
   double best_s = -1.0;
-  for (int ch = 1; ch <= std::max(1, nx1 / 4); ++ch) {
+  for (int ch = 1; ch <= std::max(1, nx1 / 2); ++ch) {  // chunks of >= 2 layers
     const int xc = (nx1 + ch - 1) / ch, nb = nyz * ((nx1 + xc - 1) / xc);
     const int waves = (nb + wave - 1) / wave;
     const double s = double(nb) / (double(waves) * wave) * double(xc) / (xc + 1);
