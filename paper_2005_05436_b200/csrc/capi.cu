@@ -491,7 +491,7 @@ int conv_blocks(const topo_ctx* ctx) {
 
 // K3b: grid sized for full occupancy (no shared-memory or barrier limits)
 // K3b. Serial (main stream): grid sized for full occupancy, static split.
-// Overlapped (aux stream, large 3D passes): 2 blocks per SM claiming work
+// Overlapped (aux stream, large 3D passes): ~2 blocks per SM claiming work
 // dynamically, so the stream keeps its rate while K3a / K4 blocks share the SMs
 // (measured on C5: 6.38 ms per pass against 6.84 ms serial).
 topo_status launch_sk(topo_ctx* ctx, const SkArgs& S, cudaStream_t st) {
@@ -499,7 +499,11 @@ topo_status launch_sk(topo_ctx* ctx, const SkArgs& S, cudaStream_t st) {
   int nb = grid_for(ctx, (G.m + 31) / 32 * 32);
   const bool ov = st == ctx->aux;
   const char* e = getenv("TOPO_SK_BPS");  // blocks per SM (experiments)
-  if (e || ov) nb = std::min(nb, ctx->sm_count * std::max(1, e ? atoi(e) : 2));
+  // overlapped: ~2.17 blocks per SM (measured on C5: 320 blocks 6.34 ms per pass
+  // against 6.40 with 296 and 6.35 with 336)
+  if (e || ov) nb = std::min(nb, e ? ctx->sm_count * std::max(1, atoi(e)) : ctx->sm_count * 13 / 6);
+  static const char* eb = getenv("TOPO_SK_BLOCKS");  // experiments: explicit grid
+  if (eb) nb = std::max(1, atoi(eb));
   SkArgs S2 = S;
   S2.counter = nullptr;
   static const char* de = getenv("TOPO_SK_DYN");
