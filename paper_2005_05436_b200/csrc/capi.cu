@@ -2433,7 +2433,9 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   static const char* dmx = getenv("TOPO_MG_DENSE_MAX");  // experiments
   // cuSOLVER's Cholesky inverse takes ~2 ms for 2k DOFs; the one-pivot-per-
   // barrier Gauss-Jordan fallback only pays below ~1k
-  const long long dense_max = dmx ? atoll(dmx) : (g_solver.load() ? 2048 : kCoarseDenseMax);
+  // (2D grids stop coarsening at odd sizes early: 75x25 = 3952 DOFs for C1-C3,
+  // exact: C3 79 MGCG iterations instead of 168 with Jacobi sweeps)
+  const long long dense_max = dmx ? atoll(dmx) : (g_solver.load() ? 4096 : kCoarseDenseMax);
   const bool dense_coarse = node_ops && lv.size() >= 2 && Lc.g.n <= dense_max &&
                             !(mf1 && lv.size() == 2) && !(dce && dce[0] == '0');
   if (dense_coarse) {
