@@ -1034,7 +1034,10 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   // all blocks resident (cooperative)
   // (small grids: fewer blocks, cheaper grid-wide barriers)
   const int want = int(std::min<long long>(1LL << 20, (G.m + 1023) / 1024));
-  ctx->coop_eta = std::max(1, std::min(ctx->sm_count * occ2, want));
+  // eta: ~1536 elements per block on small grids (cheaper grid barriers; C4
+  // 0.034 vs 0.039 ms), the full resident grid on large ones
+  const int want_eta = int(std::min<long long>(1LL << 20, (G.m + 1535) / 1536));
+  ctx->coop_eta = std::max(1, std::min(ctx->sm_count * occ2, want_eta));
   ctx->coop_blocks = std::max(1, std::min(ctx->sm_count * occ, want));
   const size_t npart = std::max<size_t>(
       {size_t(conv_blocks(ctx)) * 3, size_t(ctx->coop_blocks) * 2 * 32 * 2,
