@@ -2541,6 +2541,28 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     if (l == 0 && dkw && use_tile_op(ctx)) return launch_tile_op(ctx, L.g, E, xin, yout, nullptr);
     if (l == 1 && mf1) return launch_tile_op(ctx, L.g, E, xin, yout, nullptr, nullptr, true);
     if (l > 0 && node_ops) return node_op(l, 0, xin, yout);
+    static const char* n2 = getenv("TOPO_MG_NODE2D");
+    if (l == 0 && dim == 2 && !(n2 && n2[0] == '0')) {
+      // 2D fine level: the node-centric gather (one launch; y = 0 on fixed DOFs,
+      // which every consumer masks anyway)
+      StateGeo S2{};
+      S2.dim = 2;
+      S2.nelx = L.g.nelx;
+      S2.nely = L.g.nely;
+      S2.nz = 1;
+      S2.nz1 = 1;
+      S2.ny1 = L.g.ny1;
+      S2.pl = L.g.pl;
+      S2.nn = L.g.nn;
+      S2.E = E;
+      S2.fixed = L.g.fixed;
+      const int nbn = grid_for(ctx, L.g.nn);
+      CK(ms.dWork.ensure(std::max(ms.dWork.bytes, sizeof(double) * size_t(nbn))));
+      k_state_matvec<2><<<nbn, kThreads, 0, ctx->stream>>>(S2, ctx->d_ke_full.as<double>(), xin,
+                                                           yout, ms.dWork.as<double>());
+      LAUNCHED();
+      return TOPO_OK;
+    }
     CK(cudaMemsetAsync(yout, 0, sizeof(double) * size_t(L.g.n), ctx->stream));
     const int nb = grid_for(ctx, std::max<long long>(1, L.g.m / 8));
     const int nbw = grid_for(ctx, std::max<long long>(1, L.g.m / 8) * 32);  // warp per element
