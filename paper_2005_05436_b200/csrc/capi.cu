@@ -2189,7 +2189,8 @@ extern "C" {
 namespace {
 struct MgLevel {
   MgGeo g{};
-  DevBuf fixed, K, diag, x, b, r, y;
+  DevBuf fixed, K, diag, x, b, r, y, bdiag;  // bdiag: 3x3 block inverses (point-block Jacobi)
+  bool block = false;
   double omega = 0.6;  // damped-Jacobi weight, (4/3) / lambda_max(D^-1 A)
 };
 
@@ -2225,7 +2226,7 @@ struct MgState {
   void release() {
     for (DevBuf* b : {&fb, &cg, &part, &sc, &dQ, &dKp, &dM, &dAc, &dWork}) b->release();
     for (auto& L : lv)
-      for (DevBuf* b : {&L.fixed, &L.K, &L.diag, &L.x, &L.b, &L.r, &L.y}) b->release();
+      for (DevBuf* b : {&L.fixed, &L.K, &L.diag, &L.x, &L.b, &L.r, &L.y, &L.bdiag}) b->release();
     lv.clear();
   }
 };
@@ -2429,6 +2430,22 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     }
     LAUNCHED();
   }
+  // point-block Jacobi on the H8 operator levels (0, and 1 when on the fly)
+  static const char* bje = getenv("TOPO_MG_BLOCK");
+  const bool blockj = dim == 3 && ctx->walsh && use_tile_op(ctx) && !(bje && bje[0] == '0');
+  for (size_t l = 0; l < lv.size() && l < 2; ++l) {
+    MgLevel& L = lv[l];
+    L.block = blockj && (l == 0 || (l == 1 && mf1));
+    if (!L.block) continue;
+    CK(L.bdiag.ensure(sizeof(double) * 9 * size_t(L.g.nn)));
+    const int nbn = grid_for(ctx, L.g.nn);
+    if (l == 0)
+      k_mg_bdiag<false><<<nbn, kThreads, 0, ctx->stream>>>(L.g, dKe, E, L.bdiag.as<double>());
+    else
+      k_mg_bdiag<true><<<nbn, kThreads, 0, ctx->stream>>>(L.g, dKp.as<double>(), E,
+                                                          L.bdiag.as<double>());
+    LAUNCHED();
+  }
   // exact coarsest solve when the coarsest stored level is small: its dense
   // matrix gathered and inverted once per solve (Gauss-Jordan, one block)
   static const char* dce = getenv("TOPO_MG_DENSE_COARSE");
@@ -2601,7 +2618,11 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     double lam = 1.0;
     for (int itp = 0; itp < 12; ++itp) {
       TRY(apply(l, x, y));
-      k_mg_dinv<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, y, L.diag.as<double>(), wv);
+      if (L.block)
+        k_mg_jacobi_b<1><<<grid_for(ctx, L.g.nn), kThreads, 0, ctx->stream>>>(
+            L.g.nn, fm, nullptr, y, L.bdiag.as<double>(), 0.0, wv);
+      else
+        k_mg_dinv<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, y, L.diag.as<double>(), wv);
       LAUNCHED();
       k_dot<<<nbd, kThreads, 0, ctx->stream>>>(nl, wv, wv, part.as<double>());
       k_dot<<<nbd, kThreads, 0, ctx->stream>>>(nl, x, x, part.as<double>() + nbd);
@@ -2680,13 +2701,22 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
         return TOPO_OK;
       }
       TRY(apply(l, L.x.as<double>(), L.y.as<double>()));
-      k_mg_jacobi<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, L.b.as<double>(), L.y.as<double>(),
-                                                      L.diag.as<double>(), w, L.x.as<double>());
+      if (L.block)
+        k_mg_jacobi_b<0><<<grid_for(ctx, L.g.nn), kThreads, 0, ctx->stream>>>(
+            L.g.nn, fm, L.b.as<double>(), L.y.as<double>(), L.bdiag.as<double>(), w,
+            L.x.as<double>());
+      else
+        k_mg_jacobi<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, L.b.as<double>(), L.y.as<double>(),
+                                                        L.diag.as<double>(), w, L.x.as<double>());
       LAUNCHED();
       return TOPO_OK;
     };
-    k_mg_jacobi<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, L.b.as<double>(), nullptr,
-                                                    L.diag.as<double>(), w, L.x.as<double>());
+    if (L.block)
+      k_mg_jacobi_b<0><<<grid_for(ctx, L.g.nn), kThreads, 0, ctx->stream>>>(
+          L.g.nn, fm, L.b.as<double>(), nullptr, L.bdiag.as<double>(), w, L.x.as<double>());
+    else
+      k_mg_jacobi<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, L.b.as<double>(), nullptr,
+                                                      L.diag.as<double>(), w, L.x.as<double>());
     LAUNCHED();
     for (int s2 = 1; s2 < sweeps; ++s2) TRY(sweep());
     if (last) return TOPO_OK;

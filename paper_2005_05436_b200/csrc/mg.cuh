@@ -916,6 +916,94 @@ __global__ void k_mg_diag_c1(MgGeo L, const double* __restrict__ Kp, const doubl
   }
 }
 
+// Point-block Jacobi (H8 levels 0 and 1): the inverse of each node's 3 x 3
+// diagonal block, from E and Ke (level 0) or from the fine moduli and the 8
+// Kp = Qp' Ke Qp (level 1, on the fly like the operator); fixed DOFs get
+// identity rows / columns. Stored as 9 doubles per node (row-major).
+template <bool C1>
+__global__ void k_mg_bdiag(MgGeo L, const double* __restrict__ K, const double* __restrict__ E,
+                           double* __restrict__ Binv) {
+  constexpr int D = 24, DD = D * D;
+  for (long long nd = blockIdx.x * (long long)blockDim.x + threadIdx.x; nd < L.nn;
+       nd += (long long)gridDim.x * blockDim.x) {
+    const int iy = int(nd % L.ny1);
+    const long long t = nd / L.ny1;
+    const int iz = int(t % L.nz1), ix = int(t / L.nz1);
+    double B[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    for (int q = 0; q < 8; ++q) {  // elements around the node, ascending
+      const int ex = ix - 1 + (q >> 2 & 1), ez = iz - 1 + (q >> 1 & 1), ey = iy - 1 + (q & 1);
+      if (ex < 0 || ex >= L.nelx || ez < 0 || ez >= L.nz || ey < 0 || ey >= L.nely) continue;
+      const int a = mg_local(3, iy - ey, iz - ez, ix - ex);
+      if (!C1) {
+        const double Ee = E[((long long)ex * L.nz + ez) * L.nely + ey];
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) B[i][j] = fma(Ee, K[(3 * a + j) * D + 3 * a + i], B[i][j]);
+      } else {
+        for (int p = 0; p < 8; ++p) {
+          int pi, pk, pj;
+          mg_offsets(p, pi, pk, pj);
+          const long long ef = ((long long)(2 * ex + pj) * (2 * L.nz) + 2 * ez + pk) * (2 * L.nely) +
+                               (2 * ey + pi);
+          const double Ep = E[ef];
+          for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j)
+              B[i][j] = fma(Ep, K[p * DD + (3 * a + j) * D + 3 * a + i], B[i][j]);
+        }
+      }
+    }
+    for (int c = 0; c < 3; ++c)
+      if (L.fixed[3 * nd + c])
+        for (int k = 0; k < 3; ++k) B[c][k] = B[k][c] = (k == c ? 1.0 : 0.0);
+    // symmetric 3 x 3 inverse by cofactors
+    const double c00 = B[1][1] * B[2][2] - B[1][2] * B[2][1];
+    const double c01 = B[1][2] * B[2][0] - B[1][0] * B[2][2];
+    const double c02 = B[1][0] * B[2][1] - B[1][1] * B[2][0];
+    const double det = B[0][0] * c00 + B[0][1] * c01 + B[0][2] * c02;
+    const double id = 1.0 / det;
+    double* o = Binv + 9 * nd;
+    o[0] = c00 * id;
+    o[1] = (B[0][2] * B[2][1] - B[0][1] * B[2][2]) * id;
+    o[2] = (B[0][1] * B[1][2] - B[0][2] * B[1][1]) * id;
+    o[3] = c01 * id;
+    o[4] = (B[0][0] * B[2][2] - B[0][2] * B[2][0]) * id;
+    o[5] = (B[0][2] * B[1][0] - B[0][0] * B[1][2]) * id;
+    o[6] = c02 * id;
+    o[7] = (B[0][1] * B[2][0] - B[0][0] * B[2][1]) * id;
+    o[8] = (B[0][0] * B[1][1] - B[0][1] * B[1][0]) * id;
+  }
+}
+
+// point-block Jacobi step per node: MODE 0: x = x + w Binv (b - Ax) (Ax null:
+// x = w Binv b), 0 on fixed DOFs; MODE 1: out = Binv (Ax) with Ax masked to 0
+// on fixed DOFs (power iteration for lambda_max(Binv A))
+template <int MODE>
+__global__ void k_mg_jacobi_b(long long nn, const unsigned char* __restrict__ fixed,
+                              const double* __restrict__ b, const double* __restrict__ Ax,
+                              const double* __restrict__ Binv, double w, double* __restrict__ x) {
+  for (long long nd = blockIdx.x * (long long)blockDim.x + threadIdx.x; nd < nn;
+       nd += (long long)gridDim.x * blockDim.x) {
+    double r[3];
+    bool fx[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long d = 3 * nd + c;
+      fx[c] = fixed[d] != 0;
+      const double v = MODE == 1 ? Ax[d] : (Ax ? b[d] - Ax[d] : b[d]);
+      r[c] = fx[c] ? 0.0 : v;
+    }
+    const double* m = Binv + 9 * nd;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const long long d = 3 * nd + c;
+      const double z = fma(m[3 * c], r[0], fma(m[3 * c + 1], r[1], m[3 * c + 2] * r[2]));
+      if (MODE == 1)
+        x[d] = fx[c] ? 0.0 : z;
+      else
+        x[d] = fx[c] ? 0.0 : (Ax ? x[d] : 0.0) + w * z;
+    }
+  }
+}
+
 // Jacobi diagonal (fixed DOFs: 1), node-centric
 template <int DIM, bool FINE>
 __global__ void k_mg_diag(MgGeo L, const double* __restrict__ K, const double* __restrict__ E,
