@@ -2656,6 +2656,7 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   // V-cycle: lv[l].x <- approx A_l^{-1} lv[l].b
   std::function<topo_status(size_t)> vcycle = [&](size_t l) -> topo_status {
     MgLevel& L = lv[l];
+    void* const x_entry = L.x.p;  // (node sweeps swap x / y; restored at exit)
     const long long nl = L.g.n;
     const int nbd = grid_for(ctx, nl);
     const unsigned char* fm = L.fixed.as<unsigned char>();
@@ -2747,6 +2748,11 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
                                                               L.x.as<double>());
     LAUNCHED();
     for (int s2 = 0; s2 < nu; ++s2) TRY(sweep());
+    if (L.x.p != x_entry) {  // odd number of swaps: the same buffers every cycle
+      CK(cudaMemcpyAsync(x_entry, L.x.p, sizeof(double) * size_t(L.g.n), cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+      std::swap(L.x.p, L.y.p);
+    }
     return TOPO_OK;
   };
   // PCG: r = f (0 on fixed), z = V(r), p = z
@@ -2793,7 +2799,10 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   const double ff = hs[1];
   double rel = ff > 0 ? 1.0 : 0.0;
   int it = 0;
-  while (ff > 0 && rel > rtol && it < maxit) {
+  // one PCG iteration (matvec, updates, V-cycle); with an exact coarsest solve
+  // every launch of it is plain and its buffers are fixed, so it is captured
+  // once into a CUDA graph and replayed (launch-bound small grids)
+  auto iteration = [&]() -> topo_status {
     if (tile) {
       TRY(launch_tile_op(ctx, L0, E, p, qv, pp, &nbn));
     } else {
@@ -2819,6 +2828,37 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     LAUNCHED();
     k_copy_scalar<<<1, 32, 0, ctx->stream>>>(scd + 3, scd + 0);
     LAUNCHED();
+    return TOPO_OK;
+  };
+  static const char* gre = getenv("TOPO_MG_GRAPH");
+  bool use_graph = dense_coarse && !(gre && gre[0] == '0');
+  cudaGraphExec_t gexec = nullptr;
+  struct GraphFree {
+    cudaGraphExec_t* g;
+    ~GraphFree() {
+      if (*g) cudaGraphExecDestroy(*g);
+    }
+  } free_graph{&gexec};
+  while (ff > 0 && rel > rtol && it < maxit) {
+    if (use_graph && !gexec) {
+      cudaGraph_t graph = nullptr;
+      bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      const topo_status st = ok ? iteration() : TOPO_ECUDA;
+      ok = cudaStreamEndCapture(ctx->stream, &graph) == cudaSuccess && ok && st == TOPO_OK;
+      if (ok) ok = cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
+      if (graph) cudaGraphDestroy(graph);
+      if (!ok) {  // fall back to stream launches
+        cudaGetLastError();
+        gexec = nullptr;
+        use_graph = false;
+      }
+    }
+    if (gexec) {
+      CK(cudaGraphLaunch(gexec, ctx->stream));
+      z = lv[0].x.as<double>();
+    } else {
+      TRY(iteration());
+    }
     double rr = 0;
     CK(cudaMemcpyAsync(&rr, scd + 2, sizeof rr, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
