@@ -127,3 +127,48 @@ def test_multigrid_variants_agree(P, tmp_path, env):
     with P.Context(*cfg.grid, rmin=1.0, nu=cfg.nu) as ctx:
         uj, _, _ = ctx.solve_state(sK, load_vector(cfg), fixed_dofs(cfg), rtol=1e-12)
     assert rel(u, uj) <= 1e-9, rel(u, uj)
+
+
+def test_multigrid_state_reused_across_solves(P):
+    # the context keeps its multigrid levels, coarse inverse and graph between
+    # solves: solving A, B, A on one context equals fresh contexts bit for bit
+    from paper_2005_05436_b200.configs import CONFIGS, fixed_dofs, load_vector
+    cfg = CONFIGS[5].scaled(32, 16, 16)
+    f, fixed = load_vector(cfg), fixed_dofs(cfg)
+    rng = np.random.default_rng(21)
+    sA = 1e-9 + rng.uniform(0.05, 1.0, cfg.m) ** 3
+    sB = 1e-9 + rng.uniform(0.01, 1.0, cfg.m) ** 3
+
+    def fresh(sK):
+        with P.Context(*cfg.grid, rmin=1.0, nu=cfg.nu) as c:
+            return c.solve_state(sK, f, fixed, rtol=1e-10, multigrid=True)
+
+    ra, rb = fresh(sA), fresh(sB)
+    with P.Context(*cfg.grid, rmin=1.0, nu=cfg.nu) as ctx:
+        seq = [ctx.solve_state(s, f, fixed, rtol=1e-10, multigrid=True) for s in (sA, sB, sA)]
+    for (u, it, rr), (u0, it0, rr0) in zip(seq, (ra, rb, ra)):
+        assert it == it0 and rr == rr0
+        assert np.array_equal(u, u0)
+
+
+def test_pass_c_abi_matches_python_api(P):
+    # bench.py times topo_design_pass through ctypes with prebuilt arguments:
+    # the same call as Context.design_pass, bit for bit
+    import ctypes as C
+    import math
+    import torch
+    from paper_2005_05436_b200 import _lib as L
+    from paper_2005_05436_b200.configs import CONFIGS, make_inputs
+    cfg = CONFIGS[4].scaled(24, 12, 12)
+    x, u, state = make_inputs(cfg)
+    with P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu, state=state) as ctx:
+        xd, ud = torch.from_numpy(x).cuda(), torch.from_numpy(u).cuda()
+        r = ctx.design_pass(xd, ud, beta=cfg.beta, eta0=cfg.eta0, move=cfg.move,
+                            volfrac=cfg.volfrac, outputs=False)
+        pp = L.PassParams(P.SimpParams().c(), cfg.beta, cfg.eta0, cfg.move, cfg.volfrac,
+                          math.nan, L.VOL_FILTERED, 1)
+        xn = torch.empty(cfg.m, dtype=torch.float64, device="cuda")
+        po = L.PassOut(None, None, None, None, None, xn.data_ptr(), None)
+        assert ctx.lib.topo_design_pass(ctx.h, xd.data_ptr(), ud.data_ptr(), C.byref(pp),
+                                        C.byref(po)) == 0
+        assert torch.equal(xn, r.xNew) and po.eta == r.eta and po.c == r.c
