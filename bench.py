@@ -120,54 +120,82 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- CPU samples
-def cpu_sample_config(cfg, scale: float = 1.0):
-    """A bounded sample of the workload with the same physics, filter and OC
-    parameters (per-element cost of the reference is linear in m)."""
-    from paper_2005_05436_b200.configs import Config
-    shapes = {1: (300, 100, 0), 2: (150, 50, 0), 3: (16, 400, 0), 4: (12, 48, 48),
-              5: (2, 48, 48)}
-    nx, ny, nz = shapes.get(cfg.cid, (cfg.nelx, cfg.nely, cfg.nelz))
-    nx = max(1, int(round(nx * scale)))
+def load_configs_standalone():
+    """paper_2005_05436_b200/configs.py loaded as a plain module, with the
+    oracle's copy of the Appendix B generator: the CPU reference arm never
+    imports the product package, so no product library is mapped."""
+    import importlib.util
+    from oracle import oracle as O
+    if not os.path.exists(O.PORT_LIB):
+        O.build()
+    spec = importlib.util.spec_from_file_location(
+        "topo_configs_standalone", os.path.join(ROOT, "paper_2005_05436_b200", "configs.py"))
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod  # (dataclasses resolve annotations through it)
+    spec.loader.exec_module(mod)
+    gen = O.Oracle("port")
+    mod.set_generator(lambda seed, stream, kind, a, b, count, offset:
+                      gen.generate(seed, stream, kind, a, b, count, offset))
+    return mod
+
+
+# Sample grids of the CPU legs: the config's physics, filter and OC parameters
+# on a grid whose x extent is at least 2 reach + 1 (no mirror fold wraps a whole
+# axis) and whose pass takes seconds on one core. The reference's per-element
+# cost does not depend on the grid size at fixed taps: the filter is T taps per
+# element per evaluation, and the number of OC volume evaluations is fixed by
+# the regime (16 on C1-C3, 243 on C4/C5, SURVEY.md §0.5).
+CPU_SAMPLES = {1: (300, 100, 0), 2: (150, 50, 0), 3: (70, 400, 0), 4: (12, 48, 48),
+               5: (8, 32, 32)}
+
+
+def cpu_sample_config(cfg):
+    nx, ny, nz = CPU_SAMPLES.get(cfg.cid, (cfg.nelx, cfg.nely, cfg.nelz))
     return cfg.scaled(nx, ny, nz, name=f"{cfg.name} sample {nx}x{ny}x{nz}")
 
 
-def sample_inputs(cfg, base):
-    """Seeded inputs of the sample grid (passive layout / smoothing re-derived
-    for the sample's own dimensions)."""
-    from paper_2005_05436_b200.configs import make_inputs
-    return make_inputs(cfg)
+def host_cpu():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"model": model, "nproc": os.cpu_count() or 1, "usable": usable}
 
 
-def run_cpu(cfg, steps: int, warmup: int, threads: int):
-    """Times the reference CPU path (oracle/_ref = the reference's own headers,
-    else the C restatement) on `threads` concurrent sample instances."""
+def run_cpu(cfg, steps: int, warmup: int, threads: int, single: bool = True):
+    """Times the reference CPU path (oracle/_ref = the reference's own headers
+    compiled verbatim, else the C restatement): (ii) `threads` concurrent
+    single-threaded sample passes, the reference having no threading on this
+    path; (i) one pass alone on one core."""
     from oracle import oracle as O
+    cmod = load_configs_standalone()
     kind = "reference" if os.path.exists(O.REF_LIB) else "port"
-    if not os.path.exists(O.PORT_LIB):
-        O.build()
     orc = O.Oracle(kind)
     if kind == "port":
         orc.set_threads(1)
     scfg = cpu_sample_config(cfg)
-    x, u, state = sample_inputs(scfg, cfg)
+    x, u, state = cmod.make_inputs(scfg)
     grid = scfg.grid
-    handles = []
-    for _ in range(threads):
-        if kind == "reference":
-            handles.append(orc.problem(grid, scfg.rmin, 0, scfg.nu, state))
-        else:
-            handles.append(orc.filter(grid, scfg.rmin))
+    mk = ((lambda: orc.problem(grid, scfg.rmin, 0, scfg.nu, state)) if kind == "reference"
+          else (lambda: orc.filter(grid, scfg.rmin)))
+    handles = [mk() for _ in range(threads)]
 
     def one(h):
-        if kind == "reference":
-            orc.design_pass(grid, scfg.rmin, x, u, state, beta=scfg.beta, move=scfg.move,
-                            volfrac=scfg.volfrac, problem=h)
-        else:
-            orc.design_pass(grid, scfg.rmin, x, u, state, beta=scfg.beta, move=scfg.move,
-                            volfrac=scfg.volfrac, filt=h)
+        kw = dict(beta=scfg.beta, move=scfg.move, volfrac=scfg.volfrac)
+        kw["problem" if kind == "reference" else "filt"] = h
+        orc.design_pass(grid, scfg.rmin, x, u, state, **kw)
 
-    def step():
-        ts = [threading.Thread(target=one, args=(h,)) for h in handles]
+    def step(hs):
+        ts = [threading.Thread(target=one, args=(h,)) for h in hs]
         t0 = time.perf_counter()
         for t in ts:
             t.start()
@@ -176,15 +204,22 @@ def run_cpu(cfg, steps: int, warmup: int, threads: int):
         return time.perf_counter() - t0
 
     for _ in range(warmup):
-        step()
-    times = [step() for _ in range(steps)]
+        step(handles)
+    times = [step(handles) for _ in range(steps)]
     wall = sum(times) / len(times)
     value = threads * scfg.m / wall / 1e6
-    sample = (f"{threads} concurrent instance(s) of {scfg.nelx}x{scfg.nely}x{scfg.nelz} "
-              f"({scfg.m} elements each; {cfg.name} filter/projection/OC parameters; "
-              f"literal ft=3 OC volume callback), {steps} timed step(s)")
-    return {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
-            "sec_per_step": wall}
+    res = {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+           "sec_per_step": wall, "host": host_cpu()}
+    desc = (f"{scfg.nelx}x{scfg.nely}x{scfg.nelz} grid ({scfg.m} elements) with the "
+            f"{cfg.name} filter / projection / OC parameters, literal ft=3 OC volume callback "
+            f"(one filter per evaluation)")
+    res["sample"] = (f"(ii) {threads} concurrent single-threaded passes of a {desc}, "
+                     f"{steps} timed step(s)")
+    if single:
+        t1 = step(handles[:1])
+        res["single_thread"] = {"value": scfg.m / t1 / 1e6, "unit": UNIT, "cores": 1,
+                                "sec_per_pass": t1, "sample": f"(i) one pass of the same {desc}"}
+    return res
 
 
 # ------------------------------------------------------------------- ours
@@ -324,6 +359,29 @@ def run_ours(args, cfg, rank, world, local_rank):
                 ntaps=ctx.ntaps, fp64_peak=fp64)
 
 
+def cpu_line(cb):
+    out = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"],
+           "sample": cb["sample"], "cpu_model": cb["host"]["model"],
+           "nproc": cb["host"]["nproc"]}
+    if "single_thread" in cb:
+        out["single_thread"] = cb["single_thread"]
+    return out
+
+
+def launch_ranks(n: int) -> int:
+    """`bench.py --gpus N` started without torchrun: start N ranks under
+    torch.distributed.run (one per GPU, 127.0.0.1 rendezvous) and wait."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -334,12 +392,27 @@ def main():
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "ours":
+            import torch
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                print(json.dumps({"error": f"--gpus {args.gpus} but {have} GPU(s) visible"}),
+                      flush=True)
+                sys.exit(2)
+            sys.exit(launch_ranks(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "ours" and world != args.gpus:
+        print(json.dumps({"error": f"WORLD_SIZE {world} != --gpus {args.gpus}"}), flush=True)
+        sys.exit(2)
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    from paper_2005_05436_b200.configs import CONFIGS
-    cfg = CONFIGS[args.config]
-    threads = args.cpu_threads or (os.cpu_count() or 1)
+    if args.impl == "reference":
+        cfg = load_configs_standalone().CONFIGS[args.config]  # no product library
+    else:
+        from paper_2005_05436_b200.configs import CONFIGS
+        cfg = CONFIGS[args.config]
+    threads = args.cpu_threads or host_cpu()["usable"]
     workload = {"workload": cfg.name, "grid": list(cfg.grid), "m": cfg.m, "n_dofs": cfg.n,
                 "rmin": cfg.rmin, "taps": None, "beta": cfg.beta, "move": cfg.move,
                 "volfrac": cfg.volfrac, "filter_bc": "neumann (mirror)", "ft": 3,
@@ -349,13 +422,13 @@ def main():
         if rank != 0:
             return
         cb = run_cpu(cfg, args.steps, args.warmup, threads)
+        workload["cpu_sample_grid"] = list(CPU_SAMPLES.get(cfg.cid, cfg.grid))
         line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": cb["sec_per_step"] * 1e3, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": workload,
-                "cpu_baseline": {"value": cb["value"], "unit": UNIT, "cores": cb["cores"],
-                                 "kind": cb["kind"], "sample": cb["sample"]},
+                "cpu_baseline": cpu_line(cb),
                 "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -378,7 +451,7 @@ def main():
     sk_gbs = sk_bytes / (sk_ms * 1e-3) / 1e9 if sk_ms > 0 else None
     traffic = load_traffic(cfg.cid)
     b_elem = algorithmic_bytes_per_elem(cfg)
-    pass_gbs = m * b_elem / (res["ms"] * 1e-3) / 1e9 / max(1, args.gpus)
+    pass_gbs = m * b_elem / (res["ms"] * 1e-3) / 1e9 / world  # per GPU
     # FP64 work per element: 3 convolutions x 2 T flops + the
     # sensitivity (2D 144, 3D 1200 as the dense form counts it)
     flop_elem = 6 * res["ntaps"] + (1200 if cfg.nelz else 144)
@@ -400,7 +473,7 @@ def main():
         "pass_roofline": {"bound": "hbm", "algorithmic_bytes_per_elem": b_elem,
                           "achieved": pass_gbs, "peak": peak, "unit": "GB/s",
                           "frac": pass_gbs / peak,
-                          "ceiling_melem_s": peak * 1e9 / b_elem / 1e6 * max(1, args.gpus)},
+                          "ceiling_melem_s": peak * 1e9 / b_elem / 1e6 * world},
         "fp64_roofline": {"flop_per_elem": flop_elem, "achieved": fp64_tf,
                           "peak": res["fp64_peak"], "unit": "TFLOP/s",
                           "frac": fp64_tf / res["fp64_peak"] if res["fp64_peak"] else None,
@@ -415,9 +488,7 @@ def main():
                    "c": res["r"].c},
     }
     if world == 1 and not args.no_cpu_baseline:
-        cb = run_cpu(cfg, 1, 0, threads)
-        line["cpu_baseline"] = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"],
-                                "kind": cb["kind"], "sample": cb["sample"]}
+        line["cpu_baseline"] = cpu_line(run_cpu(cfg, 1, 0, threads))
     print(json.dumps(line), flush=True)
 
 

@@ -119,6 +119,11 @@ const char* topo_last_error(const topo_ctx* ctx);
 /* run on an external stream (e.g. torch.cuda.current_stream().cuda_stream) */
 topo_status topo_set_stream(topo_ctx* ctx, void* cuda_stream);
 topo_status topo_sync(topo_ctx* ctx);
+/* order the context's stream after the work already queued on cuda_stream
+ * (the stream that produced device inputs or last used device output blocks;
+ * NULL = legacy default stream). Entry points are synchronous at return, so
+ * outputs need no fence the other way. */
+topo_status topo_wait_stream(topo_ctx* ctx, void* cuda_stream);
 topo_status topo_device_buffer(topo_ctx* ctx, int which, void** ptr, int64_t* count);
 /* device memory for callers without a CUDA runtime of their own (the C++
  * adapter's device-resident redesign loop): allocate / free on the context's

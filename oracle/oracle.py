@@ -179,6 +179,9 @@ class Oracle:
             L.orc_filter_hs.argtypes = [C.c_void_p]
             L.orc_set_threads.restype = C.c_int
             L.orc_set_threads.argtypes = [C.c_int]
+            L.orc_generate.restype = None
+            L.orc_generate.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_double, C.c_double,
+                                       C.c_int64, C.c_int64, C.c_void_p]
             fn("element_stiffness", C.c_int, C.c_int, C.c_double, f64p, f64p)
             fn("assemble_values", None, C.c_int64, C.c_int, f64p, f64p, f64p)
             fn("assemble_lower", C.c_int, Grid, C.c_double, f64p, i32p, i32p, f64p,
@@ -234,6 +237,14 @@ class Oracle:
 
     def _call(self, name, *args):
         return getattr(self.lib, self.pre + name)(*args)
+
+    def generate(self, seed: int, stream: int, kind: str, a: float, b: float, count: int,
+                 offset: int = 0) -> np.ndarray:
+        """port only: SURVEY.md Appendix B generator (same bits as topo_generate)."""
+        out = np.empty(count)
+        self.lib.orc_generate(seed, stream, 0 if kind == "uniform" else 1, a, b, offset, count,
+                              out.ctypes.data)
+        return out
 
     def set_threads(self, n: int) -> int:
         return self.lib.orc_set_threads(n) if self.kind == "port" else 1

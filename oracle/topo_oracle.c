@@ -41,6 +41,35 @@ int orc_set_threads(int n) {
 #endif
 }
 
+/* the benchmark input generator (not a reference
+ * function; both sides consume identical arrays) */
+static inline uint64_t orc_splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+void orc_generate(uint64_t seed, uint64_t stream, int kind, double a, double b, int64_t offset,
+                  int64_t count, double* out) {
+  const uint64_t key = orc_splitmix64(seed ^ orc_splitmix64(stream + 0x632BE59BD9B4E019ull));
+  const double two53 = 1.0 / 9007199254740992.0;
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < count; ++t) {
+    const uint64_t idx = (uint64_t)(offset + t);
+    if (kind == 0) {
+      out[t] = a + (b - a) * ((double)(orc_splitmix64(key + idx) >> 11) * two53);
+    } else {
+      const uint64_t k = idx >> 1;
+      const double u1 = ((double)(orc_splitmix64(key + 2 * k) >> 11) + 1.0) * two53;
+      const double u2 = (double)(orc_splitmix64(key + 2 * k + 1) >> 11) * two53;
+      const double rad = sqrt(-2.0 * log(u1));
+      const double ang = 6.283185307179586 * u2;
+      out[t] = a + b * ((idx & 1) ? rad * sin(ang) : rad * cos(ang));
+    }
+  }
+}
+
 /* std::max / std::min semantics (return the first argument unless the second
  * compares strictly greater / smaller), used by oc.hpp:36,49-51,59 */
 static inline double std_max(double a, double b) { return (a < b) ? b : a; }

@@ -35,6 +35,12 @@ typedef struct {
 const char* orc_last_error(void);
 int orc_set_threads(int n);
 
+/* SURVEY.md Appendix B input generator (counter-based splitmix64; kind 0
+ * uniform [a, b), 1 normal(a, b) by Box-Muller on index pairs). Lets the CPU
+ * reference arm build the benchmark inputs without the product library. */
+void orc_generate(uint64_t seed, uint64_t stream, int kind, double a, double b, int64_t offset,
+                  int64_t count, double* out);
+
 /* grid.hpp */
 int64_t orc_num_elements(orc_grid g);
 int64_t orc_num_dofs(orc_grid g);

@@ -21,6 +21,7 @@ BUF_SK, BUF_IK, BUF_JK, BUF_XNEW, BUF_XPHYS = range(5)
 # every symbol include/topo_capi.h declares
 EXPORTS = [
     "topo_ctx_create", "topo_ctx_destroy", "topo_last_error", "topo_set_stream", "topo_sync",
+    "topo_wait_stream",
     "topo_device_buffer", "topo_ctx_info", "topo_comm_init_nccl", "topo_element_stiffness",
     "topo_generate", "topo_build_connectivity", "topo_build_index_pairs",
     "topo_simp_interpolate", "topo_assemble_values", "topo_sensitivity", "topo_filter",
@@ -99,6 +100,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         "topo_last_error": (C.c_char_p, [vp]),
         "topo_set_stream": (C.c_int, [vp, vp]),
         "topo_sync": (C.c_int, [vp]),
+        "topo_wait_stream": (C.c_int, [vp, vp]),
         "topo_device_buffer": (C.c_int, [vp, C.c_int, p(vp), p(C.c_int64)]),
         "topo_ctx_info": (C.c_int, [vp, p(C.c_int64), p(C.c_int64), p(C.c_int32), p(C.c_int32),
                                     p(C.c_int32), p(C.c_int32), p(C.c_int32)]),

@@ -34,6 +34,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 from dataclasses import dataclass
 from typing import Callable, Optional
 
@@ -75,6 +76,47 @@ def _is_torch(a) -> bool:
     return type(a).__module__.startswith("torch")
 
 
+# Device arrays reach the library by raw pointer, but the library works on its
+# own (non-blocking) stream. Every CUDA tensor an entry point is about to see
+# (an input, or an output block torch.empty just handed out) marks the calling
+# thread; the next library call first orders the context's stream after the
+# tensor's current torch stream (topo_wait_stream). Entry points are
+# synchronous at return, so results need no fence back.
+_tls = threading.local()
+
+
+def _note_cuda(t) -> None:
+    _tls.pending = t.device
+
+
+class _FencedLib:
+    """The ctypes library of one Context: calls taking the context handle are
+    preceded by the stream fence when CUDA tensors were staged for them."""
+
+    def __init__(self, lib, owner: "Context"):
+        self._lib = lib
+        self._owner = owner
+
+    def __getattr__(self, name):
+        f = getattr(self._lib, name)
+        if not name.startswith("topo_") or name in ("topo_last_error", "topo_wait_stream"):
+            return f
+
+        def call(*args):
+            dev = getattr(_tls, "pending", None)
+            h = getattr(self._owner, "h", None)
+            if dev is not None and h:
+                _tls.pending = None
+                import torch
+                s = torch.cuda.current_stream(dev).cuda_stream
+                st = self._lib.topo_wait_stream(h, s)
+                if st:
+                    _raise(st, self._lib.topo_last_error(h).decode())
+            return f(*args)
+
+        return call
+
+
 class _Arr:
     """Keeps a contiguous float64 / int32 / uint8 buffer alive and exposes its pointer."""
 
@@ -85,6 +127,8 @@ class _Arr:
             if a.dtype != tdt:
                 a = a.to(tdt)
             a = a.contiguous()
+            if a.is_cuda:
+                _note_cuda(a)
             self.obj = a
             self.ptr = a.data_ptr()
             self.size = a.numel()
@@ -104,6 +148,7 @@ def _empty(n: int, like_device: bool, dtype=np.float64):
         import torch
         tdt = {np.float64: torch.float64, np.int32: torch.int32, np.int64: torch.int64}[dtype]
         t = torch.empty(n, dtype=tdt, device="cuda")
+        _note_cuda(t)
         return t, t.data_ptr()
     a = np.empty(n, dtype=dtype)
     return a, a.ctypes.data
@@ -254,7 +299,7 @@ class Context:
                  bc: int = L.BC_NEUMANN, nu: float = 0.3, state=None, device: int = -1,
                  rank: int = 0, nranks: int = 1, j0: int = 0, j1: int = 0,
                  ke_full=None, ke_lower=None):
-        self.lib = L.load()
+        self.lib = _FencedLib(L.load(), self)
         self.grid = (nelx, nely, nelz)
         desc = L.GridDesc(nelx, nely, nelz, rmin, bc, nu, device, rank, nranks, j0, j1)
         h = C.c_void_p()

@@ -101,7 +101,20 @@ def passive_state(cfg: Config) -> Optional[np.ndarray]:
     return state.reshape(-1)
 
 
+_GENERATOR = None  # override of the library's topo_generate (same bits), see set_generator
+
+
+def set_generator(fn) -> None:
+    """Use fn(seed, stream, kind, a, b, count, offset) instead of the library's
+    generator: lets a process that must not load the product library (bench.py's
+    CPU reference arm, which loads this file standalone) build identical inputs."""
+    global _GENERATOR
+    _GENERATOR = fn
+
+
 def _gen(kind, seed, stream, a, b, count, offset=0):
+    if _GENERATOR is not None:
+        return _GENERATOR(seed, stream, kind, a, b, count, offset)
     from .api import generate
     return generate(seed, stream, kind, a, b, count, offset)
 

@@ -46,6 +46,20 @@ struct DevBuf {
   }
 };
 
+// every entry point runs on its context's device and restores the caller's
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes a;
@@ -68,6 +82,7 @@ struct topo_ctx {
   cudaStream_t stream = nullptr, aux = nullptr, cstream = nullptr;  // main, sK, copies
   bool own_stream = true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_x = nullptr, ev_u = nullptr;
+  cudaEvent_t ev_in = nullptr;  // topo_wait_stream: caller's stream -> ctx->stream
   static constexpr int kUChunks = 8;  // host U copied in x-chunks, K3a per chunk
   cudaEvent_t ev_uc[kUChunks] = {};
   int sm_count = 148;
@@ -406,11 +421,11 @@ topo_status launch_conv3_t(topo_ctx* ctx, const Geo& G, ConvGeom T, const ConvAr
   T.zb = z0;
   dim3 grid((G.nely + T.TI - 1) / T.TI, (T.run_n + T.TR - 1) / T.TR, z1 - z0);
   const size_t smem = conv_smem(T);
-  static bool attr_done = false;  // per instantiation
-  if (!attr_done) {
+  static unsigned long long attr_done = 0;  // per instantiation, bit per device
+  if (!(attr_done >> ctx->device & 1)) {
     CK(cudaFuncSetAttribute(k_conv3<NF, MODE, AR, kC3R, kC3T>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024 + 4096));
-    attr_done = true;
+    attr_done |= 1ull << ctx->device;
   }
   k_conv3<NF, MODE, AR, kC3R, kC3T><<<grid, kThreads, smem, ctx->stream>>>(
       G, T, ctx->d_w3.as<double>(), A);
@@ -442,15 +457,15 @@ topo_status launch_conv_t(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* n
   dim3 grid((G.nely + T.TI - 1) / T.TI, (T.run_n + T.TR - 1) / T.TR,
             (T.other_n + T.TO - 1) / T.TO);
   const size_t smem = conv_smem(T);
-  static bool attr_done = false;  // per instantiation
-  if (!attr_done) {
+  static unsigned long long attr_done = 0;  // per instantiation, bit per device
+  if (!(attr_done >> ctx->device & 1)) {
     int optin = 0;
     CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
     cudaFuncAttributes fa;
     CK(cudaFuncGetAttributes(&fa, k_conv<NF, MODE, R, AW>));
     CK(cudaFuncSetAttribute(k_conv<NF, MODE, R, AW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             optin - int(fa.sharedSizeBytes)));
-    attr_done = true;
+    attr_done |= 1ull << ctx->device;
   }
   k_conv<NF, MODE, R, AW><<<grid, kThreads, smem, ctx->stream>>>(
       G, T, ctx->d_cols.as<ConvCol>(), int(ctx->cols.size()), ctx->d_wpad.as<double>(), A);
@@ -522,15 +537,15 @@ topo_status launch_sk(topo_ctx* ctx, const SkArgs& S, cudaStream_t st) {
 // The SM's L1 / shared split is fixed while any block is resident. Kernels
 // that co-run with the adjoint filter (k_conv3, ~100 KB per block) prefer the
 // maximum shared carveout, or the filter's blocks wait for the SMs to drain.
-topo_status set_overlap_carveout() {
-  static bool done = false;
-  if (done) return TOPO_OK;
+topo_status set_overlap_carveout(int device) {
+  static unsigned long long done = 0;  // bit per device
+  if (done >> device & 1) return TOPO_OK;
   for (const void* f : {(const void*)k_sk_store<300>, (const void*)k_sk_store<36>,
                         (const void*)k_elem_walsh})
     if (cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                              int(cudaSharedmemCarveoutMaxShared)) != cudaSuccess)
       return TOPO_ECUDA;
-  done = true;
+  done |= 1ull << device;
   return TOPO_OK;
 }
 
@@ -992,8 +1007,9 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   CKC(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
   CKC(cudaEventCreateWithFlags(&ctx->ev_x, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_u, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
   for (auto& e : ctx->ev_uc) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  if (ctx->overlap_sk && set_overlap_carveout() != TOPO_OK)
+  if (ctx->overlap_sk && set_overlap_carveout(ctx->device) != TOPO_OK)
     return bail(fail(ctx, TOPO_ECUDA, "cannot set the shared-memory carveout"));
   CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
@@ -1093,6 +1109,7 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->ev_x) cudaEventDestroy(ctx->ev_x);
   if (ctx->ev_u) cudaEventDestroy(ctx->ev_u);
+  if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
   for (auto& e : ctx->ev_uc)
     if (e) cudaEventDestroy(e);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
@@ -1103,6 +1120,7 @@ void topo_ctx_destroy(topo_ctx* ctx) {
 
 topo_status topo_set_timing(topo_ctx* ctx, int on) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   if (on && !ctx->tev[0])
     for (int q = 0; q < 2 * TOPO_NSTAGES; ++q) CK(cudaEventCreate(&ctx->tev[q]));
   ctx->timing = on != 0;
@@ -1143,12 +1161,14 @@ topo_status topo_fp64_peak(int device, double* tflops) {
 
 topo_status topo_stage_times(topo_ctx* ctx, double* times_ms) {
   if (!ctx || !times_ms) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   for (int q = 0; q < TOPO_NSTAGES; ++q) times_ms[q] = ctx->stage_ms[q];
   return TOPO_OK;
 }
 
 topo_status topo_set_stream(topo_ctx* ctx, void* s) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   CK(cudaStreamSynchronize(ctx->stream));
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   ctx->stream = static_cast<cudaStream_t>(s);
@@ -1156,8 +1176,22 @@ topo_status topo_set_stream(topo_ctx* ctx, void* s) {
   return TOPO_OK;
 }
 
+// order the context's stream after all work already queued on `s` (the
+// caller's stream, e.g. torch's current stream, which produced the inputs or
+// last used the output blocks); NULL = the legacy default stream
+topo_status topo_wait_stream(topo_ctx* ctx, void* s) {
+  if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
+  const cudaStream_t cs = static_cast<cudaStream_t>(s);
+  if (cs == ctx->stream) return TOPO_OK;
+  CK(cudaEventRecord(ctx->ev_in, cs));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_in, 0));
+  return TOPO_OK;
+}
+
 topo_status topo_sync(topo_ctx* ctx) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaStreamSynchronize(ctx->aux));
   return TOPO_OK;
@@ -1178,6 +1212,7 @@ topo_status topo_ctx_info(const topo_ctx* ctx, int64_t* m, int64_t* n, int32_t* 
 
 topo_status topo_device_buffer(topo_ctx* ctx, int which, void** ptr, int64_t* count) {
   if (!ctx || !ptr) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   const Geo& G = ctx->G;
   switch (which) {
     case TOPO_BUF_SK: *ptr = ctx->sK.p; if (count) *count = ctx->sK.p ? G.m * G.P : 0; break;
@@ -1195,6 +1230,7 @@ topo_status topo_device_buffer(topo_ctx* ctx, int which, void** ptr, int64_t* co
 
 topo_status topo_device_alloc(topo_ctx* ctx, int64_t bytes, void** ptr) {
   if (!ctx || !ptr || bytes < 0) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   *ptr = nullptr;
   CK(cudaMalloc(ptr, size_t(bytes > 0 ? bytes : 16)));
   return TOPO_OK;
@@ -1202,12 +1238,14 @@ topo_status topo_device_alloc(topo_ctx* ctx, int64_t bytes, void** ptr) {
 
 topo_status topo_device_free(topo_ctx* ctx, void* ptr) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   if (ptr) CK(cudaFree(ptr));
   return TOPO_OK;
 }
 
 topo_status topo_copy(topo_ctx* ctx, void* dst, const void* src, int64_t bytes) {
   if (!ctx || bytes < 0 || (bytes > 0 && (!dst || !src))) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   if (bytes == 0) return TOPO_OK;
   CK(cudaMemcpyAsync(dst, src, size_t(bytes), cudaMemcpyDefault, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1216,6 +1254,7 @@ topo_status topo_copy(topo_ctx* ctx, void* dst, const void* src, int64_t bytes) 
 
 topo_status topo_filter_taps(topo_ctx* ctx, int32_t* di, int32_t* dj, int32_t* dk, double* w) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   for (size_t t = 0; t < ctx->w.size(); ++t) {
     if (di) di[t] = ctx->di[t];
     if (dj) dj[t] = ctx->dj[t];
@@ -1227,6 +1266,7 @@ topo_status topo_filter_taps(topo_ctx* ctx, int32_t* di, int32_t* dj, int32_t* d
 
 topo_status topo_filter_hs(topo_ctx* ctx, double* hs) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   bool host;
   double* o = out_ptr(ctx, hs, ctx->tmp1, ctx->G.m, &host);
@@ -1240,6 +1280,7 @@ topo_status topo_filter_hs(topo_ctx* ctx, double* hs) {
 // ---------------------------------------------------------------- K0
 topo_status topo_build_connectivity(topo_ctx* ctx, int32_t* dofs) {
   if (!ctx || !dofs) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   const Geo& G = ctx->G;
   const size_t bytes = sizeof(int32_t) * size_t(G.m) * G.d;
@@ -1263,6 +1304,7 @@ topo_status topo_build_connectivity(topo_ctx* ctx, int32_t* dofs) {
 
 topo_status topo_build_index_pairs(topo_ctx* ctx, int32_t* iK, int32_t* jK) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   const Geo& G = ctx->G;
   const size_t bytes = sizeof(int32_t) * size_t(G.m) * size_t(G.P);
@@ -1295,6 +1337,7 @@ topo_status topo_build_index_pairs(topo_ctx* ctx, int32_t* iK, int32_t* jK) {
 topo_status topo_simp_interpolate(topo_ctx* ctx, const double* xhat, const topo_simp* prm,
                                   double* sK, double* dsK) {
   if (!ctx || !prm) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   const long long m = ctx->G.m;
   const double* x;
@@ -1313,6 +1356,7 @@ topo_status topo_simp_interpolate(topo_ctx* ctx, const double* xhat, const topo_
 
 topo_status topo_assemble_values(topo_ctx* ctx, const double* sKe, double* vals) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   const Geo& G = ctx->G;
   const double* s;
@@ -1477,6 +1521,7 @@ static topo_status csc_values_dev(topo_ctx* ctx, const double* E, double* vals, 
 
 topo_status topo_csc_pattern(topo_ctx* ctx, int64_t* col_ptr, int32_t* row_idx, int64_t* nnz) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   TRY(csc_setup(ctx));
   if (nnz) *nnz = ctx->csc_nnz;
@@ -1493,6 +1538,7 @@ topo_status topo_csc_pattern(topo_ctx* ctx, int64_t* col_ptr, int32_t* row_idx, 
 topo_status topo_csc_set_fixed(topo_ctx* ctx, const int32_t* fixed, int64_t nfixed,
                                int64_t* num_free) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   if (ctx->nranks > 1) return fail(ctx, TOPO_EINVAL, "csc: single-rank contexts only");
   ctx->launches = 0;
   ctx->csc_nnz = -1;  // the pattern follows the new numbering
@@ -1525,6 +1571,7 @@ topo_status topo_csc_set_fixed(topo_ctx* ctx, const int32_t* fixed, int64_t nfix
 
 topo_status topo_csc_values(topo_ctx* ctx, const double* sKe, double* values) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   TRY(csc_setup(ctx));
   const Geo& G = ctx->G;
@@ -1563,6 +1610,7 @@ static topo_status launch_elem(topo_ctx* ctx, const ElemArgs& A, int nb) {
 topo_status topo_sensitivity(topo_ctx* ctx, const double* U, const double* xhat,
                              const topo_simp* prm, double* c, double* dc) {
   if (!ctx || !prm) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   const Geo& G = ctx->G;
   const double *u, *x;
@@ -1598,6 +1646,7 @@ topo_status topo_sensitivity(topo_ctx* ctx, const double* U, const double* xhat,
 // ------------------------------------------------------------- filter.hpp
 topo_status topo_filter(topo_ctx* ctx, const double* x, double* xTilde, int pin) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   const Geo& G = ctx->G;
   const double* xs;
@@ -1618,6 +1667,7 @@ topo_status topo_filter(topo_ctx* ctx, const double* x, double* xTilde, int pin)
 
 topo_status topo_filter_adjoint(topo_ctx* ctx, const double* g, double* out) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   const Geo& G = ctx->G;
   const double* gs;
@@ -1637,6 +1687,7 @@ topo_status topo_filter_adjoint(topo_ctx* ctx, const double* g, double* out) {
 static topo_status project_impl(topo_ctx* ctx, const double* xt, double eta, double beta,
                                 double* out, int deriv) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   const long long m = ctx->G.m;
   const double* x;
@@ -1657,10 +1708,10 @@ topo_status topo_project_derivative(topo_ctx* ctx, const double* xt, double eta,
                                     double* out) {
   return project_impl(ctx, xt, eta, beta, out, 1);
 }
-
 topo_status topo_backfilter(topo_ctx* ctx, const double* g, const double* xt, double eta,
                             double beta, int proj_on, double* out) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   const Geo& G = ctx->G;
   const double *gd, *xd = nullptr;
@@ -1685,6 +1736,7 @@ topo_status topo_backfilter(topo_ctx* ctx, const double* g, const double* xt, do
 topo_status topo_solve_eta(topo_ctx* ctx, const double* xTilde, double beta, double eta0,
                            double* eta, int32_t* iters) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   if (!(beta > 0)) return fail(ctx, TOPO_EINVAL, "eta solve: beta must be positive");
   const double* x;
@@ -1703,6 +1755,7 @@ topo_status topo_lambda_upper(topo_ctx* ctx, int64_t nact, const double* xAct,
                               const double* dcAct, const double* dVAct, double volfrac,
                               int64_t mTotal, double* lambda) {
   if (!ctx || !lambda) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   if (nact == 0) {
     const double root = 0.0 / (double(mTotal) * volfrac);
@@ -1736,6 +1789,7 @@ topo_status topo_oc_candidate(topo_ctx* ctx, int64_t nact, const double* xAct,
                               const double* dcAct, const double* dVAct, double lambda,
                               double move, double* out) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   if (!(lambda > 0)) return fail(ctx, TOPO_EINVAL, "oc: multiplier must be positive");  // oc.hpp:74
   if (nact == 0) return TOPO_OK;
@@ -1759,6 +1813,7 @@ topo_status topo_oc_bisect(topo_ctx* ctx, const double* x, const double* dc, con
                            topo_volume_fn cb, void* user, double* xNew, double* lambda,
                            int32_t* bisections, int32_t* evaluations) {
   if (!ctx || !prm) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   if (volume_mode < TOPO_VOL_CALLBACK || volume_mode > TOPO_VOL_FILTERED)
     return fail(ctx, TOPO_EINVAL, "oc: unknown volume mode %d", volume_mode);
@@ -1800,6 +1855,7 @@ topo_status topo_oc_primal_dual(topo_ctx* ctx, const double* x, const double* dc
                                 double* xNew, double* lambda, int32_t* iterations,
                                 int32_t* fell_back) {
   if (!ctx || !prm) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   const Geo& G = ctx->G;
   const double *xd, *dcd, *dVd;
@@ -1915,14 +1971,14 @@ static topo_status launch_tile_op(topo_ctx* ctx, const MgGeo& L, const double* E
 #define TILE_KERNELS(X)                                                                    \
   X(kEpiApply, false) X(kEpiCG, false) X(kEpiJacobi, false) X(kEpiResidual, false)          \
   X(kEpiApply, true) X(kEpiJacobi, true) X(kEpiResidual, true)
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;  // bit per device
+  if (!(attr >> ctx->device & 1)) {
 #define TILE_ATTR(E_, C_)                                                               \
   CK(cudaFuncSetAttribute((const void*)k_mg_apply_tile<E_, C_>,                          \
                           cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
     TILE_KERNELS(TILE_ATTR)
 #undef TILE_ATTR
-    attr = true;
+    attr |= 1ull << ctx->device;
   }
   if (!ctx->d_kwp.p) {
     double kwp[48];
@@ -1974,6 +2030,7 @@ static MgGeo state_mg_geo(const StateGeo& S, long long m) {
 topo_status topo_apply_stiffness(topo_ctx* ctx, const double* sK, const double* x, double* y,
                                  int32_t variant) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   if (ctx->nranks > 1) return fail(ctx, TOPO_EINVAL, "apply: single-rank contexts only");
   if (variant < 0 || variant > 2) return fail(ctx, TOPO_EINVAL, "apply: variant must be 0, 1 or 2");
   if (variant == 1 && !(ctx->G.is3d && ctx->walsh))
@@ -2037,6 +2094,7 @@ topo_status topo_solve_state(topo_ctx* ctx, const double* sK, const double* f,
                              const int32_t* fixed, int64_t nfixed, double rtol, int32_t maxit,
                              double* u, int32_t* iterations, double* relres) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   if (ctx->nranks > 1) return fail(ctx, TOPO_EINVAL, "solve: single-rank contexts only");
   if (!(rtol > 0) || maxit < 0) return fail(ctx, TOPO_EINVAL, "solve: rtol > 0, maxit >= 0");
   ctx->launches = 0;
@@ -2242,6 +2300,7 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
                                 const int32_t* fixed, int64_t nfixed, double rtol, int32_t maxit,
                                 double* u, int32_t* iterations, double* relres) {
   if (!ctx) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   if (ctx->nranks > 1) return fail(ctx, TOPO_EINVAL, "solve: single-rank contexts only");
   if (!(rtol > 0) || maxit < 0) return fail(ctx, TOPO_EINVAL, "solve: rtol > 0, maxit >= 0");
   const Geo& G = ctx->G;
@@ -2881,6 +2940,7 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
 topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
                              const topo_pass_params* prm, topo_pass_out* out) {
   if (!ctx || !prm || !out) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
   ctx->oc_blocks_now = 0;
   const Geo& G = ctx->G;
@@ -3341,6 +3401,7 @@ extern "C" topo_status topo_nccl_unique_id(void* out128) {
 
 extern "C" topo_status topo_comm_init_nccl(topo_ctx* ctx, const void* uid) {
   if (!ctx || !uid) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   if (ctx->comm) return fail(ctx, TOPO_EINVAL, "communicator already initialised");
   std::string err;
   if (!g_nccl.load(&err)) return fail(ctx, TOPO_ENCCL, "%s", err.c_str());
@@ -3360,6 +3421,7 @@ extern "C" topo_status topo_comm_init_nccl(topo_ctx* ctx, const void* uid) {
 
 extern "C" topo_status topo_comm_init_host(topo_ctx* ctx, const topo_host_comm* hc) {
   if (!ctx || !hc || !hc->exchange || !hc->allreduce_sum) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
   if (ctx->comm) return fail(ctx, TOPO_EINVAL, "communicator already initialised");
   Comm* c = new Comm;
   c->kind = 2;

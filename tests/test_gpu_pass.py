@@ -109,7 +109,7 @@ def test_pass_config3_identity(P, oracle_port):
     from paper_2005_05436_b200.configs import CONFIGS, make_inputs
     cfg = CONFIGS[3]
     x, u, state = make_inputs(cfg)
-    check_pass(P, oracle_port, cfg, x, u, state, IDENTITY, check_sk=False)
+    check_pass(P, oracle_port, cfg, x, u, state, IDENTITY, check_sk=True)
 
 
 def test_pass_config5_subgrid(P, oracle_port):
@@ -119,6 +119,83 @@ def test_pass_config5_subgrid(P, oracle_port):
     x, u, state = rand_case(cfg.grid, 55)
     g, _, _ = check_pass(P, oracle_port, cfg, x, u, state, IDENTITY)
     assert g.bisections == 200 and g.evaluations == 243
+
+
+# ------------------------------------------------ C5 at full size (the benched config)
+# 384 x 192 x 192: 14.2M elements, 4.25e9 sK values (34 GB, offsets > 2^31).
+# Only this size takes the overlapped sK stream (sK >= 4 GB), its dynamic
+# work claiming and the 8-chunk host-U pipeline, so it is compared here at full
+# size: all per-element arrays against the oracle conditioned on eta_gpu, and
+# sK in x-layer chunks (the oracle cannot hold 34 GB): the first 8 layers, the
+# 8 layers whose flat offsets straddle 2^31, and the last 8.
+C5_LAYERS = {"first8": (0, 8), "straddle_2p31": (190, 198), "last8": (376, 384)}
+
+
+@pytest.fixture(scope="module")
+def c5_full(P, oracle_port):
+    import torch
+    from paper_2005_05436_b200.configs import CONFIGS, make_inputs
+    cfg = CONFIGS[5]
+    x, u, state = make_inputs(cfg)
+    assert state is None
+    S = cfg.nely * cfg.nelz
+    assert S * 190 * cfg.P < 2 ** 31 < S * 198 * cfg.P
+    kw = dict(beta=cfg.beta, eta0=cfg.eta0, move=cfg.move, volfrac=cfg.volfrac)
+    out = {}
+    with P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu) as ctx:
+        for name, xin, uin in (("device", torch.from_numpy(x).cuda(), torch.from_numpy(u).cuda()),
+                               ("host", x, u)):
+            # host inputs, device outputs: the chunked host-U pipeline, sK on device
+            g = ctx.design_pass(xin, uin, return_sk=True, out_device=True, **kw)
+            arrs = {k: getattr(g, k).cpu().numpy() for k in
+                    ("xTilde", "xPhys", "dcPhys", "dc", "dV", "xNew")}
+            sk = {c: g.sK[a * S * cfg.P:b * S * cfg.P].cpu().numpy()
+                  for c, (a, b) in C5_LAYERS.items()}
+            out[name] = (g, arrs, sk)
+            del g.sK, g
+            torch.cuda.empty_cache()
+    oracle_port.set_threads(0)
+    f = oracle_port.filter(cfg.grid, cfg.rmin)
+    xt = oracle_port.apply_filter(f, x)
+    eta_ref, it_ref = oracle_port.solve_eta(xt, cfg.beta, cfg.eta0)
+    g = out["device"][0]
+    rc = oracle_port.design_pass(cfg.grid, cfg.rmin, x, u, None, volume_mode=IDENTITY, filt=f,
+                                 eta_override=g.eta, **kw)
+    return cfg, out, rc, xt, eta_ref
+
+
+def test_pass_config5_full_device(P, oracle_port, c5_full):
+    cfg, out, rc, xt, eta_ref = c5_full
+    g, arrs, sk = out["device"]
+    # stage 1: eta
+    assert abs(g.eta - eta_ref) <= 5e-8, (g.eta, eta_ref)
+    assert abs(oracle_port.eta_mismatch(xt, cfg.beta, g.eta)) <= 1e-6
+    # stage 2: conditioned on eta_gpu
+    errs = {k: rel(arrs[k], getattr(rc, k)) for k in arrs}
+    assert all(e <= 1e-12 for e in errs.values()), errs
+    assert abs(g.c - rc.c) <= 1e-12 * abs(rc.c)
+    assert g.bisections == rc.bisections == 200 and g.evaluations == rc.evaluations == 243
+    assert abs(g.lam - rc.lam) <= 1e-10 * abs(rc.lam)
+    _, kl = oracle_port.element_stiffness(3, cfg.nu)
+    S = cfg.nely * cfg.nelz
+    for c, (a, b) in C5_LAYERS.items():
+        ref = oracle_port.assemble_values(rc.sKe[a * S:b * S], kl)
+        assert rel(sk[c], ref) <= 1e-12, c
+
+
+def test_pass_config5_full_host_inputs(c5_full):
+    """Host x / U (the e2e path: x first, U in 8 x-chunks on a copy stream with
+    K3a and K4 chunks trailing them) gives the device-input pass bit for bit;
+    only c's reduction tree differs (per-chunk block partials)."""
+    _, out, _, _, _ = c5_full
+    gd, ad, sd = out["device"]
+    gh, ah, sh = out["host"]
+    assert gh.eta == gd.eta and gh.lam == gd.lam and gh.bisections == gd.bisections
+    for k in ad:
+        assert np.array_equal(ah[k], ad[k]), k
+    for c in sd:
+        assert np.array_equal(sh[c], sd[c]), c
+    assert abs(gh.c - gd.c) <= 1e-13 * abs(gd.c)
 
 
 def test_pass_deterministic(P):
