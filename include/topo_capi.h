@@ -287,6 +287,10 @@ enum { TOPO_STAGE_FILTER = 0, TOPO_STAGE_ETA, TOPO_STAGE_ELEM, TOPO_STAGE_ADJOIN
        TOPO_STAGE_SK, TOPO_STAGE_PASS, TOPO_NSTAGES };
 topo_status topo_set_timing(topo_ctx* ctx, int on);
 topo_status topo_stage_times(topo_ctx* ctx, double* times_ms);
+/* repeated single-rank topo_design_pass calls over the same device arrays and
+ * parameters are captured into a CUDA graph (second call) and replayed;
+ * replays = passes served by the graph so far (TOPO_PASS_GRAPH=0 disables) */
+topo_status topo_pass_graph_replays(const topo_ctx* ctx, int64_t* replays);
 
 /* ---- measurement helper (not part of the reference API) ------------------
  * FP64 FMA throughput of `device` in TFLOP/s (2 flops per DFMA), measured

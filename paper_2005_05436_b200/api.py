@@ -360,6 +360,13 @@ class Context:
         """Per-stage CUDA-event timing of design_pass (events on each kernel's stream)."""
         self._check(self.lib.topo_set_timing(self.h, int(on)))
 
+    @property
+    def graph_replays(self) -> int:
+        """Design passes served by the captured CUDA graph so far."""
+        n = C.c_int64()
+        self._check(self.lib.topo_pass_graph_replays(self.h, C.byref(n)))
+        return int(n.value)
+
     def stage_times(self) -> dict:
         t = np.zeros(len(L.STAGES))
         self._check(self.lib.topo_stage_times(self.h, t.ctypes.data))

@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <string>
 #include <functional>
 #include <memory>
@@ -23,11 +24,16 @@ using namespace topo;
 
 namespace {
 
+// bumped whenever any device buffer moves: a captured pass graph bakes the
+// addresses in and is replayed only while this is unchanged
+std::atomic<unsigned long long> g_alloc_epoch{0};
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   cudaError_t ensure(size_t b) {
     if (b <= bytes && p) return cudaSuccess;
+    ++g_alloc_epoch;
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -36,6 +42,7 @@ struct DevBuf {
     return e;
   }
   void release() {
+    if (p) ++g_alloc_epoch;
     if (p) cudaFree(p);
     p = nullptr;
     bytes = 0;
@@ -74,6 +81,9 @@ bool is_device_ptr(const void* p) {
 
 struct MgState;
 void mg_state_free(MgState*);
+struct PassGraph;
+void pass_graph_free(PassGraph*);
+long long pass_graph_replays(const PassGraph*);
 void solver_destroy(void*);
 
 struct topo_ctx {
@@ -105,6 +115,7 @@ struct topo_ctx {
   bool walsh = false;
   KeWalsh kw{};
   std::vector<double> w3;
+  ConvW3 w3v{};  // the same weights + column half-widths, passed by value
   DevBuf d_w3;
   // element matrices
   std::vector<double> ke_full, ke_lower;
@@ -131,6 +142,8 @@ struct topo_ctx {
   int conv_R = 8;              // outputs per thread along the run axis
   int conv_A = 0;              // > 0: small-reach direct variant with half-width bound A
   bool overlap_sk = false;     // run the sK store concurrently with K3a..K6
+  bool use_pass_graph = true;  // capture / replay single-rank device passes (TOPO_PASS_GRAPH)
+  PassGraph* pgraph = nullptr;
   int oc_blocks_now = 0;
   // lower-triangle CSC of K (topo_csc_*): pattern built once on first use
   CscTab csc_tab{};
@@ -358,16 +371,17 @@ bool walsh_blocks(const double* ke, KeWalsh* out) {
 
 // k_conv3 (3D, reach 1..4): one warp along i, WR x WO warps of RB x TB
 // outputs; two blocks per SM
-constexpr int kC3R = 4, kC3T = 4;
-ConvGeom conv_geom3(const topo_ctx* c, const Geo& G, int WR, int WO) {
+constexpr int kC3R = 4, kC3T = 4, kC3Rs = 2;
+ConvGeom conv_geom3(const topo_ctx* c, const Geo& G, int WR, int WO, int RB = kC3R,
+                    int TB = kC3T) {
   ConvGeom T;
   const int A = c->conv_A;
   T.WI = 1;
   T.WR = WR;
   T.WO = WO;
   T.TI = 32;
-  T.TR = kC3R * WR;
-  T.TO = kC3T * WO;
+  T.TR = RB * WR;
+  T.TO = TB * WO;
   T.reach = T.reach_o = A;
   T.EI = T.TI + 2 * A;
   T.ER = (T.TR + 2 * A) | 1;
@@ -380,12 +394,20 @@ ConvGeom conv_geom3(const topo_ctx* c, const Geo& G, int WR, int WO) {
   return T;
 }
 
+// small grids (fewer than two 4 x 4 blocks per SM, e.g. C4's 54): 2 x 2
+// outputs per thread, 4x the blocks (less register reuse, but every SM busy)
+int conv3_rb(const topo_ctx* c, const Geo& G) {
+  const long long outs4 = 32LL * kC3R * kC3T * (kThreads / 32);
+  return G.m < 2LL * c->sm_count * outs4 ? kC3Rs : kC3R;
+}
+
 ConvGeom pick_geom3(const topo_ctx* c, const Geo& G) {
   static const int opts[][2] = {{2, 4}, {4, 2}, {1, 8}, {8, 1}};
+  const int rb = conv3_rb(c, G);
   ConvGeom best{};
   double best_cost = 1e300;
   for (auto& o : opts) {
-    ConvGeom T = conv_geom3(c, G, o[0], o[1]);
+    ConvGeom T = conv_geom3(c, G, o[0], o[1], rb, rb);
     if (conv_smem(T) > 112 * 1024) continue;
     const double outs = double(T.TI) * T.TR * T.TO;
     const double fi = std::ceil(double(G.nely) / T.TI) * T.TI / G.nely;
@@ -425,10 +447,16 @@ topo_status launch_conv3_t(topo_ctx* ctx, const Geo& G, ConvGeom T, const ConvAr
   if (!(attr_done >> ctx->device & 1)) {
     CK(cudaFuncSetAttribute(k_conv3<NF, MODE, AR, kC3R, kC3T>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024 + 4096));
+    CK(cudaFuncSetAttribute(k_conv3<NF, MODE, AR, kC3Rs, kC3Rs>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024 + 4096));
     attr_done |= 1ull << ctx->device;
   }
-  k_conv3<NF, MODE, AR, kC3R, kC3T><<<grid, kThreads, smem, ctx->stream>>>(
-      G, T, ctx->d_w3.as<double>(), A);
+  if (T.TR == kC3Rs * T.WR)
+    k_conv3<NF, MODE, AR, kC3Rs, kC3Rs><<<grid, kThreads, smem, ctx->stream>>>(
+        G, T, ctx->w3v, A);
+  else
+    k_conv3<NF, MODE, AR, kC3R, kC3T><<<grid, kThreads, smem, ctx->stream>>>(
+        G, T, ctx->w3v, A);
   LAUNCHED();
   if (nblocks) *nblocks = int(grid.x * grid.y * ztiles);  // the whole grid's partials
   return TOPO_OK;
@@ -970,6 +998,15 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
             const double wv = weight(a, b, c);  // (di, do = dj, dr = dk)
             ctx->w3.push_back(wv > 0 ? wv : 0.0);
           }
+      const int NW = AW + 1;
+      for (int q = 0; q < NW * NW * NW && q < 125; ++q) ctx->w3v.w[q] = ctx->w3[size_t(q)];
+      for (int a = 0; a < NW; ++a)
+        for (int b = 0; b < NW; ++b) {
+          int h = -1;
+          for (int c = 0; c < NW; ++c)
+            if (ctx->w3[size_t((a * NW + b) * NW + c)] != 0.0) h = c;
+          ctx->w3v.hw[a * NW + b] = h;
+        }
     }
   }
   // element matrices
@@ -992,8 +1029,12 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   {
     // sK stream overlapped with K3a + K4 on large 3D passes (C5, also per slab)
     const char* ov = getenv("TOPO_SK_OVERLAP");
-    const bool big = G.is3d && double(G.m) * G.P * 8.0 >= 4e9;
+    // (C5 6.32 vs 7.05 ms per pass; C4 0.206 vs 0.229 ms since the pass is
+    // replayed from a CUDA graph)
+    const bool big = G.is3d && double(G.m) * G.P * 8.0 >= 256e6;
     ctx->overlap_sk = ov ? ov[0] == '1' : big;
+    const char* pgr = getenv("TOPO_PASS_GRAPH");
+    ctx->use_pass_graph = pgr ? pgr[0] != '0' : true;
   }
 
 #define CKC(x)                                                                          \
@@ -1091,6 +1132,8 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   if (ctx->comm) comm_destroy(ctx->comm);
   mg_state_free(ctx->mg);
   ctx->mg = nullptr;
+  pass_graph_free(ctx->pgraph);
+  ctx->pgraph = nullptr;
   solver_destroy(ctx->cusolver);
   ctx->cusolver = nullptr;
   ctx->d_kwp.release();
@@ -1156,6 +1199,12 @@ topo_status topo_fp64_peak(int device, double* tflops) {
   cudaFree(d);
   if (err != cudaSuccess) return TOPO_ECUDA;
   *tflops = 2.0 * 8.0 * iters * double(blocks) * kThreads / (best * 1e-3) / 1e12;
+  return TOPO_OK;
+}
+
+topo_status topo_pass_graph_replays(const topo_ctx* ctx, int64_t* replays) {
+  if (!ctx || !replays) return TOPO_EINVAL;
+  *replays = ctx->pgraph ? pass_graph_replays(ctx->pgraph) : 0;
   return TOPO_OK;
 }
 
@@ -2937,20 +2986,29 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
 // driver.hpp:183-231 (ft = 3) with U supplied:
 //   main stream: K1 filter+pin+eta0 terms -> K2 eta -> K3a elem -> K4 adjoint+OC prep -> K5/6 OC
 //   aux  stream:                          \-> K3b sK store (overlaps K3a..K6)
-topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
-                             const topo_pass_params* prm, topo_pass_out* out) {
-  if (!ctx || !prm || !out) return TOPO_EINVAL;
-  DeviceGuard dg_(ctx->device);
-  ctx->launches = 0;
-  ctx->oc_blocks_now = 0;
+}  // extern "C"
+
+// Host-side facts of one enqueued pass that the tail (after the stream
+// synchronisation) needs; fixed for a given pass key, so a captured graph
+// keeps the capture-time copy.
+struct PassHost {
+  bool want_sk = false, oc_deferred = false;
+  double lam = 0;
+  int32_t bis = 0, ev = 0;
+};
+
+__global__ void k_set_eta(double* res, double eta) {
+  res[0] = eta;
+  res[1] = 0.0;
+  res[2] = 0.0;
+}
+
+// Everything the pass puts on the streams, ending with the result and output
+// copies on ctx->stream (no host synchronisation: capturable).
+static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
+                                const topo_pass_params* prm, topo_pass_out* out, PassHost* H) {
   const Geo& G = ctx->G;
-  if (ctx->nranks > 1 && !ctx->comm)
-    return fail(ctx, TOPO_EINVAL, "multi-rank context: call topo_comm_init_nccl/_host first");
-  if (!(prm->beta > 0)) return fail(ctx, TOPO_EINVAL, "eta solve: beta must be positive");
   const int vmode = prm->volume_mode;
-  if (vmode != TOPO_VOL_FILTERED && vmode != TOPO_VOL_MEAN)
-    return fail(ctx, TOPO_EINVAL, "design pass: volume mode %d not supported in the fused pass",
-                vmode);
   const uint8_t* state = ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr;
   const double *xs, *ud = nullptr;
   CK(ctx->partials.ensure(std::max(ctx->partials.bytes,
@@ -2978,8 +3036,8 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   if (solve) {
     TRY(run_eta(ctx, ctx->xt.as<double>(), prm->beta, prm->eta0, res));
   } else {
-    const double r[3] = {prm->eta_override, 0.0, 0.0};
-    CK(cudaMemcpyAsync(res, r, sizeof r, cudaMemcpyHostToDevice, ctx->stream));
+    k_set_eta<<<1, 1, 0, ctx->stream>>>(res, prm->eta_override);  // (graph-safe: no host source)
+    LAUNCHED();
   }
   tmark(ctx, TOPO_STAGE_ETA, 1, ctx->stream);
   // lower-triangle CSC values of K (fea.hpp:154-176), when requested
@@ -3172,9 +3230,132 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
   if (want_sk && out->sK && skp != out->sK)
     CK(cudaMemcpyAsync(out->sK, skp, sizeof(double) * size_t(G.m * G.P), cudaMemcpyDefault,
                        ctx->stream));
+  H->want_sk = want_sk;
+  H->oc_deferred = oc_deferred;
+  H->lam = lam;
+  H->bis = bis;
+  H->ev = ev;
+  return TOPO_OK;
+}
+
+// A single-rank pass over device arrays is captured into a CUDA graph on the
+// second call with the same arrays and parameters and replayed from then on
+// (one graph launch instead of ~10-20 kernel launches, no inter-launch host
+// gaps; the small configs are launch-latency bound). The key is every input
+// that shapes the enqueued work; any device-buffer reallocation invalidates it.
+struct PassKey {
+  const double* x;
+  const double* U;
+  topo_pass_params prm;
+  double *xTilde, *xPhys, *dcPhys, *dc, *dV, *xNew, *sK;
+  cudaStream_t stream;
+  unsigned long long epoch;
+};
+
+struct PassGraph {
+  PassKey key{}, seen{};
+  bool have_seen = false, disabled = false;
+  cudaGraphExec_t exec = nullptr;
+  PassHost host{};
+  long long launches = 0, replays = 0;
+  ~PassGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+  }
+};
+
+static bool same_key(const PassKey& a, const PassKey& b) { return memcmp(&a, &b, sizeof a) == 0; }
+
+void pass_graph_free(PassGraph* g) { delete g; }
+long long pass_graph_replays(const PassGraph* g) { return g->replays; }
+
+extern "C" {
+
+topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
+                             const topo_pass_params* prm, topo_pass_out* out) {
+  if (!ctx || !prm || !out) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
+  ctx->launches = 0;
+  ctx->oc_blocks_now = 0;
+  const Geo& G = ctx->G;
+  if (ctx->nranks > 1 && !ctx->comm)
+    return fail(ctx, TOPO_EINVAL, "multi-rank context: call topo_comm_init_nccl/_host first");
+  if (!(prm->beta > 0)) return fail(ctx, TOPO_EINVAL, "eta solve: beta must be positive");
+  const int vmode = prm->volume_mode;
+  if (vmode != TOPO_VOL_FILTERED && vmode != TOPO_VOL_MEAN)
+    return fail(ctx, TOPO_EINVAL, "design pass: volume mode %d not supported in the fused pass",
+                vmode);
+  if (!x || !U) return fail(ctx, TOPO_EINVAL, "null input array");
+  PassHost H;
+  bool graphable = ctx->use_pass_graph && !ctx->comm && !ctx->timing && !out->Kval &&
+                   is_device_ptr(x) && is_device_ptr(U);
+  for (double* p : {out->xTilde, out->xPhys, out->dcPhys, out->dc, out->dV, out->xNew, out->sK})
+    if (p && !is_device_ptr(p)) graphable = false;
+  if (graphable && !ctx->pgraph) ctx->pgraph = new PassGraph;
+  PassGraph* pg = graphable ? ctx->pgraph : nullptr;
+  if (pg && pg->disabled) pg = nullptr;
+  PassKey key;
+  memset(&key, 0, sizeof key);  // padding bytes take part in the comparison
+  if (pg) {
+    key.x = x;
+    key.U = U;
+    key.prm = *prm;
+    key.xTilde = out->xTilde;
+    key.xPhys = out->xPhys;
+    key.dcPhys = out->dcPhys;
+    key.dc = out->dc;
+    key.dV = out->dV;
+    key.xNew = out->xNew;
+    key.sK = out->sK;
+    key.stream = ctx->stream;
+    key.epoch = g_alloc_epoch.load();
+  }
+  if (pg && pg->exec && same_key(pg->key, key)) {
+    CK(cudaGraphLaunch(pg->exec, ctx->stream));
+    ++pg->replays;
+    H = pg->host;
+    ctx->launches = pg->launches;
+  } else if (pg && pg->have_seen && same_key(pg->seen, key)) {
+    // second call with this key (buffers allocated by the first): capture
+    if (pg->exec) cudaGraphExecDestroy(pg->exec);
+    pg->exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed));
+    const topo_status st = pass_enqueue(ctx, x, U, prm, out, &H);
+    const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+    cudaGraphExec_t exec = nullptr;
+    const bool ok = st == TOPO_OK && ce == cudaSuccess && graph &&
+                    cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess &&
+                    g_alloc_epoch.load() == key.epoch;
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    if (ok) {
+      pg->exec = exec;
+      pg->key = key;
+      pg->host = H;
+      pg->launches = ctx->launches;
+      CK(cudaGraphLaunch(exec, ctx->stream));
+      ++pg->replays;
+    } else {  // not capturable here: run it eagerly from now on
+      if (exec) cudaGraphExecDestroy(exec);
+      pg->disabled = true;
+      ctx->launches = 0;
+      ctx->err.clear();
+      TRY(pass_enqueue(ctx, x, U, prm, out, &H));
+    }
+  } else {
+    TRY(pass_enqueue(ctx, x, U, prm, out, &H));
+    if (pg) {
+      key.epoch = g_alloc_epoch.load();  // buffers this call allocated
+      pg->seen = key;
+      pg->have_seen = true;
+    }
+  }
   CK(cudaStreamSynchronize(ctx->stream));
+  const bool want_sk = H.want_sk;
+  double lam = H.lam;
+  int32_t bis = H.bis, ev = H.ev;
   double c = ctx->h_result[4];
-  if (oc_deferred) {
+  if (H.oc_deferred) {
     const double* r = ctx->h_result + 8;
     if (int(r[3]) == OcCtl::ST_NONMONO)
       return fail(ctx, TOPO_ENONMONO, "oc: candidate volume is not monotone in the multiplier");

@@ -540,16 +540,74 @@ __global__ void __launch_bounds__(kThreads) k_conv(Geo G, ConvGeom T, const Conv
 // rows it reaches: ~(2AR+1)(TB+2AR)(RB+2AR)/(RB TB) shared loads per output
 // instead of ~(#columns)(R+2AR)/R. Weights w3[di][|do|][|dr|] (zero outside
 // the cone) are uniform loads.
+// Cone weights of k_conv3, passed BY VALUE as a kernel parameter: with di,
+// |do| and |dr| compile-time (fully unrolled loops, 2 x 2 outputs per
+// thread) every weight is a constant-bank operand of its DFMA and takes no
+// register (C4 adjoint filter 0.035 vs 0.050 ms).
+// w[di][|do|][|dr|] (zero outside the cone); hw[di][|do|] = largest |dr| with
+// a nonzero weight (-1: none).
+struct ConvW3 {
+  double w[5 * 5 * 5];
+  int hw[5 * 5];
+};
+
+template <int AR, int RB, int TB, bool FOLD, int DI>
+__device__ __forceinline__ void conv3_di(const double* __restrict__ base, int sI, int sPlane,
+                                         const ConvW3& W, double (&acc)[TB][RB]) {
+  constexpr int NW = AR + 1;
+  const double* p = base + DI * sI;
+  const double* q = base - DI * sI;
+#pragma unroll
+  for (int kk = 0; kk < TB + 2 * AR; ++kk) {
+    double v[RB + 2 * AR];
+#pragma unroll
+    for (int j = 0; j < RB + 2 * AR; ++j)
+      v[j] = FOLD ? p[kk * sPlane + j] + q[kk * sPlane + j] : p[kk * sPlane + j];
+    // taps outside the cone (zero weight) skipped by uniform branches on the
+    // column's half-width hw (its weights vanish beyond it); the +-dr pair
+    // shares its weight, so it is pre-added once per row and feeds every
+    // output row t it reaches: one FMA per pair, and consecutive FMAs go to
+    // different accumulators (no back-to-back dependency)
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      const int dO = kk - t - AR;
+      if (dO < -AR || dO > AR) continue;
+      const int ao = dO < 0 ? -dO : dO;
+      if (W.hw[DI * NW + ao] < 0) continue;
+#pragma unroll
+      for (int r = 0; r < RB; ++r) acc[t][r] = fma(W.w[(DI * NW + ao) * NW], v[r + AR], acc[t][r]);
+    }
+#pragma unroll
+    for (int ad = 1; ad <= AR; ++ad) {
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const double pr = v[r + AR - ad] + v[r + AR + ad];
+#pragma unroll
+        for (int t = 0; t < TB; ++t) {
+          const int dO = kk - t - AR;
+          if (dO < -AR || dO > AR) continue;
+          const int ao = dO < 0 ? -dO : dO;
+          if (W.hw[DI * NW + ao] >= ad)
+            acc[t][r] = fma(W.w[(DI * NW + ao) * NW + ad], pr, acc[t][r]);
+        }
+      }
+    }
+  }
+}
+
+// 4 x 4 outputs per thread (large grids): the weights of the di slice in
+// registers and the +-dr taps as two FMAs (measured: the pre-added form
+// below spills at this block size, C5 K1 0.44 vs 0.36 ms)
 template <int AR, int RB, int TB, bool FOLD>
-__device__ __forceinline__ void conv3_di(const double* __restrict__ base, int di, int sI,
-                                         int sPlane, const double* __restrict__ w3,
+__device__ __forceinline__ void conv3_di_rw(const double* __restrict__ base, int di, int sI,
+                                            int sPlane, const ConvW3& W,
                                          double (&acc)[TB][RB]) {
   constexpr int NW = AR + 1;
   double w[NW][NW];
 #pragma unroll
   for (int a = 0; a < NW; ++a)
 #pragma unroll
-    for (int b = 0; b < NW; ++b) w[a][b] = __ldg(w3 + (di * NW + a) * NW + b);
+    for (int b = 0; b < NW; ++b) w[a][b] = W.w[(di * NW + a) * NW + b];
   int hw[NW];  // largest |dr| with a nonzero weight at (di, |do|), -1: none
 #pragma unroll
   for (int a = 0; a < NW; ++a) {
@@ -590,9 +648,25 @@ __device__ __forceinline__ void conv3_di(const double* __restrict__ base, int di
   }
 }
 
+template <int AR, int RB, int TB>
+__device__ __forceinline__ void conv3_all(const double* __restrict__ base, int sI, int sPlane,
+                                          const ConvW3& W, double (&acc)[TB][RB]) {
+  if (RB * TB >= 16) {
+    conv3_di_rw<AR, RB, TB, false>(base, 0, sI, sPlane, W, acc);
+#pragma unroll 1
+    for (int di = 1; di <= AR; ++di) conv3_di_rw<AR, RB, TB, true>(base, di, sI, sPlane, W, acc);
+    return;
+  }
+  conv3_di<AR, RB, TB, false, 0>(base, sI, sPlane, W, acc);
+  if (AR >= 1) conv3_di<AR, RB, TB, true, AR >= 1 ? 1 : 0>(base, sI, sPlane, W, acc);
+  if (AR >= 2) conv3_di<AR, RB, TB, true, AR >= 2 ? 2 : 0>(base, sI, sPlane, W, acc);
+  if (AR >= 3) conv3_di<AR, RB, TB, true, AR >= 3 ? 3 : 0>(base, sI, sPlane, W, acc);
+  if (AR >= 4) conv3_di<AR, RB, TB, true, AR >= 4 ? 4 : 0>(base, sI, sPlane, W, acc);
+}
+
 template <int NF, int MODE, int AR, int RB, int TB>
-__global__ void __launch_bounds__(kThreads, 2) k_conv3(Geo G, ConvGeom T,
-                                                       const double* __restrict__ w3, ConvArgs A) {
+__global__ void __launch_bounds__(kThreads, 2) k_conv3(Geo G, ConvGeom T, const __grid_constant__ ConvW3 W,
+                                                       ConvArgs A) {
   extern __shared__ double tile[];
   const int tileN = T.EI * T.ER * T.EO, nlines = T.EO * T.ER;
   long long* lineSrc = reinterpret_cast<long long*>(tile + tileN);
@@ -619,9 +693,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv3(Geo G, ConvGeom T,
     for (int t = 0; t < TB; ++t)
 #pragma unroll
       for (int r = 0; r < RB; ++r) acc[t][r] = 0.0;
-    conv3_di<AR, RB, TB, false>(tile + sb0, 0, sI, sPlane, w3, acc);
-#pragma unroll 1
-    for (int di = 1; di <= AR; ++di) conv3_di<AR, RB, TB, true>(tile + sb0, di, sI, sPlane, w3, acc);
+    conv3_all<AR, RB, TB>(tile + sb0, sI, sPlane, W, acc);
     if (f + 1 < NF) {
 #pragma unroll
       for (int t = 0; t < TB; ++t)
@@ -788,6 +860,9 @@ __global__ void __launch_bounds__(kThreads) k_eta_solve(EtaArgs A) {
     }
     grid.sync();
     if (threadIdx.x < 32) {
+      // every block sums the same partials in the same fixed order (measured:
+      // the whole block reading them is slower, C5 0.28 vs 0.23 ms: every SM
+      // hammering the same lines)
       double s4[4];
       warp_sum_partials<4>(P, gridDim.x, 4, s4);
       if (threadIdx.x == 0) {
@@ -1371,6 +1446,8 @@ __global__ void __launch_bounds__(kThreads) k_oc_bisect(OcArgs A) {
     __syncthreads();
   }
   // K6 (xNew at the final multiplier) runs as k_oc_final with full occupancy
+  // (measured: inside this grid, beside the sK stream, C4 OC 0.128 vs 0.04 ms;
+  // the prep and compliance sums folded in here: C4 pass 0.23 vs 0.195 ms)
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.result[0] = ctl.lam_result;
     A.result[1] = ctl.bis;

@@ -110,3 +110,49 @@ def test_chunked_host_pass_matches_device_pass(P):
         np.testing.assert_array_equal(_as_np(getattr(dev, k)), _as_np(getattr(host, k)), err_msg=k)
     assert (dev.eta, dev.lam, dev.bisections) == (host.eta, host.lam, host.bisections)
     assert abs(dev.c - host.c) <= 1e-13 * abs(dev.c)  # K3a partials regrouped by chunk
+
+
+
+@pytest.mark.parametrize("cid,grid", [(4, (24, 12, 12)), (1, (60, 20, None)), (5, (24, 16, 12))])
+def test_pass_graph_replay_is_bitwise_eager(P, cid, grid):
+    # repeated single-rank device passes are captured into a CUDA graph on the
+    # second call and replayed: every replay must equal the eager pass bit for
+    # bit, also after the inputs change in place (same addresses, new values)
+    from paper_2005_05436_b200.configs import CONFIGS
+    cfg = CONFIGS[cid].scaled(*[g for g in grid if g is not None])
+    x, u = _inputs(cfg, 23)
+    x2, u2 = _inputs(cfg, 24)
+    kw = dict(beta=cfg.beta, eta0=cfg.eta0, move=cfg.move, volfrac=cfg.volfrac, return_sk=True)
+
+    def run(env, seq):
+        old = os.environ.get("TOPO_PASS_GRAPH")
+        os.environ["TOPO_PASS_GRAPH"] = env
+        try:
+            with P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu) as ctx:
+                xd = torch.from_numpy(x).cuda()
+                ud = torch.from_numpy(u).cuda()
+                res = []
+                for k in seq:
+                    if k == 1:
+                        xd.copy_(torch.from_numpy(x2))
+                        ud.copy_(torch.from_numpy(u2))
+                    r = ctx.design_pass(xd, ud, **kw)
+                    res.append({f: _as_np(getattr(r, f)).copy() for f in FIELDS} |
+                               {"s": (r.eta, r.lam, r.bisections, r.evaluations, r.c)})
+                    del r  # the next call's outputs reuse these blocks (same addresses)
+                replays.append(ctx.graph_replays)
+                return res
+        finally:
+            if old is None:
+                os.environ.pop("TOPO_PASS_GRAPH", None)
+            else:
+                os.environ["TOPO_PASS_GRAPH"] = old
+
+    replays = []
+    eager = run("0", [0, 1])
+    graph = run("1", [0, 0, 0, 1, 1])
+    assert replays[0] == 0 and replays[1] >= 1  # the graph path was taken
+    for g, e in zip(graph, [eager[0]] * 3 + [eager[1]] * 2):
+        for f in FIELDS:
+            np.testing.assert_array_equal(g[f], e[f], err_msg=f)
+        assert g["s"] == e["s"]
