@@ -127,7 +127,6 @@ struct topo_ctx {
   double nS_total = 0;  // |P1| over all ranks
   double m_total = 0;   // global element count
   // fields
-  DevBuf e1;  // exp(2 beta xTilde) for the eta passes
   OcRecs oc_view{};  // the records run_oc reads (set by their producer)
   DevBuf hs, hs_st, cw, x_st, xt, xphys, dcphys, dc, dV, xnew, a1_st, a2_st, rec, u, tmp0, tmp1,
       tmp_st;
@@ -138,6 +137,7 @@ struct topo_ctx {
   double kwp_host[48] = {};
   DevBuf d_kwp;  // Walsh blocks, plain (k00 k01 k02 k11 k12 k22 per signature), for k_mg_apply_tile
   DevBuf partials, partials0, result;
+  DevBuf cpart;  // K3a compliance partials (kept until the pass tail sums them)
   double* h_result = nullptr;  // pinned
   int conv_R = 8;              // outputs per thread along the run axis
   int conv_A = 0;              // > 0: small-reach direct variant with half-width bound A
@@ -619,35 +619,29 @@ topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
   A.beta = beta;
   A.eta0 = eta0;
   A.mtotal = ctx->m_total;
-  A.e1 = ctx->e1.as<double>();
   A.partials = ctx->partials.as<double>();
   A.result = eta_dev_out;
   if (!ctx->comm) return coop_launch(ctx, (const void*)k_eta_solve, &A, ctx->coop_eta);
-  // multi-GPU: the Newton replay on the device, one allreduce of the four sums
-  // per evaluation on the stream; evaluations are issued in batches of 4 and
-  // the host reads the `done` flag once per batch (no-ops after convergence)
+  // multi-GPU: the moment sums of every rank, allreduced on the stream, and
+  // the Newton replay on the device; the host reads `go` once per round
+  // (normally one round)
   CK(ctx->eta_dev.ensure(sizeof(EtaDev)));
   EtaDev* st = ctx->eta_dev.as<EtaDev>();
-  double* sums = ctx->result.as<double>() + 56;
+  double* sums = ctx->result.as<double>() + 64;  // kEtaNS doubles (64..92)
   k_eta_dev_init<<<1, 1, 0, ctx->stream>>>(st, eta0);
   LAUNCHED();
-  constexpr int kBatch = 4;
-  int first = 1;
-  for (int round = 0; round < 64; round += kBatch) {  // filter.hpp:213: at most 50 iterations
-    for (int q = 0; q < kBatch; ++q) {
-      k_eta_partials_dev<<<ctx->coop_eta, kThreads, 0, ctx->stream>>>(A, st, first);
-      LAUNCHED();
-      k_reduce_partials<4><<<1, 32, 0, ctx->stream>>>(A.partials, ctx->coop_eta, 4, sums);
-      LAUNCHED();
-      TRY(comm_allreduce(ctx->comm, ctx, sums, 4));
-      k_eta_dev_step<<<1, 1, 0, ctx->stream>>>(st, sums, first, beta, ctx->m_total, eta_dev_out);
-      LAUNCHED();
-      first = 0;
-    }
-    int done = 0;
-    CK(cudaMemcpyAsync(&done, &st->ctl.done, sizeof done, cudaMemcpyDeviceToHost, ctx->stream));
+  for (int round = 0; round < 64; ++round) {  // every round feeds >= 1 evaluation (<= 51)
+    k_eta_moments_dev<<<ctx->coop_eta, kThreads, 0, ctx->stream>>>(A, st);
+    LAUNCHED();
+    k_eta_reduce<<<1, kThreads, 0, ctx->stream>>>(A.partials, ctx->coop_eta, sums);
+    LAUNCHED();
+    TRY(comm_allreduce(ctx->comm, ctx, sums, kEtaNS));
+    k_eta_dev_step<<<1, 1, 0, ctx->stream>>>(st, sums, beta, ctx->m_total, eta_dev_out);
+    LAUNCHED();
+    int go = 0;
+    CK(cudaMemcpyAsync(&go, &st->go, sizeof go, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    if (done) return TOPO_OK;
+    if (!go) return TOPO_OK;
   }
   return fail(ctx, TOPO_ENONMONO, "eta solve did not terminate");
 }
@@ -1075,7 +1069,7 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   CKC(cudaMemcpy(ctx->d_ke_lower.p, ctx->ke_lower.data(), sizeof(double) * size_t(G.P),
                  cudaMemcpyHostToDevice));
   for (DevBuf* b : {&ctx->hs, &ctx->cw, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
-                    &ctx->xnew, &ctx->tmp0, &ctx->tmp1, &ctx->e1})
+                    &ctx->xnew, &ctx->tmp0, &ctx->tmp1})
     CKC(b->ensure(md));
   for (DevBuf* b : {&ctx->hs_st, &ctx->a1_st, &ctx->a2_st, &ctx->tmp_st}) CKC(b->ensure(sd));
   CKC(ctx->rec.ensure(sizeof(double) * size_t(G.m)));
@@ -1098,11 +1092,12 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   ctx->coop_blocks = std::max(1, std::min(ctx->sm_count * occ, want));
   const size_t npart = std::max<size_t>(
       {size_t(conv_blocks(ctx)) * 3, size_t(ctx->coop_blocks) * 2 * 32 * 2,
-       size_t(ctx->coop_eta) * 2 * 4,
+       size_t(ctx->coop_eta) * kEtaNS + 2,
        size_t(ctx->sm_count) * 8 * 4});
   CKC(ctx->partials.ensure(sizeof(double) * npart));
+  CKC(ctx->cpart.ensure(sizeof(double) * size_t(topo_ctx::kUChunks) * size_t(ctx->sm_count) * 8));
   CKC(ctx->partials0.ensure(sizeof(double) * npart));
-  CKC(ctx->result.ensure(sizeof(double) * 64));
+  CKC(ctx->result.ensure(sizeof(double) * 128));
 
   if (elem_state) {
     ctx->has_state = true;
@@ -1143,7 +1138,7 @@ void topo_ctx_destroy(topo_ctx* ctx) {
                     &ctx->cw, &ctx->x_st, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
                     &ctx->xnew, &ctx->a1_st, &ctx->a2_st, &ctx->rec, &ctx->u, &ctx->tmp0,
                     &ctx->tmp1, &ctx->tmp_st, &ctx->sK, &ctx->iK, &ctx->jK, &ctx->partials,
-                    &ctx->partials0, &ctx->result, &ctx->e1})
+                    &ctx->partials0, &ctx->result, &ctx->cpart})
     b->release();
   if (ctx->h_result) cudaFreeHost(ctx->h_result);
   for (int q = 0; q < 2 * TOPO_NSTAGES; ++q)
@@ -3163,7 +3158,7 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
     if (hostU) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_uc[std::min(k + 1, nch - 1)], 0));
     E.e_begin = (long long)col0(k) * G.S;
     E.e_end = k + 1 < nch ? (long long)col0(k + 1) * G.S : G.m;
-    E.partials = ctx->partials.as<double>() + (long long)k * nbc;
+    E.partials = ctx->cpart.as<double>() + (long long)k * nbc;
     TRY(launch_elem(ctx, E, nbc));
     while (k4chunks && next_a < nch) {
       const int z0 = ztile0(next_a), z1 = ztile0(next_a + 1);
@@ -3173,10 +3168,7 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
       ++next_a;
     }
   }
-  E.partials = ctx->partials.as<double>();
-  k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(E.partials, nbe, 1, res + 4);
-  LAUNCHED();
-  if (ctx->comm) TRY(comm_allreduce(ctx->comm, ctx, res + 4, 1));  // c, on the stream
+  // c (res[4]) is summed at the tail of the pass, off the K3a -> K4 -> OC chain
   if (ctx->comm) {
     TRY(comm_halo(ctx->comm, ctx, ctx->a1_st.as<double>()));
     TRY(comm_halo(ctx->comm, ctx, ctx->a2_st.as<double>()));
@@ -3209,6 +3201,9 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
              &bis, &ev, 0.0, prm->beta, nullptr, nullptr, &oc_deferred));
   tmark(ctx, TOPO_STAGE_OC, 1, ctx->stream);
   ctx->oc_blocks_now = 0;
+  k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(ctx->cpart.as<double>(), nbe, 1, res + 4);
+  LAUNCHED();
+  if (ctx->comm) TRY(comm_allreduce(ctx->comm, ctx, res + 4, 1));  // c, on the stream
   if (oc_early) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
   if (want_sk && !overlap) {
     tmark(ctx, TOPO_STAGE_SK, 0, ctx->stream);

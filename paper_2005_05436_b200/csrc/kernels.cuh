@@ -154,36 +154,12 @@ struct ConvArgs {
   double* ocp;       // ocP per element, -1 for passives (OcRecs)
 };
 
-// eta pass terms for one filtered value t (filter.hpp:187-201), evaluated
-// through E1 = exp(2 b t), computed once per element in the first pass:
-//   tanh(b (t - eta)) = (E - 1) / (E + 1),  E = E1 exp(-2 b eta)
-//   sech^2 = 1 - tanh^2
+// eta terms are evaluated through E1 = exp(2 b t) (K2 below):
+//   tanh(b (t - c)) = (E - 1) / (E + 1),  E = E1 exp(-2 b c)
 //   sinh(b t) sinh(b (1 - t)) = cosh(b) / 2 - (E1 e^-b + e^b / E1) / 4
 // (exact identities; rounding differs from the reference's tanh / cosh /
 // sinh expression at the 1e-16 level, and eta parity is judged by the
 // conditioned protocol of SURVEY.md §8(c)).
-struct EtaConsts {
-  double a, den, c0, k, half_coshb, eb, emb;
-};
-__device__ __forceinline__ EtaConsts eta_consts(double beta, double eta) {
-  EtaConsts c;
-  c.a = tanh(beta * eta);
-  c.den = c.a + tanh(beta * (1.0 - eta));
-  c.c0 = -beta / sinh(beta);
-  c.k = exp(-2.0 * beta * eta);
-  c.half_coshb = 0.5 * cosh(beta);
-  c.eb = exp(beta);
-  c.emb = exp(-beta);
-  return c;
-}
-__device__ __forceinline__ void eta_terms(const EtaConsts& c, double t, double E1, double& g,
-                                          double& gp) {
-  const double E = E1 * c.k;
-  const double th = (E - 1.0) / (E + 1.0);
-  g = (c.a + th) / c.den - t;  // true division: unbiased like the reference's
-  const double S = c.half_coshb - 0.25 * fma(E1, c.emb, c.eb / E1);
-  gp = c.c0 * (1.0 - th * th) * S;
-}
 
 // Candidate record of oc.hpp:44-61 for one element; passives get lb = ub = x,
 // which makes every candidate equal x (their xNew entries stay untouched).
@@ -756,8 +732,7 @@ struct EtaArgs {
   const double* xt;
   const uint8_t* state;
   double beta, eta0, mtotal;
-  double* e1;               // exp(2 b t) per element, written by the first pass
-  double* partials;         // [2][gridDim][2]
+  double* partials;         // [gridDim][kEtaNS] + 2 control words
   double* result;           // eta, iterations (as double), g
 };
 
@@ -771,19 +746,50 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(r, e, r);
 }
 
-// Partial sums of this thread's active elements (grid-stride, 4 in flight):
-//   [0] sum th, th = tanh(beta (t - eta)) = 1 - 2 / (E + 1), E = E1 exp(-2 beta eta)
-//   [1] sum of the slope terms (filter.hpp:195-199), 1 - th^2 = 4 E / (E + 1)^2
-//   [2] sum t, [3] active count (first evaluation only)
-// with E1 = exp(2 beta t) cached by the first evaluation. The mismatch is then
-// g = ((n a + sum th) / den - sum t) / m (filter.hpp:187-192): one division
-// per evaluation instead of one per element.
-template <bool FIRST>
-__device__ __forceinline__ void eta_block_eval(const EtaArgs& A, double eta, double (&red)[4]) {
-  const EtaConsts c = eta_consts(A.beta, eta);
+// K2 from moment sums: one pass over xTilde per centre c (normally one in
+// all). With T = tanh(beta (t - c)) and d = tanh(beta (eta - c)), the addition
+// theorem gives tanh(beta (t - eta)) = (T - d) / (1 - T d), hence for every eta
+//   sum th(eta)           = M1 - sum_{k=1..} d^k G_{k-1},   G_j = sum (1 - T^2) T^j
+//   sum f sech^2(eta)     = (1 - d^2) sum_{k=0..} (k+1) d^k F_k,   F_k = sum f (1 - T^2) T^k
+// with M1 = sum T and f = sinh(beta t) sinh(beta (1 - t)) (filter.hpp:157-161),
+// so the mismatch g = ((n a + sum th) / den - sum t) / m (filter.hpp:187-192)
+// and the slope (:194-198) of ANY eta follow from 2K + 4 sums. Truncated
+// after K terms the remainder is below n |d|^(K+1) / (1 - |d|) < 1e-17 n for
+// |d| <= kEtaDmax, under the rounding of the sums themselves; a Newton
+// request beyond that re-centres (one more pass at that eta, where d = 0).
+// The replay (EtaCtl, filter.hpp:200-226) runs on one thread. Against one
+// pass per evaluation: C5 4 passes (+ an exp(2 beta t) cache written and read
+// back) -> 1, and one grid-wide barrier instead of one per evaluation.
+constexpr int kEtaK = 12;
+constexpr int kEtaNS = 2 * kEtaK + 4;  // [0] sum t, [1] n, [2] M1, [3..3+K) G, [3+K..4+2K) F
+constexpr double kEtaDmax = 0.045;     // 0.045^13 / 0.955 = 3.3e-18
+
+struct EtaSeries {
+  double beta, c, mtotal;
+  const double* s;  // kEtaNS sums about c
+  __host__ __device__ double dval(double eta) const { return tanh(beta * (eta - c)); }
+  __host__ __device__ void eval(double eta, double d, double* g, double* gp) const {
+    const double a = tanh(beta * eta);
+    const double den = a + tanh(beta * (1.0 - eta));
+    double acc = 0.0;
+    for (int j = kEtaK - 1; j >= 0; --j) acc = fma(acc, d, s[3 + j]);
+    const double sum_th = fma(-d, acc, s[2]);
+    *g = ((s[1] * a + sum_th) / den - s[0]) / mtotal;
+    double q = 0.0;
+    for (int k = kEtaK; k >= 0; --k) q = fma(q, d, double(k + 1) * s[3 + kEtaK + k]);
+    *gp = -beta / sinh(beta) * ((1.0 - d * d) * q) / mtotal;
+  }
+};
+
+// this thread's share of the kEtaNS sums about centre c (active elements,
+// grid-stride, 4 loads in flight)
+__device__ __forceinline__ void eta_moments(const EtaArgs& A, double c, double (&red)[kEtaNS]) {
+  const double kc = exp(-2.0 * A.beta * c);
+  const double half_coshb = 0.5 * cosh(A.beta), eb = exp(A.beta), emb = exp(-A.beta);
+#pragma unroll
+  for (int q = 0; q < kEtaNS; ++q) red[q] = 0.0;
   constexpr int U = 4;
   const long long S = (long long)gridDim.x * blockDim.x;
-  red[0] = red[1] = red[2] = red[3] = 0.0;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < A.G.m; e += U * S) {
     double v[U];
     bool act[U];
@@ -791,156 +797,176 @@ __device__ __forceinline__ void eta_block_eval(const EtaArgs& A, double eta, dou
     for (int u = 0; u < U; ++u) {
       const long long q = e + u * S;
       act[u] = q < A.G.m && elem_state(A.state, q) == 0;  // active set (filter.hpp:190)
-      v[u] = act[u] ? (FIRST ? A.xt[q] : A.e1[q]) : 0.0;
+      v[u] = act[u] ? A.xt[q] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (!act[u]) continue;
-      double E1 = v[u];
-      if (FIRST) {
-        red[2] += v[u];
-        red[3] += 1.0;
-        E1 = exp(2.0 * A.beta * v[u]);
-        A.e1[e + u * S] = E1;
-      }
-      const double E = E1 * c.k;
-      double th, w;
+      const double t = v[u];
+      red[0] += t;
+      red[1] += 1.0;
+      const double E1 = exp(2.0 * A.beta * t);
+      const double E = E1 * kc;
+      double T, w;  // T = tanh(beta (t - c)) = 1 - 2 / (E + 1), w = 1 - T^2 = 4 E / (E + 1)^2
       if (E < INFINITY) {
         const double r = rcp_nr(E + 1.0);
-        th = fma(-2.0, r, 1.0);
+        T = fma(-2.0, r, 1.0);
         w = 4.0 * E * r * r;
       } else {
-        th = 1.0;
+        T = 1.0;
         w = 0.0;
       }
-      const double Sv = c.half_coshb - 0.25 * fma(E1, c.emb, c.eb * rcp_nr(E1));
-      red[0] += th;
-      red[1] += c.c0 * w * Sv;
-    }
-  }
-}
-
-__host__ __device__ __forceinline__ double eta_mismatch_from_sums(double beta, double eta,
-                                                                  double sum_th, double sum_t,
-                                                                  double n_act, double m) {
-  const double a = tanh(beta * eta);
-  const double den = a + tanh(beta * (1.0 - eta));
-  return ((n_act * a + sum_th) / den - sum_t) / m;
-}
-
-// one (g, g') evaluation per grid-wide step; every block reduces the same
-// partials in the same order and takes the same Newton decision
-__global__ void __launch_bounds__(kThreads) k_eta_solve(EtaArgs A) {
-  cg::grid_group grid = cg::this_grid();
-  EtaCtl ctl;  // replayed by thread 0 of every block (registers, not shared memory)
-  __shared__ double scratch[4 * 32];
-  __shared__ int cont;
-  __shared__ double s_eta;
-  if (threadIdx.x == 0) {
-    ctl.init(A.eta0);
-    s_eta = ctl.eta;
-  }
-  __syncthreads();
-  int buf = 0;
-  bool first = true;
-  double sum_t = 0.0, n_act = 0.0;  // thread 0: from the first evaluation
-  for (;;) {
-    double red[4];
-    if (first)
-      eta_block_eval<true>(A, s_eta, red);
-    else
-      eta_block_eval<false>(A, s_eta, red);
-    block_sum<4>(red, scratch);
-    double* P = A.partials + (long long)buf * 4 * gridDim.x;
-    if (threadIdx.x == 0) {
-      P[4 * blockIdx.x] = red[0];
-      P[4 * blockIdx.x + 1] = red[1];
-      P[4 * blockIdx.x + 2] = red[2];
-      P[4 * blockIdx.x + 3] = red[3];
-    }
-    grid.sync();
-    if (threadIdx.x < 32) {
-      // every block sums the same partials in the same fixed order (measured:
-      // the whole block reading them is slower, C5 0.28 vs 0.23 ms: every SM
-      // hammering the same lines)
-      double s4[4];
-      warp_sum_partials<4>(P, gridDim.x, 4, s4);
-      if (threadIdx.x == 0) {
-        if (first) {
-          sum_t = s4[2];
-          n_act = s4[3];
-        }
-        const double g = eta_mismatch_from_sums(A.beta, s_eta, s4[0], sum_t, n_act, A.mtotal);
-        cont = ctl.feed(g, s4[1] / A.mtotal);
-        s_eta = ctl.eta;
+      const double f = half_coshb - 0.25 * fma(E1, emb, eb * rcp_nr(E1));
+      red[2] += T;
+      double p = w;
+#pragma unroll
+      for (int j = 0; j < kEtaK; ++j) {
+        red[3 + j] += p;
+        p *= T;
+      }
+      double q = w * f;
+#pragma unroll
+      for (int k = 0; k <= kEtaK; ++k) {
+        red[3 + kEtaK + k] += q;
+        q *= T;
       }
     }
-    first = false;
-    buf ^= 1;
+  }
+}
+
+// Fixed-order sum of the kEtaNS-wide partial records of `nb` blocks into
+// out[0..kEtaNS) (shared memory) by one block: 8 threads per component, each
+// with all its loads in flight, then a fixed 8-lane shuffle tree (one L2 round
+// trip per 8 records instead of one per component)
+__device__ __forceinline__ void eta_sum_partials(const double* __restrict__ P, int nb,
+                                                 double* out) {
+  static_assert(kEtaNS * 8 <= kThreads, "8 threads per component");
+  const int q = threadIdx.x >> 3, sub = threadIdx.x & 7;
+  double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (q < kEtaNS) {
+    int b = sub;
+    for (; b + 56 < nb; b += 64)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] += __ldcg(P + (long long)(b + 8 * u) * kEtaNS + q);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (b + 8 * u < nb) a[u] += __ldcg(P + (long long)(b + 8 * u) * kEtaNS + q);
+  }
+  double v = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  if (q < kEtaNS && sub == 0) out[q] = v;
+  __syncthreads();
+}
+
+// Newton replay from the sums about `c`: feeds ctl until it finishes (returns
+// false) or requests an eta too far from c (returns true, *c_next = it)
+__host__ __device__ inline bool eta_replay(EtaCtl& ctl, const EtaSeries& S, double* c_next) {
+  while (!ctl.done) {
+    const double d = S.dval(ctl.eta);
+    if (!(fabs(d) <= kEtaDmax)) {
+      *c_next = ctl.eta;
+      return true;
+    }
+    double g, gp;
+    S.eval(ctl.eta, d, &g, &gp);
+    ctl.feed(g, gp);
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(kThreads) k_eta_solve(EtaArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double scratch[kEtaNS * 32];
+  __shared__ double s_c;
+  __shared__ int s_go;
+  EtaCtl ctl;  // block 0, thread 0
+  if (threadIdx.x == 0) {
+    ctl.init(A.eta0);
+    s_c = ctl.eta;
+  }
+  __syncthreads();
+  double* ctrl = A.partials + (long long)kEtaNS * gridDim.x;  // go flag, next centre
+  for (int round = 0; round < 64; ++round) {
+    const double c = s_c;
+    double red[kEtaNS];
+    eta_moments(A, c, red);
+    block_sum<kEtaNS>(red, scratch);
+    if (threadIdx.x == 0)
+      for (int q = 0; q < kEtaNS; ++q) A.partials[(long long)kEtaNS * blockIdx.x + q] = red[q];
+    grid.sync();
+    if (blockIdx.x == 0) {  // one block sums in a fixed order and decides
+      eta_sum_partials(A.partials, gridDim.x, scratch);
+      if (threadIdx.x == 0) {
+        const EtaSeries S{A.beta, c, A.mtotal, scratch};
+        double cn = c;
+        const bool go = eta_replay(ctl, S, &cn);
+        ctrl[0] = go ? 1.0 : 0.0;
+        ctrl[1] = cn;
+        if (!go) {
+          A.result[0] = ctl.eta;
+          A.result[1] = double(ctl.it);
+          A.result[2] = ctl.g;
+        }
+      }
+    }
+    grid.sync();
+    if (threadIdx.x == 0) {
+      s_go = __ldcg(ctrl) != 0.0;
+      s_c = __ldcg(ctrl + 1);
+    }
     __syncthreads();
-    if (!cont) break;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    A.result[0] = ctl.eta;
-    A.result[1] = double(ctl.it);
-    A.result[2] = ctl.g;
+    if (!s_go) break;
   }
 }
 
-// plain partial sums at one eta: the multi-GPU / host-driven variant
-__global__ void __launch_bounds__(kThreads) k_eta_partials(EtaArgs A, double eta, int first) {
-  __shared__ double scratch[4 * 32];
-  double red[4];
-  if (first)
-    eta_block_eval<true>(A, eta, red);
-  else
-    eta_block_eval<false>(A, eta, red);
-  block_sum<4>(red, scratch);
-  if (threadIdx.x == 0)
-    for (int q = 0; q < 4; ++q) A.partials[4 * blockIdx.x + q] = red[q];
-}
-
-// Multi-GPU eta without host round trips: the Newton state lives on the
-// device; per evaluation partials -> on-device sum -> allreduce (NCCL, on the
-// stream) -> one-thread Newton step. Evaluations after convergence are no-ops,
-// so the host launches them in batches and checks `done` once per batch.
+// Multi-GPU eta: the same sums per rank -> on-device sum -> allreduce (NCCL,
+// on the stream) -> one-thread replay; the host reads `go` once per round
+// (normally one round: one host synchronisation per eta solve).
 struct EtaDev {
   EtaCtl ctl;
-  double sum_t, n_act;
+  double c;
+  int go;
 };
 
 __global__ void k_eta_dev_init(EtaDev* st, double eta0) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) st->ctl.init(eta0);
-}
-
-__global__ void __launch_bounds__(kThreads) k_eta_partials_dev(EtaArgs A, const EtaDev* st,
-                                                               int first) {
-  if (st->ctl.done) return;
-  __shared__ double scratch[4 * 32];
-  double red[4];
-  const double eta = st->ctl.eta;
-  if (first)
-    eta_block_eval<true>(A, eta, red);
-  else
-    eta_block_eval<false>(A, eta, red);
-  block_sum<4>(red, scratch);
-  if (threadIdx.x == 0)
-    for (int q = 0; q < 4; ++q) A.partials[4 * blockIdx.x + q] = red[q];
-}
-
-// sums: the allreduced (sum th, sum slope, sum t, active count) at ctl.eta
-__global__ void k_eta_dev_step(EtaDev* st, const double* __restrict__ sums, int first, double beta,
-                               double mtotal, double* __restrict__ result) {
-  if (threadIdx.x != 0 || blockIdx.x != 0 || st->ctl.done) return;
-  if (first) {
-    st->sum_t = sums[2];
-    st->n_act = sums[3];
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    st->ctl.init(eta0);
+    st->c = st->ctl.eta;
+    st->go = 1;
   }
-  const double g = eta_mismatch_from_sums(beta, st->ctl.eta, sums[0], st->sum_t, st->n_act, mtotal);
-  st->ctl.feed(g, sums[1] / mtotal);
-  result[0] = st->ctl.eta;
-  result[1] = double(st->ctl.it);
-  result[2] = st->ctl.g;
+}
+
+__global__ void __launch_bounds__(kThreads) k_eta_moments_dev(EtaArgs A, const EtaDev* st) {
+  __shared__ double scratch[kEtaNS * 32];
+  double red[kEtaNS];
+  eta_moments(A, st->c, red);
+  block_sum<kEtaNS>(red, scratch);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < kEtaNS; ++q) A.partials[(long long)kEtaNS * blockIdx.x + q] = red[q];
+}
+
+__global__ void __launch_bounds__(kThreads) k_eta_reduce(const double* __restrict__ P, int nb,
+                                                         double* __restrict__ sums) {
+  __shared__ double out[kEtaNS];
+  eta_sum_partials(P, nb, out);
+  if (threadIdx.x < kEtaNS) sums[threadIdx.x] = out[threadIdx.x];
+}
+
+// sums: the allreduced kEtaNS sums about st->c
+__global__ void k_eta_dev_step(EtaDev* st, const double* __restrict__ sums, double beta,
+                               double mtotal, double* __restrict__ result) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  EtaCtl ctl = st->ctl;
+  const EtaSeries S{beta, st->c, mtotal, sums};
+  double cn = st->c;
+  st->go = eta_replay(ctl, S, &cn) ? 1 : 0;
+  st->c = cn;
+  st->ctl = ctl;
+  result[0] = ctl.eta;
+  result[1] = double(ctl.it);
+  result[2] = ctl.g;
 }
 
 // ============================================================================
