@@ -116,6 +116,7 @@ struct topo_ctx {
   KeWalsh kw{};
   std::vector<double> w3;
   ConvW3 w3v{};  // the same weights + column half-widths, passed by value
+  int cone_r2 = -1;  // taps exactly di^2 + do^2 + dr^2 <= cone_r2 (compile-time cone kernels), else -1
   DevBuf d_w3;
   // element matrices
   std::vector<double> ke_full, ke_lower;
@@ -128,7 +129,7 @@ struct topo_ctx {
   double m_total = 0;   // global element count
   // fields
   OcRecs oc_view{};  // the records run_oc reads (set by their producer)
-  DevBuf hs, hs_st, cw, x_st, xt, xphys, dcphys, dc, dV, xnew, a1_st, a2_st, rec, u, tmp0, tmp1,
+  DevBuf hs, ihs, hs_st, cw, x_st, xt, xphys, dcphys, dc, dV, xnew, a1_st, a2_st, rec, u, tmp0, tmp1,
       tmp_st;
   DevBuf sK, iK, jK;
   DevBuf eta_dev;  // EtaDev: multi-GPU Newton state
@@ -435,6 +436,32 @@ ConvGeom plan_geom(const topo_ctx* c, const Geo& G, bool* use3) {
   return pick_geom(c, G);
 }
 
+// (the dual-field kernels keep the runtime-shaped loop: unrolled, the 4 x 4
+// one spills its 16 kept field-0 sums and the 2 x 2 one is slower, C4 K4
+// 0.047 vs 0.036 ms)
+template <int NF, int MODE, int AR, int R2IN>
+topo_status launch_conv3_k(topo_ctx* ctx, const Geo& G, const ConvGeom& T, const ConvArgs& A,
+                           dim3 grid) {
+  constexpr int R2 = NF == 2 ? -1 : R2IN;
+  const size_t smem = conv_smem(T);
+  static unsigned long long attr_done = 0;  // per instantiation, bit per device
+  if (!(attr_done >> ctx->device & 1)) {
+    CK(cudaFuncSetAttribute(k_conv3<NF, MODE, AR, kC3R, kC3T, R2>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024 + 4096));
+    CK(cudaFuncSetAttribute(k_conv3<NF, MODE, AR, kC3Rs, kC3Rs, R2>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024 + 4096));
+    attr_done |= 1ull << ctx->device;
+  }
+  if (T.TR == kC3Rs * T.WR)
+    k_conv3<NF, MODE, AR, kC3Rs, kC3Rs, R2><<<grid, kThreads, smem, ctx->stream>>>(
+        G, T, ctx->w3v, A);
+  else
+    k_conv3<NF, MODE, AR, kC3R, kC3T, R2><<<grid, kThreads, smem, ctx->stream>>>(
+        G, T, ctx->w3v, A);
+  LAUNCHED();
+  return TOPO_OK;
+}
+
 template <int NF, int MODE, int AR>
 topo_status launch_conv3_t(topo_ctx* ctx, const Geo& G, ConvGeom T, const ConvArgs& A,
                            int* nblocks, int z0 = 0, int z1 = -1) {
@@ -442,24 +469,18 @@ topo_status launch_conv3_t(topo_ctx* ctx, const Geo& G, ConvGeom T, const ConvAr
   if (z1 < 0) z1 = ztiles;
   T.zb = z0;
   dim3 grid((G.nely + T.TI - 1) / T.TI, (T.run_n + T.TR - 1) / T.TR, z1 - z0);
-  const size_t smem = conv_smem(T);
-  static unsigned long long attr_done = 0;  // per instantiation, bit per device
-  if (!(attr_done >> ctx->device & 1)) {
-    CK(cudaFuncSetAttribute(k_conv3<NF, MODE, AR, kC3R, kC3T>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024 + 4096));
-    CK(cudaFuncSetAttribute(k_conv3<NF, MODE, AR, kC3Rs, kC3Rs>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024 + 4096));
-    attr_done |= 1ull << ctx->device;
-  }
-  if (T.TR == kC3Rs * T.WR)
-    k_conv3<NF, MODE, AR, kC3Rs, kC3Rs><<<grid, kThreads, smem, ctx->stream>>>(
-        G, T, ctx->w3v, A);
-  else
-    k_conv3<NF, MODE, AR, kC3R, kC3T><<<grid, kThreads, smem, ctx->stream>>>(
-        G, T, ctx->w3v, A);
-  LAUNCHED();
   if (nblocks) *nblocks = int(grid.x * grid.y * ztiles);  // the whole grid's partials
-  return TOPO_OK;
+  // compile-time cones of the benchmark radii (rmin sqrt 3 and 1.5: R2 2;
+  // 2 sqrt 3: 11; 4: 14, since 15 is no sum of three squares), the runtime-shaped loop otherwise
+  const int r2 = ctx->cone_r2;
+  if constexpr (AR == 1) {
+    if (r2 == 2) return launch_conv3_k<NF, MODE, AR, 2>(ctx, G, T, A, grid);
+  }
+  if constexpr (AR == 3) {
+    if (r2 == 14) return launch_conv3_k<NF, MODE, AR, 14>(ctx, G, T, A, grid);
+    if (r2 == 11) return launch_conv3_k<NF, MODE, AR, 11>(ctx, G, T, A, grid);
+  }
+  return launch_conv3_k<NF, MODE, AR, -1>(ctx, G, T, A, grid);
 }
 
 // tile range [z0, z1) along "other" of a k_conv3 launch (chunked K4); returns
@@ -769,7 +790,7 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
       TRY(stage_field_storage(ctx, xnew_dev, ctx->tmp_st, &xs));
       ConvArgs C{};
       C.in0 = xs;
-      C.hs = ctx->hs.as<double>();
+      C.ihs = ctx->ihs.as<double>();
       C.out0 = ctx->tmp1.as<double>();
       C.state = ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr;
       C.pin = 1;
@@ -845,6 +866,10 @@ topo_status setup_filter_fields(topo_ctx* ctx) {
   TRY(launch_conv<1, CONV_PLAIN>(ctx, Gs, A));
   CK(cudaMemcpyAsync(ctx->hs.p, ctx->hs_st.as<double>() + (long long)(G.j0 - G.sj0) * G.S,
                      sizeof(double) * size_t(G.m), cudaMemcpyDeviceToDevice, ctx->stream));
+  // 1 / hs: the filter divisions (filter.hpp:121, :128) become products (<= 1.5 ulp)
+  k_recip<<<grid_for(ctx, G.m), kThreads, 0, ctx->stream>>>(G.m, ctx->hs.as<double>(),
+                                                            ctx->ihs.as<double>());
+  LAUNCHED();
   // volume weights c = H' 1_notP = conv(1_notP / hs)
   std::vector<uint8_t> st;
   std::vector<double> notP(size_t(G.m), 1.0);
@@ -1001,6 +1026,18 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
             if (ctx->w3[size_t((a * NW + b) * NW + c)] != 0.0) h = c;
           ctx->w3v.hw[a * NW + b] = h;
         }
+      int r2 = -1;
+      for (int a = 0; a < NW; ++a)
+        for (int b = 0; b < NW; ++b)
+          for (int c = 0; c < NW; ++c)
+            if (ctx->w3[size_t((a * NW + b) * NW + c)] > 0.0) r2 = std::max(r2, a * a + b * b + c * c);
+      bool exact = r2 >= 0;
+      for (int a = 0; a < NW; ++a)
+        for (int b = 0; b < NW; ++b)
+          for (int c = 0; c < NW; ++c)
+            exact &= (ctx->w3[size_t((a * NW + b) * NW + c)] > 0.0) == (a * a + b * b + c * c <= r2);
+      const char* ec = getenv("TOPO_CONE");  // experiments / tests: 0 = runtime-shaped loop
+      ctx->cone_r2 = exact && !(ec && ec[0] == '0') ? r2 : -1;
     }
   }
   // element matrices
@@ -1068,7 +1105,7 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   CKC(ctx->d_ke_lower.ensure(sizeof(double) * size_t(G.P)));
   CKC(cudaMemcpy(ctx->d_ke_lower.p, ctx->ke_lower.data(), sizeof(double) * size_t(G.P),
                  cudaMemcpyHostToDevice));
-  for (DevBuf* b : {&ctx->hs, &ctx->cw, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
+  for (DevBuf* b : {&ctx->hs, &ctx->ihs, &ctx->cw, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
                     &ctx->xnew, &ctx->tmp0, &ctx->tmp1})
     CKC(b->ensure(md));
   for (DevBuf* b : {&ctx->hs_st, &ctx->a1_st, &ctx->a2_st, &ctx->tmp_st}) CKC(b->ensure(sd));
@@ -1134,7 +1171,7 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   ctx->d_kwp.release();
   for (DevBuf* b : {&ctx->d_map, &ctx->d_clean, &ctx->eta_dev}) b->release();
   for (DevBuf* b : {&ctx->d_csc_tab, &ctx->d_csc_int, &ctx->csc_colptr, &ctx->csc_rows, &ctx->csc_E}) b->release();
-  for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_w3, &ctx->d_ke_lower, &ctx->d_ke_full, &ctx->d_state, &ctx->hs, &ctx->hs_st,
+  for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_w3, &ctx->d_ke_lower, &ctx->d_ke_full, &ctx->d_state, &ctx->hs, &ctx->ihs, &ctx->hs_st,
                     &ctx->cw, &ctx->x_st, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
                     &ctx->xnew, &ctx->a1_st, &ctx->a2_st, &ctx->rec, &ctx->u, &ctx->tmp0,
                     &ctx->tmp1, &ctx->tmp_st, &ctx->sK, &ctx->iK, &ctx->jK, &ctx->partials,
@@ -1667,7 +1704,7 @@ topo_status topo_sensitivity(topo_ctx* ctx, const double* U, const double* xhat,
   A.input_is_phys = 1;
   A.U = u;
   A.state = ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr;
-  A.hs = ctx->hs.as<double>();
+  A.ihs = ctx->ihs.as<double>();
   A.beta = 1.0;
   A.e0 = prm->e0;
   A.emin = prm->emin;
@@ -1699,7 +1736,7 @@ topo_status topo_filter(topo_ctx* ctx, const double* x, double* xTilde, int pin)
   double* o = out_ptr(ctx, xTilde, ctx->tmp1, G.m, &h);
   ConvArgs A{};
   A.in0 = xs;
-  A.hs = ctx->hs.as<double>();
+  A.ihs = ctx->ihs.as<double>();
   A.out0 = o;
   A.state = ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr;
   A.pin = pin;
@@ -1763,7 +1800,7 @@ topo_status topo_backfilter(topo_ctx* ctx, const double* g, const double* xt, do
   if (proj_on) TRY(stage_in(ctx, xt, G.m, ctx->tmp1, &xd));
   CK(ctx->a1_st.ensure(sizeof(double) * size_t(ctx->m_st)));
   k_prescale<<<grid_for(ctx, G.m), kThreads, 0, ctx->stream>>>(
-      G, gd, xd, eta, beta, proj_on, ctx->hs.as<double>(), ctx->a1_st.as<double>());
+      G, gd, xd, eta, beta, proj_on, ctx->ihs.as<double>(), ctx->a1_st.as<double>());
   LAUNCHED();
   if (ctx->comm) TRY(comm_halo(ctx->comm, ctx, ctx->a1_st.as<double>()));
   bool h;
@@ -3020,7 +3057,7 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
   const bool solve = isnan(prm->eta_override);
   ConvArgs A1{};
   A1.in0 = xs;
-  A1.hs = ctx->hs.as<double>();
+  A1.ihs = ctx->ihs.as<double>();
   A1.out0 = ctx->xt.as<double>();
   A1.state = state;
   A1.pin = 1;
@@ -3114,7 +3151,7 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
   E.eta_ptr = res;
   E.U = ud;
   E.state = state;
-  E.hs = ctx->hs.as<double>();
+  E.ihs = ctx->ihs.as<double>();
   E.beta = prm->beta;
   E.e0 = prm->simp.e0;
   E.emin = prm->simp.emin;

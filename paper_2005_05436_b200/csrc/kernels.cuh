@@ -140,7 +140,7 @@ enum ConvMode {
 struct ConvArgs {
   const double* in0;  // storage-indexed (halo-extended) inputs
   const double* in1;
-  const double* hs;   // owned-indexed
+  const double* ihs;  // owned-indexed 1 / hs (CONV_FWD: xTilde = (H x) * ihs)
   const double* hs_st;  // storage-indexed hs (CONV_ADJ_DIV)
   double* out0;       // owned-indexed outputs
   double* out1;
@@ -396,7 +396,7 @@ __device__ __forceinline__ void conv_store(const Geo& G, const ConvArgs& A, long
   if (MODE == CONV_PLAIN || MODE == CONV_ADJ_DIV) {
     A.out0[e] = v0;
   } else if (MODE == CONV_FWD) {
-    double v = v0 / A.hs[e];  // filter.hpp:121 cwiseQuotient(hs)
+    double v = v0 * A.ihs[e];  // filter.hpp:121 cwiseQuotient(hs), as a product with 1 / hs
     const int s = elem_state(A.state, e);
     if (A.pin && s == 1) v = 1.0;  // driver.hpp:130-133
     if (A.pin && s == 2) v = 0.0;
@@ -414,7 +414,7 @@ __device__ __forceinline__ void conv_store(const Geo& G, const ConvArgs& A, long
   }
 }
 
-// conv_store with the per-element inputs already loaded: l0 = hs (FWD) or x
+// conv_store with the per-element inputs already loaded: l0 = 1 / hs (FWD) or x
 // (ADJ2_OC), l1 = cw (ADJ2_OC), st = element state
 template <int NF, int MODE>
 __device__ __forceinline__ void conv_store_pre(const ConvArgs& A, long long e, double v0, double v1,
@@ -422,7 +422,7 @@ __device__ __forceinline__ void conv_store_pre(const ConvArgs& A, long long e, d
   if (MODE == CONV_PLAIN || MODE == CONV_ADJ_DIV) {
     A.out0[e] = v0;
   } else if (MODE == CONV_FWD) {
-    double v = v0 / l0;  // filter.hpp:121 cwiseQuotient(hs)
+    double v = v0 * l0;  // filter.hpp:121 cwiseQuotient(hs); l0 = 1 / hs
     if (A.pin && st == 1) v = 1.0;  // driver.hpp:130-133
     if (A.pin && st == 2) v = 0.0;
     A.out0[e] = v;
@@ -624,9 +624,78 @@ __device__ __forceinline__ void conv3_di_rw(const double* __restrict__ base, int
   }
 }
 
-template <int AR, int RB, int TB>
+// Compile-time cone (R2 >= 0: the taps are exactly di^2 + do^2 + dr^2 <= R2,
+// checked on the host from the weights): every loop bound, skip and weight
+// index is a constant, so there are no branches, the weights are constant-bank
+// DFMA operands, and the +-dr pair of a row is pre-added once for all output
+// rows it feeds. C5 (rmin 4: AR 3, R2 14): 87 FMA + 49 DADD per output
+// against 148 + 19 with the runtime-shaped loop.
+__host__ __device__ constexpr int isqrt_c(int n) {
+  int r = 0;
+  while ((r + 1) * (r + 1) <= n) ++r;
+  return r;
+}
+__host__ __device__ constexpr int cone_hw(int R2, int AR, int di, int ao) {
+  return di * di + ao * ao > R2 ? -1 : (isqrt_c(R2 - di * di - ao * ao) < AR ? isqrt_c(R2 - di * di - ao * ao) : AR);
+}
+
+template <int AR, int R2, int RB, int TB, int DI>
+__device__ __forceinline__ void conv3_cone_di(const double* __restrict__ base, int sI, int sPlane,
+                                              const ConvW3& W, double (&acc)[TB][RB]) {
+  constexpr int NW = AR + 1;
+  const double* p = base + DI * sI;
+  const double* q = base - DI * sI;
+#pragma unroll
+  for (int kk = 0; kk < TB + 2 * AR; ++kk) {
+    // rows of this slice that reach no output row (all |do| out of the cone) are skipped
+    bool any = false;
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      const int dO = kk - t - AR;
+      const int ao = dO < 0 ? -dO : dO;
+      if (ao <= AR && cone_hw(R2, AR, DI, ao) >= 0) any = true;
+    }
+    if (!any) continue;
+    double v[RB + 2 * AR];
+#pragma unroll
+    for (int j = 0; j < RB + 2 * AR; ++j)
+      v[j] = DI > 0 ? p[kk * sPlane + j] + q[kk * sPlane + j] : p[kk * sPlane + j];
+#pragma unroll
+    for (int t = 0; t < TB; ++t) {
+      const int dO = kk - t - AR;
+      const int ao = dO < 0 ? -dO : dO;
+      if (ao > AR || cone_hw(R2, AR, DI, ao) < 0) continue;
+#pragma unroll
+      for (int r = 0; r < RB; ++r) acc[t][r] = fma(W.w[(DI * NW + ao) * NW], v[r + AR], acc[t][r]);
+    }
+#pragma unroll
+    for (int ad = 1; ad <= AR; ++ad) {
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const double pr = v[r + AR - ad] + v[r + AR + ad];
+#pragma unroll
+        for (int t = 0; t < TB; ++t) {
+          const int dO = kk - t - AR;
+          const int ao = dO < 0 ? -dO : dO;
+          if (ao > AR || cone_hw(R2, AR, DI, ao) < ad) continue;
+          acc[t][r] = fma(W.w[(DI * NW + ao) * NW + ad], pr, acc[t][r]);
+        }
+      }
+    }
+  }
+}
+
+template <int AR, int R2, int RB, int TB>
 __device__ __forceinline__ void conv3_all(const double* __restrict__ base, int sI, int sPlane,
                                           const ConvW3& W, double (&acc)[TB][RB]) {
+  if (R2 >= 0) {
+    conv3_cone_di<AR, R2, RB, TB, 0>(base, sI, sPlane, W, acc);
+    if (AR >= 1) conv3_cone_di<AR, R2, RB, TB, AR >= 1 ? 1 : 0>(base, sI, sPlane, W, acc);
+    if (AR >= 2) conv3_cone_di<AR, R2, RB, TB, AR >= 2 ? 2 : 0>(base, sI, sPlane, W, acc);
+    if (AR >= 3) conv3_cone_di<AR, R2, RB, TB, AR >= 3 ? 3 : 0>(base, sI, sPlane, W, acc);
+    if (AR >= 4) conv3_cone_di<AR, R2, RB, TB, AR >= 4 ? 4 : 0>(base, sI, sPlane, W, acc);
+    return;
+  }
   if (RB * TB >= 16) {
     conv3_di_rw<AR, RB, TB, false>(base, 0, sI, sPlane, W, acc);
 #pragma unroll 1
@@ -640,7 +709,7 @@ __device__ __forceinline__ void conv3_all(const double* __restrict__ base, int s
   if (AR >= 4) conv3_di<AR, RB, TB, true, AR >= 4 ? 4 : 0>(base, sI, sPlane, W, acc);
 }
 
-template <int NF, int MODE, int AR, int RB, int TB>
+template <int NF, int MODE, int AR, int RB, int TB, int R2>
 __global__ void __launch_bounds__(kThreads, 2) k_conv3(Geo G, ConvGeom T, const __grid_constant__ ConvW3 W,
                                                        ConvArgs A) {
   extern __shared__ double tile[];
@@ -669,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv3(Geo G, ConvGeom T, const 
     for (int t = 0; t < TB; ++t)
 #pragma unroll
       for (int r = 0; r < RB; ++r) acc[t][r] = 0.0;
-    conv3_all<AR, RB, TB>(tile + sb0, sI, sPlane, W, acc);
+    conv3_all<AR, R2, RB, TB>(tile + sb0, sI, sPlane, W, acc);
     if (f + 1 < NF) {
 #pragma unroll
       for (int t = 0; t < TB; ++t)
@@ -704,7 +773,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_conv3(Geo G, ConvGeom T, const 
         l0[r] = l1[r] = 0.0;
         sv[r] = 0;
         if (ok) {
-          if (MODE == CONV_FWD) l0[r] = A.hs[eo[r]];
+          if (MODE == CONV_FWD) l0[r] = A.ihs[eo[r]];
           if (MODE == CONV_ADJ2_OC) {
             l0[r] = A.x[eo[r]];
             l1[r] = A.cw ? A.cw[eo[r]] : 1.0;
@@ -985,7 +1054,7 @@ struct ElemArgs {
   const double* eta_ptr; // device scalar eta (written by K2)
   const double* U;       // slab node planes [j0, j0 + jn]
   const uint8_t* state;
-  const double* hs;      // owned
+  const double* ihs;     // owned 1 / hs
   double beta, e0, emin, penal, inv_m;
   double* xPhys;         // owned, may be null
   double* dcPhys;        // owned, may be null
@@ -1072,7 +1141,7 @@ __global__ void __launch_bounds__(kThreads, 4 - NE) k_elem_sens(Geo G, KeFull<D>
       if (A.xPhys) A.xPhys[e] = xphys[n];
       if (A.dcPhys) A.dcPhys[e] = dcp;
       if (A.a1) {
-        const double ih = 1.0 / A.hs[e];
+        const double ih = A.ihs[e];
         const long long es = e + (long long)(G.j0 - G.sj0) * G.S;
         A.a1[es] = (dH[n] * dcp) * ih;                        // backfilter, filter.hpp:170, :128
         A.a2[es] = (dH[n] * dv0) * ih;
@@ -1114,7 +1183,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, El
     elem_ijk(G, e, i, k, j);
     // every load of the element first (latency overlap): x~, hs, state, u_e
     const double t = A.xt[e];
-    const double hsv = A.a1 ? A.hs[e] : 1.0;
+    const double ihv = A.a1 ? A.ihs[e] : 1.0;
     const int st = elem_state(A.state, e);
     const long long n0 = (long long)(j - G.j0) * pl + (long long)k * ny1 + i;  // node (i, k, j)
     double h[3][8];  // [component][binary node index oi + 2 ok + 4 oj]
@@ -1169,7 +1238,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, El
     if (A.xPhys) A.xPhys[e] = xphys;
     if (A.dcPhys) A.dcPhys[e] = dcp;
     if (A.a1) {
-      const double ih = 1.0 / hsv;
+      const double ih = ihv;
       const long long es = e + (long long)(G.j0 - G.sj0) * G.S;
       A.a1[es] = (dH * dcp) * ih;  // backfilter, filter.hpp:170, :128
       A.a2[es] = (dH * dv0) * ih;
@@ -1285,6 +1354,12 @@ __global__ void k_project(long long m, const double* __restrict__ xt, double eta
   }
 }
 
+__global__ void k_recip(long long m, const double* __restrict__ a, double* __restrict__ out) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = 1.0 / a[e];
+}
+
 __global__ void k_simp(long long m, const double* __restrict__ x, double e0, double emin,
                        double p, double* __restrict__ sK, double* __restrict__ dsK) {
   const double de = e0 - emin;
@@ -1299,7 +1374,7 @@ __global__ void k_simp(long long m, const double* __restrict__ x, double e0, dou
 // out_storage[e] = (dH[e] * g[e]) (projection on) or g[e]; already divided by
 // hs when `div_hs` (backfilter pre-adjoint field)
 __global__ void k_prescale(Geo G, const double* __restrict__ g, const double* __restrict__ xt,
-                           double eta, double beta, int proj_on, const double* __restrict__ hs,
+                           double eta, double beta, int proj_on, const double* __restrict__ ihs,
                            double* __restrict__ out_st) {
   const double denom = tanh(beta * eta) + tanh(beta * (1.0 - eta));
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < G.m;
@@ -1309,7 +1384,7 @@ __global__ void k_prescale(Geo G, const double* __restrict__ g, const double* __
       const double th = tanh(beta * (xt[e] - eta));
       v = (beta * (1.0 - th * th) / denom) * v;
     }
-    out_st[e + (long long)(G.j0 - G.sj0) * G.S] = v / hs[e];
+    out_st[e + (long long)(G.j0 - G.sj0) * G.S] = v * ihs[e];
   }
 }
 

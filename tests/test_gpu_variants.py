@@ -156,3 +156,20 @@ def test_pass_graph_replay_is_bitwise_eager(P, cid, grid):
         for f in FIELDS:
             np.testing.assert_array_equal(g[f], e[f], err_msg=f)
         assert g["s"] == e["s"]
+
+
+@pytest.mark.parametrize("cid,grid,rmin", [(5, (30, 20, 16), None), (4, (24, 16, 12), None),
+                                           (4, (40, 20, 18), 1.5), (4, (36, 20, 16), 2 * 3 ** 0.5)])
+def test_compile_time_cone_matches_runtime_loop(P, cid, grid, rmin):
+    # k_conv3 with the cone unrolled at compile time (rmin 4, sqrt 3, 1.5, 2 sqrt 3)
+    # against the runtime-shaped loop (TOPO_CONE=0): reassociated sums, 1e-13
+    from paper_2005_05436_b200.configs import CONFIGS
+    cfg = CONFIGS[cid].scaled(*grid)
+    if rmin is not None:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, rmin=rmin)
+    x, u = _inputs(cfg, 29)
+    a = _pass(P, cfg, x, u, {"TOPO_CONE": "0"}, eta_override=0.5)
+    b = _pass(P, cfg, x, u, {"TOPO_CONE": "1"}, eta_override=0.5)
+    for k in ("xTilde", "dc", "dV", "xNew"):
+        assert rel(_as_np(getattr(b, k)), _as_np(getattr(a, k))) <= 1e-13, k
