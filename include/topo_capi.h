@@ -104,7 +104,8 @@ typedef struct {
 } topo_pass_out;
 
 /* device buffers owned by the context, for zero-copy consumers (the state
- * solve) */
+ * solve). xPhys is written by the fused pass only
+ * once TOPO_BUF_XPHYS has been requested (from then on, every pass). */
 enum { TOPO_BUF_SK = 0, TOPO_BUF_IK = 1, TOPO_BUF_JK = 2, TOPO_BUF_XNEW = 3, TOPO_BUF_XPHYS = 4 };
 
 /* ---- lifecycle ---------------------------------------------------------- */

@@ -143,6 +143,7 @@ struct topo_ctx {
   int conv_R = 8;              // outputs per thread along the run axis
   int conv_A = 0;              // > 0: small-reach direct variant with half-width bound A
   bool overlap_sk = false;     // run the sK store concurrently with K3a..K6
+  bool keep_xphys = false;     // K3a writes xPhys for topo_device_buffer consumers
   bool use_pass_graph = true;  // capture / replay single-rank device passes (TOPO_PASS_GRAPH)
   PassGraph* pgraph = nullptr;
   int oc_blocks_now = 0;
@@ -1300,10 +1301,11 @@ topo_status topo_device_buffer(topo_ctx* ctx, int which, void** ptr, int64_t* co
     case TOPO_BUF_IK: *ptr = ctx->iK.p; if (count) *count = ctx->iK.p ? G.m * G.P : 0; break;
     case TOPO_BUF_JK: *ptr = ctx->jK.p; if (count) *count = ctx->jK.p ? G.m * G.P : 0; break;
     case TOPO_BUF_XNEW: *ptr = ctx->xnew.p; if (count) *count = G.m; break;
-    case TOPO_BUF_XPHYS: *ptr = ctx->xphys.p; if (count) *count = G.m; break;
-    case 100: *ptr = ctx->cw.p; if (count) *count = G.m; break;       // debugging aids
-    case 101: *ptr = ctx->hs_st.p; if (count) *count = ctx->m_st; break;
-    case 102: *ptr = ctx->hs.p; if (count) *count = G.m; break;
+    case TOPO_BUF_XPHYS:  // maintained by every pass from the first request on
+      ctx->keep_xphys = true;
+      *ptr = ctx->xphys.p;
+      if (count) *count = G.m;
+      break;
     default: return fail(ctx, TOPO_EINVAL, "unknown buffer %d", which);
   }
   return TOPO_OK;
@@ -3157,7 +3159,8 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
   E.emin = prm->simp.emin;
   E.penal = prm->simp.penal;
   E.inv_m = 1.0 / ctx->m_total;
-  E.xPhys = ctx->xphys.as<double>();
+  // xPhys only when someone reads it (113 MB of stores on C5 otherwise)
+  E.xPhys = out->xPhys || ctx->keep_xphys ? ctx->xphys.as<double>() : nullptr;
   E.dcPhys = out->dcPhys ? ctx->dcphys.as<double>() : nullptr;  // only when requested
   E.a1 = ctx->a1_st.as<double>();
   E.a2 = ctx->a2_st.as<double>();
@@ -3282,6 +3285,7 @@ struct PassKey {
   double *xTilde, *xPhys, *dcPhys, *dc, *dV, *xNew, *sK;
   cudaStream_t stream;
   unsigned long long epoch;
+  bool keep_xphys;
 };
 
 struct PassGraph {
@@ -3340,6 +3344,7 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     key.sK = out->sK;
     key.stream = ctx->stream;
     key.epoch = g_alloc_epoch.load();
+    key.keep_xphys = ctx->keep_xphys;
   }
   if (pg && pg->exec && same_key(pg->key, key)) {
     CK(cudaGraphLaunch(pg->exec, ctx->stream));
