@@ -105,7 +105,9 @@ typedef struct {
 
 /* device buffers owned by the context, for zero-copy consumers (the state
  * solve). xPhys is written by the fused pass only
- * once TOPO_BUF_XPHYS has been requested (from then on, every pass). */
+ * once TOPO_BUF_XPHYS has been requested (from then on, every pass); xNew
+ * holds the last pass's result when that pass got no device xNew array (a
+ * device output array is written in place instead of through the context). */
 enum { TOPO_BUF_SK = 0, TOPO_BUF_IK = 1, TOPO_BUF_JK = 2, TOPO_BUF_XNEW = 3, TOPO_BUF_XPHYS = 4 };
 
 /* ---- lifecycle ---------------------------------------------------------- */

@@ -3159,9 +3159,17 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
   E.emin = prm->simp.emin;
   E.penal = prm->simp.penal;
   E.inv_m = 1.0 / ctx->m_total;
+  // outputs the kernels write straight into caller device arrays (no copy
+  // at the end of the pass, e.g. 113 MB of xNew on C5 after the sK stream)
+  auto direct = [&](double* user) { return user && is_device_ptr(user) ? user : nullptr; };
+  double* const xphys_p = ctx->keep_xphys || !direct(out->xPhys) ? ctx->xphys.as<double>() : out->xPhys;
+  double* const dcphys_p = direct(out->dcPhys) ? out->dcPhys : ctx->dcphys.as<double>();
+  double* const dc_p = direct(out->dc) ? out->dc : ctx->dc.as<double>();
+  double* const dV_p = direct(out->dV) ? out->dV : ctx->dV.as<double>();
+  double* const xnew_p = direct(out->xNew) ? out->xNew : ctx->xnew.as<double>();
   // xPhys only when someone reads it (113 MB of stores on C5 otherwise)
-  E.xPhys = out->xPhys || ctx->keep_xphys ? ctx->xphys.as<double>() : nullptr;
-  E.dcPhys = out->dcPhys ? ctx->dcphys.as<double>() : nullptr;  // only when requested
+  E.xPhys = out->xPhys || ctx->keep_xphys ? xphys_p : nullptr;
+  E.dcPhys = out->dcPhys ? dcphys_p : nullptr;  // only when requested
   E.a1 = ctx->a1_st.as<double>();
   E.a2 = ctx->a2_st.as<double>();
   const int nbc = grid_for(ctx, (G.m + nch - 1) / nch);  // blocks per chunk
@@ -3170,8 +3178,8 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
   ConvArgs A4{};
   A4.in0 = ctx->a1_st.as<double>();
   A4.in1 = ctx->a2_st.as<double>();
-  A4.out0 = out->dc ? ctx->dc.as<double>() : nullptr;  // written only when requested
-  A4.out1 = out->dV ? ctx->dV.as<double>() : nullptr;
+  A4.out0 = out->dc ? dc_p : nullptr;  // written only when requested
+  A4.out1 = out->dV ? dV_p : nullptr;
   A4.state = state;
   A4.x = xown;
   A4.cw = vmode == TOPO_VOL_FILTERED ? ctx->cw.as<double>() : nullptr;
@@ -3237,7 +3245,7 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
   double lam = 0;
   int32_t bis = 0, ev = 0;
   bool oc_deferred = false;
-  TRY(run_oc(ctx, &oc, vmode, ctx->partials0.as<double>(), nb4, ctx->xnew.as<double>(), &lam,
+  TRY(run_oc(ctx, &oc, vmode, ctx->partials0.as<double>(), nb4, xnew_p, &lam,
              &bis, &ev, 0.0, prm->beta, nullptr, nullptr, &oc_deferred));
   tmark(ctx, TOPO_STAGE_OC, 1, ctx->stream);
   ctx->oc_blocks_now = 0;
@@ -3255,12 +3263,12 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
   // outputs
   struct {
     double* user;
-    const DevBuf* src;
-  } outs[] = {{out->xTilde, &ctx->xt}, {out->xPhys, &ctx->xphys}, {out->dcPhys, &ctx->dcphys},
-              {out->dc, &ctx->dc},     {out->dV, &ctx->dV},       {out->xNew, &ctx->xnew}};
+    const double* src;
+  } outs[] = {{out->xTilde, ctx->xt.as<double>()}, {out->xPhys, xphys_p}, {out->dcPhys, dcphys_p},
+              {out->dc, dc_p},     {out->dV, dV_p},       {out->xNew, xnew_p}};
   for (auto& o : outs)
-    if (o.user)
-      CK(cudaMemcpyAsync(o.user, o.src->p, sizeof(double) * size_t(G.m), cudaMemcpyDefault,
+    if (o.user && o.user != o.src)
+      CK(cudaMemcpyAsync(o.user, o.src, sizeof(double) * size_t(G.m), cudaMemcpyDefault,
                          ctx->stream));
   if (want_sk && out->sK && skp != out->sK)
     CK(cudaMemcpyAsync(out->sK, skp, sizeof(double) * size_t(G.m * G.P), cudaMemcpyDefault,
