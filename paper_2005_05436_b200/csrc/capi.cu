@@ -90,6 +90,8 @@ struct topo_ctx {
   std::string err;
   int device = 0;
   cudaStream_t stream = nullptr, aux = nullptr, cstream = nullptr;  // main, sK, copies
+  cudaStream_t hstream = nullptr;  // multi-rank: K1 interior tiles beside the halo exchange
+  cudaEvent_t ev_h0 = nullptr, ev_h1 = nullptr;
   bool own_stream = true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_x = nullptr, ev_u = nullptr;
   cudaEvent_t ev_in = nullptr;  // topo_wait_stream: caller's stream -> ctx->stream
@@ -133,6 +135,7 @@ struct topo_ctx {
       tmp_st;
   DevBuf sK, iK, jK;
   DevBuf eta_dev;  // EtaDev: multi-GPU Newton state
+  DevBuf oc_dev;   // OcDev: multi-GPU OC bisection state
   struct MgState* mg = nullptr;  // multigrid levels and scratch, kept between solves
   void* cusolver = nullptr;      // cusolverDn handle (coarsest-grid inverse), lazily created
   double kwp_host[48] = {};
@@ -144,6 +147,7 @@ struct topo_ctx {
   int conv_A = 0;              // > 0: small-reach direct variant with half-width bound A
   bool overlap_sk = false;     // run the sK store concurrently with K3a..K6
   bool keep_xphys = false;     // K3a writes xPhys for topo_device_buffer consumers
+  bool eta_safe = false;       // multi-rank eta: host check per round (re-run after a miss)
   bool use_pass_graph = true;  // capture / replay single-rank device passes (TOPO_PASS_GRAPH)
   PassGraph* pgraph = nullptr;
   int oc_blocks_now = 0;
@@ -221,7 +225,7 @@ topo_status stage_in(topo_ctx* ctx, const double* p, long long count, DevBuf& sc
 
 // Input field -> storage (halo-extended) device array, halo filled.
 topo_status stage_field_storage(topo_ctx* ctx, const double* p, DevBuf& st_buf,
-                                const double** out) {
+                                const double** out, bool halo = true) {
   const Geo& G = ctx->G;
   if (!p) return fail(ctx, TOPO_EINVAL, "null input field");
   const bool dev = is_device_ptr(p);
@@ -233,7 +237,7 @@ topo_status stage_field_storage(topo_ctx* ctx, const double* p, DevBuf& st_buf,
   double* dst = st_buf.as<double>() + (long long)(G.j0 - G.sj0) * G.S;
   CK(cudaMemcpyAsync(dst, p, sizeof(double) * size_t(G.m),
                      dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
-  if (ctx->comm) TRY(comm_halo(ctx->comm, ctx, st_buf.as<double>()));
+  if (ctx->comm && halo) TRY(comm_halo(ctx->comm, ctx, st_buf.as<double>()));
   *out = st_buf.as<double>();
   return TOPO_OK;
 }
@@ -633,7 +637,7 @@ topo_status coop_launch(topo_ctx* ctx, const void* fn, void* args, int blocks) {
 
 // ------------------------------------------------------------------ eta
 topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
-                    double* eta_dev_out) {
+                    double* eta_dev_out, bool speculative = false) {
   EtaArgs A;
   A.G = ctx->G;
   A.xt = xt;
@@ -645,14 +649,17 @@ topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
   A.result = eta_dev_out;
   if (!ctx->comm) return coop_launch(ctx, (const void*)k_eta_solve, &A, ctx->coop_eta);
   // multi-GPU: the moment sums of every rank, allreduced on the stream, and
-  // the Newton replay on the device; the host reads `go` once per round
-  // (normally one round)
+  // the Newton replay on the device. In the fused pass (`speculative`) two
+  // rounds are enqueued without a host round trip (the second is a no-op
+  // unless the first had to re-centre) and the caller checks `go` after its
+  // final synchronisation (ctx->h_result[16]); otherwise the host reads `go`
+  // after every round.
   CK(ctx->eta_dev.ensure(sizeof(EtaDev)));
   EtaDev* st = ctx->eta_dev.as<EtaDev>();
   double* sums = ctx->result.as<double>() + 64;  // kEtaNS doubles (64..92)
   k_eta_dev_init<<<1, 1, 0, ctx->stream>>>(st, eta0);
   LAUNCHED();
-  for (int round = 0; round < 64; ++round) {  // every round feeds >= 1 evaluation (<= 51)
+  auto round = [&]() -> topo_status {
     k_eta_moments_dev<<<ctx->coop_eta, kThreads, 0, ctx->stream>>>(A, st);
     LAUNCHED();
     k_eta_reduce<<<1, kThreads, 0, ctx->stream>>>(A.partials, ctx->coop_eta, sums);
@@ -660,6 +667,18 @@ topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
     TRY(comm_allreduce(ctx->comm, ctx, sums, kEtaNS));
     k_eta_dev_step<<<1, 1, 0, ctx->stream>>>(st, sums, beta, ctx->m_total, eta_dev_out);
     LAUNCHED();
+    return TOPO_OK;
+  };
+  if (speculative) {
+    const char* sr = getenv("TOPO_ETA_SPEC_ROUNDS");  // tests: 1 forces the re-run path
+    const int nspec = sr ? std::max(1, atoi(sr)) : 2;
+    for (int r = 0; r < nspec; ++r) TRY(round());
+    CK(cudaMemcpyAsync(ctx->h_result + 16, &st->go, sizeof(int), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    return TOPO_OK;
+  }
+  for (int r = 0; r < 64; ++r) {  // every round feeds >= 1 evaluation (<= 51)
+    TRY(round());
     int go = 0;
     CK(cudaMemcpyAsync(&go, &st->go, sizeof go, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -669,6 +688,83 @@ topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
 }
 
 // ------------------------------------------------------------------- OC
+// Multi-rank identity-volume OC with the replay on the device (OcDev): prep
+// sums and every batch of speculative volumes allreduced on the stream. One
+// batch round is enqueued right away (enough for the bound-shortcut regime of
+// C4 / C5: no host round trip at all); the result words land in h_result[8..16)
+// ([7] = done). oc_dev_complete() finishes a replay that needs more rounds,
+// one host check per round.
+void oc_dev_round(topo_ctx* ctx, OcDev* st, double add_const, topo_status* rs) {
+  const Geo& G = ctx->G;
+  const int nb = grid_for(ctx, G.m);
+  double* sums = ctx->result.as<double>() + 96;  // kOcK doubles (96..112)
+  k_oc_batch_dev<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->oc_view, st, ctx->partials.as<double>());
+  k_reduce_rows<<<kOcK, 256, 0, ctx->stream>>>(ctx->partials.as<double>(), nb, sums);
+  ctx->launches += 2;
+  *rs = comm_allreduce(ctx->comm, ctx, sums, kOcK);
+  if (*rs) return;
+  k_oc_dev_feed<<<1, 1, 0, ctx->stream>>>(st, sums, add_const, ctx->m_total);
+  ++ctx->launches;
+}
+
+void oc_dev_tail(topo_ctx* ctx, OcDev* st, double* xnew_dev) {
+  const Geo& G = ctx->G;
+  k_oc_dev_final<<<grid_for(ctx, G.m), kThreads, 0, ctx->stream>>>(G.m, ctx->oc_view, st, xnew_dev);
+  k_oc_dev_result<<<1, 1, 0, ctx->stream>>>(st, ctx->result.as<double>() + 8);
+  ctx->launches += 2;
+  cudaMemcpyAsync(ctx->h_result + 8, ctx->result.as<double>() + 8, sizeof(double) * 8,
+                  cudaMemcpyDeviceToHost, ctx->stream);
+}
+
+// after the caller's synchronisation: more rounds while not done, then xNew
+topo_status oc_dev_complete(topo_ctx* ctx, double add_const, double* xnew_dev, double* lam,
+                            int32_t* bis, int32_t* evals) {
+  OcDev* st = ctx->oc_dev.as<OcDev>();
+  int rounds = 0;
+  while (ctx->h_result[15] == 0.0) {
+    if (++rounds > 64) return fail(ctx, TOPO_ENONMONO, "oc: replay did not terminate");
+    topo_status rs;
+    oc_dev_round(ctx, st, add_const, &rs);
+    TRY(rs);
+    oc_dev_tail(ctx, st, xnew_dev);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
+  const double* r = ctx->h_result + 8;
+  if (int(r[3]) == OcCtl::ST_NONMONO)
+    return fail(ctx, TOPO_ENONMONO, "oc: candidate volume is not monotone in the multiplier");
+  *lam = r[0];
+  *bis = int32_t(r[1]);
+  *evals = int32_t(r[2]);
+  return TOPO_OK;
+}
+
+topo_status run_oc_dev(topo_ctx* ctx, const topo_oc_params* prm, double add_const,
+                       const double* prep, int n_prep, double* xnew_dev, double* lam,
+                       int32_t* bis, int32_t* evals, bool* deferred) {
+  CK(ctx->oc_dev.ensure(sizeof(OcDev)));
+  OcDev* st = ctx->oc_dev.as<OcDev>();
+  double* s3 = ctx->result.as<double>() + 56;
+  k_reduce_partials<3><<<1, 32, 0, ctx->stream>>>(prep, n_prep, 3, s3);
+  LAUNCHED();
+  TRY(comm_allreduce(ctx->comm, ctx, s3, 3));
+  OcDevParams P{prm->volfrac, prm->bisect_rel_tol, prm->volume_tol, prm->abs_tol,
+                prm->lambda_max, ctx->m_total, add_const, 1e-12, prm->lambda_space};
+  k_oc_dev_init<<<1, 1, 0, ctx->stream>>>(st, s3, P);
+  LAUNCHED();
+  topo_status rs;
+  oc_dev_round(ctx, st, add_const, &rs);
+  TRY(rs);
+  oc_dev_tail(ctx, st, xnew_dev);
+  CK(cudaGetLastError());
+  if (deferred) {  // the caller synchronises, then calls oc_dev_complete
+    *deferred = true;
+    return TOPO_OK;
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return oc_dev_complete(ctx, add_const, xnew_dev, lam, bis, evals);
+}
+
 // records (ctx->rec) and prep partials must be ready; writes xNew (device)
 topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const double* prep,
                    int n_prep, double* xnew_dev, double* lam, int32_t* bis, int32_t* evals,
@@ -731,7 +827,9 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
     *evals = int32_t(r[2]);
     return TOPO_OK;
   }
-  // host-driven replay: multi-GPU identity volumes, projected volume, callback
+  if ((mode == TOPO_VOL_MEAN || mode == TOPO_VOL_FILTERED) && ctx->comm && !force_host)
+    return run_oc_dev(ctx, prm, add_const, prep, n_prep, xnew_dev, lam, bis, evals, deferred);
+  // host-driven replay: projected volume, callback (and the TOPO_OC_HOST aid)
   TRY(reduce_to_host<3>(ctx, prep, n_prep));
   double lamMax = prm->lambda_max;
   if (!(prm->lambda_max > 0)) {
@@ -1078,6 +1176,9 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   CKC(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
   CKC(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
+  CKC(cudaStreamCreateWithFlags(&ctx->hstream, cudaStreamNonBlocking));
+  CKC(cudaEventCreateWithFlags(&ctx->ev_h0, cudaEventDisableTiming));
+  CKC(cudaEventCreateWithFlags(&ctx->ev_h1, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_x, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_u, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
@@ -1170,7 +1271,7 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   solver_destroy(ctx->cusolver);
   ctx->cusolver = nullptr;
   ctx->d_kwp.release();
-  for (DevBuf* b : {&ctx->d_map, &ctx->d_clean, &ctx->eta_dev}) b->release();
+  for (DevBuf* b : {&ctx->d_map, &ctx->d_clean, &ctx->eta_dev, &ctx->oc_dev}) b->release();
   for (DevBuf* b : {&ctx->d_csc_tab, &ctx->d_csc_int, &ctx->csc_colptr, &ctx->csc_rows, &ctx->csc_E}) b->release();
   for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_w3, &ctx->d_ke_lower, &ctx->d_ke_full, &ctx->d_state, &ctx->hs, &ctx->ihs, &ctx->hs_st,
                     &ctx->cw, &ctx->x_st, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
@@ -1190,6 +1291,9 @@ void topo_ctx_destroy(topo_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->cstream) cudaStreamDestroy(ctx->cstream);
+  if (ctx->hstream) cudaStreamDestroy(ctx->hstream);
+  if (ctx->ev_h0) cudaEventDestroy(ctx->ev_h0);
+  if (ctx->ev_h1) cudaEventDestroy(ctx->ev_h1);
   if (ctx->stream && ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -3027,6 +3131,10 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
 // keeps the capture-time copy.
 struct PassHost {
   bool want_sk = false, oc_deferred = false;
+  bool oc_dev = false;    // multi-rank device OC: finish with oc_dev_complete
+  bool eta_spec = false;  // multi-rank eta enqueued speculatively (check h_result[16])
+  double oc_add = 0;
+  double* xnew_p = nullptr;
   double lam = 0;
   int32_t bis = 0, ev = 0;
 };
@@ -3047,7 +3155,22 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
   const double *xs, *ud = nullptr;
   CK(ctx->partials.ensure(std::max(ctx->partials.bytes,
                                    sizeof(double) * size_t(grid_for(ctx, G.m)) * 8)));
-  TRY(stage_field_storage(ctx, x, ctx->x_st.p ? ctx->x_st : ctx->tmp_st, &xs));
+  // multi-rank 3D: K1's interior tiles (no halo column in their window) run
+  // on hstream while the x halo is exchanged on the main stream; the
+  // boundary tiles follow the exchange (the same launches' partial layout)
+  bool use3k1 = false;
+  const ConvGeom T1 = plan_geom(ctx, G, &use3k1);
+  int z_lo = 0, z_hi = 0;
+  if (ctx->comm && use3k1) {
+    const int zt = (T1.other_n + T1.TO - 1) / T1.TO, h = ctx->reach;
+    const bool left = G.j0 > 0, right = G.j0 + G.jn < G.nelx;
+    z_lo = left ? (h + T1.TO - 1) / T1.TO : 0;
+    z_hi = zt;
+    while (right && z_hi > z_lo && (long long)z_hi * T1.TO + h > G.jn) --z_hi;
+  }
+  const bool halo_overlap = z_hi > z_lo;
+  DevBuf& xbuf = ctx->x_st.p ? ctx->x_st : ctx->tmp_st;
+  TRY(stage_field_storage(ctx, x, xbuf, &xs, !halo_overlap));
   if (!U) return fail(ctx, TOPO_EINVAL, "null input array");
   CK(cudaEventRecord(ctx->ev_x, ctx->stream));  // x staged: a host U may follow on the link
   const double* xown = xs + (long long)(G.j0 - G.sj0) * G.S;
@@ -3063,12 +3186,29 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
   A1.out0 = ctx->xt.as<double>();
   A1.state = state;
   A1.pin = 1;
-  TRY((launch_conv<1, CONV_FWD>(ctx, G, A1)));
+  if (halo_overlap) {
+    const int zt = (T1.other_n + T1.TO - 1) / T1.TO;
+    CK(cudaEventRecord(ctx->ev_h0, ctx->stream));  // x staged
+    CK(cudaStreamWaitEvent(ctx->hstream, ctx->ev_h0, 0));
+    const cudaStream_t main = ctx->stream;
+    ctx->stream = ctx->hstream;  // (launch_conv3_range launches on ctx->stream)
+    const topo_status si = launch_conv3_range<1, CONV_FWD>(ctx, G, A1, z_lo, z_hi, nullptr);
+    ctx->stream = main;
+    TRY(si);
+    CK(cudaEventRecord(ctx->ev_h1, ctx->hstream));
+    TRY(comm_halo(ctx->comm, ctx, xbuf.as<double>()));
+    if (z_lo > 0) TRY((launch_conv3_range<1, CONV_FWD>(ctx, G, A1, 0, z_lo, nullptr)));
+    if (z_hi < zt) TRY((launch_conv3_range<1, CONV_FWD>(ctx, G, A1, z_hi, zt, nullptr)));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_h1, 0));
+  } else {
+    TRY((launch_conv<1, CONV_FWD>(ctx, G, A1)));
+  }
   tmark(ctx, TOPO_STAGE_FILTER, 1, ctx->stream);
   // K2
   tmark(ctx, TOPO_STAGE_ETA, 0, ctx->stream);
   if (solve) {
-    TRY(run_eta(ctx, ctx->xt.as<double>(), prm->beta, prm->eta0, res));
+    H->eta_spec = ctx->comm && !ctx->eta_safe;
+    TRY(run_eta(ctx, ctx->xt.as<double>(), prm->beta, prm->eta0, res, H->eta_spec));
   } else {
     k_set_eta<<<1, 1, 0, ctx->stream>>>(res, prm->eta_override);  // (graph-safe: no host source)
     LAUNCHED();
@@ -3217,10 +3357,8 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
     }
   }
   // c (res[4]) is summed at the tail of the pass, off the K3a -> K4 -> OC chain
-  if (ctx->comm) {
-    TRY(comm_halo(ctx->comm, ctx, ctx->a1_st.as<double>()));
-    TRY(comm_halo(ctx->comm, ctx, ctx->a2_st.as<double>()));
-  }
+  if (ctx->comm)  // both pre-adjoint fields in one exchange
+    TRY(comm_halo(ctx->comm, ctx, ctx->a1_st.as<double>(), ctx->a2_st.as<double>()));
   tmark(ctx, TOPO_STAGE_ELEM, 1, ctx->stream);
   // K4
   tmark(ctx, TOPO_STAGE_ADJOINT, 0, ctx->stream);
@@ -3275,6 +3413,9 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
                        ctx->stream));
   H->want_sk = want_sk;
   H->oc_deferred = oc_deferred;
+  H->oc_dev = oc_deferred && ctx->comm != nullptr;
+  H->oc_add = vmode == TOPO_VOL_FILTERED ? ctx->nS_total : 0.0;
+  H->xnew_p = xnew_p;
   H->lam = lam;
   H->bis = bis;
   H->ev = ev;
@@ -3396,11 +3537,28 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     }
   }
   CK(cudaStreamSynchronize(ctx->stream));
+  if (H.eta_spec && *reinterpret_cast<const int*>(ctx->h_result + 16) != 0) {
+    // the multi-rank eta needed more than the two enqueued rounds (a second
+    // re-centring): the pass ran with an unfinished eta; redo it with a host
+    // check after every round
+    ctx->eta_safe = true;
+    const topo_status st = topo_design_pass(ctx, x, U, prm, out);
+    ctx->eta_safe = false;
+    return st;
+  }
   const bool want_sk = H.want_sk;
   double lam = H.lam;
   int32_t bis = H.bis, ev = H.ev;
   double c = ctx->h_result[4];
-  if (H.oc_deferred) {
+  if (H.oc_dev) {
+    const bool more = ctx->h_result[15] == 0.0;
+    TRY(oc_dev_complete(ctx, H.oc_add, H.xnew_p, &lam, &bis, &ev));
+    if (more && out->xNew && out->xNew != H.xnew_p) {  // xNew was final only now
+      CK(cudaMemcpyAsync(out->xNew, H.xnew_p, sizeof(double) * size_t(G.m), cudaMemcpyDefault,
+                         ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
+  } else if (H.oc_deferred) {
     const double* r = ctx->h_result + 8;
     if (int(r[3]) == OcCtl::ST_NONMONO)
       return fail(ctx, TOPO_ENONMONO, "oc: candidate volume is not monotone in the multiplier");
@@ -3512,25 +3670,36 @@ static void halo_plan(const topo_ctx* ctx, long long* sendL, long long* sendR, l
   *sendR = right ? std::min<long long>(h, G.jn) : 0;
 }
 
-topo_status comm_halo(Comm* c, topo_ctx* ctx, double* st) {
+// halo columns of storage field `st` (and of `st2` in the same NCCL group)
+topo_status comm_halo(Comm* c, topo_ctx* ctx, double* st, double* st2) {
   const Geo& G = ctx->G;
   long long sL, sR, rL, rR;
   halo_plan(ctx, &sL, &sR, &rL, &rR);
   const long long S = G.S;
+  if (c->kind == 1) {
+    NCK(g_nccl.GroupStart());
+    for (double* f : {st, st2}) {
+      if (!f) continue;
+      double* own = f + (long long)(G.j0 - G.sj0) * S;
+      const double* sendR = own + (long long)(G.jn - sR) * S;
+      double* recvR = own + (long long)G.jn * S;
+      if (sL) NCK(g_nccl.Send(own, size_t(sL * S), ncclDouble, ctx->rank - 1, c->nccl, ctx->stream));
+      if (rL) NCK(g_nccl.Recv(f, size_t(rL * S), ncclDouble, ctx->rank - 1, c->nccl, ctx->stream));
+      if (sR) NCK(g_nccl.Send(sendR, size_t(sR * S), ncclDouble, ctx->rank + 1, c->nccl, ctx->stream));
+      if (rR) NCK(g_nccl.Recv(recvR, size_t(rR * S), ncclDouble, ctx->rank + 1, c->nccl, ctx->stream));
+    }
+    NCK(g_nccl.GroupEnd());
+    return TOPO_OK;
+  }
+  if (st2) {
+    TRY(comm_halo(c, ctx, st, nullptr));
+    return comm_halo(c, ctx, st2, nullptr);
+  }
   double* own = st + (long long)(G.j0 - G.sj0) * S;
   const double* sendL = own;
   const double* sendR = own + (long long)(G.jn - sR) * S;
   double* recvL = st;
   double* recvR = own + (long long)G.jn * S;
-  if (c->kind == 1) {
-    NCK(g_nccl.GroupStart());
-    if (sL) NCK(g_nccl.Send(sendL, size_t(sL * S), ncclDouble, ctx->rank - 1, c->nccl, ctx->stream));
-    if (rL) NCK(g_nccl.Recv(recvL, size_t(rL * S), ncclDouble, ctx->rank - 1, c->nccl, ctx->stream));
-    if (sR) NCK(g_nccl.Send(sendR, size_t(sR * S), ncclDouble, ctx->rank + 1, c->nccl, ctx->stream));
-    if (rR) NCK(g_nccl.Recv(recvR, size_t(rR * S), ncclDouble, ctx->rank + 1, c->nccl, ctx->stream));
-    NCK(g_nccl.GroupEnd());
-    return TOPO_OK;
-  }
   c->sl.resize(size_t(sL * S));
   c->sr.resize(size_t(sR * S));
   c->rl.resize(size_t(rL * S));

@@ -1008,6 +1008,7 @@ __global__ void k_eta_dev_init(EtaDev* st, double eta0) {
 }
 
 __global__ void __launch_bounds__(kThreads) k_eta_moments_dev(EtaArgs A, const EtaDev* st) {
+  if (!st->go) return;  // converged: a speculative round is a no-op
   __shared__ double scratch[kEtaNS * 32];
   double red[kEtaNS];
   eta_moments(A, st->c, red);
@@ -1026,7 +1027,7 @@ __global__ void __launch_bounds__(kThreads) k_eta_reduce(const double* __restric
 // sums: the allreduced kEtaNS sums about st->c
 __global__ void k_eta_dev_step(EtaDev* st, const double* __restrict__ sums, double beta,
                                double mtotal, double* __restrict__ result) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (threadIdx.x != 0 || blockIdx.x != 0 || !st->go) return;
   EtaCtl ctl = st->ctl;
   const EtaSeries S{beta, st->c, mtotal, sums};
   double cn = st->c;
@@ -1633,6 +1634,108 @@ __global__ void k_reduce_rows(const double* __restrict__ p, int count, double* _
   for (int i = threadIdx.x; i < count; i += blockDim.x) v[0] += row[i];
   block_sum<1>(v, scratch);
   if (threadIdx.x == 0) out[blockIdx.x] = v[0];
+}
+
+// ---------------------------------------------------------------------------
+// Multi-rank OC (identity volumes) with the bisection state in device memory:
+// every rank replays the same decisions from allreduced sums, batches of
+// speculative volume sums are allreduced on the stream (NCCL), and no host
+// round trip is needed until the pass ends (oc.hpp:93-174 via OcCtl).
+struct OcDev {
+  OcCtl ctl;
+  int K;     // requests to evaluate in the next round (0: none)
+  int done;  // the replay has finished
+  double req[kOcK];
+};
+
+struct OcDevParams {
+  double volfrac, rel_tol, vol_tol, abs_tol, lambda_max, mtotal, add_const, margin;
+  int lambda_space;
+};
+
+// sums3: the allreduced (sum ocP, V(0) sum, V(inf) sum) of K4
+__global__ void k_oc_dev_init(OcDev* st, const double* __restrict__ sums3, OcDevParams P) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  OcCtl ctl;
+  double lamMax = P.lambda_max;
+  if (!(P.lambda_max > 0)) {  // oc.hpp:112-116
+    const double root = sums3[0] / (P.mtotal * P.volfrac);
+    lamMax = root * root;
+  }
+  ctl.init(lamMax, P.volfrac, P.rel_tol, P.vol_tol, P.lambda_space, P.abs_tol);
+  const double V0 = (P.add_const + sums3[1]) / P.mtotal;
+  const double Vinf = (P.add_const + sums3[2]) / P.mtotal;
+  int mode = 0;  // the bound shortcut (k_oc_bisect)
+  if (Vinf > P.volfrac + 0.5 * P.vol_tol + P.margin) mode = 1;
+  if (V0 < P.volfrac - 0.5 * P.vol_tol - P.margin) mode = -1;
+  if (mode != 0) ctl.replay_known(mode > 0 ? INFINITY : -INFINITY);
+  st->K = ctl.pending() ? oc_speculate<kOcK>(ctl, st->req) : 0;
+  st->done = !ctl.pending();
+  st->ctl = ctl;
+}
+
+// K speculative volume sums over this rank's elements (no-op when K == 0)
+__global__ void __launch_bounds__(kThreads) k_oc_batch_dev(long long m, OcRecs R,
+                                                           const OcDev* __restrict__ st,
+                                                           double* __restrict__ partials) {
+  const int K = st->K;
+  if (K == 0) return;
+  __shared__ double scratch[kOcK * 32];
+  double acc[kOcK], sq[kOcK], iq[kOcK];
+#pragma unroll
+  for (int q = 0; q < kOcK; ++q) {
+    acc[q] = 0.0;
+    sq[q] = q < K ? st->req[q] : 1.0;
+    iq[q] = 1.0 / sq[q];
+  }
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double4 r = R.get(e);
+#pragma unroll
+    for (int q = 0; q < kOcK; ++q)
+      if (q < K) acc[q] = fma(r.w, oc_cand_rcp(r, sq[q], iq[q]), acc[q]);
+  }
+  block_sum<kOcK>(acc, scratch);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < kOcK; ++q) partials[(long long)q * gridDim.x + blockIdx.x] = acc[q];
+}
+
+// sums: the allreduced volume sums of the round's requests
+__global__ void k_oc_dev_feed(OcDev* st, const double* __restrict__ sums, double add_const,
+                              double mtotal) {
+  if (threadIdx.x != 0 || blockIdx.x != 0 || st->K == 0) return;
+  OcCtl ctl = st->ctl;
+  const int K = st->K;
+  while (ctl.pending()) {
+    int hit = -1;
+    for (int q = 0; q < K; ++q)
+      if (st->req[q] == ctl.s_req) hit = q;
+    if (hit < 0) break;
+    ctl.feed((add_const + sums[hit]) / mtotal);
+  }
+  st->K = ctl.pending() ? oc_speculate<kOcK>(ctl, st->req) : 0;
+  st->done = !ctl.pending();
+  st->ctl = ctl;
+}
+
+// xNew at the final multiplier once the replay is done (oc.hpp:171)
+__global__ void k_oc_dev_final(long long m, OcRecs R, const OcDev* __restrict__ st,
+                               double* __restrict__ out) {
+  if (!st->done || st->ctl.status != OcCtl::ST_OK) return;
+  const double s = st->ctl.s_final;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = oc_cand(R.get(e), s);
+}
+
+// res[0..3] lambda, bisections, evaluations, status; res[7] done
+__global__ void k_oc_dev_result(const OcDev* __restrict__ st, double* __restrict__ res) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  res[0] = st->ctl.lam_result;
+  res[1] = st->ctl.bis;
+  res[2] = st->ctl.evals;
+  res[3] = st->ctl.status;
+  res[7] = st->done;
 }
 
 // candidate at one multiplier (host-driven OC modes and final write)

@@ -96,10 +96,42 @@ def test_slab_narrower_than_reach_rejected(P):
         P.Context(64, 10, 0, rmin=35.0, rank=1, nranks=4)
 
 
-def test_nccl_two_gpus(P):
+@pytest.mark.parametrize("cid,scale", [(4, None), (5, (48, 48, 48)), (2, (150, 50))])
+def test_nccl_two_gpus(P, oracle_port, tmp_path, cid, scale):
+    """Two processes, one GPU each, over a real NCCL clique (halo send/recv,
+    on-stream allreduces, device-resident eta and OC replays): the slabs
+    together equal the single-context pass and the oracle."""
+    import os
+    import subprocess
+    import sys
     import torch
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs (NCCL ranks cannot share a GPU)")
+    from paper_2005_05436_b200.configs import CONFIGS, make_inputs
+    cfg = CONFIGS[cid] if scale is None else CONFIGS[cid].scaled(*scale)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + cid),
+           os.path.join(root, "tests", "helpers", "nccl_rank.py"), str(cid), str(tmp_path)]
+    if scale is not None:
+        cmd.append(",".join(str(v) for v in scale))
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    rs = [np.load(tmp_path / f"rank{q}.npz") for q in range(2)]
+    x, u, state = make_inputs(cfg)
+    with P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu, state=state) as ctx:
+        ref = ctx.design_pass(x, u, beta=cfg.beta, move=cfg.move, volfrac=cfg.volfrac,
+                              return_sk=True)
+    eta = float(rs[0]["eta"])
+    assert float(rs[1]["eta"]) == eta and abs(eta - ref.eta) <= 5e-8
+    cat2 = lambda k: np.concatenate([q[k] for q in rs])  # noqa: E731
+    assert rel(cat2("xTilde"), ref.xTilde) <= 1e-12
+    rc = oracle_port.design_pass(cfg.grid, cfg.rmin, x, u, state, beta=cfg.beta, move=cfg.move,
+                                 volfrac=cfg.volfrac, eta_override=eta, volume_mode=4)
+    for k in ("xPhys", "dc", "dV", "xNew"):
+        assert rel(cat2(k), getattr(rc, k)) <= 1e-12, k
+    assert all(int(q["bisections"]) == rc.bisections for q in rs)
+    assert abs(float(rs[0]["lam"]) - rc.lam) <= 1e-10 * abs(rc.lam)
 
 
 def test_nccl_single_rank_clique_matches_plain_pass():
@@ -141,3 +173,44 @@ def test_slab_ranks_with_overlapped_sk_stream(P, nranks, monkeypatch):
     for k in ("xTilde", "xPhys", "dc", "dV", "xNew", "sK"):
         np.testing.assert_array_equal(cat(a, k), cat(b, k), err_msg=k)
     assert [r.lam for r in a] == [r.lam for r in b]
+
+
+@pytest.mark.parametrize("spec_rounds", ["1", "2"])
+def test_slab_ranks_recentred_eta(P, monkeypatch, spec_rounds):
+    """A design whose eta lies far from eta0 (x ~ U^3: the moment series must
+    re-centre): with one speculative eta round the pass detects the unfinished
+    solve after its final synchronisation and re-runs with a host check per
+    round; either way the ranks match the single context."""
+    from paper_2005_05436_b200.configs import CONFIGS
+    cfg = CONFIGS[4].scaled(24, 12, 12)
+    rng = np.random.default_rng(8)
+    x = 0.01 + 0.99 * rng.uniform(0, 1, cfg.m) ** 3
+    u = rng.normal(size=cfg.n)
+    with P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu) as ctx:
+        ref = ctx.design_pass(x, u, beta=8.0, move=cfg.move, volfrac=cfg.volfrac, return_sk=True)
+    assert abs(ref.eta - 0.5) > 0.03  # far enough to need a re-centred pass
+    monkeypatch.setenv("TOPO_ETA_SPEC_ROUNDS", spec_rounds)
+    from paper_2005_05436_b200.dist import ThreadHostComm, make_rank_context, slab_views
+    comm = ThreadHostComm(2)
+    out, err = [None, None], [None, None]
+
+    def work(r):
+        try:
+            _, _, xs, us, st = slab_views(cfg, x, u, None, r, 2)
+            with make_rank_context(cfg, st, r, 2, comm=comm.for_rank(r)) as c:
+                out[r] = c.design_pass(xs, us, beta=8.0, move=cfg.move, volfrac=cfg.volfrac)
+        except Exception:  # noqa: BLE001
+            import traceback
+            err[r] = traceback.format_exc()
+            comm.barrier.abort()
+
+    import threading
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert err == [None, None], err
+    assert out[0].eta == out[1].eta and abs(out[0].eta - ref.eta) <= 5e-8
+    assert out[0].eta_iters == ref.eta_iters
+    assert rel(np.concatenate([o.xNew for o in out]), ref.xNew) <= 1e-10
