@@ -277,6 +277,25 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
 topo_status topo_apply_stiffness(topo_ctx* ctx, const double* sK, const double* x, double* y,
                                  int32_t variant);
 
+/* ---- redesign-loop helpers on device arrays (driver.hpp:189, :235-263) ---
+ * topo_loop_records: out3 = {ch = ||xPhys - xPrev|| / sqrt(m) (driver.hpp:189),
+ * v = mean(xPhys) (:249), mnd = nondiscreteness(x) (:39-43, :251)}; xPrev is
+ * overwritten with xPhys. Fixed-order device reductions, one 24-byte read. */
+topo_status topo_loop_records(topo_ctx* ctx, const double* xPhys, double* xPrev,
+                              const double* x, double* out3);
+/* AndersonAccelerator (accel.hpp:21-95) applied as driver.hpp:235-244 does:
+ * over the active elements, x_before = the design before the update and
+ * x_inout = the updated design on entry, the extrapolated design clamped to
+ * [0, 1] on return (passives untouched). The difference window lives in the
+ * context (depth <= 8 columns of m doubles each); reset clears it. */
+typedef struct { /* AndersonOptions (accel.hpp:9-14) */
+  int32_t depth, period;
+  double mix_plain, mix_accel;
+} topo_anderson;
+topo_status topo_anderson_step(topo_ctx* ctx, const topo_anderson* opt, const double* x_before,
+                               double* x_inout);
+topo_status topo_anderson_reset(topo_ctx* ctx);
+
 /* ---- fused pass: driver.hpp:183-231 (ft = 3) minus the state solve ------ */
 topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
                              const topo_pass_params* prm, topo_pass_out* out);

@@ -1,8 +1,10 @@
 // topopt_gpu_driver.hpp — the reference's run_optimization (driver.hpp:137-265)
-// on the B200 operators of topopt_gpu.hpp: every hot-path stage and the state
-// solve on the device, the scalar bookkeeping (residual, continuation,
-// Anderson extrapolation of accel.hpp, records) on the host exactly as the
-// reference does it. Include after "topopt/driver.hpp" and "topopt_gpu.hpp".
+// on the B200 operators of topopt_gpu.hpp: every hot-path stage, the state
+// solve, the Anderson extrapolation (accel.hpp) and the record reductions on
+// the device; the scalar control (continuation, loop exit) on the host exactly
+// as the reference does it. TOPO_LOOP_DEVICE=0 runs the stage-by-stage loop
+// over host Eigen vectors instead (the reference's own AndersonAccelerator).
+// Include after "topopt/driver.hpp" and "topopt_gpu.hpp".
 // SURVEY.md §8(f) row 3 (the full redesign loop).
 #pragma once
 
@@ -30,41 +32,59 @@ struct DevVec {
 };
 }  // namespace detail
 
-/// The device-resident form of the loop below for the top3D125 default (ft = 3,
-/// OC bisection, no Anderson extrapolation, no probe): design, filtered and
-/// physical fields, moduli, displacements and the updated design stay in
-/// device memory; per iteration only xPhys (residual, volume) and the new
-/// design (nondiscreteness) come back to the host. Stages: filter + pin, eta
-/// solve, projection, SIMP moduli, multigrid solve, then the fused pass with
-/// the solved eta (sensitivity, back-filters, OC) -- the same kernels as the
-/// stage-by-stage loop.
+/// The device-resident form of driver.hpp:179-265: design, filtered and
+/// physical fields, moduli, displacements, sensitivities and the updated
+/// design stay in device memory for every filter type (ft = 1 / 2 / 3), both
+/// update strategies and the Anderson extrapolation (accel.hpp on the device,
+/// topo_anderson_step); per iteration only scalars come back (eta, c, lambda,
+/// the three records of topo_loop_records: residual ch, volume, nondiscreteness).
+/// ft = 3 with bisection runs the fused pass at the solved eta (sensitivity,
+/// back-filters, OC in one call); the other modes call the stage kernels on
+/// device arrays. A probe, when given, receives host copies of x, dc and dV
+/// (the only per-iteration transfers, made because the caller asked).
 inline void run_loop_device(const RunConfig& cfg, const Problem& prob, Device& dev,
                             Eigen::VectorXd& x, double& penal, double& beta, double& eta,
                             double& ch, Eigen::VectorXd& xPrevPhys, RunResult& result,
-                            const RecordSink& sink, double solve_rtol) {
+                            const RecordSink& sink, const OcProbe& probe, double solve_rtol) {
   topo_ctx* h = dev.handle();
   const std::int64_t m = dev.numElements(), n = dev.numDofs();
-  detail::DevVec x_d(h, m), xn_d(h, m), xt_d(h, m), xp_d(h, m), e_d(h, m), f_d(h, n), u_d(h, n);
-  check(topo_copy(h, x_d.p, x.data(), std::int64_t(sizeof(double)) * m), h);
+  const DomainPartition& part = prob.part;
+  const std::int64_t bm = std::int64_t(sizeof(double)) * m;
+  detail::DevVec x_d(h, m), xn_d(h, m), xt_d(h, m), xp_d(h, m), xprev_d(h, m), e_d(h, m),
+      f_d(h, n), u_d(h, n), dcp_d(h, m), dc_d(h, m), dv_d(h, m), dv0_d(h, m);
+  check(topo_copy(h, x_d.p, x.data(), bm), h);
+  check(topo_copy(h, xprev_d.p, xPrevPhys.data(), bm), h);
   check(topo_copy(h, f_d.p, prob.load.f.data(), std::int64_t(sizeof(double)) * n), h);
+  {
+    Eigen::VectorXd dV0 = Eigen::VectorXd::Zero(m);  // driver.hpp:155-156
+    for (auto e : part.act) dV0[e] = 1.0 / double(m);
+    check(topo_copy(h, dv0_d.p, dV0.data(), bm), h);
+  }
+  const bool fused = cfg.ft == 3 && cfg.update != UpdateStrategy::PrimalDual && !probe;
+  const bool projecting = cfg.ft >= 2;
+  const int vmode = cfg.ft == 1 ? TOPO_VOL_MEAN : cfg.ft == 2 ? TOPO_VOL_PROJECTED : TOPO_VOL_FILTERED;
+  const topo_anderson aopt{cfg.accel.depth, cfg.accel.q, cfg.accel.alpha, cfg.accel.zeta};
+  check(topo_anderson_reset(h), h);
   double* xcur = x_d.p;
   double* xnext = xn_d.p;
-  Eigen::VectorXd xPhys(m);
   for (int loop = 1; loop <= cfg.maxit && ch > cfg.tol; ++loop) {
     const auto iterStart = std::chrono::steady_clock::now();
-    // RL.1 physical density field
+    // RL.1 physical density field (driver.hpp:182-190)
     check(topo_filter(h, xcur, xt_d.p, 1), h);
-    double etaNew = eta;
-    std::int32_t etaIts = 0;
-    check(topo_solve_eta(h, xt_d.p, beta, eta, &etaNew, &etaIts), h);
-    eta = etaNew;
-    check(topo_project(h, xt_d.p, eta, beta, xp_d.p), h);
-    check(topo_copy(h, xPhys.data(), xp_d.p, std::int64_t(sizeof(double)) * m), h);
-    ch = (xPhys - xPrevPhys).norm() / std::sqrt(double(m));
-    xPrevPhys = xPhys;
+    if (cfg.ft == 3) {
+      double etaNew = eta;
+      std::int32_t etaIts = 0;
+      check(topo_solve_eta(h, xt_d.p, beta, eta, &etaNew, &etaIts), h);
+      eta = etaNew;
+    }
+    const double* xphys = xt_d.p;
+    if (projecting) {
+      check(topo_project(h, xt_d.p, eta, beta, xp_d.p), h);
+      xphys = xp_d.p;
+    }
     // RL.2 equilibrium
     const topo_simp simp{cfg.e0, cfg.eMin, penal};
-    check(topo_simp_interpolate(h, xp_d.p, &simp, e_d.p, nullptr), h);
+    check(topo_simp_interpolate(h, xphys, &simp, e_d.p, nullptr), h);
     std::int32_t its = 0;
     double rr = 0.0;
     const auto t0 = std::chrono::steady_clock::now();
@@ -77,40 +97,83 @@ inline void run_loop_device(const RunConfig& cfg, const Problem& prob, Device& d
     st.seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     st.iterations += its;
     ++st.calls;
-    // RL.3 + RL.4 sensitivities, back-filters and the OC update in one pass at this eta
-    topo_pass_params pp{};
-    pp.simp = simp;
-    pp.beta = beta;
-    pp.eta0 = eta;
-    pp.move = cfg.move;
-    pp.volfrac = cfg.volfrac;
-    pp.eta_override = eta;
-    pp.volume_mode = TOPO_VOL_FILTERED;
-    pp.write_sk = 0;
-    topo_pass_out po{};
-    po.xNew = xnext;
-    check(topo_design_pass(h, xcur, u_d.p, &pp, &po), h);
+    // RL.3 + RL.4 sensitivities, back-filters, redesign
+    double c = 0.0;
+    int bisections = 0;
+    if (fused) {  // one pass at this eta (driver.hpp:192-231)
+      topo_pass_params pp{};
+      pp.simp = simp;
+      pp.beta = beta;
+      pp.eta0 = eta;
+      pp.move = cfg.move;
+      pp.volfrac = cfg.volfrac;
+      pp.eta_override = eta;
+      pp.volume_mode = TOPO_VOL_FILTERED;
+      pp.write_sk = 0;
+      topo_pass_out po{};
+      po.xNew = xnext;
+      check(topo_design_pass(h, xcur, u_d.p, &pp, &po), h);
+      c = po.c;
+      bisections = po.bisections;
+    } else {
+      check(topo_sensitivity(h, u_d.p, xphys, &simp, &c, dcp_d.p), h);  // driver.hpp:192
+      check(topo_backfilter(h, dcp_d.p, xt_d.p, eta, beta, projecting ? 1 : 0, dc_d.p), h);
+      check(topo_backfilter(h, dv0_d.p, xt_d.p, eta, beta, projecting ? 1 : 0, dv_d.p), h);
+      if (probe) {
+        Eigen::VectorXd xh(m), dch(m), dvh(m);
+        check(topo_copy(h, xh.data(), xcur, bm), h);
+        check(topo_copy(h, dch.data(), dc_d.p, bm), h);
+        check(topo_copy(h, dvh.data(), dv_d.p, bm), h);
+        probe(loop, xh, dch, dvh);
+      }
+      double lam = 0.0;
+      if (cfg.update == UpdateStrategy::PrimalDual && cfg.ft == 1) {  // driver.hpp:211-212
+        const OcParams prm{};
+        topo_oc_params p{cfg.move, cfg.volfrac, prm.bisectRelTol, prm.volumeTol, 0, 1e-8, 0.0};
+        std::int32_t it = 0, fb = 0;
+        check(topo_oc_primal_dual(h, xcur, dc_d.p, dv_d.p, &p, prm.pdTol, xnext, &lam, &it, &fb),
+              h);
+        bisections = it;
+      } else {  // oc.hpp:93-174 with the ft's volume (driver.hpp:213-230)
+        const OcParams prm{};
+        const BisectOptions bo{};
+        topo_oc_params p{cfg.move, cfg.volfrac, prm.bisectRelTol, prm.volumeTol,
+                         bo.lambdaSpace ? 1 : 0, bo.absTol, bo.lambdaMax};
+        std::int32_t bis = 0;
+        check(topo_oc_bisect(h, xcur, dc_d.p, dv_d.p, &p, vmode, eta, beta, nullptr, nullptr,
+                             xnext, &lam, &bis, nullptr),
+              h);
+        bisections = bis;
+      }
+    }
+    // optional extrapolation on the active design (driver.hpp:235-244)
+    if (cfg.accel.enabled && loop >= cfg.accel.q0 && !part.act.empty())
+      check(topo_anderson_step(h, &aopt, xcur, xnext), h);
     std::swap(xcur, xnext);
-    check(topo_copy(h, x.data(), xcur, std::int64_t(sizeof(double)) * m), h);
     const double penalUsed = penal, betaUsed = beta;
     if (cfg.penalCont) penal = apply_continuation(penal, *cfg.penalCont, loop);
     if (cfg.betaCont) beta = apply_continuation(beta, *cfg.betaCont, loop);
-    // RL.5 record
+    // RL.5 record: ch (driver.hpp:189), v, mnd -- device reductions
+    double rec3[3];
+    check(topo_loop_records(h, xphys, xprev_d.p, xcur, rec3), h);
+    ch = rec3[0];
     IterationRecord rec;
     rec.loop = loop;
-    rec.c = po.c;
-    rec.v = xPhys.mean();
+    rec.c = c;
+    rec.v = rec3[1];
     rec.resnorm = ch;
-    rec.mnd = nondiscreteness(x);
+    rec.mnd = rec3[2];
     rec.penal = penalUsed;
     rec.beta = betaUsed;
     rec.eta = eta;
-    rec.bisections = po.bisections;
+    rec.bisections = bisections;
     rec.seconds =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - iterStart).count();
     if (sink) sink(rec);
     result.history.push_back(rec);
   }
+  check(topo_copy(h, x.data(), xcur, bm), h);
+  check(topo_copy(h, xPrevPhys.data(), xprev_d.p, bm), h);
 }
 
 /// driver.hpp:137-265 with the equilibrium solved by solve_state (rtol
@@ -153,11 +216,11 @@ inline RunResult run_optimization(const RunConfig& cfg, const Problem& prob,
                            : cfg.ft == 2 ? VolumeMode::Projected
                                          : VolumeMode::Filtered;
 
-  const char* dl = std::getenv("TOPO_LOOP_DEVICE");
-  const bool device_loop = cfg.ft == 3 && cfg.update != UpdateStrategy::PrimalDual &&
-                           !cfg.accel.enabled && !probe && !(dl && dl[0] == '0');
+  const char* dl = std::getenv("TOPO_LOOP_DEVICE");  // 0: the stage-by-stage host loop below
+  const bool device_loop = !(dl && dl[0] == '0');
   if (device_loop)
-    run_loop_device(cfg, prob, dev, x, penal, beta, eta, ch, xPrevPhys, result, sink, solve_rtol);
+    run_loop_device(cfg, prob, dev, x, penal, beta, eta, ch, xPrevPhys, result, sink, probe,
+                    solve_rtol);
   for (int loop = 1; !device_loop && loop <= cfg.maxit && ch > cfg.tol; ++loop) {
     const auto iterStart = std::chrono::steady_clock::now();
     // RL.1 physical density field

@@ -29,7 +29,8 @@ EXPORTS = [
     "topo_filter_adjoint", "topo_project", "topo_project_derivative", "topo_backfilter",
     "topo_solve_eta", "topo_filter_taps", "topo_filter_hs", "topo_lambda_upper",
     "topo_oc_candidate", "topo_oc_bisect", "topo_design_pass", "topo_last_launch_count",
-    "topo_set_timing", "topo_stage_times", "topo_pass_graph_replays", "topo_host_oc_replay", "topo_host_eta_replay",
+    "topo_set_timing", "topo_stage_times", "topo_pass_graph_replays", "topo_loop_records",
+    "topo_anderson_step", "topo_anderson_reset", "topo_host_oc_replay", "topo_host_eta_replay",
     "topo_nccl_unique_id", "topo_comm_init_host", "topo_slab_plan", "topo_fp64_peak",
     "topo_csc_pattern", "topo_csc_values", "topo_csc_set_fixed", "topo_oc_primal_dual",
     "topo_solve_state", "topo_solve_state_mg", "topo_apply_stiffness",
@@ -134,6 +135,9 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         "topo_set_timing": (C.c_int, [vp, C.c_int]),
         "topo_stage_times": (C.c_int, [vp, vp]),
         "topo_pass_graph_replays": (C.c_int, [vp, vp]),
+        "topo_loop_records": (C.c_int, [vp, vp, vp, vp, vp]),
+        "topo_anderson_step": (C.c_int, [vp, vp, vp, vp]),
+        "topo_anderson_reset": (C.c_int, [vp]),
         "topo_fp64_peak": (C.c_int, [C.c_int, vp]),
         "topo_csc_pattern": (C.c_int, [vp, vp, vp, vp]),
         "topo_csc_values": (C.c_int, [vp, vp, vp]),

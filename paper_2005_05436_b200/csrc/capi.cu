@@ -136,6 +136,10 @@ struct topo_ctx {
   DevBuf sK, iK, jK;
   DevBuf eta_dev;  // EtaDev: multi-GPU Newton state
   DevBuf oc_dev;   // OcDev: multi-GPU OC bisection state
+  // Anderson window (topo_anderson_step): dx, dr [depth][m], prevX, prevR, gamma
+  DevBuf and_dx, and_dr, and_px, and_pr, and_gamma;
+  int and_depth = 0, and_cols = 0, and_next = 0, and_counter = 0;
+  bool and_has_prev = false;
   struct MgState* mg = nullptr;  // multigrid levels and scratch, kept between solves
   void* cusolver = nullptr;      // cusolverDn handle (coarsest-grid inverse), lazily created
   double kwp_host[48] = {};
@@ -1271,7 +1275,9 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   solver_destroy(ctx->cusolver);
   ctx->cusolver = nullptr;
   ctx->d_kwp.release();
-  for (DevBuf* b : {&ctx->d_map, &ctx->d_clean, &ctx->eta_dev, &ctx->oc_dev}) b->release();
+  for (DevBuf* b : {&ctx->d_map, &ctx->d_clean, &ctx->eta_dev, &ctx->oc_dev, &ctx->and_dx,
+                    &ctx->and_dr, &ctx->and_px, &ctx->and_pr, &ctx->and_gamma})
+    b->release();
   for (DevBuf* b : {&ctx->d_csc_tab, &ctx->d_csc_int, &ctx->csc_colptr, &ctx->csc_rows, &ctx->csc_E}) b->release();
   for (DevBuf* b : {&ctx->d_cols, &ctx->d_wpad, &ctx->d_w3, &ctx->d_ke_lower, &ctx->d_ke_full, &ctx->d_state, &ctx->hs, &ctx->ihs, &ctx->hs_st,
                     &ctx->cw, &ctx->x_st, &ctx->xt, &ctx->xphys, &ctx->dcphys, &ctx->dc, &ctx->dV,
@@ -1336,6 +1342,96 @@ topo_status topo_fp64_peak(int device, double* tflops) {
   cudaFree(d);
   if (err != cudaSuccess) return TOPO_ECUDA;
   *tflops = 2.0 * 8.0 * iters * double(blocks) * kThreads / (best * 1e-3) / 1e12;
+  return TOPO_OK;
+}
+
+topo_status topo_loop_records(topo_ctx* ctx, const double* xPhys, double* xPrev,
+                              const double* x, double* out3) {
+  if (!ctx || !xPhys || !xPrev || !x || !out3) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
+  ctx->launches = 0;
+  if (ctx->nranks > 1) return fail(ctx, TOPO_EINVAL, "loop records: single-rank contexts");
+  for (const void* p : {(const void*)xPhys, (const void*)xPrev, (const void*)x})
+    if (!is_device_ptr(p)) return fail(ctx, TOPO_EINVAL, "loop records: device arrays expected");
+  const Geo& G = ctx->G;
+  const int nb = grid_for(ctx, G.m);
+  k_loop_records<<<nb, kThreads, 0, ctx->stream>>>(G.m, xPhys, xPrev, x, ctx->partials.as<double>());
+  LAUNCHED();
+  double* r = ctx->result.as<double>() + 56;
+  k_reduce_partials<3><<<1, 32, 0, ctx->stream>>>(ctx->partials.as<double>(), nb, 3, r);
+  LAUNCHED();
+  CK(cudaMemcpyAsync(ctx->h_result, r, sizeof(double) * 3, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const double md = double(G.m);
+  out3[0] = std::sqrt(ctx->h_result[0]) / std::sqrt(md);  // driver.hpp:189
+  out3[1] = ctx->h_result[1] / md;                        // VectorXd::mean
+  out3[2] = 400.0 * ctx->h_result[2] / md;                // driver.hpp:39-43
+  return TOPO_OK;
+}
+
+topo_status topo_anderson_reset(topo_ctx* ctx) {
+  if (!ctx) return TOPO_EINVAL;
+  ctx->and_cols = ctx->and_next = ctx->and_counter = 0;
+  ctx->and_has_prev = false;
+  return TOPO_OK;
+}
+
+topo_status topo_anderson_step(topo_ctx* ctx, const topo_anderson* opt, const double* x_before,
+                               double* x_inout) {
+  if (!ctx || !opt || !x_before || !x_inout) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
+  ctx->launches = 0;
+  if (opt->depth < 1 || opt->period < 1)
+    return fail(ctx, TOPO_EINVAL, "anderson: depth and period must be >= 1");  // accel.hpp:24
+  if (opt->depth > kAndMax)
+    return fail(ctx, TOPO_EINVAL, "anderson: depth %d > %d", opt->depth, kAndMax);
+  if (ctx->nranks > 1) return fail(ctx, TOPO_EINVAL, "anderson: single-rank contexts");
+  if (!is_device_ptr(x_before) || !is_device_ptr(x_inout))
+    return fail(ctx, TOPO_EINVAL, "anderson: device arrays expected");
+  const Geo& G = ctx->G;
+  const size_t col = sizeof(double) * size_t(G.m);
+  if (ctx->and_depth != opt->depth || !ctx->and_dx.p) {  // accel.hpp:40-44 (resize + reset)
+    CK(ctx->and_dx.ensure(col * size_t(opt->depth)));
+    CK(ctx->and_dr.ensure(col * size_t(opt->depth)));
+    CK(ctx->and_px.ensure(col));
+    CK(ctx->and_pr.ensure(col));
+    CK(ctx->and_gamma.ensure(sizeof(double) * kAndMax));
+    ctx->and_depth = opt->depth;
+    topo_anderson_reset(ctx);
+  }
+  const uint8_t* st = ctx->has_state ? ctx->d_state.as<uint8_t>() : nullptr;
+  const int nb = grid_for(ctx, G.m);
+  const int t = ctx->and_counter++;
+  const int slot = ctx->and_next;
+  k_and_hist<<<nb, kThreads, 0, ctx->stream>>>(G.m, st, x_before, x_inout, ctx->and_dx.as<double>(),
+                                               ctx->and_dr.as<double>(), ctx->and_px.as<double>(),
+                                               ctx->and_pr.as<double>(), slot,
+                                               ctx->and_has_prev ? 1 : 0);
+  LAUNCHED();
+  if (ctx->and_has_prev) {  // accel.hpp:47-52
+    ctx->and_next = (ctx->and_next + 1) % opt->depth;
+    ctx->and_cols = std::min(ctx->and_cols + 1, opt->depth);
+  }
+  ctx->and_has_prev = true;
+  const bool extrapolate = (t % opt->period == 0) && ctx->and_cols >= 2;  // :57
+  const double mix = extrapolate ? opt->mix_accel : opt->mix_plain;
+  if (extrapolate) {
+    constexpr int NQ = kAndMax * (kAndMax + 1) / 2 + kAndMax;
+    CK(ctx->partials.ensure(std::max(ctx->partials.bytes, sizeof(double) * size_t(NQ) * nb)));
+    k_and_gram<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->and_cols, ctx->and_dr.as<double>(),
+                                                 ctx->and_pr.as<double>(),
+                                                 ctx->partials.as<double>());
+    LAUNCHED();
+    k_and_solve<<<1, 64, 0, ctx->stream>>>(ctx->partials.as<double>(), nb, ctx->and_cols,
+                                           ctx->and_gamma.as<double>());
+    LAUNCHED();
+  }
+  k_and_apply<<<nb, kThreads, 0, ctx->stream>>>(G.m, st, x_before, x_inout,
+                                                ctx->and_dx.as<double>(), ctx->and_dr.as<double>(),
+                                                ctx->and_gamma.as<double>(),
+                                                extrapolate ? ctx->and_cols : 0, mix);
+  LAUNCHED();
+  CK(cudaStreamSynchronize(ctx->stream));
   return TOPO_OK;
 }
 

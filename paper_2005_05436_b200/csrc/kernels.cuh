@@ -1738,6 +1738,179 @@ __global__ void k_oc_dev_result(const OcDev* __restrict__ st, double* __restrict
   res[7] = st->done;
 }
 
+// ---------------------------------------------------------------------------
+// Redesign-loop helpers (SURVEY.md §8(f) row 3, driver.hpp:189, :235-263)
+
+// per block: sum (xPhys - xPrev)^2, sum xPhys, sum x (1 - x); xPrev <- xPhys
+__global__ void __launch_bounds__(kThreads) k_loop_records(long long m, const double* __restrict__ xp,
+                                                           double* __restrict__ xprev,
+                                                           const double* __restrict__ x,
+                                                           double* __restrict__ partials) {
+  __shared__ double scratch[3 * 32];
+  double red[3] = {0.0, 0.0, 0.0};
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double v = xp[e], d = v - xprev[e], xv = x[e];
+    red[0] = fma(d, d, red[0]);
+    red[1] += v;
+    red[2] = fma(xv, 1.0 - xv, red[2]);
+    xprev[e] = v;
+  }
+  block_sum<3>(red, scratch);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < 3; ++q) partials[3 * blockIdx.x + q] = red[q];
+}
+
+// Anderson extrapolation (accel.hpp:21-95) over the active elements of the
+// device design: column `slot` of the cyclic difference window, then prevX /
+// prevR <- (x_before, x_new - x_before); passives hold zeros throughout
+__global__ void k_and_hist(long long m, const uint8_t* __restrict__ state,
+                           const double* __restrict__ xb, const double* __restrict__ xn,
+                           double* __restrict__ dx, double* __restrict__ dr,
+                           double* __restrict__ px, double* __restrict__ pr, int slot,
+                           int has_prev) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x) {
+    const bool act = elem_state(state, e) == 0;
+    const double xa = act ? xb[e] : 0.0, ra = act ? xn[e] - xb[e] : 0.0;
+    if (has_prev) {
+      dx[(long long)slot * m + e] = xa - px[e];
+      dr[(long long)slot * m + e] = ra - pr[e];
+    }
+    px[e] = xa;
+    pr[e] = ra;
+  }
+}
+
+constexpr int kAndMax = 8;  // window columns supported on the device
+
+// per block: the upper triangle of R'R (cols (cols+1)/2) then R'r (cols)
+__global__ void __launch_bounds__(kThreads) k_and_gram(long long m, int cols,
+                                                       const double* __restrict__ dr,
+                                                       const double* __restrict__ pr,
+                                                       double* __restrict__ partials) {
+  constexpr int NQ = kAndMax * (kAndMax + 1) / 2 + kAndMax;
+  __shared__ double scratch[NQ * 32];
+  double red[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) red[q] = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x) {
+    double c[kAndMax];
+#pragma unroll
+    for (int i = 0; i < kAndMax; ++i) c[i] = i < cols ? dr[(long long)i * m + e] : 0.0;
+    const double r = pr[e];
+    int q = 0;
+#pragma unroll
+    for (int i = 0; i < kAndMax; ++i)
+#pragma unroll
+      for (int j = i; j < kAndMax; ++j, ++q) red[q] = fma(c[i], c[j], red[q]);
+#pragma unroll
+    for (int i = 0; i < kAndMax; ++i, ++q) red[q] = fma(c[i], r, red[q]);
+  }
+  block_sum<NQ>(red, scratch);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < NQ; ++q) partials[(long long)NQ * blockIdx.x + q] = red[q];
+}
+
+// gamma = sum over eigenpairs of R'R with ev > 1e-13 max|ev| of v (v'R'r) / ev
+// (accel.hpp:76-92): the partial records summed in a fixed order, then cyclic
+// Jacobi on the cols x cols Gram matrix (one thread), eigenvalues ascending
+__global__ void k_and_solve(const double* __restrict__ partials, int nblocks, int cols,
+                            double* __restrict__ gamma) {
+  constexpr int NQ = kAndMax * (kAndMax + 1) / 2 + kAndMax;
+  __shared__ double tot[NQ];
+  for (int q = threadIdx.x; q < NQ; q += blockDim.x)
+    tot[q] = strided_sum_l2(partials, nblocks, 0, 1, NQ, q);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double G[kAndMax][kAndMax], V[kAndMax][kAndMax], rhs[kAndMax];
+  int q = 0;
+  for (int i = 0; i < kAndMax; ++i)
+    for (int j = i; j < kAndMax; ++j) {
+      G[i][j] = G[j][i] = tot[q++];
+    }
+  for (int i = 0; i < kAndMax; ++i) rhs[i] = tot[q++];
+  for (int i = 0; i < kAndMax; ++i)
+    for (int j = 0; j < kAndMax; ++j) V[i][j] = i == j ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, diag = 0.0;
+    for (int i = 0; i < cols; ++i) {
+      diag += G[i][i] * G[i][i];
+      for (int j = i + 1; j < cols; ++j) off += G[i][j] * G[i][j];
+    }
+    if (!(off > 1e-32 * diag)) break;
+    for (int p = 0; p < cols; ++p)
+      for (int r = p + 1; r < cols; ++r) {
+        if (G[p][r] == 0.0) continue;
+        const double theta = (G[r][r] - G[p][p]) / (2.0 * G[p][r]);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < cols; ++k) {  // G <- J' G J
+          const double gkp = G[k][p], gkr = G[k][r];
+          G[k][p] = c * gkp - s * gkr;
+          G[k][r] = s * gkp + c * gkr;
+        }
+        for (int k = 0; k < cols; ++k) {
+          const double gpk = G[p][k], grk = G[r][k];
+          G[p][k] = c * gpk - s * grk;
+          G[r][k] = s * gpk + c * grk;
+        }
+        for (int k = 0; k < cols; ++k) {  // V <- V J
+          const double vkp = V[k][p], vkr = V[k][r];
+          V[k][p] = c * vkp - s * vkr;
+          V[k][r] = s * vkp + c * vkr;
+        }
+      }
+  }
+  int ord[kAndMax];
+  for (int i = 0; i < cols; ++i) ord[i] = i;
+  for (int i = 1; i < cols; ++i)  // ascending eigenvalues (SelfAdjointEigenSolver order)
+    for (int j = i; j > 0 && G[ord[j]][ord[j]] < G[ord[j - 1]][ord[j - 1]]; --j) {
+      const int t = ord[j];
+      ord[j] = ord[j - 1];
+      ord[j - 1] = t;
+    }
+  double amax = 0.0;
+  for (int i = 0; i < cols; ++i) amax = fmax(amax, fabs(G[i][i]));
+  const double cutoff = amax * 1e-13;
+  double g[kAndMax];
+  for (int i = 0; i < kAndMax; ++i) g[i] = 0.0;
+  if (cutoff > 0) {
+    for (int ii = 0; ii < cols; ++ii) {
+      const int i = ord[ii];
+      const double ev = G[i][i];
+      if (!(ev > cutoff)) continue;
+      double vr = 0.0;
+      for (int k = 0; k < cols; ++k) vr += V[k][i] * rhs[k];
+      const double f = vr / ev;
+      for (int k = 0; k < cols; ++k) g[k] += V[k][i] * f;
+    }
+  }
+  for (int i = 0; i < kAndMax; ++i) gamma[i] = g[i];
+}
+
+// xn[e] <- clamp(x + mix r - (X + mix R) gamma, 0, 1) on the active elements
+// (accel.hpp:64-71, driver.hpp:240-243)
+__global__ void k_and_apply(long long m, const uint8_t* __restrict__ state,
+                            const double* __restrict__ xb, double* __restrict__ xn,
+                            const double* __restrict__ dx, const double* __restrict__ dr,
+                            const double* __restrict__ gamma, int cols, double mix) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (elem_state(state, e) != 0) continue;
+    const double xa = xb[e], ra = xn[e] - xa;
+    double out = xa + mix * ra;
+    if (cols > 0) {
+      double corr = 0.0;
+      for (int j = 0; j < cols; ++j)
+        corr += (dx[(long long)j * m + e] + mix * dr[(long long)j * m + e]) * gamma[j];
+      out -= corr;
+    }
+    xn[e] = fmin(fmax(out, 0.0), 1.0);
+  }
+}
+
 // candidate at one multiplier (host-driven OC modes and final write)
 __global__ void k_oc_candidates(long long m, OcRecs R, double s, double* __restrict__ out) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;

@@ -63,7 +63,6 @@ static int bench(int nelx, int nely, int nelz, int maxit) {
 int main(int argc, char** argv) {
   if (argc == 6 && std::string(argv[1]) == "--bench")
     return bench(std::atoi(argv[2]), std::atoi(argv[3]), std::atoi(argv[4]), std::atoi(argv[5]));
-  const bool frame = argc > 1 && std::string(argv[1]) == "--frame";  // slow: dense shim Cholesky
   {  // ft = 3 volume-preserving projection, MBB (top99neo defaults)
     RunConfig cfg;
     cfg.nelx = 30, cfg.nely = 10, cfg.rmin = 2.4, cfg.ft = 3, cfg.maxit = 8;
@@ -91,12 +90,29 @@ int main(int argc, char** argv) {
     cfg.penalCont = ContinuationSchedule{1, 4.0, 2, 0.5};
     compare("MBB 20x10 ft=2 + penal continuation", cfg, preset_mbb_2d(20, 10));
   }
-  if (frame) {  // frame reinforcement preset: passive frame and void opening (driver.hpp:306-341);
-                // ~12 min, the shim factorises 5202 DOFs densely (measured: 1.3e-8 / 9.3e-9)
+  {  // frame reinforcement preset: passive solid frame and void opening (driver.hpp:306-341),
+     // 5202 DOFs (the smallest size the preset accepts; the shim's envelope Cholesky)
     RunConfig cfg;
     cfg.nelx = 50, cfg.nely = 50, cfg.rmin = 2.5, cfg.ft = 3, cfg.maxit = 3;
     cfg.volfrac = 0.4;
     compare("frame 50x50 ft=3 (passives)", cfg, preset_frame_2d(50, 50, 1));
+  }
+  {  // ft = 3 with Anderson extrapolation (device accel.hpp) and the frame's passives
+    RunConfig cfg;
+    cfg.nelx = 50, cfg.nely = 50, cfg.rmin = 2.5, cfg.ft = 3, cfg.maxit = 10;
+    cfg.volfrac = 0.4;
+    cfg.accel.enabled = true;
+    cfg.accel.q0 = 2;
+    cfg.accel.q = 3;
+    compare("frame 50x50 ft=3 + Anderson", cfg, preset_frame_2d(50, 50, -1));
+  }
+  {  // ft = 2 with Anderson, bisection on the projected volume
+    RunConfig cfg;
+    cfg.nelx = 24, cfg.nely = 12, cfg.rmin = 2.0, cfg.ft = 2, cfg.maxit = 9;
+    cfg.accel.enabled = true;
+    cfg.accel.q0 = 1;
+    cfg.accel.depth = 3;
+    compare("MBB 24x12 ft=2 + Anderson", cfg, preset_mbb_2d(24, 12));
   }
   std::printf("%d failure(s)\n", failures);
   return failures ? 1 : 0;
