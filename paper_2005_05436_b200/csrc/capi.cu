@@ -84,7 +84,6 @@ void mg_state_free(MgState*);
 struct PassGraph;
 void pass_graph_free(PassGraph*);
 long long pass_graph_replays(const PassGraph*);
-void solver_destroy(void*);
 
 struct topo_ctx {
   std::string err;
@@ -141,7 +140,6 @@ struct topo_ctx {
   int and_depth = 0, and_cols = 0, and_next = 0, and_counter = 0;
   bool and_has_prev = false;
   struct MgState* mg = nullptr;  // multigrid levels and scratch, kept between solves
-  void* cusolver = nullptr;      // cusolverDn handle (coarsest-grid inverse), lazily created
   double kwp_host[48] = {};
   DevBuf d_kwp;  // Walsh blocks, plain (k00 k01 k02 k11 k12 k22 per signature), for k_mg_apply_tile
   DevBuf partials, partials0, result;
@@ -1272,8 +1270,6 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   ctx->mg = nullptr;
   pass_graph_free(ctx->pgraph);
   ctx->pgraph = nullptr;
-  solver_destroy(ctx->cusolver);
-  ctx->cusolver = nullptr;
   ctx->d_kwp.release();
   for (DevBuf* b : {&ctx->d_map, &ctx->d_clean, &ctx->eta_dev, &ctx->oc_dev, &ctx->and_dx,
                     &ctx->and_dr, &ctx->and_px, &ctx->and_pr, &ctx->and_gamma})
@@ -2479,54 +2475,7 @@ topo_status topo_solve_state(topo_ctx* ctx, const double* sK, const double* f,
 }
 
 // ------------------------------------------- multigrid-preconditioned solve
-// cuSOLVER (dlopen'ed; the library is used only for the coarsest grid's dense
-// Cholesky inverse at solve setup): potrf + potri on the device
-#include <dlfcn.h>
-namespace {
-struct SolverApi {
-  void* h = nullptr;
-  bool tried = false;
-  typedef int (*Create_t)(void**);
-  typedef int (*SetStream_t)(void*, cudaStream_t);
-  typedef int (*Buf_t)(void*, int, int, double*, int, int*);
-  typedef int (*Potrf_t)(void*, int, int, double*, int, double*, int, int*);
-  Create_t Create = nullptr;
-  SetStream_t SetStream = nullptr;
-  Buf_t PotrfBuf = nullptr, PotriBuf = nullptr;
-  Potrf_t Potrf = nullptr, Potri = nullptr;
-  typedef int (*Destroy_t)(void*);
-  Destroy_t Destroy = nullptr;
-  bool load() {
-    if (tried) return h != nullptr;
-    tried = true;
-    for (const char* name : {"libcusolver.so.11", "libcusolver.so",
-                             "/usr/local/cuda/lib64/libcusolver.so.11"}) {
-      h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
-      if (h) break;
-    }
-    if (!h) return false;
-    Create = (Create_t)dlsym(h, "cusolverDnCreate");
-    SetStream = (SetStream_t)dlsym(h, "cusolverDnSetStream");
-    PotrfBuf = (Buf_t)dlsym(h, "cusolverDnDpotrf_bufferSize");
-    PotriBuf = (Buf_t)dlsym(h, "cusolverDnDpotri_bufferSize");
-    Potrf = (Potrf_t)dlsym(h, "cusolverDnDpotrf");
-    Potri = (Potrf_t)dlsym(h, "cusolverDnDpotri");
-    Destroy = (Destroy_t)dlsym(h, "cusolverDnDestroy");
-    if (!Create || !SetStream || !PotrfBuf || !PotriBuf || !Potrf || !Potri) {
-      dlclose(h);
-      h = nullptr;
-    }
-    return h != nullptr;
-  }
-};
-SolverApi g_solver;
-}  // namespace
-}  // extern "C" (a C++ helper between the entry points)
-void solver_destroy(void* hnd) {
-  if (hnd && g_solver.Destroy) g_solver.Destroy(hnd);
-}
-extern "C" {
-
+// ------------------------------------------- multigrid-preconditioned solve
 namespace {
 struct MgLevel {
   MgGeo g{};
@@ -2793,16 +2742,14 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   static const char* dce = getenv("TOPO_MG_DENSE_COARSE");
   const MgLevel& Lc = lv.back();
   static const char* dmx = getenv("TOPO_MG_DENSE_MAX");  // experiments
-  // cuSOLVER's Cholesky inverse takes ~2 ms for 2k DOFs; the one-pivot-per-
-  // barrier Gauss-Jordan fallback only pays below ~1k
   // (2D grids stop coarsening at odd sizes early: 75x25 = 3952 DOFs for C1-C3,
   // exact: C3 79 MGCG iterations instead of 168 with Jacobi sweeps)
-  const long long dense_max = dmx ? atoll(dmx) : (g_solver.load() ? 4096 : kCoarseDenseMax);
-  const bool dense_coarse = node_ops && lv.size() >= 2 && Lc.g.n <= dense_max &&
-                            !(mf1 && lv.size() == 2) && !(dce && dce[0] == '0');
+  const long long dense_max = dmx ? atoll(dmx) : kCoarseDenseMax;
+  bool dense_coarse = node_ops && lv.size() >= 2 && Lc.g.n <= dense_max &&
+                      !(mf1 && lv.size() == 2) && !(dce && dce[0] == '0');
   if (dense_coarse) {
     const long long nc = Lc.g.n;
-    CK(ms.dAc.ensure(sizeof(double) * size_t(nc * nc + 4 * nc)));
+    CK(ms.dAc.ensure(sizeof(double) * size_t(nc * nc + 2 * kGjB * nc + kGjB * kGjB + 1)));
     if (dim == 3)
       k_mg_dense_gather<3><<<grid_for(ctx, nc * nc), kThreads, 0, ctx->stream>>>(
           Lc.g, Lc.K.as<double>(), ms.dAc.as<double>());
@@ -2810,45 +2757,26 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
       k_mg_dense_gather<2><<<grid_for(ctx, nc * nc), kThreads, 0, ctx->stream>>>(
           Lc.g, Lc.K.as<double>(), ms.dAc.as<double>());
     LAUNCHED();
-    static const char* gje = getenv("TOPO_MG_GJ");  // force the Gauss-Jordan kernel
-    bool inverted = false;
-    if (!(gje && gje[0] == '1') && g_solver.load()) {
-      // Cholesky (potrf) + inverse from it (potri, lower triangle), then mirror;
-      // the dense matrix is symmetric, so row- and column-major coincide
-      if (!ctx->cusolver) {
-        if (g_solver.Create(&ctx->cusolver) != 0) return fail(ctx, TOPO_ECUDA, "cusolverDnCreate");
-      }
-      if (g_solver.SetStream(ctx->cusolver, ctx->stream) != 0)
-        return fail(ctx, TOPO_ECUDA, "cusolverDnSetStream");
-      double* Ad = ms.dAc.as<double>();
-      const int ni = int(nc);
-      int l1 = 0, l2 = 0;
-      if (g_solver.PotrfBuf(ctx->cusolver, 0 /*lower*/, ni, Ad, ni, &l1) != 0 ||
-          g_solver.PotriBuf(ctx->cusolver, 0, ni, Ad, ni, &l2) != 0)
-        return fail(ctx, TOPO_ECUDA, "cusolver workspace query");
-      CK(ms.dWork.ensure(sizeof(double) * size_t(std::max(l1, l2) + 2)));
-      double* work = ms.dWork.as<double>();
-      int* info = reinterpret_cast<int*>(work + std::max(l1, l2));
-      if (g_solver.Potrf(ctx->cusolver, 0, ni, Ad, ni, work, l1, info) != 0 ||
-          g_solver.Potri(ctx->cusolver, 0, ni, Ad, ni, work, l2, info) != 0)
-        return fail(ctx, TOPO_ECUDA, "cusolver potrf/potri");
-      k_mirror_lower<<<grid_for(ctx, nc * nc), kThreads, 0, ctx->stream>>>(ni, Ad);
-      LAUNCHED();
-      inverted = true;
-    }
-    if (!inverted) {
-      int occ = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_dense_inverse, 256, 0));
-      const int nb = std::max(1, std::min(occ * ctx->sm_count,
-                                          int(std::min<long long>(ctx->sm_count, (nc * nc + 255) / 256))));
-      int ni = int(nc);
-      double* Ad = ms.dAc.as<double>();
-      double* rbuf = Ad + nc * nc;
-      double* cbuf = rbuf + 2 * nc;
-      void* args[] = {&ni, &Ad, &rbuf, &cbuf};
-      CK(cudaLaunchCooperativeKernel((const void*)k_dense_inverse, nb, 256, args, 0, ctx->stream));
-      LAUNCHED();
-    }
+    // blocked Gauss-Jordan inverse (mg.cuh), once per solve
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_dense_inverse, kGjThreads, 0));
+    const long long tiles = ((nc + kGjT - 1) / kGjT) * ((nc + kGjT - 1) / kGjT);
+    const int nb = int(std::max<long long>(1, std::min<long long>(occ * ctx->sm_count, tiles)));
+    int ni = int(nc);
+    double* Ad = ms.dAc.as<double>();
+    double* Wb = Ad + nc * nc;
+    double* Cb = Wb + kGjB * nc;
+    double* Pb = Cb + kGjB * nc;
+    int* bad = reinterpret_cast<int*>(Pb + kGjB * kGjB);
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+    void* args[] = {&ni, &Ad, &Wb, &Cb, &Pb, &bad};
+    CK(cudaLaunchCooperativeKernel((const void*)k_dense_inverse, nb, kGjThreads, args, 0,
+                                   ctx->stream));
+    LAUNCHED();
+    int hbad = 0;  // one read per solve: a singular coarse operator (e.g. fixed DOFs lost
+    CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));  // by the coarse mask) falls back to sweeps
+    if (hbad) dense_coarse = false;
   }
   // fine level in Walsh form when Ke allows (plain symmetric block entries)
   DevBuf dkwb;

@@ -745,9 +745,9 @@ __global__ void __launch_bounds__(256) k_mg_node_lanes(MgGeo L, const double* __
 
 // Exact solve on a small coarsest level (n <= kCoarseDenseMax): the dense
 // matrix is gathered from the element matrices (fixed DOFs: identity rows and
-// columns), inverted once per solve by Gauss-Jordan in one block (SPD, no
-// pivoting), and each V-cycle applies x = A^-1 b with one warp per row.
-constexpr int kCoarseDenseMax = 1024;
+// columns), inverted once per solve by blocked Gauss-Jordan (k_dense_inverse,
+// SPD, no pivoting), and each V-cycle applies x = A^-1 b with one warp per row.
+constexpr int kCoarseDenseMax = 4096;
 
 // A[i][j] = sum over the elements holding both DOFs (ascending) of K_e(li, lj)
 template <int DIM>
@@ -782,46 +782,143 @@ __global__ void k_mg_dense_gather(MgGeo L, const double* __restrict__ K, double*
   }
 }
 
-// in-place Gauss-Jordan inverse of an SPD n x n matrix (row-major, no
-// pivoting), cooperative: one grid barrier per pivot. Step k reads the pivot
-// row and column as they were at its start from double buffers (rb, cb: 2 x n
-// each), which the same step refills for pivot k + 1.
-__global__ void __launch_bounds__(256) k_dense_inverse(int n, double* __restrict__ A,
-                                                       double* __restrict__ rb,
-                                                       double* __restrict__ cb) {
+// In-place inverse of the SPD coarsest-grid matrix (row-major n x n) by
+// blocked Gauss-Jordan (the sweep operator on panels of kGjB pivots), one
+// cooperative launch, three grid barriers per panel (n = 1911 for C4 / C5:
+// 60 panels). For pivot block P = A[K,K] and the rest R:
+//   A[K,K] <- P^-1, A[K,R] <- W = P^-1 A[K,R], A[R,K] <- -A[R,K] P^-1,
+//   A[R,R] <- A[R,R] - A[R,K] W
+// (the column panel is copied to C first: its old values feed the update).
+// No pivoting (SPD); a non-positive or non-finite pivot sets *bad (the caller
+// then falls back to Jacobi sweeps on the coarsest grid).
+constexpr int kGjB = 32, kGjT = 64;  // panel width, update tile (measured: 64-wide
+                                     // panels are slower, C1 solve 55 vs 37 ms)
+constexpr int kGjThreads = 128;
+__global__ void __launch_bounds__(kGjThreads) k_dense_inverse(int n, double* __restrict__ A,
+                                                              double* __restrict__ W,
+                                                              double* __restrict__ Cp,
+                                                              double* __restrict__ Pinv,
+                                                              int* __restrict__ bad) {
   cg::grid_group grid = cg::this_grid();
-  const long long nn = (long long)n * n;
+  __shared__ double sP[kGjB][kGjB + 1];
+  __shared__ double sC[kGjT][kGjB + 1];
+  __shared__ double sW[kGjB][kGjT + 1];
+  __shared__ double rowk[kGjB], colk[kGjB];
+  const int tid = threadIdx.x;
   const long long S = (long long)gridDim.x * blockDim.x;
-  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  for (long long t = t0; t < n; t += S) {
-    rb[t] = A[t];                  // row 0
-    cb[t] = A[t * n];              // column 0
-  }
-  for (int k = 0; k < n; ++k) {
-    grid.sync();
-    const double* r = rb + (k & 1) * n;
-    const double* c = cb + (k & 1) * n;
-    double* r1 = rb + ((k + 1) & 1) * n;
-    double* c1 = cb + ((k + 1) & 1) * n;
-    const double inv = 1.0 / r[k];
-    for (long long t = t0; t < nn; t += S) {
-      const int i = int(t / n), j = int(t - (long long)i * n);
-      const double rk = (j == k ? 1.0 : r[j]) * inv;  // the scaled pivot row
-      const double v = i == k ? rk : fma(-c[i], rk, j == k ? 0.0 : A[t]);
-      A[t] = v;
-      if (j == k + 1) c1[i] = v;
-      if (i == k + 1) r1[j] = v;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + tid;
+  const int ntile = (n + kGjT - 1) / kGjT;
+  for (int k0 = 0; k0 < n; k0 += kGjB) {
+    const int b = min(kGjB, n - k0);
+    // phase 1: block 0 inverts the pivot block; everyone copies the column panel
+    if (blockIdx.x == 0) {
+      for (int q = tid; q < b * b; q += blockDim.x) sP[q / b][q % b] = A[(long long)(k0 + q / b) * n + k0 + q % b];
+      __syncthreads();
+      for (int kk = 0; kk < b; ++kk) {
+        if (tid < b) {
+          rowk[tid] = sP[kk][tid];
+          colk[tid] = sP[tid][kk];
+        }
+        __syncthreads();
+        double piv = rowk[kk];
+        if (!(piv > 0.0) || !(piv < INFINITY)) {
+          if (tid == 0) *bad = 1;
+          piv = 1.0;
+        }
+        const double inv = 1.0 / piv;
+        for (int q = tid; q < b * b; q += blockDim.x) {
+          const int i = q / b, j = q % b;
+          double v;
+          if (i == kk)
+            v = j == kk ? inv : rowk[j] * inv;
+          else
+            v = j == kk ? -colk[i] * inv : fma(-colk[i], rowk[j] * inv, sP[i][j]);
+          sP[i][j] = v;
+        }
+        __syncthreads();
+      }
+      for (int q = tid; q < b * b; q += blockDim.x) Pinv[q] = sP[q / b][q % b];
     }
-  }
-}
-
-// column-major lower triangle (cuSOLVER potri output) -> full symmetric matrix
-__global__ void k_mirror_lower(int n, double* __restrict__ A) {
-  const long long nn = (long long)n * n;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < nn;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int j = int(t / n), i = int(t - (long long)j * n);  // column-major (i, j)
-    if (i < j) A[t] = A[(long long)i * n + j];                  // upper <- lower (j, i)
+    for (long long t = t0; t < (long long)n * b; t += S) {
+      const int i = int(t / b), c = int(t % b);
+      Cp[t] = A[(long long)i * n + k0 + c];
+    }
+    grid.sync();
+    // phase 2: W = P^-1 A[K, :]
+    for (long long t = t0; t < (long long)b * n; t += S) {
+      const int r = int(t / n), j = int(t % n);
+      double pv[kGjB], av[kGjB];  // every load of the row issued before the FMAs
+#pragma unroll
+      for (int q = 0; q < kGjB; ++q) {
+        pv[q] = q < b ? __ldcg(Pinv + r * b + q) : 0.0;
+        av[q] = q < b ? A[(long long)(k0 + q) * n + j] : 0.0;
+      }
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < kGjB; ++q) acc = fma(pv[q], av[q], acc);
+      W[t] = acc;
+    }
+    grid.sync();
+    // phase 3: every 64 x 64 tile of A, 8 x 4 outputs per thread
+    for (int tile = blockIdx.x; tile < ntile * ntile; tile += gridDim.x) {
+      const int I0 = (tile / ntile) * kGjT, J0 = (tile % ntile) * kGjT;
+      __syncthreads();
+      {  // tile fill: all 2 x 16 loads of a thread in flight at once
+        constexpr int NL = kGjT * kGjB / kGjThreads;
+        double lc[NL], lw[NL];
+#pragma unroll
+        for (int it = 0; it < NL; ++it) {
+          const int q = tid + kGjThreads * it;
+          const int i = q / kGjB, c = q % kGjB;
+          lc[it] = (I0 + i < n && c < b) ? __ldcg(Cp + (long long)(I0 + i) * b + c) : 0.0;
+          const int r = q / kGjT, j = q % kGjT;
+          lw[it] = (J0 + j < n && r < b) ? __ldcg(W + (long long)r * n + J0 + j) : 0.0;
+        }
+#pragma unroll
+        for (int it = 0; it < NL; ++it) {
+          const int q = tid + kGjThreads * it;
+          sC[q / kGjB][q % kGjB] = lc[it];
+          sW[q / kGjT][q % kGjT] = lw[it];
+        }
+      }
+      for (int q = tid; q < b * b; q += blockDim.x)  // (block-local copy of P^-1)
+        sP[q / b][q % b] = __ldcg(Pinv + q);
+      __syncthreads();
+      const int ti = (tid / 16) * 8, tj = (tid % 16) * 4;
+      double acc[8][4] = {};
+      for (int c = 0; c < b; ++c) {
+        double cv[8], wv[4];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) cv[u] = sC[ti + u][c];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) wv[v] = sW[c][tj + v];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc[u][v] = fma(cv[u], wv[v], acc[u][v]);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int i = I0 + ti + u, j = J0 + tj + v;
+          if (i >= n || j >= n) continue;
+          const bool iK = i >= k0 && i < k0 + b, jK = j >= k0 && j < k0 + b;
+          double* a = A + (long long)i * n + j;
+          if (iK && jK) {
+            *a = sP[i - k0][j - k0];
+          } else if (iK) {
+            *a = sW[i - k0][tj + v];
+          } else if (jK) {
+            double s2 = 0.0;
+            for (int c = 0; c < b; ++c) s2 = fma(sC[ti + u][c], sP[c][j - k0], s2);
+            *a = -s2;
+          } else {
+            *a -= acc[u][v];
+          }
+        }
+    }
+    grid.sync();
   }
 }
 

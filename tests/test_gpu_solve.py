@@ -108,7 +108,7 @@ print(it, rr)
 @pytest.mark.parametrize("env", [{}, {"TOPO_MG_FUSE": "1"}, {"TOPO_MG_MF1": "0"},
                                  {"TOPO_MG_NODE": "0"}, {"TOPO_MG_TILE": "0"},
                                  {"TOPO_MG_DENSE_COARSE": "0"}, {"TOPO_MG_LANES_MAX": "0"},
-                                 {"TOPO_MG_GJ": "1"}, {"TOPO_MG_BLOCK": "0"},
+                                 {"TOPO_MG_DENSE_MAX": "100"}, {"TOPO_MG_BLOCK": "0"},
                                  {"TOPO_MG_GRAPH": "0"}])
 def test_multigrid_variants_agree(P, tmp_path, env):
     import os, subprocess, sys
