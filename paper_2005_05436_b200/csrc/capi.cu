@@ -2,6 +2,7 @@
 // staging, and the stream-ordered orchestration of the kernels in
 // kernels.cuh. One context per GPU (x-slab rank).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
@@ -264,7 +265,23 @@ topo_status finish_out(topo_ctx* ctx, double* user, const double* dev, long long
 }
 
 // stage timing: events bracket each stage on the stream it runs on
+struct NvtxRange {  // entry-point ranges for Nsight Systems (no-ops without a tool)
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
+// stage boundaries: CUDA events when timing is on, NVTX ranges always (host
+// enqueue ranges, nested LIFO; free without an attached tool)
 inline void tmark(topo_ctx* c, int stage, int end, cudaStream_t s) {
+  static const char* const names[TOPO_NSTAGES] = {"K1 filter",       "K2 eta",     "K3a element",
+                                                  "K4 adjoint + OC prep", "K5/K6 OC", "K3b sK store",
+                                                  "design pass"};
+  if (end)
+    nvtxRangePop();
+  else
+    nvtxRangePushA(names[stage]);
   if (c->timing) cudaEventRecord(c->tev[2 * stage + end], s);
 }
 
@@ -569,12 +586,9 @@ topo_status launch_sk(topo_ctx* ctx, const SkArgs& S, cudaStream_t st) {
   const Geo& G = ctx->G;
   int nb = grid_for(ctx, (G.m + 31) / 32 * 32);
   const bool ov = st == ctx->aux;
-  const char* e = getenv("TOPO_SK_BPS");  // blocks per SM (experiments)
   // overlapped: ~2.17 blocks per SM (measured on C5: 320 blocks 6.34 ms per pass
-  // against 6.40 with 296 and 6.35 with 336)
-  if (e || ov) nb = std::min(nb, e ? ctx->sm_count * std::max(1, atoi(e)) : ctx->sm_count * 13 / 6);
-  static const char* eb = getenv("TOPO_SK_BLOCKS");  // experiments: explicit grid
-  if (eb) nb = std::max(1, atoi(eb));
+  // against 6.40 with 296 and 6.35 with 336; 3 per SM 6.48)
+  if (ov) nb = std::min(nb, ctx->sm_count * 13 / 6);
   SkArgs S2 = S;
   S2.counter = nullptr;
   static const char* de = getenv("TOPO_SK_DYN");
@@ -774,8 +788,7 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
                    bool* deferred = nullptr) {
   const Geo& G = ctx->G;
   const double add_const = mode == TOPO_VOL_FILTERED ? ctx->nS_total : 0.0;
-  static const bool force_host = getenv("TOPO_OC_HOST") != nullptr;  // debugging aid
-  if ((mode == TOPO_VOL_MEAN || mode == TOPO_VOL_FILTERED) && !ctx->comm && !force_host) {
+  if ((mode == TOPO_VOL_MEAN || mode == TOPO_VOL_FILTERED) && !ctx->comm) {
     OcArgs A;
     A.m = G.m;
     A.R = ctx->oc_view;
@@ -796,22 +809,10 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
     A.xNew = xnew_dev;
     A.result = ctx->result.as<double>() + 8;
     A.dbg = nullptr;
-    static const bool prof = getenv("TOPO_OC_PROFILE") != nullptr;  // profiling aid
-    if (prof) {
-      CK(ctx->tmp1.ensure(sizeof(long long) * 128));
-      A.dbg = ctx->tmp1.as<long long>();
-    }
     // 4 bisection levels per grid-wide round (k_oc_bisect<32> does 5 levels;
     // measured slower on C1-C3: 224 registers, one block per SM)
-    const int ocb = ctx->oc_blocks_now > 0 ? ctx->oc_blocks_now : ctx->coop_blocks;
-    TRY(coop_launch(ctx, (const void*)k_oc_bisect<16>, &A, ocb));
-    if (prof) {
-      long long h[128];
-      CK(cudaMemcpy(h, A.dbg, sizeof h, cudaMemcpyDeviceToHost));
-      fprintf(stderr, "[oc profile] blocks %d marks %lld:", ocb, h[127]);
-      for (int q = 1; q < h[127]; ++q) fprintf(stderr, " %lld", h[q] - h[q - 1]);
-      fprintf(stderr, "\n");
-    }
+    TRY(coop_launch(ctx, (const void*)k_oc_bisect<16>, &A,
+                    ctx->oc_blocks_now > 0 ? ctx->oc_blocks_now : ctx->coop_blocks));
     k_oc_final<<<grid_for(ctx, G.m), kThreads, 0, ctx->stream>>>(G.m, A.R, A.result, xnew_dev);
     LAUNCHED();
     CK(cudaMemcpyAsync(ctx->h_result + 8, A.result, sizeof(double) * 7, cudaMemcpyDeviceToHost,
@@ -829,9 +830,9 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
     *evals = int32_t(r[2]);
     return TOPO_OK;
   }
-  if ((mode == TOPO_VOL_MEAN || mode == TOPO_VOL_FILTERED) && ctx->comm && !force_host)
+  if (mode == TOPO_VOL_MEAN || mode == TOPO_VOL_FILTERED)  // multi-rank
     return run_oc_dev(ctx, prm, add_const, prep, n_prep, xnew_dev, lam, bis, evals, deferred);
-  // host-driven replay: projected volume, callback (and the TOPO_OC_HOST aid)
+  // host-driven replay: projected volume (one filter per evaluation), callback
   TRY(reduce_to_host<3>(ctx, prep, n_prep));
   double lamMax = prm->lambda_max;
   if (!(prm->lambda_max > 0)) {
@@ -843,37 +844,6 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
            prm->abs_tol);
   std::vector<double> hx;
   const int nb = grid_for(ctx, G.m);
-  if (mode == TOPO_VOL_MEAN || mode == TOPO_VOL_FILTERED) {
-    // multi-GPU identity volumes: the device kernel's bound shortcut and
-    // speculative batches, one allreduce of K sums per batch
-    const double V0 = (add_const + ctx->h_result[1]) / ctx->m_total;
-    const double Vinf = (add_const + ctx->h_result[2]) / ctx->m_total;
-    int smode = 0;
-    if (Vinf > prm->volfrac + 0.5 * prm->volume_tol + 1e-12) smode = 1;
-    if (V0 < prm->volfrac - 0.5 * prm->volume_tol - 1e-12) smode = -1;
-    if (smode != 0) {
-      ctl.replay_known(smode > 0 ? INFINITY : -INFINITY);
-    }
-    double req[kOcK], val[kOcK];
-    static const bool dbg = getenv("TOPO_DEBUG") != nullptr;
-    if (dbg)
-      fprintf(stderr, "[rank %d] oc host: lamMax %.17g V0 %.17g Vinf %.17g add %.17g smode %d\n",
-              ctx->rank, lamMax, V0, Vinf, add_const, smode);
-    while (ctl.pending()) {
-      const int K = oc_speculate<kOcK>(ctl, req);
-      TRY(comm_oc_volumes(ctx->comm, ctx, req, K, add_const, val));
-      if (dbg)
-        for (int q = 0; q < K; ++q)
-          fprintf(stderr, "[rank %d]   s %.17g V %.17g\n", ctx->rank, req[q], val[q]);
-      while (ctl.pending()) {
-        int hit = -1;
-        for (int q = 0; q < K; ++q)
-          if (req[q] == ctl.s_req) hit = q;
-        if (hit < 0) break;
-        ctl.feed(val[hit]);
-      }
-    }
-  }
   while (ctl.pending()) {
     const double s = ctl.s_req;
     double v = 0;
@@ -886,7 +856,7 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
                          cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
       v = cb(user, hx.data(), G.m);
-    } else if (mode == TOPO_VOL_PROJECTED) {
+    } else {  // TOPO_VOL_PROJECTED
       const double* xs = nullptr;
       TRY(stage_field_storage(ctx, xnew_dev, ctx->tmp_st, &xs));
       ConvArgs C{};
@@ -901,8 +871,6 @@ topo_status run_oc(topo_ctx* ctx, const topo_oc_params* prm, int mode, const dou
       LAUNCHED();
       TRY(reduce_to_host<1>(ctx, ctx->partials.as<double>(), nb));
       v = ctx->h_result[0] / ctx->m_total;
-    } else {  // multi-GPU identity volume (ft = 1 / ft = 3)
-      TRY(comm_oc_volume(ctx->comm, ctx, s, add_const, &v));
     }
     ctl.feed(v);
   }
@@ -1343,6 +1311,7 @@ topo_status topo_fp64_peak(int device, double* tflops) {
 
 topo_status topo_loop_records(topo_ctx* ctx, const double* xPhys, double* xPrev,
                               const double* x, double* out3) {
+  NvtxRange nvtx_("topo_loop_records");
   if (!ctx || !xPhys || !xPrev || !x || !out3) return TOPO_EINVAL;
   DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
@@ -1374,6 +1343,7 @@ topo_status topo_anderson_reset(topo_ctx* ctx) {
 
 topo_status topo_anderson_step(topo_ctx* ctx, const topo_anderson* opt, const double* x_before,
                                double* x_inout) {
+  NvtxRange nvtx_("topo_anderson_step");
   if (!ctx || !opt || !x_before || !x_inout) return TOPO_EINVAL;
   DeviceGuard dg_(ctx->device);
   ctx->launches = 0;
@@ -1872,11 +1842,7 @@ static topo_status launch_elem(topo_ctx* ctx, const ElemArgs& A, int nb) {
   } else if (G.is3d) {
     KeFull<24> K;
     memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
-    static const int ne = getenv("TOPO_ELEM_NE") ? atoi(getenv("TOPO_ELEM_NE")) : 1;
-    if (ne == 2)
-      k_elem_sens<24, 2><<<nb, kThreads, 0, ctx->stream>>>(G, K, A);
-    else
-      k_elem_sens<24, 1><<<nb, kThreads, 0, ctx->stream>>>(G, K, A);
+    k_elem_sens<24, 1><<<nb, kThreads, 0, ctx->stream>>>(G, K, A);
   } else {
     KeFull<8> K;
     memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
@@ -2247,9 +2213,7 @@ static topo_status launch_tile_op(topo_ctx* ctx, const MgGeo& L, const double* E
                                   double* y, double* partials, int* nblocks = nullptr,
                                   bool c1 = false, int epi = -1, const double* b = nullptr,
                                   const double* diag = nullptr, double w = 0.0) {
-#define TILE_KERNELS(X)                                                                    \
-  X(kEpiApply, false) X(kEpiCG, false) X(kEpiJacobi, false) X(kEpiResidual, false)          \
-  X(kEpiApply, true) X(kEpiJacobi, true) X(kEpiResidual, true)
+#define TILE_KERNELS(X) X(kEpiApply, false) X(kEpiCG, false) X(kEpiApply, true)
   static unsigned long long attr = 0;  // bit per device
   if (!(attr >> ctx->device & 1)) {
 #define TILE_ATTR(E_, C_)                                                               \
@@ -2531,6 +2495,7 @@ extern "C" {
 topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f,
                                 const int32_t* fixed, int64_t nfixed, double rtol, int32_t maxit,
                                 double* u, int32_t* iterations, double* relres) {
+  NvtxRange nvtx_("topo_solve_state_mg");
   if (!ctx) return TOPO_EINVAL;
   DeviceGuard dg_(ctx->device);
   if (ctx->nranks > 1) return fail(ctx, TOPO_EINVAL, "solve: single-rank contexts only");
@@ -2910,11 +2875,9 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     // omega = (4/3) / lambda_max, the classical smoothing optimum (measured: C5
     // 23 MGCG iterations against 25 at 1.2; 1.7 diverges, the power-iteration
     // estimate of lambda_max is low)
-    static const char* omf = getenv("TOPO_MG_OMEGA");  // experiments: omega * lambda_max
-    L.omega = (omf ? atof(omf) : 4.0 / 3.0) / std::max(lam, 1e-30);
+    L.omega = (4.0 / 3.0) / std::max(lam, 1e-30);
   }
-  static const char* nue = getenv("TOPO_MG_NU");  // experiments: sweeps per side
-  const int nu = nue ? std::max(1, atoi(nue)) : 2, ncoarse = 40;
+  const int nu = 2, ncoarse = 40;  // sweeps per side (measured: 1 and 3 slower on C5)
   int coarse_grid = 0;  // resident blocks of the cooperative coarsest-level kernel
   {
     int occ = 0;
@@ -2954,20 +2917,11 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
       return TOPO_OK;
     }
     // one damped-Jacobi sweep from x (node kernels: into y, then the buffers swap)
-    // tile-operator levels (fine Walsh level, on-the-fly level 1): fused epilogues
-    // (off by default: measured 3% slower on C5 than the apply + elementwise
-    // sweep, the epilogue's extra loads sit in the latency-bound tile loop)
-    static const char* fz = getenv("TOPO_MG_FUSE");
-    const bool tiled = (fz && fz[0] == '1') && ((l == 0 && dkw && use_tile_op(ctx)) || (l == 1 && mf1));
+    // (a Jacobi / residual epilogue fused into the tile operator measured 3%
+    // slower on C5 than the apply + elementwise sweep: removed)
     auto sweep = [&]() -> topo_status {
       if (nodes) {
         TRY(node_op(l, 1, L.x.as<double>(), L.y.as<double>()));
-        std::swap(L.x.p, L.y.p);
-        return TOPO_OK;
-      }
-      if (tiled) {
-        TRY(launch_tile_op(ctx, L.g, E, L.x.as<double>(), L.y.as<double>(), nullptr, nullptr,
-                           l == 1, kEpiJacobi, L.b.as<double>(), L.diag.as<double>(), w));
         std::swap(L.x.p, L.y.p);
         return TOPO_OK;
       }
@@ -2993,9 +2947,6 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     if (last) return TOPO_OK;
     if (nodes) {
       TRY(node_op(l, 2, L.x.as<double>(), L.r.as<double>()));
-    } else if (tiled) {
-      TRY(launch_tile_op(ctx, L.g, E, L.x.as<double>(), L.r.as<double>(), nullptr, nullptr, l == 1,
-                         kEpiResidual, L.b.as<double>(), L.diag.as<double>(), w));
     } else {
       TRY(apply(l, L.x.as<double>(), L.y.as<double>()));
       k_mg_residual<<<nbd, kThreads, 0, ctx->stream>>>(nl, fm, L.b.as<double>(),
@@ -3109,11 +3060,15 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
       if (*g) cudaGraphExecDestroy(*g);
     }
   } free_graph{&gexec};
+  long long graph_launches = 0;  // kernels per captured iteration (counted on each replay)
   while (ff > 0 && rel > rtol && it < maxit) {
     if (use_graph && !gexec) {
       cudaGraph_t graph = nullptr;
       bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      const long long l0 = ctx->launches;
       const topo_status st = ok ? iteration() : TOPO_ECUDA;
+      graph_launches = ctx->launches - l0;
+      ctx->launches = l0;
       ok = cudaStreamEndCapture(ctx->stream, &graph) == cudaSuccess && ok && st == TOPO_OK;
       if (ok) ok = cudaGraphInstantiate(&gexec, graph, 0) == cudaSuccess;
       if (graph) cudaGraphDestroy(graph);
@@ -3125,6 +3080,7 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
     }
     if (gexec) {
       CK(cudaGraphLaunch(gexec, ctx->stream));
+      ctx->launches += graph_launches;
       z = lv[0].x.as<double>();
     } else {
       TRY(iteration());
@@ -3520,6 +3476,7 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
     key.keep_xphys = ctx->keep_xphys;
   }
   if (pg && pg->exec && same_key(pg->key, key)) {
+    NvtxRange nvtx_("design pass (graph replay)");
     CK(cudaGraphLaunch(pg->exec, ctx->stream));
     ++pg->replays;
     H = pg->host;
@@ -3767,30 +3724,6 @@ topo_status comm_allreduce_host(Comm* c, topo_ctx* ctx, double* host, int n) {
   CK(cudaMemcpyAsync(host, c->dtmp.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return TOPO_OK;
-}
-
-// K speculative OC volume sums over this slab, allreduced: V(s_q) for q < K
-topo_status comm_oc_volumes(Comm* c, topo_ctx* ctx, const double* s, int K, double add_const,
-                            double* v) {
-  const Geo& G = ctx->G;
-  const int nb = grid_for(ctx, G.m);
-  double* dreq = ctx->result.as<double>() + 40;  // K <= 16 requests
-  CK(cudaMemcpyAsync(dreq, s, sizeof(double) * K, cudaMemcpyHostToDevice, ctx->stream));
-  k_oc_batch<<<nb, kThreads, 0, ctx->stream>>>(G.m, ctx->oc_view, dreq, K,
-                                                ctx->partials.as<double>());
-  LAUNCHED();
-  double* sums = ctx->partials0.as<double>();
-  k_reduce_rows<<<K, 256, 0, ctx->stream>>>(ctx->partials.as<double>(), nb, sums);
-  LAUNCHED();
-  if (c) TRY(comm_allreduce(c, ctx, sums, K));
-  CK(cudaMemcpyAsync(v, sums, sizeof(double) * K, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  for (int q = 0; q < K; ++q) v[q] = (add_const + v[q]) / ctx->m_total;
-  return TOPO_OK;
-}
-
-topo_status comm_oc_volume(Comm* c, topo_ctx* ctx, double s, double add_const, double* v) {
-  return comm_oc_volumes(c, ctx, &s, 1, add_const, v);
 }
 
 void comm_destroy(Comm* c) {

@@ -12,7 +12,4 @@ struct Comm;
 topo_status comm_halo(Comm* c, topo_ctx* ctx, double* storage, double* storage2 = nullptr);
 topo_status comm_allreduce(Comm* c, topo_ctx* ctx, double* dev, int n);
 topo_status comm_allreduce_host(Comm* c, topo_ctx* ctx, double* host, int n);
-topo_status comm_oc_volume(Comm* c, topo_ctx* ctx, double s, double add_const, double* v);
-topo_status comm_oc_volumes(Comm* c, topo_ctx* ctx, const double* s, int K, double add_const,
-                            double* v);
 void comm_destroy(Comm* c);

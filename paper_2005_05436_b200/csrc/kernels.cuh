@@ -1574,32 +1574,6 @@ __global__ void __launch_bounds__(kThreads) k_oc_final(long long m, OcRecs R,
     out[e] = oc_cand(R.get(e), s);
 }
 
-// K block partial volume sums at the multipliers s[0..K) (multi-GPU OC round)
-__global__ void __launch_bounds__(kThreads) k_oc_batch(long long m, OcRecs R,
-                                                       const double* __restrict__ s, int K,
-                                                       double* __restrict__ partials) {
-  __shared__ double scratch[kOcK * 32];
-  __shared__ double sreq[kOcK];
-  if (threadIdx.x < kOcK) sreq[threadIdx.x] = threadIdx.x < K ? s[threadIdx.x] : 0.0;
-  __syncthreads();
-  double acc[kOcK], sq[kOcK], iq[kOcK];
-#pragma unroll
-  for (int q = 0; q < kOcK; ++q) {
-    acc[q] = 0.0;
-    sq[q] = q < K ? sreq[q] : 1.0;
-    iq[q] = 1.0 / sq[q];
-  }
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m;
-       e += (long long)gridDim.x * blockDim.x) {
-    const double4 r = R.get(e);
-#pragma unroll
-    for (int q = 0; q < kOcK; ++q)
-      if (q < K) acc[q] = fma(r.w, oc_cand_rcp(r, sq[q], iq[q]), acc[q]);
-  }
-  block_sum<kOcK>(acc, scratch);
-  if (threadIdx.x == 0)
-    for (int q = 0; q < K; ++q) partials[(long long)q * gridDim.x + blockIdx.x] = acc[q];
-}
 
 // oc.hpp:209-222: block partial (sumClamped, sumMid, numMid) of the
 // primal-dual iteration at the sqrt multiplier lm, over active elements
