@@ -2521,8 +2521,8 @@ topo_status topo_solve_state_mg(topo_ctx* ctx, const double* sK, const double* f
   for (;;) {
     const MgGeo c = lvg.back().g;  // (copy: emplace_back below may reallocate)
     const bool even = c.nelx % 2 == 0 && c.nely % 2 == 0 && (dim == 2 || c.nz % 2 == 0);
-    static const long long min_dofs =
-        getenv("TOPO_MG_MIN_DOFS") ? atoll(getenv("TOPO_MG_MIN_DOFS")) : 2000;  // (measured:
+    const char* mde = getenv("TOPO_MG_MIN_DOFS");  // (read per solve: tests coarsen tiny grids)
+    const long long min_dofs = mde ? atoll(mde) : 2000;  // (measured:
     // coarsest ~2k DOFs solved exactly: C5 25 MGCG iterations, a sharpening 96x48x48
     // design 44 instead of 81 with ~300 DOFs; Jacobi sweeps on ~13k DOFs: C5 59)
     if (!even || c.n <= min_dofs || lvg.size() >= 8) break;

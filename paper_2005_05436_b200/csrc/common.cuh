@@ -4,10 +4,31 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 namespace topo {
 
 namespace cg = cooperative_groups;
+
+// Bounds checks of the checked build (-DTOPO_CHECKED, libtopo_b200_checked.so,
+// tests/test_gpu_checked.py): a computed index outside its array traps the
+// kernel with a message. compute-sanitizer is unavailable on the GPU pool, so
+// these asserts on the computed (gather / scatter / mirror-folded) indices
+// stand in for memcheck. No code in the default build.
+#ifdef TOPO_CHECKED
+#define TOPO_CHECK(cond)                                                             \
+  do {                                                                               \
+    if (!(cond)) {                                                                   \
+      printf("TOPO_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, \
+             __LINE__, int(blockIdx.x), int(threadIdx.x));                           \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+#else
+#define TOPO_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 // std::max / std::min argument semantics (oc.hpp:36,49-51,59): the first
 // argument wins unless the second compares strictly greater / smaller. CUDA's

@@ -323,7 +323,10 @@ __device__ __forceinline__ void conv_tables(const Geo& G, const ConvGeom& T, con
     if (t >= 0 && t < n) return t;
     return G.bc == 0 ? reflect_index(t, n) : -1;
   };
-  for (int q = tid; q < T.EI; q += blockDim.x) mapI[q] = fold(bi + q - T.reach, G.nely);
+  for (int q = tid; q < T.EI; q += blockDim.x) {
+    mapI[q] = fold(bi + q - T.reach, G.nely);
+    TOPO_CHECK(mapI[q] >= -1 && mapI[q] < G.nely);
+  }
   for (int line = tid; line < nlines; line += blockDim.x) {
     const int to = line / T.ER, tr = line - to * T.ER;
     int jo, jr;
@@ -348,6 +351,8 @@ __device__ __forceinline__ void conv_tables(const Geo& G, const ConvGeom& T, con
         src = G.is3d ? ((long long)(jo - G.sj0) * G.nz + jr) * G.nely
                      : (long long)(jr - G.sj0) * G.nely;
     }
+    TOPO_CHECK(src >= -1 && src + G.nely <= (long long)G.sjn * G.S);
+    TOPO_CHECK(to * sPlane + tr < T.EI * T.ER * T.EO);
     lineSrc[line] = src;
     lineDst[line] = to * sPlane + tr;
   }
@@ -1106,7 +1111,10 @@ __global__ void __launch_bounds__(kThreads, 4 - NE) k_elem_sens(Geo G, KeFull<D>
       int dofs[24];
       element_dofs(G, i, k, j, G.j0, dofs);
 #pragma unroll
-      for (int q = 0; q < D; ++q) ue[n][q] = __ldg(A.U + dofs[q]);
+      for (int q = 0; q < D; ++q) {
+        TOPO_CHECK(dofs[q] >= 0 && dofs[q] < G.dim * (G.jn + 1) * (G.nely + 1) * (G.is3d ? G.nz + 1 : 1));
+        ue[n][q] = __ldg(A.U + dofs[q]);
+      }
     }
     // quad = ue . (Ke ue) (fea.hpp:267), on the symmetric upper half
     double quad[NE];
@@ -1192,6 +1200,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, El
       // the element's nodes are 4 (k, j) pairs of 2 consecutive i: 6 doubles each
       const double* u0 = A.U + 3 * n0;
       const double* up[4] = {u0, u0 + 3 * ny1, u0 + 3 * pl, u0 + 3 * (pl + ny1)};
+      TOPO_CHECK(n0 >= 0 && n0 + pl + ny1 + 1 < (long long)(G.jn + 1) * pl);
 #pragma unroll
       for (int b = 0; b < 8; ++b)
 #pragma unroll
@@ -1316,6 +1325,7 @@ __global__ void __launch_bounds__(kThreads) k_sk_store(Geo G, SkArgs A) {
       const int el = min(v / PV, 31);
       const double se = __shfl_sync(0xffffffffu, s, el);
       if (v < nv) {
+        TOPO_CHECK(e0 * P + 4 * (long long)v + 3 < G.m * P && v - el * PV < PV);
         const double4 k = kl[v - el * PV];
         st256_cs(out + 4 * (long long)v, se * k.x, se * k.y, se * k.z, se * k.w);  // fea.hpp:168
       }
