@@ -4,6 +4,7 @@ roofline `traffic`."""
 import csv, io, json, subprocess, sys
 
 rep, src = sys.argv[1], sys.argv[2]
+dst = sys.argv[3] if len(sys.argv) > 3 else "profiles/ncu_summary.json"
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h, units, data = rows[0], rows[1], rows[2:]
@@ -24,5 +25,5 @@ for r in data:
                   "duration_ms": val(r, "gpu__time_duration.sum")}
 sk = [v for k, v in kern.items() if "k_sk_store" in k][0]
 json.dump({"C5": {"sk_store_dram_bytes": sk["dram_read_bytes"] + sk["dram_write_bytes"], "source": src},
-           "kernels_c5": kern}, open("profiles/ncu_summary.json", "w"), indent=1)
+           "kernels_c5": kern}, open(dst, "w"), indent=1)
 print(json.dumps(kern, indent=1)[:400])
