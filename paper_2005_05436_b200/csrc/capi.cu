@@ -92,9 +92,6 @@ struct topo_ctx {
   cudaStream_t stream = nullptr, aux = nullptr, cstream = nullptr;  // main, sK, copies
   cudaStream_t hstream = nullptr;  // multi-rank: K1 interior tiles beside the halo exchange
   cudaEvent_t ev_h0 = nullptr, ev_h1 = nullptr;
-  cudaEvent_t ev_q0 = nullptr, ev_q2 = nullptr;  // the u' Ke u prepass (copy stream)
-  bool q2_prepass = true;  // TOPO_Q2_PREPASS
-  DevBuf q2;
   bool own_stream = true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_x = nullptr, ev_u = nullptr;
   cudaEvent_t ev_in = nullptr;  // topo_wait_stream: caller's stream -> ctx->stream
@@ -588,14 +585,20 @@ int conv_blocks(const topo_ctx* ctx) {
 topo_status launch_sk(topo_ctx* ctx, const SkArgs& S, cudaStream_t st) {
   const Geo& G = ctx->G;
   int nb = grid_for(ctx, (G.m + 31) / 32 * 32);
+  // Overlapped on large grids (C5): ~2.17 persistent blocks per SM claiming
+  // runs of element groups from a counter, so the stream keeps its rate while
+  // K3a / K4 blocks share the SMs (measured on C5: 320 blocks 6.34 ms per
+  // pass against 6.40 with 296, 6.35 with 336, 6.48 with 3 per SM; the full
+  // static grid 6.66: K3a / K4 wait for the store's blocks). Small grids
+  // (sK < 2 GB, C4) keep the full static grid also when overlapped: the store
+  // runs at full rate and the short K3a -> K4 -> OC chain fills in (C4 0.176
+  // against 0.210 ms with the persistent grid).
   const bool ov = st == ctx->aux;
-  // overlapped: ~2.17 blocks per SM (measured on C5: 320 blocks 6.34 ms per pass
-  // against 6.40 with 296 and 6.35 with 336; 3 per SM 6.48)
-  if (ov) nb = std::min(nb, ctx->sm_count * 13 / 6);
+  const bool dyn = ov && double(G.m) * G.P * 8.0 >= 2e9;
+  if (dyn) nb = std::min(nb, ctx->sm_count * 13 / 6);
   SkArgs S2 = S;
   S2.counter = nullptr;
-  static const char* de = getenv("TOPO_SK_DYN");
-  if (de ? atoi(de) != 0 : ov) {
+  if (dyn) {
     S2.counter = reinterpret_cast<unsigned long long*>(ctx->result.as<double>() + 63);
     CK(cudaMemsetAsync(S2.counter, 0, sizeof(unsigned long long), st));
   }
@@ -614,8 +617,7 @@ topo_status set_overlap_carveout(int device) {
   static unsigned long long done = 0;  // bit per device
   if (done >> device & 1) return TOPO_OK;
   for (const void* f : {(const void*)k_sk_store<300>, (const void*)k_sk_store<36>,
-                        (const void*)k_elem_walsh<0>, (const void*)k_elem_walsh<1>,
-                        (const void*)k_elem_walsh<2>})
+                        (const void*)k_elem_walsh})
     if (cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                              int(cudaSharedmemCarveoutMaxShared)) != cudaSuccess)
       return TOPO_ECUDA;
@@ -1139,8 +1141,6 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
     ctx->overlap_sk = ov ? ov[0] == '1' : big;
     const char* pgr = getenv("TOPO_PASS_GRAPH");
     ctx->use_pass_graph = pgr ? pgr[0] != '0' : true;
-    const char* q2e = getenv("TOPO_Q2_PREPASS");
-    ctx->q2_prepass = q2e ? q2e[0] != '0' : true;
   }
 
 #define CKC(x)                                                                          \
@@ -1150,13 +1150,12 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
       return bail(fail(ctx, TOPO_ECUDA, "%s failed: %s", #x, cudaGetErrorString(e_)));  \
   } while (0)
   CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-  CKC(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+  CKC(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));  // (measured: stream
+                                                                      // priorities change nothing)
   CKC(cudaStreamCreateWithFlags(&ctx->cstream, cudaStreamNonBlocking));
   CKC(cudaStreamCreateWithFlags(&ctx->hstream, cudaStreamNonBlocking));
   CKC(cudaEventCreateWithFlags(&ctx->ev_h0, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_h1, cudaEventDisableTiming));
-  CKC(cudaEventCreateWithFlags(&ctx->ev_q0, cudaEventDisableTiming));
-  CKC(cudaEventCreateWithFlags(&ctx->ev_q2, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_x, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_u, cudaEventDisableTiming));
   CKC(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
@@ -1272,9 +1271,6 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   if (ctx->hstream) cudaStreamDestroy(ctx->hstream);
   if (ctx->ev_h0) cudaEventDestroy(ctx->ev_h0);
   if (ctx->ev_h1) cudaEventDestroy(ctx->ev_h1);
-  if (ctx->ev_q0) cudaEventDestroy(ctx->ev_q0);
-  if (ctx->ev_q2) cudaEventDestroy(ctx->ev_q2);
-  ctx->q2.release();
   if (ctx->stream && ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -1846,21 +1842,11 @@ topo_status topo_csc_values(topo_ctx* ctx, const double* sKe, double* values) {
   return TOPO_OK;
 }
 
-// qm: 0 the whole K3a, 1 the u' Ke u prepass into A.q2 (Walsh form only),
-// 2 the rest from A.q2; on stream st (default ctx->stream)
-static topo_status launch_elem(topo_ctx* ctx, const ElemArgs& A, int nb, int qm = 0,
-                               cudaStream_t st = nullptr) {
+static topo_status launch_elem(topo_ctx* ctx, const ElemArgs& A, int nb) {
   const Geo& G = ctx->G;
-  if (!st) st = ctx->stream;
-  if (qm != 0 && !(G.is3d && ctx->walsh))
-    return fail(ctx, TOPO_EINVAL, "internal: the q2 prepass needs the Walsh-form K3a");
+  cudaStream_t st = ctx->stream;
   if (G.is3d && ctx->walsh) {
-    if (qm == 1)
-      k_elem_walsh<1><<<nb, kThreads, 0, st>>>(G, ctx->kw, A);
-    else if (qm == 2)
-      k_elem_walsh<2><<<nb, kThreads, 0, st>>>(G, ctx->kw, A);
-    else
-      k_elem_walsh<0><<<nb, kThreads, 0, st>>>(G, ctx->kw, A);
+    k_elem_walsh<<<nb, kThreads, 0, st>>>(G, ctx->kw, A);
   } else if (G.is3d) {
     KeFull<24> K;
     memcpy(K.k, ctx->ke_full.data(), sizeof K.k);
@@ -3174,26 +3160,6 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
   DevBuf& xbuf = ctx->x_st.p ? ctx->x_st : ctx->tmp_st;
   TRY(stage_field_storage(ctx, x, xbuf, &xs, !halo_overlap));
   if (!U) return fail(ctx, TOPO_EINVAL, "null input array");
-  // small 3D grids: u_e' Ke u_e (the U gather, no eta needed) on the copy
-  // stream beside K1 / K2, which leave most of the machine idle there; K3a
-  // then only reads it (C4: the chain after eta that shares the SMs with the
-  // sK stream shrinks by the gather)
-  const bool q2pre = ctx->q2_prepass && G.is3d && ctx->walsh && is_device_ptr(U) &&
-                     conv3_rb(ctx, G) == kC3Rs;
-  if (q2pre) {
-    CK(ctx->q2.ensure(sizeof(double) * size_t(G.m)));
-    CK(cudaEventRecord(ctx->ev_q0, ctx->stream));
-    CK(cudaStreamWaitEvent(ctx->cstream, ctx->ev_q0, 0));
-    ElemArgs Q{};
-    Q.xt = ctx->xt.as<double>();
-    Q.eta_ptr = ctx->result.as<double>();
-    Q.U = U;
-    Q.state = state;
-    Q.ihs = ctx->ihs.as<double>();
-    Q.q2 = ctx->q2.as<double>();
-    TRY(launch_elem(ctx, Q, grid_for(ctx, G.m), 1, ctx->cstream));
-    CK(cudaEventRecord(ctx->ev_q2, ctx->cstream));
-  }
   CK(cudaEventRecord(ctx->ev_x, ctx->stream));  // x staged: a host U may follow on the link
   const double* xown = xs + (long long)(G.j0 - G.sj0) * G.S;
   double* res = ctx->result.as<double>();
@@ -3364,16 +3330,12 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
     return k;
   };
   int next_a = 0;
-  if (q2pre) {
-    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_q2, 0));
-    E.q2 = ctx->q2.as<double>();
-  }
   for (int k = 0; k < nch; ++k) {
     if (hostU) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_uc[std::min(k + 1, nch - 1)], 0));
     E.e_begin = (long long)col0(k) * G.S;
     E.e_end = k + 1 < nch ? (long long)col0(k + 1) * G.S : G.m;
     E.partials = ctx->cpart.as<double>() + (long long)k * nbc;
-    TRY(launch_elem(ctx, E, nbc, q2pre ? 2 : 0));
+    TRY(launch_elem(ctx, E, nbc));
     while (k4chunks && next_a < nch) {
       const int z0 = ztile0(next_a), z1 = ztile0(next_a + 1);
       const int last_col = std::min(G.jn, z1 * T4.TO + ctx->reach) - 1;

@@ -1068,7 +1068,6 @@ struct ElemArgs {
   double* a2;
   double* partials;      // per block: compliance partial
   long long e_begin, e_end;  // element range of this launch (e_end 0: all)
-  double* q2;            // u_e' Ke u_e per element (the small-grid prepass, k_elem_walsh<1 / 2>)
 };
 
 __device__ __forceinline__ double simp_xp(double x, double p) {
@@ -1178,13 +1177,9 @@ struct KeWalsh {
 // (component 0 = x flips with j, 1 = y with i, 2 = z with k)
 __host__ __device__ constexpr int walsh_axis(int c) { return c == 0 ? 2 : (c == 1 ? 0 : 1); }
 
-// QM (small grids, the u' Ke u prepass): 0 = the whole K3a; 1 = only q2 =
-// u_e' Ke u_e into A.q2 (needs no eta: runs beside K1 / K2 on a side stream);
-// 2 = the rest of K3a from A.q2 (no U gather after eta)
-template <int QM>
 __global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, ElemArgs A) {
   __shared__ double scratch[32];
-  const double eta = (A.input_is_phys || QM == 1) ? 0.5 : *A.eta_ptr;
+  const double eta = A.input_is_phys ? 0.5 : *A.eta_ptr;
   const double a = tanh(A.beta * eta);
   const double denom = a + tanh(A.beta * (1.0 - eta));
   const double de = A.e0 - A.emin;
@@ -1201,7 +1196,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, El
     const int st = elem_state(A.state, e);
     const long long n0 = (long long)(j - G.j0) * pl + (long long)k * ny1 + i;  // node (i, k, j)
     double h[3][8];  // [component][binary node index oi + 2 ok + 4 oj]
-    if (QM != 2) {
+    {
       // the element's nodes are 4 (k, j) pairs of 2 consecutive i: 6 doubles each
       const double* u0 = A.U + 3 * n0;
       const double* up[4] = {u0, u0 + 3 * ny1, u0 + 3 * pl, u0 + 3 * (pl + ny1)};
@@ -1223,10 +1218,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, El
     const double xp = simp_xp(xphys, A.penal);
     const double sK = A.emin + xp * xphys * de;  // fea.hpp:142
     const double dsK = A.penal * xp * de;        // fea.hpp:143
-    double q2 = 0.0;  // u' Ke u (fea.hpp:267)
-    if (QM == 2) {
-      q2 = A.q2[e];
-    } else {
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -1238,6 +1229,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, El
             h[c][b] = hi + lo;
             h[c][b | bit] = hi - lo;
           }
+    double q2 = 0.0;  // u' Ke u (fea.hpp:267)
 #pragma unroll
     for (int sig = 0; sig < 8; ++sig) {
       const double m0 = h[0][sig ^ (1 << walsh_axis(0))];
@@ -1249,11 +1241,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, El
       q2 = fma(m0, r0, q2);
       q2 = fma(m1, r1, q2);
       q2 = fma(m2, kk[5] * m2, q2);
-    }
-    }
-    if (QM == 1) {
-      A.q2[e] = q2;
-      continue;
     }
     csum = fma(sK, q2, csum);
     const double dcp = st == 0 ? -dsK * q2 : 0.0;
@@ -1267,7 +1254,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, El
       A.a2[es] = (dH * dv0) * ih;
     }
   }
-  if (QM == 1) return;
   double red[1] = {csum};
   block_sum<1>(red, scratch);
   if (threadIdx.x == 0) A.partials[blockIdx.x] = red[0];

@@ -174,17 +174,3 @@ def test_compile_time_cone_matches_runtime_loop(P, cid, grid, rmin):
     for k in ("xTilde", "dc", "dV", "xNew"):
         assert rel(_as_np(getattr(b, k)), _as_np(getattr(a, k))) <= 1e-13, k
 
-
-@pytest.mark.parametrize("grid", [(24, 16, 12), (96, 48, 48)])
-def test_q2_prepass_is_bitwise_single_k3a(P, grid):
-    # small 3D grids: u' Ke u on the copy stream beside K1/K2, then K3a from
-    # it (TOPO_Q2_PREPASS) against the single K3a: the same arithmetic
-    from paper_2005_05436_b200.configs import CONFIGS
-    cfg = CONFIGS[4].scaled(*grid)
-    x, u = _inputs(cfg, 31)
-    xd, ud = torch.from_numpy(x).cuda(), torch.from_numpy(u).cuda()
-    a = _pass(P, cfg, xd, ud, {"TOPO_Q2_PREPASS": "0"})
-    b = _pass(P, cfg, xd, ud, {"TOPO_Q2_PREPASS": "1"})
-    for k in FIELDS:
-        np.testing.assert_array_equal(_as_np(getattr(a, k)), _as_np(getattr(b, k)), err_msg=k)
-    assert (a.eta, a.lam, a.bisections, a.c) == (b.eta, b.lam, b.bisections, b.c)
