@@ -577,35 +577,39 @@ int conv_blocks(const topo_ctx* ctx) {
          ((T.other_n + T.TO - 1) / T.TO);
 }
 
-// K3b: grid sized for full occupancy (no shared-memory or barrier limits)
-// K3b. Serial (main stream): grid sized for full occupancy, static split.
-// Overlapped (aux stream, large 3D passes): ~2 blocks per SM claiming work
-// dynamically, so the stream keeps its rate while K3a / K4 blocks share the SMs
-// (measured on C5: 6.38 ms per pass against 6.84 ms serial).
+// K3b. Serial (main stream) and 2D: k_sk_store, grid sized for full occupancy,
+// static split. Overlapped 3D passes (aux stream, beside K3a / K4 / OC):
+// k_sk_store_tma, one persistent 4-warp block per SM with 6 x 4800 B stages
+// per warp (115 KB of shared memory, 96 KB in flight), claiming runs of groups
+// from a counter. Measured on C5 (profiles/r02/ab_store.txt): pass 6.11 ms, the
+// same as ~2.2 persistent k_sk_store blocks per SM (the window moves 36.3 GB
+// at 6.38 TB/s, the write ceiling store_bench measures), but K3a -> K4 -> OC
+// finish after 3.9 instead of 5.7 ms; 4 / 3 / 2 stages 8.2 / 8.3 / 8.4 ms (too
+// few bytes in flight). On C4 the full static k_sk_store grid made K3a wait for
+// its first wave of blocks.
+constexpr int kSkTmaStages = 6;
 topo_status launch_sk(topo_ctx* ctx, const SkArgs& S, cudaStream_t st) {
   const Geo& G = ctx->G;
-  int nb = grid_for(ctx, (G.m + 31) / 32 * 32);
-  // Overlapped on large grids (C5): ~2.17 persistent blocks per SM claiming
-  // runs of element groups from a counter, so the stream keeps its rate while
-  // K3a / K4 blocks share the SMs (measured on C5: 320 blocks 6.34 ms per
-  // pass against 6.40 with 296, 6.35 with 336, 6.48 with 3 per SM; the full
-  // static grid 6.66: K3a / K4 wait for the store's blocks). Small grids
-  // (sK < 2 GB, C4) keep the full static grid also when overlapped: the store
-  // runs at full rate and the short K3a -> K4 -> OC chain fills in (C4 0.176
-  // against 0.210 ms with the persistent grid).
-  const bool ov = st == ctx->aux;
-  const bool dyn = ov && double(G.m) * G.P * 8.0 >= 2e9;
-  if (dyn) nb = std::min(nb, ctx->sm_count * 13 / 6);
   SkArgs S2 = S;
   S2.counter = nullptr;
-  if (dyn) {
+  S2.gch = 0;
+  const char* tme = getenv("TOPO_SK_TMA");  // 0: k_sk_store also when overlapped (tests, A/B)
+  if (st == ctx->aux && G.is3d && !(tme && tme[0] == '0')) {
+    constexpr int th = 128;
+    const long long ngroups = (G.m + 31) / 32;
+    const int nb = int(std::min<long long>(ctx->sm_count, (ngroups + th / 32 - 1) / (th / 32)));
+    S2.gch = int(std::max(1LL, std::min(8LL, ngroups / (16LL * nb * (th / 32)))));
     S2.counter = reinterpret_cast<unsigned long long*>(ctx->result.as<double>() + 63);
     CK(cudaMemsetAsync(S2.counter, 0, sizeof(unsigned long long), st));
+    constexpr size_t smem = size_t(th / 32) * kSkTmaStages * 4800;
+    k_sk_store_tma<kSkTmaStages><<<nb, th, smem, st>>>(G, S2);
+  } else {
+    const int nb = grid_for(ctx, (G.m + 31) / 32 * 32);
+    if (G.is3d)
+      k_sk_store<300><<<nb, kThreads, 0, st>>>(G, S2);
+    else
+      k_sk_store<36><<<nb, kThreads, 0, st>>>(G, S2);
   }
-  if (G.is3d)
-    k_sk_store<300><<<nb, kThreads, 0, st>>>(G, S2);
-  else
-    k_sk_store<36><<<nb, kThreads, 0, st>>>(G, S2);
   LAUNCHED();
   return TOPO_OK;
 }
@@ -617,10 +621,14 @@ topo_status set_overlap_carveout(int device) {
   static unsigned long long done = 0;  // bit per device
   if (done >> device & 1) return TOPO_OK;
   for (const void* f : {(const void*)k_sk_store<300>, (const void*)k_sk_store<36>,
-                        (const void*)k_elem_walsh})
+                        (const void*)k_sk_store_tma<kSkTmaStages>, (const void*)k_elem_walsh})
     if (cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                              int(cudaSharedmemCarveoutMaxShared)) != cudaSuccess)
       return TOPO_ECUDA;
+  if (cudaFuncSetAttribute(k_sk_store_tma<kSkTmaStages>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           4 * kSkTmaStages * 4800) != cudaSuccess)
+    return TOPO_ECUDA;
   done |= 1ull << device;
   return TOPO_OK;
 }
@@ -1138,7 +1146,7 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
     // (C5 6.32 vs 7.05 ms per pass; C4 0.206 vs 0.229 ms since the pass is
     // replayed from a CUDA graph)
     const bool big = G.is3d && double(G.m) * G.P * 8.0 >= 256e6;
-    ctx->overlap_sk = ov ? ov[0] == '1' : big;
+    ctx->overlap_sk = ov ? ov[0] != '0' : big;
     const char* pgr = getenv("TOPO_PASS_GRAPH");
     ctx->use_pass_graph = pgr ? pgr[0] != '0' : true;
   }

@@ -1271,7 +1271,8 @@ struct SkArgs {
   const double* eta_ptr;  // device scalar eta
   double beta, e0, emin, penal;
   double* sK;
-  unsigned long long* counter;  // non-null: dynamic work distribution (zeroed before launch)
+  unsigned long long* counter;  // k_sk_store_tma: work counter (zeroed before launch)
+  int gch;                      // groups per claim
 };
 
 // 256-bit streaming store (STG.E.EF.ENL2.256 on sm_100a): evict-first, the
@@ -1331,23 +1332,132 @@ __global__ void __launch_bounds__(kThreads) k_sk_store(Geo G, SkArgs A) {
       }
     }
   };
-  if (A.counter) {
-    // dynamic: warps claim runs of GCH groups, so blocks that share an SM with
-    // other kernels simply claim fewer (the static split would wait on them)
-    constexpr int GCH = 4;
-    for (;;) {
-      unsigned long long g0 = 0;
-      if (lane == 0) g0 = atomicAdd(A.counter, (unsigned long long)GCH);
-      g0 = __shfl_sync(0xffffffffu, g0, 0);
-      if ((long long)g0 >= ngroups) break;
-      const long long g1 = min((long long)g0 + GCH, ngroups);
-      for (long long g = (long long)g0; g < g1; ++g) group(g);
-    }
-    return;
-  }
   const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
   for (long long g = warp0; g < ngroups; g += nwarps) group(g);
+}
+
+// K3b beside other kernels (the overlapped 3D pass), through the bulk-copy
+// (TMA) engine. One persistent block of 4 warps per SM. A group of 32 elements
+// is written as 16 element pairs (A, B) of 150 32-byte vectors; lane l owns
+// vector l + 32 j of every pair, i.e. always the same five Ke_lower slices (A:
+// l, 32 + l, 64 + l for l < 11; B: l - 11 for l >= 11, 21 + l, 53 + l for
+// l < 22), held in registers for the kernel's lifetime. The products of a pair
+// (4800 B) go to a warp-private stage in shared memory and lane 0 hands the
+// stage to `cp.async.bulk` (shared -> global, L2 evict-first). D stages per
+// warp, D - 1 copies in flight, no block barriers. Why not plain stores
+// (scripts/store_bench.cu, profiles/r02/store_bench.txt): a store instruction
+// keeps its source registers until its data has left the SM, microseconds
+// beside a saturated write stream, so the bytes in flight (~100 KB per SM for
+// the full rate) would live in registers the co-running filter and sensitivity
+// kernels need; here they live in shared memory, the block takes 90 x 128
+// registers, and the copies bypass the LSU queue the co-runners' loads wait
+// in. Runs of `gch` groups are claimed from a counter; the claim of the run
+// after next and the input of the next group are in flight while a group is
+// written, so no read latency sits in front of the copies. Same products as
+// k_sk_store: bitwise equal.
+template <int D>
+__global__ void __launch_bounds__(128) k_sk_store_tma(Geo G, SkArgs A) {
+  constexpr int P = 300, PV = 75, CH = 2 * P * 8;  // bytes per element pair
+  extern __shared__ __align__(128) unsigned char sk_ring[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* mine = sk_ring + (size_t)wib * D * CH;
+  const double4* kl = reinterpret_cast<const double4*>(A.ke_lower);
+  const double4 k0 = kl[lane], k1 = kl[32 + lane];
+  const double4 k2 = kl[lane < 11 ? 64 + lane : lane - 11];
+  const double4 k3 = kl[21 + lane], k4 = kl[min(53 + lane, PV - 1)];
+  double a = 0, denom = 1, de = 0, eta = 0;
+  if (A.xt) {
+    eta = *A.eta_ptr;
+    a = tanh(A.beta * eta);
+    denom = a + tanh(A.beta * (1.0 - eta));
+    de = A.e0 - A.emin;
+  }
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  const long long ngroups = (G.m + 31) >> 5;
+  const double* src = A.xt ? A.xt : A.sKe;
+  auto ldx = [&](long long g) {
+    const long long e = (g << 5) + lane;
+    return g < ngroups && e < G.m ? __ldg(src + e) : 0.0;
+  };
+  auto modulus = [&](double v) {
+    if (!A.xt) return v;
+    const double xphys = (a + tanh(A.beta * (v - eta))) / denom;  // filter.hpp:142
+    const double xp = simp_xp(xphys, A.penal);
+    return A.emin + xp * xphys * de;  // fea.hpp:142
+  };
+  const int GCH = A.gch;
+  auto claim = [&]() {
+    return lane == 0 ? atomicAdd(A.counter, (unsigned long long)GCH) : 0ull;
+  };
+  unsigned long long pend = claim();
+  long long g0 = (long long)__shfl_sync(0xffffffffu, pend, 0);
+  pend = claim();
+  int stage = 0;
+  if (g0 < ngroups) {
+    double xv = ldx(g0);
+    for (;;) {
+      const long long ng0 = (long long)__shfl_sync(0xffffffffu, pend, 0);
+      pend = claim();
+      const long long g1 = min(g0 + GCH, ngroups);
+      for (long long g = g0; g < g1; ++g) {
+        const double s = modulus(xv);
+        xv = ldx(g + 1 < g1 ? g + 1 : ng0);
+        const long long e0 = g << 5;
+        const int ne = int(min(32LL, G.m - e0));
+        if (ne == 32) {
+          TOPO_CHECK((e0 + 32) * P <= G.m * P);
+#pragma unroll 2
+          for (int k = 0; k < 16; ++k) {
+            const double sa = __shfl_sync(0xffffffffu, s, 2 * k);
+            const double sb = __shfl_sync(0xffffffffu, s, 2 * k + 1);
+            const double sm = lane < 11 ? sa : sb;
+            // the copy that read this stage D pairs ago has finished reading
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(D - 1) : "memory");
+            __syncwarp();
+            double2* st = reinterpret_cast<double2*>(mine + (size_t)stage * CH) + 2 * lane;
+            st[0] = make_double2(sa * k0.x, sa * k0.y);  // fea.hpp:168
+            st[1] = make_double2(sa * k0.z, sa * k0.w);
+            st[64] = make_double2(sa * k1.x, sa * k1.y);
+            st[65] = make_double2(sa * k1.z, sa * k1.w);
+            st[128] = make_double2(sm * k2.x, sm * k2.y);
+            st[129] = make_double2(sm * k2.z, sm * k2.w);
+            st[192] = make_double2(sb * k3.x, sb * k3.y);
+            st[193] = make_double2(sb * k3.z, sb * k3.w);
+            if (lane < 22) {
+              st[256] = make_double2(sb * k4.x, sb * k4.y);
+              st[257] = make_double2(sb * k4.z, sb * k4.w);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              const unsigned sa32 = (unsigned)__cvta_generic_to_shared(mine + (size_t)stage * CH);
+              double* gp = A.sK + (e0 + 2 * k) * P;
+              asm volatile(
+                  "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gp),
+                  "r"(sa32), "n"(CH), "l"(pol)
+                  : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            stage = stage + 1 == D ? 0 : stage + 1;
+          }
+        } else {  // ragged last group: element by element, direct stores
+          for (int el = 0; el < ne; ++el) {
+            const double se = __shfl_sync(0xffffffffu, s, el);
+            for (int v = lane; v < PV; v += 32) {
+              const double4 k = kl[v];
+              st256_cs(A.sK + (e0 + el) * P + 4 * v, se * k.x, se * k.y, se * k.z, se * k.w);
+            }
+          }
+        }
+      }
+      g0 = ng0;
+      if (g0 >= ngroups) break;
+    }
+  }
+  // shared memory must outlive the copies that read it
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
 // ============================================================================

@@ -49,7 +49,7 @@ def _as_np(a):
 FIELDS = ("xTilde", "xPhys", "dcPhys", "dc", "dV", "xNew", "sK")
 
 
-@pytest.mark.parametrize("grid", [(24, 16, 12), (40, 24, 16)])
+@pytest.mark.parametrize("grid", [(24, 16, 12), (40, 24, 16), (13, 8, 7)])
 def test_overlapped_sk_stream_is_bitwise_serial(P, grid):
     from paper_2005_05436_b200.configs import CONFIGS
     cfg = CONFIGS[5].scaled(*grid)
@@ -60,6 +60,11 @@ def test_overlapped_sk_stream_is_bitwise_serial(P, grid):
     for k in FIELDS:
         np.testing.assert_array_equal(_as_np(getattr(a, k)), _as_np(getattr(b, k)), err_msg=k)
     assert (a.eta, a.lam, a.bisections, a.c) == (b.eta, b.lam, b.bisections, b.c)
+    # (overlapped: k_sk_store_tma, bulk copies from warp-private stages, ragged
+    # last group by direct stores; TOPO_SK_TMA=0: k_sk_store on the aux stream)
+    d = _pass(P, cfg, xd, ud, {"TOPO_SK_OVERLAP": "1", "TOPO_SK_TMA": "0"})
+    for k in FIELDS:
+        np.testing.assert_array_equal(_as_np(getattr(a, k)), _as_np(getattr(d, k)), err_msg=k)
 
 
 @pytest.mark.parametrize("overlap", ["0", "1"])
