@@ -299,6 +299,16 @@ topo_status topo_anderson_reset(topo_ctx* ctx);
 /* ---- fused pass: driver.hpp:183-231 (ft = 3) minus the state solve ------ */
 topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
                              const topo_pass_params* prm, topo_pass_out* out);
+/* The same pass in two halves, for callers that overlap host work with it or
+ * time it on the device: _begin validates, enqueues everything on the
+ * context's stream(s) and returns without waiting (x, U and the arrays in
+ * `out` must stay valid and untouched until _end); _end waits for the stream,
+ * completes the host-side parts (multi-rank OC / eta completion) and fills the
+ * scalars of `out` (pass the same `out`). topo_design_pass = _begin + _end.
+ * One pass in flight per context. */
+topo_status topo_design_pass_begin(topo_ctx* ctx, const double* x, const double* U,
+                                   const topo_pass_params* prm, topo_pass_out* out);
+topo_status topo_design_pass_end(topo_ctx* ctx, topo_pass_out* out);
 /* number of this library's kernel launches issued by the last call */
 int64_t topo_last_launch_count(const topo_ctx* ctx);
 /* per-stage CUDA-event timing of topo_design_pass (off by default). times_ms

@@ -28,7 +28,8 @@ EXPORTS = [
     "topo_simp_interpolate", "topo_assemble_values", "topo_sensitivity", "topo_filter",
     "topo_filter_adjoint", "topo_project", "topo_project_derivative", "topo_backfilter",
     "topo_solve_eta", "topo_filter_taps", "topo_filter_hs", "topo_lambda_upper",
-    "topo_oc_candidate", "topo_oc_bisect", "topo_design_pass", "topo_last_launch_count",
+    "topo_oc_candidate", "topo_oc_bisect", "topo_design_pass", "topo_design_pass_begin",
+    "topo_design_pass_end", "topo_last_launch_count",
     "topo_set_timing", "topo_stage_times", "topo_pass_graph_replays", "topo_loop_records",
     "topo_anderson_step", "topo_anderson_reset", "topo_host_oc_replay", "topo_host_eta_replay",
     "topo_nccl_unique_id", "topo_comm_init_host", "topo_slab_plan", "topo_fp64_peak",
@@ -131,6 +132,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
                                      C.c_double, VOLUME_FN, vp, vp, p(C.c_double), p(C.c_int32),
                                      p(C.c_int32)]),
         "topo_design_pass": (C.c_int, [vp, vp, vp, p(PassParams), p(PassOut)]),
+        "topo_design_pass_begin": (C.c_int, [vp, vp, vp, p(PassParams), p(PassOut)]),
+        "topo_design_pass_end": (C.c_int, [vp, p(PassOut)]),
         "topo_last_launch_count": (C.c_int64, [vp]),
         "topo_set_timing": (C.c_int, [vp, C.c_int]),
         "topo_stage_times": (C.c_int, [vp, vp]),

@@ -84,6 +84,8 @@ struct MgState;
 void mg_state_free(MgState*);
 struct PassGraph;
 void pass_graph_free(PassGraph*);
+struct PassPending;
+void pass_pending_free(PassPending*);
 long long pass_graph_replays(const PassGraph*);
 
 struct topo_ctx {
@@ -153,6 +155,7 @@ struct topo_ctx {
   bool eta_safe = false;       // multi-rank eta: host check per round (re-run after a miss)
   bool use_pass_graph = true;  // capture / replay single-rank device passes (TOPO_PASS_GRAPH)
   PassGraph* pgraph = nullptr;
+  PassPending* pending = nullptr;  // topo_design_pass_begin without its _end yet
   int oc_blocks_now = 0;
   // lower-triangle CSC of K (topo_csc_*): pattern built once on first use
   CscTab csc_tab{};
@@ -599,8 +602,7 @@ topo_status launch_sk(topo_ctx* ctx, const SkArgs& S, cudaStream_t st) {
     const long long ngroups = (G.m + 31) / 32;
     const int nb = int(std::min<long long>(ctx->sm_count, (ngroups + th / 32 - 1) / (th / 32)));
     S2.gch = int(std::max(1LL, std::min(8LL, ngroups / (16LL * nb * (th / 32)))));
-    S2.counter = reinterpret_cast<unsigned long long*>(ctx->result.as<double>() + 63);
-    CK(cudaMemsetAsync(S2.counter, 0, sizeof(unsigned long long), st));
+    S2.counter = reinterpret_cast<unsigned long long*>(ctx->result.as<double>() + 126);
     constexpr size_t smem = size_t(th / 32) * kSkTmaStages * 4800;
     k_sk_store_tma<kSkTmaStages><<<nb, th, smem, st>>>(G, S2);
   } else {
@@ -645,7 +647,8 @@ topo_status reduce_on_device(topo_ctx* ctx, const double* partials, int count, d
 
 // device scratch layout of ctx->result (64 doubles): [0..5) pass scalars
 // (eta, iterations, g, -, c), [8..15) OC results, [24..36) pre-reductions,
-// [40..56) OC requests, [56..63) reduce_to_host, [63] sK work counter
+// [40..56) OC requests, [56..63) reduce_to_host, [64..112) eta / OC sums,
+// [126..128) sK work counters (zero between launches)
 template <int N>
 topo_status reduce_to_host(topo_ctx* ctx, const double* partials, int count) {
   double* dst = ctx->result.as<double>() + 56;
@@ -1222,6 +1225,7 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   CKC(ctx->cpart.ensure(sizeof(double) * size_t(topo_ctx::kUChunks) * size_t(ctx->sm_count) * 8));
   CKC(ctx->partials0.ensure(sizeof(double) * npart));
   CKC(ctx->result.ensure(sizeof(double) * 128));
+  CKC(cudaMemset(ctx->result.p, 0, sizeof(double) * 128));
 
   if (elem_state) {
     ctx->has_state = true;
@@ -1253,6 +1257,8 @@ void topo_ctx_destroy(topo_ctx* ctx) {
   ctx->mg = nullptr;
   pass_graph_free(ctx->pgraph);
   ctx->pgraph = nullptr;
+  pass_pending_free(ctx->pending);
+  ctx->pending = nullptr;
   ctx->d_kwp.release();
   for (DevBuf* b : {&ctx->d_map, &ctx->d_clean, &ctx->eta_dev, &ctx->oc_dev, &ctx->and_dx,
                     &ctx->and_dr, &ctx->and_px, &ctx->and_pr, &ctx->and_gamma})
@@ -3383,8 +3389,7 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
              &bis, &ev, 0.0, prm->beta, nullptr, nullptr, &oc_deferred));
   tmark(ctx, TOPO_STAGE_OC, 1, ctx->stream);
   ctx->oc_blocks_now = 0;
-  k_reduce_partials<1><<<1, 32, 0, ctx->stream>>>(ctx->cpart.as<double>(), nbe, 1, res + 4);
-  LAUNCHED();
+  TRY(reduce_on_device<1>(ctx, ctx->cpart.as<double>(), nbe, res + 4));
   if (ctx->comm) TRY(comm_allreduce(ctx->comm, ctx, res + 4, 1));  // c, on the stream
   if (oc_early) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
   if (want_sk && !overlap) {
@@ -3449,12 +3454,30 @@ static bool same_key(const PassKey& a, const PassKey& b) { return memcmp(&a, &b,
 void pass_graph_free(PassGraph* g) { delete g; }
 long long pass_graph_replays(const PassGraph* g) { return g->replays; }
 
+// a pass that topo_design_pass_begin enqueued and topo_design_pass_end has not
+// completed yet (the inputs are kept for the rare multi-rank eta re-run)
+struct PassPending {
+  bool active = false;
+  PassHost H{};
+  const double *x = nullptr, *U = nullptr;
+  topo_pass_params prm{};
+};
+void pass_pending_free(PassPending* p) { delete p; }
+
 extern "C" {
 
 topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
                              const topo_pass_params* prm, topo_pass_out* out) {
+  const topo_status st = topo_design_pass_begin(ctx, x, U, prm, out);
+  return st == TOPO_OK ? topo_design_pass_end(ctx, out) : st;
+}
+
+topo_status topo_design_pass_begin(topo_ctx* ctx, const double* x, const double* U,
+                                   const topo_pass_params* prm, topo_pass_out* out) {
   if (!ctx || !prm || !out) return TOPO_EINVAL;
   DeviceGuard dg_(ctx->device);
+  if (ctx->pending && ctx->pending->active)
+    return fail(ctx, TOPO_EINVAL, "design pass: the previous topo_design_pass_begin has no _end");
   ctx->launches = 0;
   ctx->oc_blocks_now = 0;
   const Geo& G = ctx->G;
@@ -3533,13 +3556,31 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
       pg->have_seen = true;
     }
   }
+  if (!ctx->pending) ctx->pending = new PassPending;
+  ctx->pending->active = true;
+  ctx->pending->H = H;
+  ctx->pending->x = x;
+  ctx->pending->U = U;
+  ctx->pending->prm = *prm;
+  return TOPO_OK;
+}
+
+topo_status topo_design_pass_end(topo_ctx* ctx, topo_pass_out* out) {
+  if (!ctx || !out) return TOPO_EINVAL;
+  DeviceGuard dg_(ctx->device);
+  if (!ctx->pending || !ctx->pending->active)
+    return fail(ctx, TOPO_EINVAL, "design pass: topo_design_pass_end without a _begin");
+  ctx->pending->active = false;
+  const PassHost H = ctx->pending->H;
+  const Geo& G = ctx->G;
   CK(cudaStreamSynchronize(ctx->stream));
   if (H.eta_spec && *reinterpret_cast<const int*>(ctx->h_result + 16) != 0) {
     // the multi-rank eta needed more than the two enqueued rounds (a second
     // re-centring): the pass ran with an unfinished eta; redo it with a host
     // check after every round
     ctx->eta_safe = true;
-    const topo_status st = topo_design_pass(ctx, x, U, prm, out);
+    const topo_pass_params prm = ctx->pending->prm;
+    const topo_status st = topo_design_pass(ctx, ctx->pending->x, ctx->pending->U, &prm, out);
     ctx->eta_safe = false;
     return st;
   }

@@ -1271,7 +1271,7 @@ struct SkArgs {
   const double* eta_ptr;  // device scalar eta
   double beta, e0, emin, penal;
   double* sK;
-  unsigned long long* counter;  // k_sk_store_tma: work counter (zeroed before launch)
+  unsigned long long* counter;  // k_sk_store_tma: {next group, finished warps}, zero between launches
   int gch;                      // groups per claim
 };
 
@@ -1458,6 +1458,17 @@ __global__ void __launch_bounds__(128) k_sk_store_tma(Geo G, SkArgs A) {
   }
   // shared memory must outlive the copies that read it
   if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  // the last warp to finish re-arms the counters for the next launch (no
+  // memset node on the critical path between K2 and the store)
+  if (lane == 0) {
+    __threadfence();
+    const unsigned long long nw = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(A.counter + 1, 1ull) == nw - 1) {
+      A.counter[0] = 0;
+      A.counter[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // ============================================================================

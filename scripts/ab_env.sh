@@ -5,5 +5,5 @@ c=$1; n=$2; shift 2
 for rep in 1 2; do for v in "$@"; do
   e="$v"; [ "$v" = "-" ] && e=""
   env $e python bench.py --config $c --steps $n --warmup 4 --no-cpu-baseline 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('[$v]', round(d['ms_per_step'],4), round(d['value'],1), {k:round(v,4) for k,v in d['stages_ms'].items()}, flush=True)"
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('[$v]', round(d['ms_per_step'],4), round(d['value'],1), 'e2e_ms', round(d['e2e']['ms_per_step'],3), {k:round(v,4) for k,v in d['stages_ms'].items()}, flush=True)"
 done; done
