@@ -477,7 +477,9 @@ def main():
         "data": "synthetic (seeded x~U(0.01,1), U~N(0,1); SURVEY.md Appendix B)",
         "config": dict(workload, l2=("flushed between passes (256 MiB write)" if res["flushed"]
                                      else "inputs/outputs larger than L2 (no flush)")),
-        "roofline": {"bound": "hbm", "kernel": "k_sk_store (K3b, fea.hpp:135-146 + :162-169)",
+        "roofline": {"bound": "hbm",
+                     "kernel": ("k_sk_store_tma" if cfg.nelz and m * cfg.P * 8 >= 256e6
+                                else "k_sk_store") + " (K3b, fea.hpp:135-146 + :162-169)",
                      "achieved": sk_gbs, "peak": peak, "unit": "GB/s",
                      "frac": (sk_gbs / peak) if sk_gbs else None, "traffic": traffic,
                      "bytes_per_launch": sk_bytes, "ms_per_launch": sk_ms,
