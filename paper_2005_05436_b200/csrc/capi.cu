@@ -151,7 +151,6 @@ struct topo_ctx {
   int conv_R = 8;              // outputs per thread along the run axis
   int conv_A = 0;              // > 0: small-reach direct variant with half-width bound A
   bool overlap_sk = false;     // run the sK store concurrently with K3a..K6
-  int conv3_rb_force = 0;      // k_conv3 outputs per thread edge for the next plan (0: by grid size)
   bool keep_xphys = false;     // K3a writes xPhys for topo_device_buffer consumers
   bool eta_safe = false;       // multi-rank eta: host check per round (re-run after a miss)
   bool use_pass_graph = true;  // capture / replay single-rank device passes (TOPO_PASS_GRAPH)
@@ -426,7 +425,6 @@ ConvGeom conv_geom3(const topo_ctx* c, const Geo& G, int WR, int WO, int RB = kC
 // small grids (fewer than two 4 x 4 blocks per SM, e.g. C4's 54): 2 x 2
 // outputs per thread, 4x the blocks (less register reuse, but every SM busy)
 int conv3_rb(const topo_ctx* c, const Geo& G) {
-  if (c->conv3_rb_force) return c->conv3_rb_force;
   const long long outs4 = 32LL * kC3R * kC3T * (kThreads / 32);
   return G.m < 2LL * c->sm_count * outs4 ? kC3Rs : kC3R;
 }
@@ -1220,7 +1218,7 @@ topo_status topo_ctx_create(const topo_grid_desc* d, const double* ke_full,
   ctx->coop_eta = std::max(1, std::min(ctx->sm_count * occ2, want_eta));
   ctx->coop_blocks = std::max(1, std::min(ctx->sm_count * occ, want));
   const size_t npart = std::max<size_t>(
-      {size_t(conv_blocks(ctx)) * 3 * 4, size_t(ctx->coop_blocks) * 2 * 32 * 2,
+      {size_t(conv_blocks(ctx)) * 3, size_t(ctx->coop_blocks) * 2 * 32 * 2,
        size_t(ctx->coop_eta) * kEtaNS + 2,
        size_t(ctx->sm_count) * 8 * 4});
   CKC(ctx->partials.ensure(sizeof(double) * npart));
@@ -3336,14 +3334,6 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
   // as the K3a chunks covering its columns plus the filter reach are done;
   // the per-block partials keep the layout of one launch (same results)
   bool use3 = false;
-  struct RbGuard {  // K4's tile shape for this pass only
-    topo_ctx* c;
-    ~RbGuard() { c->conv3_rb_force = 0; }
-  } rb_guard{ctx};
-  {
-    const char* k4s = getenv("TOPO_K4_SMALL");  // EXPERIMENT
-    if (overlap && k4s && k4s[0] == '1') ctx->conv3_rb_force = kC3Rs;
-  }
   const ConvGeom T4 = plan_geom(ctx, G, &use3);
   const bool k4chunks = nch > 1 && use3 && !ctx->comm;
   const int ztiles = use3 ? (T4.other_n + T4.TO - 1) / T4.TO : 0;
@@ -3384,7 +3374,6 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
     TRY((launch_conv<2, CONV_ADJ2_OC>(ctx, G, A4, &nb4)));
   }
   tmark(ctx, TOPO_STAGE_ADJOINT, 1, ctx->stream);
-  ctx->conv3_rb_force = 0;
   // K5 + K6: beside the overlapped sK stream, with one cooperative block per
   // SM (all resident next to its 2 blocks per SM); else after the join
   static const char* oce = getenv("TOPO_OC_EARLY");

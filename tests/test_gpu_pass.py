@@ -209,6 +209,41 @@ def test_pass_deterministic(P):
     assert np.array_equal(a.xNew, b.xNew) and np.array_equal(a.dc, b.dc)
 
 
+@pytest.mark.parametrize("cid,grid", [(1, None), (4, (24, 16, 12))])
+def test_pass_begin_end_halves(P, cid, grid):
+    """topo_design_pass_begin enqueues and returns, _end waits and fills the
+    scalars: same bits as the one-call pass (eager, captured and replayed);
+    a second _begin before _end and an _end without _begin are refused."""
+    import ctypes as C
+    import torch
+    from paper_2005_05436_b200 import _lib as L
+    from paper_2005_05436_b200.configs import CONFIGS
+    cfg = CONFIGS[cid] if grid is None else CONFIGS[cid].scaled(*grid)
+    rng = np.random.default_rng(11)
+    x, u = rng.uniform(0.01, 1.0, cfg.m), rng.normal(size=cfg.n)
+    xd, ud = torch.from_numpy(x).cuda(), torch.from_numpy(u).cuda()
+    with P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu) as ctx:
+        ref = ctx.design_pass(xd, ud, beta=cfg.beta, eta0=cfg.eta0, move=cfg.move,
+                              volfrac=cfg.volfrac, outputs=False)
+        pp = L.PassParams(P.SimpParams().c(), cfg.beta, cfg.eta0, cfg.move, cfg.volfrac, math.nan,
+                          L.VOL_FILTERED, 1)
+        xnew = torch.zeros(cfg.m, dtype=torch.float64, device="cuda")
+        po = L.PassOut(None, None, None, None, None, xnew.data_ptr(), None)
+        lib, h = ctx.lib, ctx.h
+        assert lib.topo_design_pass_end(h, C.byref(po)) == L.TOPO_EINVAL  # nothing pending
+        for _ in range(3):  # eager, capture, replay
+            xnew.zero_()
+            assert lib.topo_design_pass_begin(h, xd.data_ptr(), ud.data_ptr(), C.byref(pp),
+                                              C.byref(po)) == 0
+            assert lib.topo_design_pass_begin(h, xd.data_ptr(), ud.data_ptr(), C.byref(pp),
+                                              C.byref(po)) == L.TOPO_EINVAL  # one pass in flight
+            assert lib.topo_design_pass_end(h, C.byref(po)) == 0
+            assert (po.eta, po.lambda_, po.c, po.bisections) == (ref.eta, ref.lam, ref.c,
+                                                                 ref.bisections)
+            assert torch.equal(xnew, ref.xNew)
+        assert lib.topo_design_pass_end(h, C.byref(po)) == L.TOPO_EINVAL
+
+
 # ------------------------------------------------ reference golden fixtures
 import glob as _glob
 import hashlib as _hashlib
