@@ -3359,12 +3359,31 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
     }
   }
   // c (res[4]) is summed at the tail of the pass, off the K3a -> K4 -> OC chain
-  if (ctx->comm)  // both pre-adjoint fields in one exchange
+  // Multi-rank: both pre-adjoint fields' halos go in one exchange; with
+  // k_conv3, K4's interior tiles (the z range K1 used: no halo column in their
+  // window) run on hstream meanwhile and the boundary tiles follow the
+  // exchange, as for K1 (same partial layout as one launch).
+  const bool halo_overlap4 = halo_overlap && use3 && nch == 1;
+  if (halo_overlap4) {
+    CK(cudaEventRecord(ctx->ev_h0, ctx->stream));  // K3a done
+    CK(cudaStreamWaitEvent(ctx->hstream, ctx->ev_h0, 0));
+    const cudaStream_t main = ctx->stream;
+    ctx->stream = ctx->hstream;
+    const topo_status si = launch_conv3_range<2, CONV_ADJ2_OC>(ctx, G, A4, z_lo, z_hi, &nb4);
+    ctx->stream = main;
+    TRY(si);
+    CK(cudaEventRecord(ctx->ev_h1, ctx->hstream));
+  }
+  if (ctx->comm)
     TRY(comm_halo(ctx->comm, ctx, ctx->a1_st.as<double>(), ctx->a2_st.as<double>()));
   tmark(ctx, TOPO_STAGE_ELEM, 1, ctx->stream);
   // K4
   tmark(ctx, TOPO_STAGE_ADJOINT, 0, ctx->stream);
-  if (k4chunks) {
+  if (halo_overlap4) {
+    if (z_lo > 0) TRY((launch_conv3_range<2, CONV_ADJ2_OC>(ctx, G, A4, 0, z_lo, &nb4)));
+    if (z_hi < ztiles) TRY((launch_conv3_range<2, CONV_ADJ2_OC>(ctx, G, A4, z_hi, ztiles, &nb4)));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_h1, 0));
+  } else if (k4chunks) {
     while (next_a < nch) {  // (none left normally)
       const int z0 = ztile0(next_a), z1 = ztile0(next_a + 1);
       if (z1 > z0) TRY((launch_conv3_range<2, CONV_ADJ2_OC>(ctx, G, A4, z0, z1, &nb4)));
