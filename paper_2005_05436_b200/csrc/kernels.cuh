@@ -1456,8 +1456,9 @@ __global__ void __launch_bounds__(128) k_sk_store_tma(Geo G, SkArgs A) {
       if (g0 >= ngroups) break;
     }
   }
-  // shared memory must outlive the copies that read it
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  // the copies must have completed (shared memory read, global memory
+  // written) before the warp retires
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   // the last warp to finish re-arms the counters for the next launch (no
   // memset node on the critical path between K2 and the store)
   if (lane == 0) {
