@@ -305,7 +305,8 @@ topo_status topo_design_pass(topo_ctx* ctx, const double* x, const double* U,
  * `out` must stay valid and untouched until _end); _end waits for the stream,
  * completes the host-side parts (multi-rank OC / eta completion) and fills the
  * scalars of `out` (pass the same `out`). topo_design_pass = _begin + _end.
- * One pass in flight per context. */
+ * One pass in flight per context, and no other call on the context between
+ * the two halves (they share its scratch buffers and result words). */
 topo_status topo_design_pass_begin(topo_ctx* ctx, const double* x, const double* U,
                                    const topo_pass_params* prm, topo_pass_out* out);
 topo_status topo_design_pass_end(topo_ctx* ctx, topo_pass_out* out);
