@@ -320,26 +320,53 @@ size_t conv_smem(const ConvGeom& T) {
          sizeof(int) * size_t(T.EI) + 16;
 }
 
-// 8 warps per block; pick the warp split that loads the fewest tile values per
-// output (halo overhead and partial tiles) within the shared-memory budget
+// Tile shape of k_conv. 3D (small reach handled by k_conv3; this is the
+// fallback): 8 warps, the split that loads the fewest tile values per output.
+// 2D: every split of 1..8 warps over (i, run) is a candidate and the estimate
+// is the busiest SM's time: a thread's work (R outputs x the folded taps + its
+// share of the tile fill) times the warps that SM gets beyond one per
+// scheduler. The grids are small (with 8 warps per block C1 has 20 blocks on 148
+// SMs, C2 70, C3 247 = 1.7 per SM), so the shape that spreads over the SMs
+// wins over the one with the least halo: C1 / C2 32 x 32-output tiles of 4
+// warps (40 / 133 blocks), C3 32 x 56 of 7 warps (286 blocks, two per SM).
+// Measured: C1 0.165 -> 0.152, C2 0.258 -> 0.249, C3 0.645 -> 0.629 ms per pass
+// (less than the estimate promises: the kernel's fill and weight-load latencies
+// are exposed at these occupancies).
 ConvGeom pick_geom(const topo_ctx* c, const Geo& G) {
-  static const int opts3[][3] = {{1, 2, 4}, {1, 4, 2}, {1, 1, 8}, {1, 8, 1}};
-  static const int opts2[][3] = {{2, 4, 1}, {4, 2, 1}, {1, 8, 1}, {8, 1, 1}};
   ConvGeom best{};
   double best_cost = 1e300;
-  for (int q = 0; q < 4; ++q) {
-    const int* o = G.is3d ? opts3[q] : opts2[q];
-    ConvGeom T = conv_geom(c, G, o[0], o[1], o[2]);
-    if (conv_smem(T) > 200 * 1024 || double(T.EI) * T.ER * T.EO >= (1 << 20)) continue;
+  auto consider = [&](int wi, int wr, int wo, bool waves) {
+    ConvGeom T = conv_geom(c, G, wi, wr, wo);
+    if (conv_smem(T) > 200 * 1024 || double(T.EI) * T.ER * T.EO >= (1 << 20)) return;
     const double outs = double(T.TI) * T.TR * T.TO;
-    const double fi = std::ceil(double(G.nely) / T.TI) * T.TI / G.nely;
-    const double fr = std::ceil(double(T.run_n) / T.TR) * T.TR / T.run_n;
-    const double fo = std::ceil(double(T.other_n) / T.TO) * T.TO / T.other_n;
-    const double cost = (double(T.EI) * T.ER * T.EO / outs + 64.0) * fi * fr * fo;
+    const long long bi = (G.nely + T.TI - 1) / T.TI, br = (T.run_n + T.TR - 1) / T.TR,
+                    bo = (T.other_n + T.TO - 1) / T.TO;
+    double cost;
+    if (!waves) {
+      const double fi = double(bi) * T.TI / G.nely, fr = double(br) * T.TR / T.run_n,
+                   fo = double(bo) * T.TO / T.other_n;
+      cost = (double(T.EI) * T.ER * T.EO / outs + 64.0) * fi * fr * fo;
+    } else {
+      const int w = wi * wr * wo;
+      const double taps = 0.5 * double(c->w.size());  // mirror-folded: ~2 taps per FP64 op
+      const double per_thread = c->conv_R * taps + 8.0 * double(T.EI) * T.ER * T.EO / (32.0 * w);
+      const long long on_sm = (bi * br * bo + c->sm_count - 1) / c->sm_count;  // blocks, busiest SM
+      cost = per_thread * std::max(1.0, double(on_sm) * w / 4.0) - 1e-6 * w;   // (ties: more warps)
+    }
     if (cost < best_cost) {
       best_cost = cost;
       best = T;
     }
+  };
+  if (G.is3d) {
+    static const int opts3[][3] = {{1, 2, 4}, {1, 4, 2}, {1, 1, 8}, {1, 8, 1}};
+    for (auto& o : opts3) consider(o[0], o[1], o[2], false);
+  } else {
+    static const char* ge = getenv("TOPO_CONV_GEOM");  // 0: the 8-warp shapes only (A/B)
+    const bool all = !(ge && ge[0] == '0');
+    for (int wi : {1, 2, 4, 8})
+      for (int wr = 1; wr * wi <= 8; ++wr)
+        if (all || wi * wr == 8) consider(wi, wr, 1, all);
   }
   return best;
 }
@@ -543,7 +570,7 @@ topo_status launch_conv_t(topo_ctx* ctx, const Geo& G, const ConvArgs& A, int* n
                             optin - int(fa.sharedSizeBytes)));
     attr_done |= 1ull << ctx->device;
   }
-  k_conv<NF, MODE, R, AW><<<grid, kThreads, smem, ctx->stream>>>(
+  k_conv<NF, MODE, R, AW><<<grid, 32 * T.WI * T.WR * T.WO, smem, ctx->stream>>>(
       G, T, ctx->d_cols.as<ConvCol>(), int(ctx->cols.size()), ctx->d_wpad.as<double>(), A);
   LAUNCHED();
   if (nblocks) *nblocks = int(grid.x * grid.y * grid.z);
