@@ -231,8 +231,19 @@ __device__ __forceinline__ void conv_columns(const double* __restrict__ tile, in
                                              int sPlane, const ConvCol* __restrict__ cols, int c0,
                                              int c1, const double* __restrict__ wts,
                                              double (&acc)[R]) {
+  if (c0 >= c1) return;
+  // the column record and the weights of the next chunk are loaded while the
+  // current chunk's FMAs run (they are global loads: exposed, they were the
+  // top stall of the large-reach 2D filter)
+  ConvCol col = cols[c0];
+  double2 wn[R / 2];
+  {
+    const double2* w2 = reinterpret_cast<const double2*>(wts + col.woff);
+#pragma unroll
+    for (int t = 0; t < R / 2; ++t) wn[t] = __ldg(w2 + t);
+  }
   for (int c = c0; c < c1; ++c) {
-    const ConvCol col = cols[c];
+    const ConvCol ncol = c + 1 < c1 ? cols[c + 1] : col;
     const int base = sb - col.a;
     const int oi = col.di * sI, oo = col.dother * sPlane;
     const double* p0 = tile + base + oi + oo;
@@ -247,20 +258,23 @@ __device__ __forceinline__ void conv_columns(const double* __restrict__ tile, in
       return v;
     };
     const double2* w2 = reinterpret_cast<const double2*>(wts + col.woff);
+    const double2* w2n = reinterpret_cast<const double2*>(wts + ncol.woff);
     const int nch = (2 * col.a + R) / R;  // ceil((2a + 1) / R)
     double v[2 * R - 1];
 #pragma unroll
     for (int s = 0; s < R - 1; ++s) v[s] = colval(s);
     for (int ch = 0; ch < nch; ++ch) {
-#pragma unroll
-      for (int s = 0; s < R; ++s) v[R - 1 + s] = colval(ch * R + R - 1 + s);
       double wv[R];
 #pragma unroll
       for (int t = 0; t < R / 2; ++t) {
-        const double2 ww = __ldg(w2 + ch * (R / 2) + t);
-        wv[2 * t] = ww.x;
-        wv[2 * t + 1] = ww.y;
+        wv[2 * t] = wn[t].x;
+        wv[2 * t + 1] = wn[t].y;
       }
+      const double2* wnext = ch + 1 < nch ? w2 + (ch + 1) * (R / 2) : w2n;
+#pragma unroll
+      for (int t = 0; t < R / 2; ++t) wn[t] = __ldg(wnext + t);
+#pragma unroll
+      for (int s = 0; s < R; ++s) v[R - 1 + s] = colval(ch * R + R - 1 + s);
 #pragma unroll
       for (int t = 0; t < R; ++t)
 #pragma unroll
@@ -268,6 +282,7 @@ __device__ __forceinline__ void conv_columns(const double* __restrict__ tile, in
 #pragma unroll
       for (int s = 0; s < R - 1; ++s) v[s] = v[R + s];
     }
+    col = ncol;
   }
 }
 
