@@ -3341,7 +3341,14 @@ static topo_status pass_enqueue(topo_ctx* ctx, const double* x, const double* U,
   E.dcPhys = out->dcPhys ? dcphys_p : nullptr;  // only when requested
   E.a1 = ctx->a1_st.as<double>();
   E.a2 = ctx->a2_st.as<double>();
-  const int nbc = grid_for(ctx, (G.m + nch - 1) / nch);  // blocks per chunk
+  // blocks per chunk. 3D: one resident wave (2 blocks per SM), so the grid
+  // sweeps the element layers in x order and a node plane of U is still in L2
+  // when the next layer gathers it; with more blocks than are resident, each
+  // wave ran through all of its strided chunks before the next wave started
+  // and the planes between their strips were read twice (C5: 512 MB of U
+  // reads for 344 MB).
+  int nbc = grid_for(ctx, (G.m + nch - 1) / nch);
+  if (G.is3d) nbc = std::min(nbc, 2 * ctx->sm_count);
   const int nbe = nbc * nch;
   // K4 arguments (dual-field adjoint + OC records)
   ConvArgs A4{};
