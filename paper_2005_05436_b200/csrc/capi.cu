@@ -153,6 +153,8 @@ struct topo_ctx {
   bool overlap_sk = false;     // run the sK store concurrently with K3a..K6
   bool keep_xphys = false;     // K3a writes xPhys for topo_device_buffer consumers
   bool eta_safe = false;       // multi-rank eta: host check per round (re-run after a miss)
+  int eta_spec_rounds = 2;     // multi-rank eta rounds enqueued without a host check: 2, or 1
+  int eta_calm = 0;            //   after 4 passes in a row that converged in their first round
   bool use_pass_graph = true;  // capture / replay single-rank device passes (TOPO_PASS_GRAPH)
   PassGraph* pgraph = nullptr;
   PassPending* pending = nullptr;  // topo_design_pass_begin without its _end yet
@@ -731,10 +733,10 @@ topo_status run_eta(topo_ctx* ctx, const double* xt, double beta, double eta0,
   };
   if (speculative) {
     const char* sr = getenv("TOPO_ETA_SPEC_ROUNDS");  // tests: 1 forces the re-run path
-    const int nspec = sr ? std::max(1, atoi(sr)) : 2;
+    const int nspec = sr ? std::max(1, atoi(sr)) : ctx->eta_spec_rounds;
     for (int r = 0; r < nspec; ++r) TRY(round());
-    CK(cudaMemcpyAsync(ctx->h_result + 16, &st->go, sizeof(int), cudaMemcpyDeviceToHost,
-                       ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_result + 16, &st->go, 2 * sizeof(int), cudaMemcpyDeviceToHost,
+                       ctx->stream));  // {go, rounds}
     return TOPO_OK;
   }
   for (int r = 0; r < 64; ++r) {  // every round feeds >= 1 evaluation (<= 51)
@@ -3627,8 +3629,22 @@ topo_status topo_design_pass_end(topo_ctx* ctx, topo_pass_out* out) {
   const PassHost H = ctx->pending->H;
   const Geo& G = ctx->G;
   CK(cudaStreamSynchronize(ctx->stream));
+  if (H.eta_spec) {
+    // Speculation depth for the next passes: the second round (4 launches and
+    // an allreduce in front of the store) is dropped while passes converge in
+    // their first round, and comes back with the first re-centring. Every
+    // rank sees the same {go, rounds} (identical allreduced sums), so the
+    // ranks keep enqueueing the same collectives.
+    const int* gr = reinterpret_cast<const int*>(ctx->h_result + 16);
+    if (gr[0] != 0 || gr[1] > 1) {
+      ctx->eta_spec_rounds = 2;
+      ctx->eta_calm = 0;
+    } else if (++ctx->eta_calm >= 4) {
+      ctx->eta_spec_rounds = 1;
+    }
+  }
   if (H.eta_spec && *reinterpret_cast<const int*>(ctx->h_result + 16) != 0) {
-    // the multi-rank eta needed more than the two enqueued rounds (a second
+    // the multi-rank eta needed more rounds than were enqueued (a further
     // re-centring): the pass ran with an unfinished eta; redo it with a host
     // check after every round
     ctx->eta_safe = true;

@@ -1016,7 +1016,8 @@ __global__ void __launch_bounds__(kThreads) k_eta_solve(EtaArgs A) {
 struct EtaDev {
   EtaCtl ctl;
   double c;
-  int go;
+  int go;      // another round is needed
+  int rounds;  // rounds that did work so far (the host adapts its speculation to it)
 };
 
 __global__ void k_eta_dev_init(EtaDev* st, double eta0) {
@@ -1024,6 +1025,7 @@ __global__ void k_eta_dev_init(EtaDev* st, double eta0) {
     st->ctl.init(eta0);
     st->c = st->ctl.eta;
     st->go = 1;
+    st->rounds = 0;
   }
 }
 
@@ -1052,6 +1054,7 @@ __global__ void k_eta_dev_step(EtaDev* st, const double* __restrict__ sums, doub
   const EtaSeries S{beta, st->c, mtotal, sums};
   double cn = st->c;
   st->go = eta_replay(ctl, S, &cn) ? 1 : 0;
+  st->rounds += 1;
   st->c = cn;
   st->ctl = ctl;
   result[0] = ctl.eta;

@@ -214,3 +214,54 @@ def test_slab_ranks_recentred_eta(P, monkeypatch, spec_rounds):
     assert out[0].eta == out[1].eta and abs(out[0].eta - ref.eta) <= 5e-8
     assert out[0].eta_iters == ref.eta_iters
     assert rel(np.concatenate([o.xNew for o in out]), ref.xNew) <= 1e-10
+
+
+def test_slab_ranks_adaptive_eta_speculation(P):
+    """The number of eta rounds a multi-rank pass enqueues without a host check
+    adapts: two at first, one after four passes in a row that converged in
+    their first round (fewer launches), two again after a design that needs a
+    re-centred round (detected after the pass, which is re-run). Every pass
+    matches the single context."""
+    import threading
+    from paper_2005_05436_b200.configs import CONFIGS
+    from paper_2005_05436_b200.dist import ThreadHostComm, make_rank_context, slab_views
+    cfg = CONFIGS[4].scaled(24, 12, 12)
+    rng = np.random.default_rng(8)
+    calm = rng.uniform(0.01, 1.0, cfg.m)
+    far = 0.01 + 0.99 * rng.uniform(0, 1, cfg.m) ** 3
+    u = rng.normal(size=cfg.n)
+    seq = [calm] * 6 + [far, calm]
+    kw = dict(beta=4.0, move=cfg.move, volfrac=cfg.volfrac)  # calm: d = 0.017, far: d = -0.44
+    with P.Context(*cfg.grid, rmin=cfg.rmin, nu=cfg.nu) as ctx:
+        ref = [ctx.design_pass(x, u, outputs=False, **kw) for x in (calm, far)]
+    assert abs(ref[1].eta - 0.5) > 0.03  # `far` needs a re-centred round
+    comm = ThreadHostComm(2)
+    out, err = [[], []], [None, None]
+
+    def work(r):
+        try:
+            views = {id(x): slab_views(cfg, x, u, None, r, 2) for x in (calm, far)}
+            st = views[id(calm)][4]
+            with make_rank_context(cfg, st, r, 2, comm=comm.for_rank(r)) as c:
+                for x in seq:
+                    _, _, xs, us, _ = views[id(x)]
+                    out[r].append(c.design_pass(xs, us, outputs=False, **kw))
+        except Exception:  # noqa: BLE001
+            import traceback
+            err[r] = traceback.format_exc()
+            comm.barrier.abort()
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert err == [None, None], err
+    for k, x in enumerate(seq):
+        want = ref[0] if x is calm else ref[1]
+        a, b = out[0][k], out[1][k]
+        assert a.eta == b.eta and abs(a.eta - want.eta) <= 5e-8 and a.eta_iters == want.eta_iters, k
+        assert rel(np.concatenate([a.xNew, b.xNew]), want.xNew) <= 1e-10, k
+    launches = [o.launches for o in out[0]]
+    assert launches[5] < launches[0]   # the second speculative round was dropped
+    assert launches[7] == launches[0]  # and came back after the re-centred pass
