@@ -1364,7 +1364,7 @@ __global__ void __launch_bounds__(kThreads) k_sk_store(Geo G, SkArgs A) {
 // (4800 B) go to a warp-private stage in shared memory and lane 0 hands the
 // stage to `cp.async.bulk` (shared -> global, L2 evict-first). D stages per
 // warp, D - 1 copies in flight, no block barriers. Why not plain stores
-// (scripts/store_bench.cu, profiles/r02/store_bench.txt): a store instruction
+// (scripts/store_bench.cu, profiles/r02/store_bench_*.txt): a store instruction
 // keeps its source registers until its data has left the SM, microseconds
 // beside a saturated write stream, so the bytes in flight (~100 KB per SM for
 // the full rate) would live in registers the co-running filter and sensitivity
