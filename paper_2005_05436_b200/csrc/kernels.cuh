@@ -1195,7 +1195,12 @@ struct KeWalsh {
 // (component 0 = x flips with j, 1 = y with i, 2 = z with k)
 __host__ __device__ constexpr int walsh_axis(int c) { return c == 0 ? 2 : (c == 1 ? 0 : 1); }
 
-__global__ void __launch_bounds__(kThreads, 2) k_elem_walsh(Geo G, KeWalsh K, ElemArgs A) {
+// 104 registers (20 doubles spill to local memory; the kernel is gather-latency
+// bound): two of its blocks and the store's block (128 x 96) fill the register
+// file exactly, so the overlapped store is resident from the start instead of
+// waiting for K3a's first wave to drain (C5 pass 6.05 -> 5.91 ms, C4 0.130 ->
+// 0.1245 ms on the same box).
+__global__ void __maxnreg__(104) k_elem_walsh(Geo G, KeWalsh K, ElemArgs A) {
   __shared__ double scratch[32];
   const double eta = A.input_is_phys ? 0.5 : *A.eta_ptr;
   const double a = tanh(A.beta * eta);
