@@ -2172,12 +2172,35 @@ topo_status topo_oc_primal_dual(topo_ctx* ctx, const double* x, const double* dc
   const double budget = prm->volfrac * ctx->m_total - ctx->nS_total;  // oc.hpp:195
   double lm = 0;
   if (budget <= 0) fb = 1;
-  if (!fb) {
+  const char* pde = getenv("TOPO_OC_PD_DEVICE");  // 0: host-driven loop also on one rank (tests)
+  const bool pd_host = ctx->comm || (pde && pde[0] == '0');
+  if (!fb && !pd_host) {
+    // single rank: the dual iteration in one cooperative launch (k_oc_pd), one
+    // host synchronisation in all instead of one per dual iteration
+    OcPdArgs A;
+    A.m = G.m;
+    A.R = ctx->oc_view;
+    A.prep = ctx->partials0.as<double>();
+    A.n_prep = nb;
+    A.budget = budget;
+    A.pd_tol = pd_tol;
+    A.mtotal = ctx->m_total;
+    A.volfrac = prm->volfrac;
+    A.partials = ctx->partials.as<double>();
+    A.result = ctx->result.as<double>() + 56;
+    TRY(coop_launch(ctx, (const void*)k_oc_pd, &A, ctx->coop_blocks));
+    CK(cudaMemcpyAsync(ctx->h_result, A.result, sizeof(double) * 3, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    lm = ctx->h_result[0];
+    it = int32_t(ctx->h_result[1]);
+    fb = int32_t(ctx->h_result[2]);
+  } else if (!fb) {
     TRY(reduce_to_host<3>(ctx, ctx->partials0.as<double>(), nb));  // sum ocP (oc.hpp:204)
     lm = ctx->h_result[0] / (ctx->m_total * prm->volfrac);
     if (!(lm > 0)) fb = 1;
   }
-  for (; !fb; ++it) {
+  for (; !fb && pd_host; ++it) {  // multi-rank: host-driven, one allreduce per iteration
     if (it >= 1000) {
       fb = 1;
       break;

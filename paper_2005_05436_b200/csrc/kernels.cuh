@@ -2066,6 +2066,97 @@ __global__ void __launch_bounds__(kThreads) k_sum(long long m, const double* __r
 }
 
 // fixed-order final reduction of `count` partials (stride) into out[0..N)
+// oc.hpp:195-236 on the device (single rank): the whole dual fixed-point
+// iteration lm <- sumMid(lm) / (budget - sumClamped(lm)) in one cooperative
+// launch, one grid barrier per iteration. Every block sums the per-block
+// records in the same fixed order (warp_sum_partials, the order of the
+// host-driven loop's reductions) and takes the same decisions, so the
+// multiplier sequence is bitwise that of the host-driven loop.
+// result: {lm, iterations, fell_back}.
+struct OcPdArgs {
+  long long m;
+  OcRecs R;
+  const double* prep;  // K4-style prep records (stride 3): [0] = sum ocP
+  int n_prep;
+  double budget, pd_tol, mtotal, volfrac;
+  double* partials;    // [2][3 * gridDim]
+  double* result;
+};
+
+__global__ void __launch_bounds__(kThreads) k_oc_pd(OcPdArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double scratch[3 * 32];
+  __shared__ double s_lm;
+  __shared__ int s_state;  // 0: iterate, 1: converged, 2: fall back
+  if (threadIdx.x < 32) {
+    double s[3];
+    warp_sum_partials<3>(A.prep, A.n_prep, 3, s);
+    if (threadIdx.x == 0) {
+      s_lm = s[0] / (A.mtotal * A.volfrac);  // oc.hpp:204
+      s_state = s_lm > 0 ? 0 : 2;
+    }
+  }
+  __syncthreads();
+  double lm = s_lm;
+  int it = 0, fb = s_state == 2, buf = 0;
+  for (; !fb; ++it) {
+    if (it >= 1000) {
+      fb = 1;
+      break;
+    }
+    double red[3] = {0.0, 0.0, 0.0};
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < A.m;
+         e += (long long)gridDim.x * blockDim.x) {
+      if (A.R.ocp[e] < 0.0) continue;  // passive
+      const double4 r = A.R.get(e);
+      const double f = r.z / lm;
+      if (f > r.y)
+        red[0] += r.y;
+      else if (f < r.x)
+        red[0] += r.x;
+      else {
+        red[1] += r.z;
+        red[2] += 1.0;
+      }
+    }
+    block_sum<3>(red, scratch);
+    double* P = A.partials + (long long)buf * 3 * gridDim.x;
+    if (threadIdx.x == 0)
+      for (int q = 0; q < 3; ++q) P[3 * blockIdx.x + q] = red[q];
+    grid.sync();
+    if (threadIdx.x < 32) {
+      double s[3];
+      warp_sum_partials<3>(P, gridDim.x, 3, s);
+      if (threadIdx.x == 0) {
+        const double sumClamped = s[0], sumMid = s[1], numMid = s[2];
+        const double den = A.budget - sumClamped;
+        const double lmNext = sumMid / den;
+        if (numMid == 0 || den <= 0 || !(lmNext > 0) || !isfinite(lmNext)) {
+          s_state = 2;
+        } else {
+          s_state = fabs(lmNext - lm) <= A.pd_tol ? 1 : 0;
+          s_lm = lmNext;
+        }
+      }
+    }
+    __syncthreads();
+    const int state = s_state;
+    if (state == 2) {
+      fb = 1;
+      break;
+    }
+    lm = s_lm;
+    buf ^= 1;
+    __syncthreads();  // (s_state / s_lm are rewritten in the next iteration)
+    if (state == 1) break;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.result[0] = lm;
+    A.result[1] = double(it);
+    A.result[2] = double(fb);
+  }
+}
+
 template <int N>
 __global__ void k_reduce_partials(const double* __restrict__ p, int count, int stride,
                                   double* __restrict__ out) {

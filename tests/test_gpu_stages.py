@@ -387,3 +387,24 @@ def test_primal_dual_reference_known_answers(P):  # test_oc.cpp:195-240
         r = ctx.primal_dual_update(x, dc, dV, P.OcParams(move=0.01, volfrac=0.5))
     assert abs(r.xNew.mean() - 0.5) <= 1e-3
     assert np.all(np.abs(r.xNew - x) <= 0.01 + 1e-14)
+
+
+def test_primal_dual_device_loop_is_bitwise_host_loop(P, monkeypatch):
+    """k_oc_pd (the dual fixed-point iteration in one cooperative launch) takes
+    the reductions and decisions of the host-driven loop (TOPO_OC_PD_DEVICE=0,
+    the multi-rank path) in the same order: same multiplier bits, iteration
+    count and update, with and without the bisection fallback."""
+    rng = np.random.default_rng(5)
+    m = 48 * 24
+    for move, volfrac in ((0.2, 0.5), (0.45, 0.3), (0.01, 0.5)):
+        x = rng.uniform(0.05, 1.0, m)
+        dc = -rng.uniform(0.1, 2.0, m)
+        dV = np.full(m, 1.0 / m)
+        res = []
+        for dev in ("1", "0"):
+            monkeypatch.setenv("TOPO_OC_PD_DEVICE", dev)
+            with P.Context(48, 24, 0, rmin=1.5) as ctx:
+                res.append(ctx.primal_dual_update(x, dc, dV, P.OcParams(move=move, volfrac=volfrac)))
+        a, b = res
+        assert (a.lam, a.bisections, a.fell_back) == (b.lam, b.bisections, b.fell_back)
+        assert np.array_equal(a.xNew, b.xNew)
